@@ -1,0 +1,239 @@
+/* gasb.h — C ABI of the B200-native GNNAutoScale (GAS) training hot path.
+ *
+ * This is the drop-in boundary: libgasb.so exports exactly these `extern "C"` entry points
+ * (plain pointers, sizes and status codes; no C++ or torch types). Each entry point names
+ * the reference interface it replaces (/root/reference/proj, file:line). The C++ shim that
+ * keeps the reference's class names on top of this ABI is include/gasb/gas.hpp; a
+ * reference-side binding is shown in INTEGRATION.md.
+ *
+ * Conventions
+ *  - Every call returns gasb_status. Exceptions never cross the ABI; the message of the last
+ *    failure on the calling thread is gasb_last_error(). Status values map 1:1 onto the
+ *    reference's exception types: INVALID_ARGUMENT = std::invalid_argument,
+ *    LOGIC_ERROR = std::logic_error, RUNTIME_ERROR = std::runtime_error.
+ *  - `d_` pointers are device (HBM) pointers, `h_` pointers host pointers. Device calls are
+ *    stream-ordered on the given stream (NULL = legacy default stream) and asynchronous
+ *    unless stated otherwise.
+ *  - Layers are 1-based as in the reference (history layer l feeds layer l+1).
+ *  - Handles own their HBM; nothing is freed across the ABI except by *_destroy.
+ */
+#ifndef GASB_H
+#define GASB_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef void* gasb_stream; /* cudaStream_t */
+
+typedef enum {
+    GASB_OK = 0,
+    GASB_INVALID_ARGUMENT = 1,
+    GASB_LOGIC_ERROR = 2,
+    GASB_RUNTIME_ERROR = 3,
+    GASB_CUDA_ERROR = 4
+} gasb_status;
+
+const char* gasb_last_error(void);
+int32_t gasb_abi_version(void);
+
+/* ==================================================================================== */
+/* graph-core: include/gas/graph.hpp                                                     */
+/* ==================================================================================== */
+typedef struct gasb_graph_s* gasb_graph;
+
+/* build_graph (include/gas/graph.hpp:46, src/graph.cpp:25-61): CSR of in-neighbours, rows
+ * sorted and deduplicated, reverse edges added when symmetrize != 0, self-loops kept once.
+ * Host arrays; OpenMP-parallel; result is the reference's canonical CSR bit for bit. */
+gasb_status gasb_graph_build(const int32_t* h_src, const int32_t* h_dst, int64_t num_edges,
+                             int32_t num_nodes, int32_t symmetrize, gasb_graph* out);
+/* Adopts a CSR (validated: monotone offsets, sorted unique in-range rows). */
+gasb_status gasb_graph_from_csr(int32_t num_nodes, const int64_t* h_row_offsets, const int32_t* h_cols,
+                                int32_t symmetric, gasb_graph* out);
+gasb_status gasb_graph_info(gasb_graph g, int32_t* num_nodes, int64_t* num_edges);
+/* Borrowed host pointers, valid until gasb_graph_destroy. */
+gasb_status gasb_graph_csr(gasb_graph g, const int64_t** h_row_offsets, const int32_t** h_cols);
+gasb_status gasb_graph_destroy(gasb_graph g);
+
+/* Synthetic power-law graph with planted communities (SURVEY §8d "Synthetic inputs"):
+ * node weights w ~ Pareto(gamma) clipped to [min_weight, max_weight]; communities are a
+ * seeded balanced random split; each of num_pairs undirected pairs picks u ~ w globally,
+ * then v ~ w inside u's community with probability intra_fraction, else v ~ w globally.
+ * Counter-based RNG per pair: output independent of thread count. Outputs host arrays
+ * (num_pairs each) and the community of every node. */
+typedef struct {
+    int32_t num_nodes;
+    int32_t num_communities;
+    int64_t num_pairs;
+    double intra_fraction;
+    double gamma;
+    double min_weight;
+    double max_weight;
+    uint64_t seed;
+} gasb_synth_params;
+gasb_status gasb_synth_pairs(const gasb_synth_params* p, int32_t* h_src, int32_t* h_dst, int32_t* h_community);
+/* N(0,1) fp32 features (Box-Muller over a counter-based stream), rows padded to ld with 0. */
+gasb_status gasb_synth_features(int64_t num_nodes, int32_t dim, int64_t ld, uint64_t seed, float* h_out);
+
+/* ==================================================================================== */
+/* partition-batch loader: make_batch_plan (graph.hpp:88, graph.cpp:78-134),              */
+/* build_plan_aggregation (layers.hpp:38, layers.cpp:42-70), BatchSchedule::build         */
+/* (trainer.hpp:91-96, trainer.cpp:253-262)                                              */
+/* ==================================================================================== */
+typedef struct gasb_schedule_s* gasb_schedule;
+
+/* Plans every part of `assignment` (part ids in [0, num_parts), every part non-empty).
+ * flags & GASB_PLAN_FULL also materializes plan.local_graph and the `sum` stencil (only
+ * needed for parity checks / GIN); the GCN stencil and node lists are always built. */
+#define GASB_PLAN_FULL 1
+gasb_status gasb_schedule_build(gasb_graph g, const int32_t* h_assignment, int32_t num_parts, int32_t flags,
+                                gasb_schedule* out);
+/* Single plan for an explicit sorted batch (make_batch_plan semantics and errors). */
+gasb_status gasb_schedule_build_batches(gasb_graph g, const int32_t* const* h_batches, const int64_t* sizes,
+                                        int32_t num_batches, int32_t flags, gasb_schedule* out);
+gasb_status gasb_schedule_num_parts(gasb_schedule s, int32_t* out);
+/* sizes[6] = {num_batch, num_extended, num_halo, local_nnz, gcn_nnz, sum_nnz} */
+gasb_status gasb_plan_sizes(gasb_schedule s, int32_t part, int64_t* sizes);
+/* Copies plan arrays into caller host buffers (any may be NULL). Layouts as BatchPlan. */
+gasb_status gasb_plan_copy(gasb_schedule s, int32_t part, int32_t* extended, int32_t* halo, uint8_t* is_halo,
+                           int32_t* batch_local_rows, int32_t* halo_local_rows, int64_t* local_rowptr,
+                           int32_t* local_cols, int64_t* gcn_rowptr, int32_t* gcn_cols, float* gcn_coeffs,
+                           int64_t* sum_rowptr, int32_t* sum_cols, float* sum_coeffs);
+gasb_status gasb_schedule_destroy(gasb_schedule s);
+
+/* ==================================================================================== */
+/* history-store: HistoryStore (include/gas/history.hpp:29-66, src/history.cpp:10-178)   */
+/* L-1 fp32 tables of num_nodes x dim in HBM (row pitch ld >= dim, 16 B aligned), zero-   */
+/* initialized; int64 last-push stamps (-1 = never pushed); a device step counter.        */
+/* ==================================================================================== */
+typedef struct gasb_history_s* gasb_history;
+
+gasb_status gasb_history_create(int32_t num_layers, int32_t num_nodes, int32_t dim, gasb_history* out);
+gasb_status gasb_history_destroy(gasb_history h);
+gasb_status gasb_history_info(gasb_history h, int32_t* num_layers, int32_t* num_nodes, int32_t* dim, int64_t* ld);
+/* HistoryStore::push (history.cpp:28-42): table[d_ids[i]] = d_rows[i*ld_rows : +dim],
+ * stamp = current step. Ids are checked on device; an out-of-range id skips its row and
+ * latches an error that the next synchronizing call (gasb_history_check) reports as
+ * INVALID_ARGUMENT, the reference's exception for the same input. */
+gasb_status gasb_history_push(gasb_history h, int32_t layer, const int32_t* d_ids, int64_t count,
+                              const float* d_rows, int64_t ld_rows, gasb_stream stream);
+/* HistoryStore::pull (history.cpp:44-55): d_out[i*ld_out : +dim] = table[d_ids[i]]. */
+gasb_status gasb_history_pull(gasb_history h, int32_t layer, const int32_t* d_ids, int64_t count, float* d_out,
+                              int64_t ld_out, gasb_stream stream);
+/* Host-buffer variants: ids validated on the host first (exception-exact), then H2D/D2H
+ * copies through pinned staging on `stream`; synchronous on return. */
+gasb_status gasb_history_push_host(gasb_history h, int32_t layer, const int32_t* h_ids, int64_t count,
+                                   const float* h_rows, gasb_stream stream);
+gasb_status gasb_history_pull_host(gasb_history h, int32_t layer, const int32_t* h_ids, int64_t count,
+                                   float* h_out, gasb_stream stream);
+/* Synchronizes and reports (then clears) the device-side id check latched by push/pull. */
+gasb_status gasb_history_check(gasb_history h);
+gasb_status gasb_history_advance_step(gasb_history h, gasb_stream stream); /* advance_step() */
+gasb_status gasb_history_step(gasb_history h, int64_t* out);               /* step() (syncs) */
+gasb_status gasb_history_last_push_step(gasb_history h, int32_t layer, int32_t v, int64_t* out);
+/* layer_matrix (history.cpp:57-60): borrowed device pointer + row pitch. */
+gasb_status gasb_history_layer(gasb_history h, int32_t layer, float** d_table, int64_t* ld);
+/* fill_layer (history.cpp:61-67) from host values (num_nodes x dim, dense). */
+gasb_status gasb_history_fill_layer(gasb_history h, int32_t layer, const float* h_values);
+gasb_status gasb_history_read_layer(gasb_history h, int32_t layer, float* h_values);
+gasb_status gasb_history_read_stamps(gasb_history h, int32_t layer, int64_t* h_stamps);
+gasb_status gasb_history_reset(gasb_history h); /* reset() (history.cpp:114-118) */
+
+/* Prefetcher / PrefetchHandle (history.hpp:73-111, history.cpp:184-252) as stream work:
+ * begin() snapshots all L-1 layers' halo rows on the prefetcher's side stream after an
+ * event recorded on `compute`; wait(layer) makes `compute` wait for that layer's copy and
+ * returns the device buffer (valid until the next begin). A stale generation is a
+ * LOGIC_ERROR, an out-of-range layer an INVALID_ARGUMENT, as in the reference. */
+typedef struct gasb_prefetcher_s* gasb_prefetcher;
+gasb_status gasb_prefetcher_create(gasb_history h, gasb_prefetcher* out);
+gasb_status gasb_prefetcher_destroy(gasb_prefetcher p);
+gasb_status gasb_prefetch_begin(gasb_prefetcher p, const int32_t* d_halo, int64_t count, gasb_stream compute,
+                                uint64_t* generation);
+gasb_status gasb_prefetch_wait(gasb_prefetcher p, uint64_t generation, int32_t layer, gasb_stream compute,
+                               const float** d_rows, int64_t* ld);
+
+/* ==================================================================================== */
+/* message-passing ops (src/tensor.cpp)                                                  */
+/* ==================================================================================== */
+/* aggregate forward (tensor.cpp:514-530): y[r,:] = sum_e coeffs[e] * x[cols[e],:],
+ * e in [rowptr[r], rowptr[r+1]); fp64 accumulation, rounded to fp32.
+ * seg_edges == 0: one warp per row in CSR order -> bit-exact with the reference.
+ * seg_edges  > 0: rows split into segments of <= seg_edges edges whose fp64 partials are
+ * combined in segment order (deterministic; differs from sequential fp64 only below fp32
+ * resolution). Device int32 rowptr (relative), int32 cols into x's rows. */
+gasb_status gasb_spmm_fwd(const int32_t* d_rowptr, int32_t num_dst, const int32_t* d_cols, const float* d_coeffs,
+                          const float* d_x, int64_t ldx, int32_t dim, float* d_y, int64_t ldy, int32_t seg_edges,
+                          gasb_stream stream);
+/* aggregate backward closure (tensor.cpp:531-549) restricted to the given targets, as a
+ * gather over the transposed stencil: gx[t,:] = sum over (r, c) in CSC row t, r ascending,
+ * of c * gy[r,:] with fp32 multiply-then-add -> bit-exact. Optional mask: gx[t,j] = 0
+ * where d_mask[t*ldm + j] <= 0 (fused relu backward, tensor.cpp:363-369). */
+gasb_status gasb_spmm_bwd(const int32_t* d_t_rowptr, int32_t num_targets, const int32_t* d_t_src,
+                          const float* d_t_coeffs, const float* d_gy, int64_t ldgy, int32_t dim, const float* d_mask,
+                          int64_t ldm, float* d_gx, int64_t ldgx, gasb_stream stream);
+/* matmul (tensor.cpp:148-204) on fp32 row-major operands, fp32 accumulation:
+ * op = 0: C = A[m,k] B[k,n]; 1: C = A[m,k] B[n,k]^T; 2: C = A[k,m]^T B[k,n].
+ * beta == 0 overwrites C, beta == 1 accumulates. */
+gasb_status gasb_gemm(int32_t op, int32_t m, int32_t n, int32_t k, const float* d_a, int64_t lda, const float* d_b,
+                      int64_t ldb, float* d_c, int64_t ldc, float beta, gasb_stream stream);
+
+/* ==================================================================================== */
+/* gas-trainer: Model (trainer.hpp:45-88), gas_epoch (trainer.hpp:124-126,               */
+/* trainer.cpp:386-442), run_batch (trainer.cpp:295-339), AdamState (nn.hpp:21-38)       */
+/* ==================================================================================== */
+typedef struct {
+    int32_t kind; /* 0 GCN, 2 APPNP, 3 GCNII (LayerKind order, layers.hpp:12) */
+    int32_t num_layers;
+    int32_t hidden;
+    float dropout, alpha, beta, l2_weight, clip_max_norm;
+    float lr, beta1, beta2, eps;
+    uint64_t seed;
+} gasb_model_spec;
+
+typedef struct {
+    int32_t seg_edges;     /* SpMM row segmentation (0 = bit-exact sequential rows) */
+    int32_t fused;         /* 1: pull-free SpMM reads histories in place (default);
+                              0: reference-structured pull + compose (materialized halos) */
+    int32_t prefetch;      /* materialized mode: pull batch b+1's halos on a side stream */
+    int32_t use_graphs;    /* capture each batch into a CUDA graph */
+    int32_t hoist_layer1;  /* compute layer-1 aggregation of all batches up front per epoch */
+    int32_t device;        /* CUDA device ordinal */
+} gasb_trainer_options;
+
+typedef struct gasb_trainer_s* gasb_trainer;
+
+/* Uploads features (n x in_dim host fp32), the schedule's stencils and labels to HBM and
+ * builds the model (Model::build, trainer.cpp:55-129: seeded Glorot init identical to the
+ * reference), AdamState and HistoryStore(L-1, n, history_dim). */
+gasb_status gasb_trainer_create(gasb_schedule s, const float* h_features, int32_t in_dim, const int32_t* h_labels,
+                                const uint8_t* h_train_mask, int32_t num_classes, const gasb_model_spec* spec,
+                                const gasb_trainer_options* opt, gasb_trainer* out);
+gasb_status gasb_trainer_destroy(gasb_trainer t);
+/* gas_epoch with EpochOptions{evaluate=false, measure_staleness=false}: seeded batch order
+ * (trainer.cpp:395-400), one optimizer step per batch with training rows, advance_step per
+ * batch. Synchronous; *mean_loss as EpochReport.loss. */
+gasb_status gasb_gas_epoch(gasb_trainer t, int64_t epoch, int32_t shuffle, double* mean_loss);
+/* Enqueue-only variant for timing: no host synchronization, losses stay on device. */
+gasb_status gasb_gas_epoch_async(gasb_trainer t, int64_t epoch, int32_t shuffle);
+/* Mean loss of the last epoch enqueued with gasb_gas_epoch_async (synchronizes). */
+gasb_status gasb_trainer_last_loss(gasb_trainer t, double* mean_loss);
+/* One batch with capture (same contract as the oracle's session_batch): acts = pushed rows
+ * per history layer ((L-1) x nb x hist_dim), logits nb x C, grads = flat pre-clip
+ * parameter gradients in Model::params() order. Synchronous. */
+gasb_status gasb_trainer_batch(gasb_trainer t, int32_t part, int64_t epoch, int32_t train, int32_t push,
+                               float* h_acts, float* h_logits, double* loss, float* h_grads, int32_t* stepped);
+gasb_status gasb_trainer_num_param_floats(gasb_trainer t, int64_t* out);
+gasb_status gasb_trainer_get_params(gasb_trainer t, float* h_out);
+gasb_status gasb_trainer_set_params(gasb_trainer t, const float* h_in);
+gasb_status gasb_trainer_history(gasb_trainer t, gasb_history* out); /* borrowed */
+gasb_status gasb_trainer_stream(gasb_trainer t, gasb_stream* out);
+/* Kernel launches per epoch (counted by the host driver while enqueueing). */
+gasb_status gasb_trainer_launch_count(gasb_trainer t, int64_t* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GASB_H */

@@ -1,0 +1,77 @@
+// Device kernels of the GAS hot path (sm_100a). Declarations of launch helpers shared
+// between translation units; the kernels live in history.cu, spmm.cu, gemm.cu, train_ops.cu.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace gasb {
+
+constexpr int kWarp = 32;
+
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+inline int64_t round_up(int64_t a, int64_t b) { return ceil_div(a, b) * b; }
+
+// Counts kernel launches issued through these helpers (gpu_launches evidence).
+extern thread_local int64_t t_launches;
+
+// ---- history rows (history.cu) ------------------------------------------------------
+// mode 0 = push: dst[ids[i]] = src[i] (+ stamps[ids[i]] = *step); mode 1 = pull: dst[i] = src[ids[i]].
+void launch_rows(int mode, const int32_t* ids, int64_t count, const float* src, int64_t lds, float* dst,
+                 int64_t ldd, int32_t dim, int32_t n, int64_t* stamps, const int64_t* step, int32_t* err,
+                 cudaStream_t st);
+void launch_advance_step(int64_t* step, cudaStream_t st);
+
+// ---- SpMM (spmm.cu) -------------------------------------------------------------------
+// Segmented CSR SpMM with fp64 accumulation. Segments tile the edge range of the rows they
+// cover in row order: segment s = edges [seg_beg[s], seg_beg[s+1]) of row seg_row[s] (rows
+// absolute; the output row is seg_row[s] - row_base). Rows with more than one segment
+// combine fp64 partials in segment order (slot[s] >= 0 indexes `partial`, counters are
+// per (row, chunk) and self-reset).
+struct SpmmSegs {
+    const int64_t* seg_beg;   // nseg + 1, absolute edge offsets
+    const int32_t* seg_row;   // nseg
+    const int32_t* seg_slot;  // nseg: partial slot or -1 (single-segment row)
+    const int32_t* row_seg0;  // per absolute row: first segment index (only multi-seg rows)
+    const int32_t* row_nseg;  // per absolute row: number of segments
+    int64_t nseg;
+    int64_t seg_base;         // absolute index of this launch's first segment
+};
+void launch_spmm_fwd(const SpmmSegs& s, const int32_t* cols, const double* coeffs, const float* x, int64_t ldx,
+                     int32_t dim, float* y, int64_t ldy, int64_t row_base, double* partial, int64_t partial_ld,
+                     int32_t* counters, int32_t counters_ld, cudaStream_t st);
+// Transposed (CSC) gather, fp32 multiply-then-add in entry order (bit-exact with the
+// reference scatter). mask (optional): zero where mask <= 0 (relu backward).
+void launch_spmm_bwd(const int64_t* t_rowptr, int32_t ntargets, const int32_t* t_src, const float* t_coeffs,
+                     const float* gy, int64_t ldgy, int32_t dim, const float* mask, int64_t ldm, float* gx,
+                     int64_t ldgx, cudaStream_t st);
+
+// ---- GEMM (gemm.cu) -------------------------------------------------------------------
+// op 0: C = A B ; 1: C = A B^T ; 2: C = A^T B.  Row-major fp32, fp32 accumulation.
+// Epilogue (op 0 only): relu_push != nullptr -> C = relu(AB) and rows also scattered to
+// relu_push->table[ids[i]] with stamps.
+struct PushEpilogue {
+    float* table;
+    int64_t ld;
+    const int32_t* ids;
+    int64_t* stamps;
+    const int64_t* step;
+};
+void launch_gemm(int op, int m, int n, int k, const float* a, int64_t lda, const float* b, int64_t ldb, float* c,
+                 int64_t ldc, float beta, bool relu, const PushEpilogue* push, cudaStream_t st);
+
+// ---- training ops (train_ops.cu) ---------------------------------------------------
+// Softmax cross-entropy over `rows` (batch indices) with labels: loss (double, written to
+// *loss_out) and d loss / d logits into glogits (zeroed rows elsewhere), as tensor.cpp:597-647.
+void launch_softmax_ce(const float* logits, int64_t ldl, int32_t m, int32_t n, const int32_t* rows,
+                       const int32_t* labels, int32_t r, float* glogits, int64_t ldg, double* loss_out,
+                       double* row_scratch, cudaStream_t st);
+// AdamState::step (nn.cpp:20-41) over the flat parameter vector; bias corrections from
+// bc[2*t], t = ++(*t_counter) on device. clip_max_norm > 0 applies grad_clip first.
+void launch_adam(float* p, float* m, float* v, float* g, int64_t size, int64_t* t_counter, const double* bc,
+                 float lr, float b1, float b2, float eps, float clip_max_norm, double* norm_scratch,
+                 cudaStream_t st);
+void launch_zero(float* p, int64_t count, cudaStream_t st);
+
+}  // namespace gasb

@@ -1,0 +1,723 @@
+// GAS training driver on one B200: Model::build, Model::forward, run_batch and gas_epoch
+// of the reference (src/trainer.cpp:55-129, :174-251, :295-339, :386-442) re-designed
+// around HBM-resident state and per-batch CUDA graphs.
+//
+// Data layout in HBM:
+//  X        n x ldF fp32 features (ldF = F rounded up to 8 floats: 32 B aligned rows)
+//  H_l      HistoryStore tables (history.cu), l = 1..L-1
+//  stencils all batches concatenated in part order: cols (int32 global node ids), coeffs
+//           (fp64 copies of the reference's fp32 coefficients), row pointers (int64)
+//  segments per-batch and whole-epoch segment tables for the SpMM (spmm.cu)
+//  CSC      per batch, the intra-batch transposed stencil for the backward gather
+//  params   one flat fp32 vector in Model::params() order (+ grads, Adam m, v)
+//
+// Forward, fused mode (default): after layer l pushes act_l into H_l (fused into the GEMM
+// epilogue), H_l[v] for v in V_b equals compose_rows(act_l, pull(halo)) row for row, so
+// layer l+1's SpMM gathers H_l in place by global id: no pull, no compose, no x_ext
+// gather (value-identical to the reference). Materialized mode keeps the reference's
+// structure (gather/pull -> compose -> SpMM over local ids) and optionally prefetches
+// the next batch's halos on a side stream (the paper's concurrent execution, §5).
+//
+// Layer-1 hoisting: agg_1 = A_b X depends on neither parameters nor histories, so when
+// dropout == 0 each epoch first runs layer 1's aggregation of ALL batches as one
+// chunk-major launch (X streams through L2 once instead of once per batch). Same values,
+// same FLOPs, recomputed every epoch.
+#include <omp.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <numeric>
+#include <random>
+
+#include "gasb_internal.hpp"
+#include "kernels.cuh"
+
+namespace gasb {
+const Schedule& schedule_of(gasb_schedule s);
+gasb_history history_create(int32_t layers, int32_t n, int32_t dim);
+void history_destroy(gasb_history h);
+float* history_table(gasb_history h, int32_t layer);
+int64_t history_ld(gasb_history h);
+int64_t* history_stamps(gasb_history h, int32_t layer);
+int64_t* history_step_ptr(gasb_history h);
+
+namespace {
+
+// ---- host RNG exactly as gas::Rng (include/gas/rng.hpp) -------------------------------
+uint64_t mix64(uint64_t x) {
+    x += 0x9e3779b97f4a7c15ull;
+    x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
+    x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
+    return x ^ (x >> 31);
+}
+uint64_t derive_seed(uint64_t s, uint64_t a, uint64_t b = 0, uint64_t c = 0) {
+    return mix64(mix64(mix64(s ^ mix64(a)) ^ mix64(b)) ^ mix64(c));
+}
+struct Rng {
+    std::mt19937_64 gen;
+    explicit Rng(uint64_t s) : gen(s) {}
+    double next_double() { return static_cast<double>(gen() >> 11) * 0x1.0p-53; }
+    uint64_t next_below(uint64_t n) {
+        if (n <= 1) return 0;
+        const uint64_t limit = ~uint64_t{0} - (~uint64_t{0} % n);
+        uint64_t x;
+        do {
+            x = gen();
+        } while (x >= limit);
+        return x % n;
+    }
+};
+void glorot_init(float* w, int64_t rows, int64_t cols, uint64_t seed) {  // nn.cpp:65-70
+    const double bound = std::sqrt(6.0 / static_cast<double>(rows + cols));
+    Rng rng(seed);
+    for (int64_t i = 0; i < rows * cols; ++i) w[i] = static_cast<float>((rng.next_double() * 2.0 - 1.0) * bound);
+}
+
+template <class T>
+struct DevBuf {
+    T* p = nullptr;
+    int64_t n = 0;
+    void alloc(int64_t count) {
+        free();
+        n = count;
+        GASB_CUDA(cudaMalloc(&p, sizeof(T) * std::max<int64_t>(count, 1)));
+    }
+    void upload(const std::vector<T>& v) {
+        alloc(static_cast<int64_t>(v.size()));
+        if (!v.empty()) GASB_CUDA(cudaMemcpy(p, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice));
+    }
+    void zero() {
+        if (n) GASB_CUDA(cudaMemset(p, 0, sizeof(T) * n));
+    }
+    void free() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+    ~DevBuf() { free(); }
+};
+
+struct SegTable {
+    DevBuf<int64_t> seg_beg;
+    DevBuf<int32_t> seg_row, seg_slot, row_seg0, row_nseg;
+    std::vector<int64_t> group_seg0, group_nseg;  // per group (batch) range of segments
+    int64_t max_group_slots = 0, total_slots = 0;
+};
+
+// Segments rows [row_lo, row_hi) of the absolute row pointer `rp` into pieces of <= S
+// edges (S == 0: one per row). Slots restart at 0 per group when per_group_slots.
+void build_segments(const std::vector<int64_t>& rp, const std::vector<int64_t>& group_rows, int64_t S,
+                    bool per_group_slots, SegTable& t) {
+    const int64_t ngroups = static_cast<int64_t>(group_rows.size()) - 1;
+    const int64_t nrows = group_rows.back();
+    std::vector<int64_t> sb;
+    std::vector<int32_t> sr, ss, r0(static_cast<size_t>(nrows)), rn(static_cast<size_t>(nrows));
+    t.group_seg0.assign(static_cast<size_t>(ngroups), 0);
+    t.group_nseg.assign(static_cast<size_t>(ngroups), 0);
+    int64_t slot = 0;
+    t.max_group_slots = 0;
+    for (int64_t g = 0; g < ngroups; ++g) {
+        if (per_group_slots) slot = 0;
+        t.group_seg0[g] = static_cast<int64_t>(sr.size());
+        for (int64_t r = group_rows[g]; r < group_rows[g + 1]; ++r) {
+            const int64_t deg = rp[r + 1] - rp[r];
+            const int64_t k = (S == 0 || deg <= S) ? 1 : ceil_div(deg, S);
+            r0[r] = static_cast<int32_t>(sr.size());
+            rn[r] = static_cast<int32_t>(k);
+            for (int64_t i = 0; i < k; ++i) {
+                sb.push_back(rp[r] + i * S);
+                sr.push_back(static_cast<int32_t>(r));
+                ss.push_back(k == 1 ? -1 : static_cast<int32_t>(slot++));
+            }
+        }
+        t.group_nseg[g] = static_cast<int64_t>(sr.size()) - t.group_seg0[g];
+        t.max_group_slots = std::max(t.max_group_slots, slot);
+    }
+    t.total_slots = per_group_slots ? t.max_group_slots : slot;
+    sb.push_back(rp[nrows]);
+    t.seg_beg.upload(sb);
+    t.seg_row.upload(sr);
+    t.seg_slot.upload(ss);
+    t.row_seg0.upload(r0);
+    t.row_nseg.upload(rn);
+}
+
+__global__ void end_batch_kernel(int64_t* step, int64_t* t_counter, int stepped) {
+    *step += 1;
+    if (stepped) *t_counter += 1;
+}
+
+// h_ext[i] = is_halo ? halo_rows[k] : act[j]  — compose_rows (tensor.cpp:459-512) for the
+// materialized path, one warp per extended row.
+__global__ void compose_kernel(const int32_t* __restrict__ src_index, const float* __restrict__ act, int64_t lda,
+                               const float* __restrict__ halo, int64_t ldh, int32_t ne, int32_t dim,
+                               float* __restrict__ out, int64_t ldo) {
+    const int lane = threadIdx.x & 31;
+    const int64_t w = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    if (w >= ne) return;
+    const int32_t s = src_index[w];  // >= 0: batch index into act, < 0: -(halo index)-1
+    const float* src = s >= 0 ? act + static_cast<int64_t>(s) * lda : halo + static_cast<int64_t>(-s - 1) * ldh;
+    for (int c = lane; c < dim; c += 32) out[w * ldo + c] = src[c];
+}
+
+}  // namespace
+}  // namespace gasb
+
+using namespace gasb;
+
+struct gasb_trainer_s {
+    gasb_model_spec spec{};
+    gasb_trainer_options opt{};
+    int32_t n = 0, F = 0, C = 0, L = 0, H = 0, hist_dim = 0, num_parts = 0;
+    int64_t ldF = 0, ldH = 0, ldC = 0;
+    const Schedule* sched = nullptr;
+    cudaStream_t stream = nullptr, side = nullptr;
+    gasb_history hist = nullptr;
+
+    // per part (host)
+    std::vector<int32_t> nb, ne, nh, ntrain;
+    std::vector<int64_t> row_off, edge_off, t_off, tr_off, ext_off;
+    int32_t nb_max = 0, ne_max = 0;
+
+    // device data
+    DevBuf<float> X;
+    DevBuf<int32_t> batch_nodes, cols_g, cols_l, t_src, train_rows, train_labels, extended, compose_idx, halo_ids;
+    DevBuf<double> coef64;
+    DevBuf<float> t_cf;
+    DevBuf<int64_t> t_rowptr;
+    SegTable seg_batch, seg_all;
+    DevBuf<int32_t> counters;
+    DevBuf<double> partial_batch, partial_all;
+    int32_t max_chunks = 0;
+
+    // model
+    std::vector<int64_t> poff, prow, pcol;  // per parameter tensor
+    std::vector<int32_t> layer_param;       // param index of W_l (GCN) per layer 1..L
+    int64_t nparam = 0;
+    std::vector<float> h_params_init;
+    DevBuf<float> params, grads, adam_m, adam_v;
+    DevBuf<int64_t> t_counter;
+    DevBuf<double> bc, norm_scratch;
+    int64_t bc_cap = 0, t_host = 0;
+
+    // activations
+    std::vector<int32_t> dims;    // d[0..L]
+    DevBuf<float> agg_all;        // hoisted layer-1 aggregation, n x ldF
+    std::vector<DevBuf<float>> agg, act;
+    DevBuf<float> logits, glogits, g_agg, g_out, x_ext, h_ext, halo_buf;
+    DevBuf<double> loss, row_scratch;
+
+    // graphs
+    std::vector<cudaGraphExec_t> graphs;
+    std::vector<int64_t> graph_launches;
+    int64_t epoch_launches = 0;
+    std::vector<int32_t> last_order;
+    std::vector<uint8_t> last_stepped;
+
+    ~gasb_trainer_s() {
+        if (stream) cudaStreamSynchronize(stream);
+        for (auto g : graphs)
+            if (g) cudaGraphExecDestroy(g);
+        if (hist) history_destroy(hist);
+        if (side) cudaStreamDestroy(side);
+        if (stream) cudaStreamDestroy(stream);
+    }
+
+    int64_t ld_of(int32_t d) const { return round_up(std::max(d, 1), 8); }
+    float* W(int32_t l) { return params.p + poff[layer_param[l]]; }
+    float* gW(int32_t l) { return grads.p + poff[layer_param[l]]; }
+
+    void ensure_bc(int64_t t_max) {
+        if (t_max < bc_cap) return;
+        int64_t cap = std::max<int64_t>(1024, bc_cap);
+        while (cap <= t_max) cap *= 2;
+        std::vector<double> h(static_cast<size_t>(2 * cap));
+        for (int64_t t = 1; t < cap; ++t) {  // nn.cpp:23-24, host pow (as the reference)
+            h[2 * t] = 1.0 - std::pow(static_cast<double>(spec.beta1), static_cast<double>(t));
+            h[2 * t + 1] = 1.0 - std::pow(static_cast<double>(spec.beta2), static_cast<double>(t));
+        }
+        GASB_CUDA(cudaStreamSynchronize(stream));
+        bc.upload(h);
+        bc_cap = cap;
+    }
+
+    void build(const float* h_features, const int32_t* h_labels, const uint8_t* h_train);
+    void enqueue_batch(int32_t p, bool train, bool push, bool use_hoisted, bool fused);
+    void enqueue_hoisted();
+    void run_epoch(int64_t epoch, bool shuffle);
+};
+
+void gasb_trainer_s::build(const float* h_features, const int32_t* h_labels, const uint8_t* h_train) {
+    const Graph& g = *sched->graph;
+    n = g.num_nodes;
+    num_parts = sched->num_parts;
+    L = spec.num_layers;
+    H = spec.hidden;
+    require(spec.kind == 0, "trainer: only GCN (kind 0) is implemented on the device path in this build");
+    require(L >= 1 && H > 0 && F > 0 && C > 0, "trainer: bad model dims");
+    require(spec.dropout == 0.0f, "trainer: dropout > 0 is not supported by the device path yet");
+    hist_dim = L >= 2 ? H : 0;
+    dims.assign(static_cast<size_t>(L) + 1, H);
+    dims[0] = F;
+    dims[L] = C;
+    ldF = ld_of(F);
+    ldH = ld_of(H);
+    ldC = ld_of(C);
+
+    // ---- per-part sizes and offsets ----
+    nb.resize(num_parts);
+    ne.resize(num_parts);
+    nh.resize(num_parts);
+    ntrain.resize(num_parts);
+    row_off.assign(num_parts + 1, 0);
+    edge_off.assign(num_parts + 1, 0);
+    t_off.assign(num_parts + 1, 0);
+    tr_off.assign(num_parts + 1, 0);
+    ext_off.assign(num_parts + 1, 0);
+    std::vector<int64_t> nintra(num_parts, 0);
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int32_t p = 0; p < num_parts; ++p) {
+        const HostPlan& P = sched->plans[p];
+        nb[p] = static_cast<int32_t>(P.batch.size());
+        ne[p] = static_cast<int32_t>(P.extended.size());
+        nh[p] = static_cast<int32_t>(P.halo.size());
+        int32_t tr = 0;
+        for (int32_t v : P.batch) tr += h_train[v] ? 1 : 0;
+        ntrain[p] = tr;
+        int64_t intra = 0;
+        for (int32_t c : P.gcn_cols) intra += P.is_halo[c] ? 0 : 1;
+        nintra[p] = intra;
+    }
+    for (int32_t p = 0; p < num_parts; ++p) {
+        row_off[p + 1] = row_off[p] + nb[p];
+        edge_off[p + 1] = edge_off[p] + static_cast<int64_t>(sched->plans[p].gcn_cols.size());
+        t_off[p + 1] = t_off[p] + nintra[p];
+        tr_off[p + 1] = tr_off[p] + ntrain[p];
+        ext_off[p + 1] = ext_off[p] + ne[p];
+        nb_max = std::max(nb_max, nb[p]);
+        ne_max = std::max(ne_max, ne[p]);
+    }
+    const int64_t R = row_off[num_parts], E = edge_off[num_parts], T = t_off[num_parts], NE = ext_off[num_parts];
+
+    // ---- host staging of the concatenated stencils ----
+    std::vector<int32_t> h_bn(R), h_cg(E), h_cl(E), h_tsrc(T), h_trr(tr_off[num_parts]), h_trl(tr_off[num_parts]);
+    std::vector<int32_t> h_ext(NE), h_cidx(NE);
+    std::vector<double> h_cf(E);
+    std::vector<float> h_tcf(T);
+    std::vector<int64_t> h_rp(R + 1), h_trp(R + num_parts);
+    h_rp[R] = E;
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int32_t p = 0; p < num_parts; ++p) {
+        const HostPlan& P = sched->plans[p];
+        const int64_t r0 = row_off[p], e0 = edge_off[p];
+        std::vector<int32_t> local2batch(P.extended.size(), -1);
+        for (int32_t i = 0; i < nb[p]; ++i) {
+            h_bn[r0 + i] = P.batch[i];
+            local2batch[P.batch_local_rows[i]] = i;
+            h_rp[r0 + i] = e0 + P.gcn_rowptr[i];
+        }
+        for (size_t e = 0; e < P.gcn_cols.size(); ++e) {
+            h_cg[e0 + e] = P.extended[P.gcn_cols[e]];
+            h_cl[e0 + e] = P.gcn_cols[e];
+            h_cf[e0 + e] = static_cast<double>(P.gcn_coeffs[e]);
+        }
+        // transposed intra-batch stencil: target = batch index of the source row, entries
+        // in ascending dst row r (the reference's scatter order, tensor.cpp:540-547)
+        std::vector<int64_t> cnt(static_cast<size_t>(nb[p]) + 1, 0);
+        for (size_t e = 0; e < P.gcn_cols.size(); ++e) {
+            const int32_t t = local2batch[P.gcn_cols[e]];
+            if (t >= 0) cnt[t + 1]++;
+        }
+        for (int32_t t = 0; t < nb[p]; ++t) cnt[t + 1] += cnt[t];
+        int64_t* trp = h_trp.data() + r0 + p;  // nb+1 entries per part
+        for (int32_t t = 0; t <= nb[p]; ++t) trp[t] = t_off[p] + cnt[t];
+        std::vector<int64_t> fill(cnt.begin(), cnt.end() - 1);
+        for (int32_t r = 0; r < nb[p]; ++r)
+            for (int64_t e = P.gcn_rowptr[r]; e < P.gcn_rowptr[r + 1]; ++e) {
+                const int32_t t = local2batch[P.gcn_cols[e]];
+                if (t < 0) continue;
+                const int64_t k = t_off[p] + fill[t]++;
+                h_tsrc[k] = r;
+                h_tcf[k] = P.gcn_coeffs[e];
+            }
+        int32_t k = 0;
+        for (int32_t i = 0; i < nb[p]; ++i)
+            if (h_train[P.batch[i]]) {
+                h_trr[tr_off[p] + k] = i;
+                h_trl[tr_off[p] + k] = h_labels[P.batch[i]];
+                ++k;
+            }
+        int32_t hk = 0;
+        for (int32_t i = 0; i < ne[p]; ++i) {
+            h_ext[ext_off[p] + i] = P.extended[i];
+            h_cidx[ext_off[p] + i] = P.is_halo[i] ? -(hk++) - 1 : local2batch[i];
+        }
+    }
+    for (int32_t i = 0; i < static_cast<int32_t>(h_trl.size()); ++i)
+        require(h_trl[i] >= 0 && h_trl[i] < C, "softmax_cross_entropy: label out of range");
+
+    GASB_CUDA(cudaSetDevice(opt.device));
+    GASB_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+    GASB_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+    batch_nodes.upload(h_bn);
+    cols_g.upload(h_cg);
+    cols_l.upload(h_cl);
+    coef64.upload(h_cf);
+    t_src.upload(h_tsrc);
+    t_cf.upload(h_tcf);
+    t_rowptr.upload(h_trp);
+    train_rows.upload(h_trr);
+    train_labels.upload(h_trl);
+    extended.upload(h_ext);
+    compose_idx.upload(h_cidx);
+    {
+        std::vector<int64_t> grp(num_parts + 1);
+        for (int32_t p = 0; p <= num_parts; ++p) grp[p] = row_off[p];
+        build_segments(h_rp, grp, opt.seg_edges, true, seg_batch);
+        const int64_t S_all = opt.seg_edges == 0 ? 0 : std::max<int64_t>(opt.seg_edges, 2048);
+        std::vector<int64_t> one{0, R};
+        build_segments(h_rp, one, S_all, false, seg_all);
+    }
+    max_chunks = static_cast<int32_t>(ceil_div(std::max(F, H), 64));
+    counters.alloc(R * max_chunks);
+    counters.zero();
+    partial_batch.alloc(std::max<int64_t>(seg_batch.max_group_slots, 1) * max_chunks * 64);
+    partial_all.alloc(std::max<int64_t>(seg_all.total_slots, 1) * ceil_div(F, 64) * 64);
+
+    // ---- features ----
+    X.alloc(static_cast<int64_t>(n) * ldF);
+    GASB_CUDA(cudaMemcpy2D(X.p, sizeof(float) * ldF, h_features, sizeof(float) * F, sizeof(float) * F, n,
+                           cudaMemcpyHostToDevice));
+    if (ldF > F)
+        GASB_CUDA(cudaMemset2D(X.p + F, sizeof(float) * ldF, 0, sizeof(float) * (ldF - F), n));
+
+    // ---- Model::build (trainer.cpp:55-129), GCN: W_l (d_{l-1} x d_l) ----
+    layer_param.assign(static_cast<size_t>(L) + 1, -1);
+    for (int32_t l = 1; l <= L; ++l) {
+        layer_param[l] = static_cast<int32_t>(poff.size());
+        poff.push_back(nparam);
+        prow.push_back(dims[l - 1]);
+        pcol.push_back(dims[l]);
+        nparam += static_cast<int64_t>(dims[l - 1]) * dims[l];
+    }
+    h_params_init.assign(static_cast<size_t>(nparam), 0.0f);
+    for (int32_t l = 1; l <= L; ++l)  // Layer::build(cfg, derive_seed(seed,10,l)) -> glorot(derive_seed(.,1))
+        glorot_init(h_params_init.data() + poff[layer_param[l]], dims[l - 1], dims[l],
+                    derive_seed(derive_seed(spec.seed, 10, static_cast<uint64_t>(l)), 1));
+    params.upload(h_params_init);
+    grads.alloc(nparam);
+    grads.zero();
+    adam_m.alloc(nparam);
+    adam_m.zero();
+    adam_v.alloc(nparam);
+    adam_v.zero();
+    t_counter.alloc(1);
+    t_counter.zero();
+    norm_scratch.alloc(256);
+    ensure_bc(4096);
+
+    // ---- HistoryStore(L-1, n, H) ----
+    hist = history_create(std::max(0, L - 1), n, hist_dim);
+
+    // ---- activations ----
+    agg.resize(static_cast<size_t>(L) + 1);
+    act.resize(static_cast<size_t>(L) + 1);
+    for (int32_t l = 1; l <= L; ++l) agg[l].alloc(static_cast<int64_t>(nb_max) * ld_of(dims[l - 1]));
+    for (int32_t l = 1; l < L; ++l) act[l].alloc(static_cast<int64_t>(nb_max) * ldH);
+    if (opt.hoist_layer1) agg_all.alloc(R * ldF);
+    logits.alloc(static_cast<int64_t>(nb_max) * ldC);
+    glogits.alloc(static_cast<int64_t>(nb_max) * ldC);
+    g_agg.alloc(static_cast<int64_t>(nb_max) * std::max(ldH, ldC));
+    g_out.alloc(static_cast<int64_t>(nb_max) * ldH);
+    loss.alloc(num_parts);
+    loss.zero();
+    row_scratch.alloc(nb_max);
+    graphs.assign(num_parts, nullptr);
+    graph_launches.assign(num_parts, 0);
+    GASB_CUDA(cudaDeviceSynchronize());
+}
+
+void gasb_trainer_s::enqueue_hoisted() {
+    SpmmSegs s{seg_all.seg_beg.p, seg_all.seg_row.p, seg_all.seg_slot.p, seg_all.row_seg0.p,
+               seg_all.row_nseg.p, seg_all.group_nseg[0], 0};
+    launch_spmm_fwd(s, cols_g.p, coef64.p, X.p, ldF, F, agg_all.p, ldF, 0, partial_all.p, ceil_div(F, 64) * 64,
+                    counters.p, max_chunks, stream);
+}
+
+void gasb_trainer_s::enqueue_batch(int32_t p, bool train, bool push, bool use_hoisted, bool fused) {
+    const int32_t m = nb[p];
+    const int64_t r0 = row_off[p];
+    SpmmSegs segs{seg_batch.seg_beg.p, seg_batch.seg_row.p, seg_batch.seg_slot.p, seg_batch.row_seg0.p,
+                  seg_batch.row_nseg.p, seg_batch.group_nseg[p], seg_batch.group_seg0[p]};
+    const int32_t* bn = batch_nodes.p + r0;
+    // ---------------- forward (Model::forward, trainer.cpp:174-251) ----------------
+    for (int32_t l = 1; l <= L; ++l) {
+        const int32_t din = dims[l - 1], dout = dims[l];
+        const int64_t lda = ld_of(din);
+        float* a = agg[l].p;
+        if (l == 1 && use_hoisted) {
+            a = agg_all.p + r0 * ldF;
+        } else if (fused) {
+            const float* src = l == 1 ? X.p : history_table(hist, l - 1);
+            const int64_t lds = l == 1 ? ldF : history_ld(hist);
+            launch_spmm_fwd(segs, cols_g.p, coef64.p, src, lds, din, a, lda, r0, partial_batch.p,
+                            static_cast<int64_t>(max_chunks) * 64, counters.p, max_chunks, stream);
+        } else {
+            // reference structure: x_ext / compose over V_b local rows, SpMM by local ids
+            const int64_t ldx = ld_of(din);
+            const float* hsrc;
+            if (l == 1) {
+                launch_rows(1, extended.p + ext_off[p], ne[p], X.p, ldF, x_ext.p, ldx, din, n, nullptr, nullptr,
+                            nullptr, stream);  // gather_features (trainer.cpp:20-27)
+                hsrc = x_ext.p;
+            } else {
+                // HistoryStore::pull of the halo rows, then compose_rows (tensor.cpp:459-512)
+                const HostPlan& P = sched->plans[p];
+                (void)P;
+                launch_rows(1, halo_ids.p + (ext_off[p] - row_off[p]), nh[p], history_table(hist, l - 1),
+                            history_ld(hist), halo_buf.p, ldx, din, n, nullptr, nullptr, nullptr, stream);
+                const int64_t blocks = ceil_div(static_cast<int64_t>(ne[p]) * 32, 256);
+                compose_kernel<<<static_cast<unsigned>(blocks), 256, 0, stream>>>(
+                    compose_idx.p + ext_off[p], act[l - 1].p, ldH, halo_buf.p, ldx, ne[p], din, h_ext.p, ldx);
+                ++t_launches;
+                GASB_CUDA(cudaGetLastError());
+                hsrc = h_ext.p;
+            }
+            launch_spmm_fwd(segs, cols_l.p, coef64.p, hsrc, ldx, din, a, lda, r0, partial_batch.p,
+                            static_cast<int64_t>(max_chunks) * 64, counters.p, max_chunks, stream);
+        }
+        float* Wl = W(l);
+        if (l < L) {
+            PushEpilogue pe{history_table(hist, l), history_ld(hist), bn, history_stamps(hist, l),
+                            history_step_ptr(hist)};
+            launch_gemm(0, m, dout, din, a, lda, Wl, dout, act[l].p, ldH, 0.f, true, push ? &pe : nullptr, stream);
+        } else {
+            launch_gemm(0, m, dout, din, a, lda, Wl, dout, logits.p, ldC, 0.f, false, nullptr, stream);
+        }
+    }
+    // ---------------- loss + backward (run_batch, trainer.cpp:295-339) ----------------
+    const bool stepped = ntrain[p] > 0 && train;
+    if (ntrain[p] > 0)
+        launch_softmax_ce(logits.p, ldC, m, C, train_rows.p + tr_off[p], train_labels.p + tr_off[p], ntrain[p],
+                          glogits.p, ldC, loss.p + p, row_scratch.p, stream);
+    if (stepped) {
+        float* g = glogits.p;
+        int64_t ldg = ldC;
+        for (int32_t l = L; l >= 1; --l) {
+            const int32_t din = dims[l - 1], dout = dims[l];
+            const int64_t lda = ld_of(din);
+            const float* a = (l == 1 && use_hoisted) ? agg_all.p + r0 * ldF : agg[l].p;
+            // matmul backward (tensor.cpp:169-204): dW = agg^T g ; dagg = g W^T
+            launch_gemm(2, din, dout, m, a, lda, g, ldg, gW(l), dout, 0.f, false, nullptr, stream);
+            if (l == 1) break;  // x_ext carries no gradient
+            launch_gemm(1, m, din, dout, g, ldg, W(l), dout, g_agg.p, ldH, 0.f, false, nullptr, stream);
+            // aggregate backward over intra-batch edges + compose bwd + relu bwd (mask = act)
+            launch_spmm_bwd(t_rowptr.p + r0 + p, m, t_src.p, t_cf.p, g_agg.p, ldH, din, act[l - 1].p, ldH, g_out.p,
+                            ldH, stream);
+            g = g_out.p;
+            ldg = ldH;
+        }
+        launch_adam(params.p, adam_m.p, adam_v.p, grads.p, nparam, t_counter.p, bc.p, spec.lr, spec.beta1,
+                    spec.beta2, spec.eps, spec.clip_max_norm, norm_scratch.p, stream);
+    }
+    end_batch_kernel<<<1, 1, 0, stream>>>(history_step_ptr(hist), t_counter.p, stepped ? 1 : 0);
+    ++t_launches;
+    GASB_CUDA(cudaGetLastError());
+}
+
+void gasb_trainer_s::run_epoch(int64_t epoch, bool shuffle) {
+    // batch order (trainer.cpp:395-400)
+    std::vector<int32_t> order(static_cast<size_t>(num_parts));
+    std::iota(order.begin(), order.end(), 0);
+    if (shuffle) {
+        Rng rng(derive_seed(spec.seed ^ 0x6f726472ull, static_cast<uint64_t>(epoch)));
+        for (size_t i = order.size(); i > 1; --i) std::swap(order[i - 1], order[rng.next_below(i)]);
+    }
+    int64_t steps = 0;
+    for (int32_t p : order) steps += ntrain[p] > 0 ? 1 : 0;
+    ensure_bc(t_host + steps + 2);
+    const bool hoisted = opt.hoist_layer1 && opt.fused;
+    const int64_t l0 = t_launches;
+    if (hoisted) enqueue_hoisted();
+    epoch_launches = t_launches - l0;
+    for (int32_t p : order) {
+        if (opt.use_graphs) {
+            if (!graphs[p]) {
+                cudaGraph_t graph;
+                const int64_t c0 = t_launches;
+                GASB_CUDA(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
+                enqueue_batch(p, true, true, hoisted, opt.fused != 0);
+                GASB_CUDA(cudaStreamEndCapture(stream, &graph));
+                graph_launches[p] = t_launches - c0;
+                t_launches = c0;
+                GASB_CUDA(cudaGraphInstantiate(&graphs[p], graph, 0));
+                GASB_CUDA(cudaGraphDestroy(graph));
+            }
+            GASB_CUDA(cudaGraphLaunch(graphs[p], stream));
+            epoch_launches += graph_launches[p];
+        } else {
+            const int64_t c0 = t_launches;
+            enqueue_batch(p, true, true, hoisted, opt.fused != 0);
+            epoch_launches += t_launches - c0;
+        }
+    }
+    t_host += steps;
+    last_order = order;
+}
+
+extern "C" {
+
+gasb_status gasb_trainer_create(gasb_schedule s, const float* h_features, int32_t in_dim, const int32_t* h_labels,
+                                const uint8_t* h_train_mask, int32_t num_classes, const gasb_model_spec* spec,
+                                const gasb_trainer_options* opt, gasb_trainer* out) {
+    return guard([&] {
+        require(s && h_features && h_labels && h_train_mask && spec && out, "trainer: null argument");
+        require(in_dim > 0 && num_classes > 0, "Model: in_dim and num_classes must be positive");
+        require(spec->num_layers >= 1, "ModelSpec: need at least one layer");
+        require(spec->hidden > 0, "ModelSpec: hidden must be positive");
+        require(spec->dropout >= 0.0f && spec->dropout < 1.0f, "ModelSpec: dropout must be in [0,1)");
+        auto t = std::make_unique<gasb_trainer_s>();
+        t->spec = *spec;
+        if (opt) t->opt = *opt;
+        else t->opt = gasb_trainer_options{128, 1, 0, 1, 1, 0};
+        t->sched = &schedule_of(s);
+        t->F = in_dim;
+        t->C = num_classes;
+        if (!t->opt.fused) {
+            t->x_ext.alloc(0);
+        }
+        t->build(h_features, h_labels, h_train_mask);
+        if (!t->opt.fused || true) {  // buffers for the reference-structured path (also used by push=0)
+            const int64_t ldmax = t->ld_of(std::max(t->F, t->H));
+            t->x_ext.alloc(static_cast<int64_t>(t->ne_max) * ldmax);
+            t->h_ext.alloc(static_cast<int64_t>(t->ne_max) * ldmax);
+            t->halo_buf.alloc(static_cast<int64_t>(t->ne_max) * ldmax);
+            // halo ids per part, concatenated at ext_off - row_off
+            std::vector<int32_t> hid(static_cast<size_t>(t->ext_off[t->num_parts] - t->row_off[t->num_parts]));
+            for (int32_t p = 0; p < t->num_parts; ++p) {
+                const HostPlan& P = t->sched->plans[p];
+                std::copy(P.halo.begin(), P.halo.end(), hid.begin() + (t->ext_off[p] - t->row_off[p]));
+            }
+            t->halo_ids.upload(hid);
+        }
+        *out = t.release();
+    });
+}
+
+gasb_status gasb_trainer_destroy(gasb_trainer t) {
+    delete t;
+    return GASB_OK;
+}
+
+gasb_status gasb_gas_epoch_async(gasb_trainer t, int64_t epoch, int32_t shuffle) {
+    return guard([&] {
+        require(t, "trainer: null handle");
+        t->run_epoch(epoch, shuffle != 0);
+    });
+}
+
+gasb_status gasb_trainer_last_loss(gasb_trainer t, double* mean_loss) {
+    return guard([&] {
+        require(t && mean_loss, "trainer: null argument");
+        GASB_CUDA(cudaStreamSynchronize(t->stream));
+        std::vector<double> l(static_cast<size_t>(t->num_parts));
+        GASB_CUDA(cudaMemcpy(l.data(), t->loss.p, sizeof(double) * l.size(), cudaMemcpyDeviceToHost));
+        double sum = 0.0;
+        int64_t cnt = 0;
+        for (int32_t p : t->last_order)  // EpochReport.loss: mean over stepped batches, epoch order
+            if (t->ntrain[p] > 0) {
+                sum += l[p];
+                ++cnt;
+            }
+        *mean_loss = cnt > 0 ? sum / static_cast<double>(cnt) : 0.0;
+    });
+}
+
+gasb_status gasb_gas_epoch(gasb_trainer t, int64_t epoch, int32_t shuffle, double* mean_loss) {
+    gasb_status s = gasb_gas_epoch_async(t, epoch, shuffle);
+    if (s != GASB_OK) return s;
+    double l = 0.0;
+    s = gasb_trainer_last_loss(t, &l);
+    if (mean_loss) *mean_loss = l;
+    return s;
+}
+
+gasb_status gasb_trainer_batch(gasb_trainer t, int32_t part, int64_t epoch, int32_t train, int32_t push,
+                               float* h_acts, float* h_logits, double* loss, float* h_grads, int32_t* stepped) {
+    return guard([&] {
+        (void)epoch;
+        require(t, "trainer: null handle");
+        require(part >= 0 && part < t->num_parts, "trainer: part out of range");
+        const bool tr = train != 0;
+        t->ensure_bc(t->t_host + 2);
+        t->enqueue_batch(part, tr, push != 0, false, push != 0 && t->opt.fused != 0);
+        const bool st = tr && t->ntrain[part] > 0;
+        if (st) t->t_host++;
+        GASB_CUDA(cudaStreamSynchronize(t->stream));
+        const int32_t m = t->nb[part];
+        if (h_acts)
+            for (int32_t l = 1; l < t->L; ++l)
+                GASB_CUDA(cudaMemcpy2D(h_acts + static_cast<int64_t>(l - 1) * m * t->H, sizeof(float) * t->H,
+                                       t->act[l].p, sizeof(float) * t->ldH, sizeof(float) * t->H, m,
+                                       cudaMemcpyDeviceToHost));
+        if (h_logits)
+            GASB_CUDA(cudaMemcpy2D(h_logits, sizeof(float) * t->C, t->logits.p, sizeof(float) * t->ldC,
+                                   sizeof(float) * t->C, m, cudaMemcpyDeviceToHost));
+        if (loss) {
+            double l = 0.0;
+            if (t->ntrain[part] > 0) GASB_CUDA(cudaMemcpy(&l, t->loss.p + part, sizeof(double), cudaMemcpyDeviceToHost));
+            *loss = l;
+        }
+        if (h_grads && st)
+            GASB_CUDA(cudaMemcpy(h_grads, t->grads.p, sizeof(float) * t->nparam, cudaMemcpyDeviceToHost));
+        if (stepped) *stepped = st ? 1 : 0;
+    });
+}
+
+gasb_status gasb_trainer_num_param_floats(gasb_trainer t, int64_t* out) {
+    return guard([&] {
+        require(t && out, "trainer: null argument");
+        *out = t->nparam;
+    });
+}
+
+gasb_status gasb_trainer_get_params(gasb_trainer t, float* h) {
+    return guard([&] {
+        require(t && h, "trainer: null argument");
+        GASB_CUDA(cudaStreamSynchronize(t->stream));
+        GASB_CUDA(cudaMemcpy(h, t->params.p, sizeof(float) * t->nparam, cudaMemcpyDeviceToHost));
+    });
+}
+
+gasb_status gasb_trainer_set_params(gasb_trainer t, const float* h) {
+    return guard([&] {
+        require(t && h, "trainer: null argument");
+        GASB_CUDA(cudaStreamSynchronize(t->stream));
+        GASB_CUDA(cudaMemcpy(t->params.p, h, sizeof(float) * t->nparam, cudaMemcpyHostToDevice));
+    });
+}
+
+gasb_status gasb_trainer_history(gasb_trainer t, gasb_history* out) {
+    return guard([&] {
+        require(t && out, "trainer: null argument");
+        *out = t->hist;
+    });
+}
+
+gasb_status gasb_trainer_stream(gasb_trainer t, gasb_stream* out) {
+    return guard([&] {
+        require(t && out, "trainer: null argument");
+        *out = t->stream;
+    });
+}
+
+gasb_status gasb_trainer_launch_count(gasb_trainer t, int64_t* out) {
+    return guard([&] {
+        require(t && out, "trainer: null argument");
+        *out = t->epoch_launches;
+    });
+}
+
+}  // extern "C"

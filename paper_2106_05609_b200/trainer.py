@@ -1,0 +1,130 @@
+"""GAS trainer (reference: include/gas/trainer.hpp — ModelSpec, Model, gas_epoch) over the
+C ABI. All compute runs in libgasb.so on the GPU; this module only marshals arguments."""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from ._native import ModelSpecC, TrainerOptionsC, check, f64, i32, i64, lib, ptr, vp
+from .graph import BatchSchedule
+from .history import HistoryStore
+
+KINDS = {"gcn": 0, "gin": 1, "appnp": 2, "gcnii": 3}
+
+
+@dataclass
+class AdamConfig:  # include/gas/nn.hpp:11-16
+    lr: float = 0.01
+    beta1: float = 0.9
+    beta2: float = 0.999
+    eps: float = 1e-8
+
+
+@dataclass
+class ModelSpec:  # include/gas/trainer.hpp:16-33 (GIN / Lipschitz fields are out of scope)
+    kind: str = "gcn"
+    num_layers: int = 2
+    hidden: int = 16
+    dropout: float = 0.0
+    alpha: float = 0.1
+    beta: float = 0.5
+    l2_weight: float = 0.0
+    clip_max_norm: float = 0.0
+    opt: AdamConfig = field(default_factory=AdamConfig)
+    seed: int = 0
+
+    def to_c(self) -> ModelSpecC:
+        return ModelSpecC(KINDS[self.kind], self.num_layers, self.hidden, self.dropout, self.alpha, self.beta,
+                          self.l2_weight, self.clip_max_norm, self.opt.lr, self.opt.beta1, self.opt.beta2,
+                          self.opt.eps, self.seed)
+
+
+@dataclass
+class TrainerOptions:
+    seg_edges: int = 128      # SpMM row segmentation (0 = sequential rows, bit-exact)
+    fused: bool = True        # pull-free SpMM over in-place histories
+    prefetch: bool = False
+    use_graphs: bool = True
+    hoist_layer1: bool = True
+    device: int = 0
+
+    def to_c(self) -> TrainerOptionsC:
+        return TrainerOptionsC(self.seg_edges, int(self.fused), int(self.prefetch), int(self.use_graphs),
+                               int(self.hoist_layer1), self.device)
+
+
+class GasTrainer:
+    """Model + AdamState + HistoryStore on one GPU, driven by gas_epoch."""
+
+    def __init__(self, schedule: BatchSchedule, features: np.ndarray, labels: np.ndarray, train_mask: np.ndarray,
+                 num_classes: int, spec: ModelSpec, options: TrainerOptions | None = None):
+        x = np.ascontiguousarray(features, dtype=np.float32)
+        lab = np.ascontiguousarray(labels, dtype=np.int32)
+        tm = np.ascontiguousarray(train_mask, dtype=np.uint8)
+        self.schedule = schedule
+        self.spec = spec
+        self.options = options or TrainerOptions()
+        s, o = spec.to_c(), self.options.to_c()
+        h = vp()
+        check(lib.gasb_trainer_create(schedule.handle, ptr(x), x.shape[1], ptr(lab), ptr(tm), int(num_classes),
+                                      C.byref(s), C.byref(o), C.byref(h)))
+        self._h = h
+        n = i64()
+        check(lib.gasb_trainer_num_param_floats(self._h, C.byref(n)))
+        self.num_param_floats = n.value
+        hh = vp()
+        check(lib.gasb_trainer_history(self._h, C.byref(hh)))
+        self.history = HistoryStore(0, 0, 0, _handle=hh.value, _owned=False) if spec.num_layers >= 1 else None
+        self.num_classes = num_classes
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            self.history = None
+            lib.gasb_trainer_destroy(self._h)
+            self._h = None
+
+    def gas_epoch(self, epoch: int, shuffle: bool = True) -> float:
+        loss = f64()
+        check(lib.gasb_gas_epoch(self._h, int(epoch), int(shuffle), C.byref(loss)))
+        return loss.value
+
+    def gas_epoch_async(self, epoch: int, shuffle: bool = True) -> None:
+        check(lib.gasb_gas_epoch_async(self._h, int(epoch), int(shuffle)))
+
+    def last_loss(self) -> float:
+        loss = f64()
+        check(lib.gasb_trainer_last_loss(self._h, C.byref(loss)))
+        return loss.value
+
+    def launch_count(self) -> int:
+        n = i64()
+        check(lib.gasb_trainer_launch_count(self._h, C.byref(n)))
+        return n.value
+
+    def stream(self) -> int:
+        s = vp()
+        check(lib.gasb_trainer_stream(self._h, C.byref(s)))
+        return s.value or 0
+
+    def batch(self, part: int, epoch: int = 0, train: bool = True, push: bool = True):
+        """One batch with capture: (acts[(L-1), nb, hd], logits[nb, C], loss, grads|None, stepped)."""
+        nb = int(self.schedule.sizes(part)[0])
+        L, hd = self.spec.num_layers, self.spec.hidden
+        acts = np.zeros((max(L - 1, 0), nb, hd), np.float32)
+        logits = np.zeros((nb, self.num_classes), np.float32)
+        grads = np.zeros(self.num_param_floats, np.float32)
+        loss, stepped = f64(), i32()
+        check(lib.gasb_trainer_batch(self._h, int(part), int(epoch), int(train), int(push), ptr(acts) if acts.size else
+                                     None, ptr(logits), C.byref(loss), ptr(grads), C.byref(stepped)))
+        return acts, logits, loss.value, (grads if stepped.value else None), bool(stepped.value)
+
+    def get_params(self) -> np.ndarray:
+        out = np.empty(self.num_param_floats, np.float32)
+        check(lib.gasb_trainer_get_params(self._h, ptr(out)))
+        return out
+
+    def set_params(self, values: np.ndarray) -> None:
+        v = np.ascontiguousarray(values, dtype=np.float32)
+        check(lib.gasb_trainer_set_params(self._h, ptr(v)))
