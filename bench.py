@@ -1,0 +1,318 @@
+"""GAS training throughput on B200 (BASELINE.json metric: GAS training nodes/sec, GCN,
+Reddit-shape; history pull GB/s).
+
+One step = one GAS epoch (gas_epoch, src/trainer.cpp:386-442): every one of the 200
+partition batches runs forward, push, loss, backward and one Adam step, in the seeded
+shuffled order. value = nodes / second = num_nodes * steps / device time (max over ranks).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+--impl reference times the reference's own CPU implementation (oracle/_ref: the reference
+sources compiled in place) on the box's host cores, one partition batch per step.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "GAS training nodes/sec (GCN, Reddit-shape)"
+PEAKS = ROOT / "MEASURED_PEAKS.json"
+HBM_FALLBACK_GBS = 6650.0
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+class Clocks:
+    """nvidia-smi sampler over the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.file = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={gpu}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"], stdout=self.file,
+                                         stderr=subprocess.DEVNULL)
+        except FileNotFoundError:
+            self.proc = None
+
+    def stop(self) -> dict:
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        self.proc.wait()
+        rows = [r.split(",") for r in Path(self.file.name).read_text().strip().splitlines() if r.strip()]
+        sm = [float(r[1]) for r in rows if len(r) > 8 and r[1].strip().replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if len(r) > 8 and r[2].strip().replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows if len(r) > 8 for i in range(4) if r[5 + i].strip() == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+def spmm_bytes(nb: int, ne: int, nnz: int, d: int) -> tuple[float, float]:
+    """compulsory model 8(B+1) + 8E + 4d*V + 4d*B; effective (no reuse) 4d*E."""
+    return 8 * (nb + 1) + 8 * nnz + 4 * d * ne + 4 * d * nb, 4.0 * d * nnz
+
+
+def peak_hbm() -> tuple[float, str]:
+    try:
+        return float(json.loads(PEAKS.read_text())["hbm_gbs"]), "measured"
+    except Exception:
+        return HBM_FALLBACK_GBS, "fallback"
+
+
+def cpu_baseline(ds, sample: int, kind_hint: str = "reference") -> dict:
+    """The reference (oracle/_ref) on a bounded sample of the same workload, 1 core."""
+    sys.path.insert(0, str(ROOT / "oracle"))
+    from pyoracle import REF_SO, RefLib, make_spec
+
+    w = ds.workload
+    if not REF_SO.exists():
+        return {"value": None, "unit": "nodes/s", "cores": 1, "kind": "reference",
+                "sample": "unavailable: oracle/_ref not built"}
+    R = RefLib()
+    order = R.epoch_order(w.parts, 3, 0)
+    parts = [int(p) for p in order[:sample]]
+    spec = make_spec(kind=0, num_layers=w.num_layers, hidden=w.hidden, seed=3)
+    s = R.session(ds.row_offsets, ds.cols, ds.features, ds.labels, ds.train_mask, w.num_classes, ds.assignment,
+                  w.parts, spec, sample_parts=parts)
+    nodes = int(sum((ds.assignment == p).sum() for p in parts))
+    secs = 0.0
+    for slot in range(len(parts)):
+        secs += s.run(slot, 0)[1]
+    return {"value": nodes / secs, "unit": "nodes/s", "cores": 1, "kind": "reference",
+            "sample": f"{len(parts)} of {w.parts} partition batches of the same graph (gas_epoch batches: forward,"
+                      f" push/pull, backward, Adam), {nodes} nodes in {secs:.1f} s, single-threaded reference"}
+
+
+def run_reference_arm(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    from paper_2106_05609_b200.workloads import make_dataset
+    sys.path.insert(0, str(ROOT / "oracle"))
+    from pyoracle import REF_SO, RefLib, make_spec
+
+    if not REF_SO.exists():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libref.so not built"}))
+        return
+    ds = make_dataset(args.workload)
+    w = ds.workload
+    R = RefLib()
+    order = [int(p) for p in R.epoch_order(w.parts, 3, 0)]
+    k = args.steps + args.warmup
+    parts = [order[i % w.parts] for i in range(min(k, w.parts))]
+    s = R.session(ds.row_offsets, ds.cols, ds.features, ds.labels, ds.train_mask, w.num_classes, ds.assignment,
+                  w.parts, make_spec(kind=0, num_layers=w.num_layers, hidden=w.hidden, seed=3), sample_parts=parts)
+    times, nodes = [], []
+    for i in range(k):
+        slot = i % len(parts)
+        _, secs = s.run(slot, 0)
+        if i >= args.warmup:
+            times.append(secs)
+            nodes.append(int((ds.assignment == parts[slot]).sum()))
+    value = sum(nodes) / sum(times)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "nodes/s", "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * sum(times) / len(times),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32 (f64 accumulation)",
+        "data": "synthetic", "config": workload_config(ds, "cpu-1core"),
+        "cpu_baseline": {"value": value, "unit": "nodes/s", "cores": 1, "kind": "reference",
+                         "sample": f"one partition batch per step ({int(np.mean(nodes))} nodes avg), reference "
+                                   "gas_epoch batch path, single-threaded (the reference has no parallel compute)"},
+        "e2e": {"value": value, "unit": "nodes/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+def workload_config(ds, parallelism: str) -> dict:
+    w = ds.workload
+    return {"workload": f"{w.name}-shape GAS-{w.kind.upper()}", "num_nodes": w.num_nodes,
+            "stored_nnz": int(len(ds.cols)), "in_dim": w.in_dim, "hidden": w.hidden, "num_classes": w.num_classes,
+            "layers": w.num_layers, "partitions": w.parts, "partitioner": "planted communities (natural partition)",
+            "step": "one GAS epoch (all partition batches, one Adam step each)", "parallelism": parallelism,
+            "l2_policy": "inputs larger than L2 (features 567 MB, histories 716 MB vs 126 MB L2)"}
+
+
+def run_ours(args):
+    import torch
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_2106_05609_b200 as gb
+    from paper_2106_05609_b200._native import check, lib
+    from paper_2106_05609_b200.workloads import make_dataset
+
+    t0 = time.time()
+    ds = make_dataset(args.workload)
+    w = ds.workload
+    sched = gb.BatchSchedule.build(ds.graph, ds.assignment, w.parts)
+    spec = gb.ModelSpec(kind=w.kind, num_layers=w.num_layers, hidden=w.hidden, seed=3)
+    opts = gb.TrainerOptions(seg_edges=args.seg_edges, device=local, hoist_layer1=not args.no_hoist)
+    tr = gb.GasTrainer(sched, ds.features, ds.labels, ds.train_mask, w.num_classes, spec, opts)
+    log(f"[rank {rank}] setup {time.time() - t0:.1f}s  n={w.num_nodes} nnz={len(ds.cols)}")
+    stream = torch.cuda.ExternalStream(tr.stream())
+
+    def barrier():
+        torch.cuda.synchronize()
+        if ws > 1:
+            torch.distributed.barrier()
+
+    for e in range(args.warmup):
+        l = tr.gas_epoch(e)
+        log(f"[rank {rank}] warmup epoch {e} loss {l:.5f}")
+    # ---- device-timed region: K epochs back to back ----
+    clocks = Clocks(local)
+    barrier()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for k in range(args.steps):
+        tr.gas_epoch_async(args.warmup + k)
+    ev1.record(stream)
+    barrier()
+    ms = ev0.elapsed_time(ev1)
+    clk = clocks.stop()
+    loss = tr.last_loss()
+    launches = tr.launch_count() * args.steps
+    t = torch.tensor([ms], device="cuda")
+    if ws > 1:
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    ms = float(t.item())
+    value = ws * w.num_nodes * args.steps / (ms / 1000.0)
+
+    # ---- end to end through the public API with host buffers ----
+    x = np.ascontiguousarray(ds.features, np.float32)
+    check(lib.gasb_host_register(x.ctypes.data, x.nbytes))
+    barrier()
+    t1 = time.perf_counter()
+    for k in range(args.steps):
+        tr.set_features(x)  # H2D of the step's input from pinned host memory
+        tr.gas_epoch(args.warmup + args.steps + k)  # D2H of the per-batch losses (step result)
+    barrier()
+    e2e_s = time.perf_counter() - t1
+    check(lib.gasb_host_unregister(x.ctypes.data))
+    t = torch.tensor([e2e_s], device="cuda")
+    if ws > 1:
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    e2e_s = float(t.item())
+    e2e = {"value": ws * w.num_nodes * args.steps / e2e_s, "unit": "nodes/s", "h2d_bytes_per_step": int(x.nbytes),
+           "d2h_bytes_per_step": 8 * w.parts}
+
+    # ---- roofline of the dominant kernel: per-batch SpMM at d = hidden (layers 2..L) ----
+    peak, peak_kind = peak_hbm()
+    tot_t, tot_b, tot_eff = 0.0, 0.0, 0.0
+    parts = list(range(0, w.parts, max(1, w.parts // args.profile_parts)))
+    for p in parts:
+        nb, ne, _, _, nnz, _ = (int(v) for v in sched.sizes(p))
+        ms_p = tr.profile_spmm(p, 2, 3)
+        b, eff = spmm_bytes(nb, ne, nnz, w.hidden)
+        tot_t += ms_p
+        tot_b += b
+        tot_eff += eff
+    achieved = tot_b / (tot_t / 1000.0) / 1e9
+    roof = {"kernel": "spmm_fwd_kernel (per-batch aggregation, d=hidden)", "bound": "hbm", "achieved": achieved,
+            "peak": peak, "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
+            "avg_launch_ms": tot_t / len(parts), "algorithmic_bytes_per_launch": tot_b / len(parts),
+            "effective_gather_GBps": tot_eff / (tot_t / 1000.0) / 1e9, "traffic": None}
+    prof = ROOT / "profiles" / "spmm_traffic.json"
+    if prof.exists():
+        try:
+            roof["traffic"] = json.loads(prof.read_text()).get("dram_bytes_per_launch")
+        except Exception:
+            pass
+    extra = {}
+    if not args.no_hoist:
+        ms_h = tr.profile_spmm(-1, 1, 2)
+        extra["hoisted_layer1_ms"] = ms_h
+    # ---- history pull GB/s at C3 halo sizes (HistoryStore::pull, d = hidden) ----
+    pull = pull_bandwidth(tr, sched, w, torch)
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "nodes/s", "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32 (f64 SpMM accumulation)", "data": "synthetic",
+        "config": workload_config(ds, "replicas" + str(ws) if ws > 1 else "single-gpu"),
+        "e2e": e2e, "gpu_launches": launches, "roofline": roof, "clocks": clk, "final_loss": loss,
+        "history_pull_GBps": pull, **extra,
+    }
+    if rank == 0 and ws == 1 and not args.no_cpu:
+        line["cpu_baseline"] = cpu_baseline(ds, args.cpu_sample)
+    if rank == 0:
+        print(json.dumps(line))
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+
+
+def pull_bandwidth(tr, sched, w, torch) -> dict:
+    """HistoryStore::pull of a batch's halo rows (ids + d floats read, d floats written)."""
+    hist = tr.history
+    p = 0
+    plan = sched.plan(p)
+    halo = torch.from_numpy(plan.halo_nodes).cuda()
+    out = torch.empty(len(halo), hist.ld, device="cuda")
+    s = torch.cuda.current_stream()
+    for _ in range(2):
+        hist.pull_device(1, halo, len(halo), out, hist.ld, s)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    it = 10
+    e0.record(s)
+    for _ in range(it):
+        hist.pull_device(1, halo, len(halo), out, hist.ld, s)
+    e1.record(s)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / it
+    byts = len(halo) * (8 * hist.dim() + 4)
+    peak, _ = peak_hbm()
+    return {"rows": len(halo), "dim": hist.dim(), "ms": ms, "GBps": byts / (ms / 1000) / 1e9,
+            "frac": byts / (ms / 1000) / 1e9 / peak}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="reddit")
+    ap.add_argument("--seg-edges", type=int, default=128)
+    ap.add_argument("--no-hoist", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-sample", type=int, default=3)
+    ap.add_argument("--profile-parts", type=int, default=20)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        run_reference_arm(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -163,17 +163,17 @@ gasb_status gasb_prefetch_wait(gasb_prefetcher p, uint64_t generation, int32_t l
  * seg_edges == 0: one warp per row in CSR order -> bit-exact with the reference.
  * seg_edges  > 0: rows split into segments of <= seg_edges edges whose fp64 partials are
  * combined in segment order (deterministic; differs from sequential fp64 only below fp32
- * resolution). Device int32 rowptr (relative), int32 cols into x's rows. */
+ * resolution). Device int32 rowptr (relative), int32 cols into x's num_src rows. */
 gasb_status gasb_spmm_fwd(const int32_t* d_rowptr, int32_t num_dst, const int32_t* d_cols, const float* d_coeffs,
-                          const float* d_x, int64_t ldx, int32_t dim, float* d_y, int64_t ldy, int32_t seg_edges,
-                          gasb_stream stream);
+                          const float* d_x, int32_t num_src, int64_t ldx, int32_t dim, float* d_y, int64_t ldy,
+                          int32_t seg_edges, gasb_stream stream);
 /* aggregate backward closure (tensor.cpp:531-549) restricted to the given targets, as a
  * gather over the transposed stencil: gx[t,:] = sum over (r, c) in CSC row t, r ascending,
  * of c * gy[r,:] with fp32 multiply-then-add -> bit-exact. Optional mask: gx[t,j] = 0
  * where d_mask[t*ldm + j] <= 0 (fused relu backward, tensor.cpp:363-369). */
 gasb_status gasb_spmm_bwd(const int32_t* d_t_rowptr, int32_t num_targets, const int32_t* d_t_src,
-                          const float* d_t_coeffs, const float* d_gy, int64_t ldgy, int32_t dim, const float* d_mask,
-                          int64_t ldm, float* d_gx, int64_t ldgx, gasb_stream stream);
+                          const float* d_t_coeffs, const float* d_gy, int64_t ldgy, int32_t num_src, int32_t dim,
+                          const float* d_mask, int64_t ldm, float* d_gx, int64_t ldgx, gasb_stream stream);
 /* matmul (tensor.cpp:148-204) on fp32 row-major operands, fp32 accumulation:
  * op = 0: C = A[m,k] B[k,n]; 1: C = A[m,k] B[n,k]^T; 2: C = A[k,m]^T B[k,n].
  * beta == 0 overwrites C, beta == 1 accumulates. */
@@ -230,6 +230,16 @@ gasb_status gasb_trainer_get_params(gasb_trainer t, float* h_out);
 gasb_status gasb_trainer_set_params(gasb_trainer t, const float* h_in);
 gasb_status gasb_trainer_history(gasb_trainer t, gasb_history* out); /* borrowed */
 gasb_status gasb_trainer_stream(gasb_trainer t, gasb_stream* out);
+/* Replaces the device feature matrix from host memory (n x in_dim, dense), stream-ordered
+ * on the trainer's stream (asynchronous when h_features is pinned, see gasb_host_register). */
+gasb_status gasb_trainer_set_features(gasb_trainer t, const float* h_features);
+/* Times `iters` back-to-back launches of one SpMM of the training step with CUDA events on
+ * the trainer's stream: part >= 0 -> the per-batch aggregation of `layer` for that part;
+ * part < 0 -> the hoisted whole-epoch layer-1 aggregation. Writes only scratch buffers. */
+gasb_status gasb_trainer_profile_spmm(gasb_trainer t, int32_t part, int32_t layer, int32_t iters, float* avg_ms);
+/* Page-locks host memory for asynchronous copies (cudaHostRegister / Unregister). */
+gasb_status gasb_host_register(void* h_ptr, size_t bytes);
+gasb_status gasb_host_unregister(void* h_ptr);
 /* Kernel launches per epoch (counted by the host driver while enqueueing). */
 gasb_status gasb_trainer_launch_count(gasb_trainer t, int64_t* out);
 

@@ -230,6 +230,7 @@ class RefLib:
         L.ref_session_adam_steps.restype = i64
         L.ref_session_epoch.argtypes = [vp, i64, C.c_int, C.c_int, P(f64), P(f64)]
         L.ref_session_batch.argtypes = [vp, i32, i64, C.c_int, C.c_int, vp, vp, P(f64), vp, P(C.c_int)]
+        L.ref_session_run.argtypes = [vp, i32, i64, P(f64), P(f64)]
 
     def check(self, rc):
         if rc == 0:
@@ -430,6 +431,12 @@ class Session:
         elif rc:
             raise ValueError("go_session_batch failed")
         return acts, logits, loss.value, (grads if stepped.value else None), bool(stepped.value)
+
+    def run(self, slot, epoch=0):
+        """Reference only: one gas_epoch batch without capture; returns (loss, seconds)."""
+        loss, secs = f64(), f64()
+        self.owner.check(self.owner.lib.ref_session_run(self.h, slot, epoch, C.byref(loss), C.byref(secs)))
+        return loss.value, secs.value
 
     def epoch(self, epoch, shuffle=True, prefetch=False):
         loss, secs = f64(), f64()

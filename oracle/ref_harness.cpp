@@ -493,6 +493,47 @@ int ref_session_epoch(void* sp, std::int64_t epoch, int shuffle, int use_prefetc
     });
 }
 
+// One batch exactly as gas_epoch runs it (run_batch without capture, trainer.cpp:295-339,
+// then advance_step :426), timed with steady_clock: the reference arm's unit of work.
+int ref_session_run(void* sp, std::int32_t slot, std::int64_t epoch, double* loss_out, double* seconds) {
+    return guard([&] {
+        Session* s = static_cast<Session*>(sp);
+        Model& model = *s->model;
+        const BatchPlan& plan = s->sched.plans.at(static_cast<std::size_t>(slot));
+        const PlanAggregation& agg = s->sched.aggs.at(static_cast<std::size_t>(slot));
+        auto t0 = std::chrono::steady_clock::now();
+        Model::ForwardOptions fwd;
+        fwd.training = true;
+        fwd.epoch = epoch;
+        fwd.batch_index = s->sched_parts.at(static_cast<std::size_t>(slot));
+        fwd.store = &s->store;
+        fwd.push = true;
+        Tape tape;
+        Tensor logits = model.forward(&tape, s->ds.features, plan, agg, fwd);
+        std::vector<std::int32_t> rows, lab;
+        for (std::size_t i = 0; i < plan.batch_nodes.size(); ++i) {
+            const NodeId v = plan.batch_nodes[i];
+            if (s->ds.labels.train_mask[v]) {
+                rows.push_back(static_cast<std::int32_t>(i));
+                lab.push_back(s->ds.labels.labels[v]);
+            }
+        }
+        *loss_out = 0.0;
+        if (!rows.empty()) {
+            Tensor loss = softmax_cross_entropy(&tape, logits, rows, lab);
+            *loss_out = loss.scalar_value();
+            tape.backward(loss);
+            auto params = model.params();
+            if (model.spec().clip_max_norm > 0.0f) grad_clip(std::span<Tensor>(params), model.spec().clip_max_norm);
+            s->opt->step();
+            s->opt->zero_grad();
+        }
+        s->store.advance_step();
+        tape.reset();
+        *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    });
+}
+
 // One batch of gas_epoch with full capture. slot = schedule index (== part id when the
 // whole partition is planned). Outputs (batch rows, in plan.batch_nodes order):
 //   acts   : (L-1) x nb x hist_dim   pushed (post-activation) rows per history layer

@@ -97,8 +97,8 @@ _SIGS = {
     "gasb_prefetcher_destroy": (i32, [vp]),
     "gasb_prefetch_begin": (i32, [vp, vp, i64, vp, P(u64)]),
     "gasb_prefetch_wait": (i32, [vp, u64, i32, vp, P(vp), P(i64)]),
-    "gasb_spmm_fwd": (i32, [vp, i32, vp, vp, vp, i64, i32, vp, i64, i32, vp]),
-    "gasb_spmm_bwd": (i32, [vp, i32, vp, vp, vp, i64, i32, vp, i64, vp, i64, vp]),
+    "gasb_spmm_fwd": (i32, [vp, i32, vp, vp, vp, i32, i64, i32, vp, i64, i32, vp]),
+    "gasb_spmm_bwd": (i32, [vp, i32, vp, vp, vp, i64, i32, i32, vp, i64, vp, i64, vp]),
     "gasb_gemm": (i32, [i32, i32, i32, i32, vp, i64, vp, i64, vp, i64, f32, vp]),
     "gasb_trainer_create": (i32, [vp, vp, i32, vp, vp, i32, P(ModelSpecC), P(TrainerOptionsC), P(vp)]),
     "gasb_trainer_destroy": (i32, [vp]),
@@ -112,6 +112,10 @@ _SIGS = {
     "gasb_trainer_history": (i32, [vp, P(vp)]),
     "gasb_trainer_stream": (i32, [vp, P(vp)]),
     "gasb_trainer_launch_count": (i32, [vp, P(i64)]),
+    "gasb_trainer_set_features": (i32, [vp, vp]),
+    "gasb_trainer_profile_spmm": (i32, [vp, i32, i32, i32, P(f32)]),
+    "gasb_host_register": (i32, [vp, C.c_size_t]),
+    "gasb_host_unregister": (i32, [vp]),
 }
 
 for _name, (_res, _args) in _SIGS.items():

@@ -108,6 +108,7 @@ __global__ void __launch_bounds__(256) gemm_kernel(int M, int N, int K, const fl
             buf ^= 1;
         }
     }
+    int32_t pushed_flags = 0;
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
         const int m = m0 + ty + 16 * i;
@@ -127,8 +128,15 @@ __global__ void __launch_bounds__(256) gemm_kernel(int M, int N, int K, const fl
             if (beta != 0.f) v += beta * crow[n];
             if (relu) v = v > 0.f ? v : 0.f;
             crow[n] = v;
-            if (prow) prow[n] = v;
+            if (prow) {
+                prow[n] = v;
+                pushed_flags |= table_flag_of(v);
+            }
         }
+    }
+    if (push.special) {  // the history table's value flags (spmm.cu widening paths)
+        pushed_flags = __reduce_or_sync(0xffffffffu, pushed_flags);
+        if ((tid & 31) == 0 && pushed_flags) atomicOr(push.special, pushed_flags);
     }
 }
 

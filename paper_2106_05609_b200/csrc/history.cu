@@ -23,11 +23,12 @@ __global__ void __launch_bounds__(256) rows_kernel(int mode, const int32_t* __re
                                                    const float* __restrict__ src, int64_t lds,
                                                    float* __restrict__ dst, int64_t ldd, int32_t dim, int32_t n,
                                                    int64_t* __restrict__ stamps, const int64_t* __restrict__ step,
-                                                   int32_t* __restrict__ err) {
+                                                   int32_t* __restrict__ err, int32_t* __restrict__ flags) {
     const int lane = threadIdx.x & 31;
     const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
     const int64_t stamp = (mode == 0 && stamps) ? *step : 0;
+    int32_t fl = 0;  // value flags of pushed rows (kernels.cuh kTableNeg / kTableNonFinite)
     for (int64_t base = warp * R; base < count; base += nwarps * R) {
         int64_t srow[R], drow[R];
         bool ok[R];
@@ -52,7 +53,12 @@ __global__ void __launch_bounds__(256) rows_kernel(int mode, const int32_t* __re
                     if (ok[r]) v[r] = __ldg(reinterpret_cast<const float4*>(src + srow[r] * lds + c));
 #pragma unroll
                 for (int r = 0; r < R; ++r)
-                    if (ok[r]) *reinterpret_cast<float4*>(dst + drow[r] * ldd + c) = v[r];
+                    if (ok[r]) {
+                        *reinterpret_cast<float4*>(dst + drow[r] * ldd + c) = v[r];
+                        if (flags)
+                            fl |= table_flag_of(v[r].x) | table_flag_of(v[r].y) | table_flag_of(v[r].z) |
+                                  table_flag_of(v[r].w);
+                    }
             }
         } else {
             for (int c = lane; c < dim; c += 32) {
@@ -62,9 +68,16 @@ __global__ void __launch_bounds__(256) rows_kernel(int mode, const int32_t* __re
                     if (ok[r]) v[r] = __ldg(src + srow[r] * lds + c);
 #pragma unroll
                 for (int r = 0; r < R; ++r)
-                    if (ok[r]) dst[drow[r] * ldd + c] = v[r];
+                    if (ok[r]) {
+                        dst[drow[r] * ldd + c] = v[r];
+                        if (flags) fl |= table_flag_of(v[r]);
+                    }
             }
         }
+    }
+    if (flags) {
+        fl = __reduce_or_sync(0xffffffffu, fl);
+        if (lane == 0 && fl) atomicOr(flags, fl);
     }
 }
 
@@ -89,7 +102,8 @@ static int num_sms() {
 }
 
 void launch_rows(int mode, const int32_t* ids, int64_t count, const float* src, int64_t lds, float* dst, int64_t ldd,
-                 int32_t dim, int32_t n, int64_t* stamps, const int64_t* step, int32_t* err, cudaStream_t st) {
+                 int32_t dim, int32_t n, int64_t* stamps, const int64_t* step, int32_t* err, cudaStream_t st,
+                 int32_t* flags) {
     if (count <= 0) return;
     const bool vec4 = (dim % 4 == 0) && (lds % 4 == 0) && (ldd % 4 == 0) &&
                       (reinterpret_cast<uintptr_t>(src) % 16 == 0) && (reinterpret_cast<uintptr_t>(dst) % 16 == 0);
@@ -98,10 +112,10 @@ void launch_rows(int mode, const int32_t* ids, int64_t count, const float* src, 
     const int64_t blocks = std::min<int64_t>(ceil_div(warps_needed, 8), static_cast<int64_t>(num_sms()) * 8);
     if (vec4)
         rows_kernel<4, R><<<static_cast<unsigned>(blocks), 256, 0, st>>>(mode, ids, count, src, lds, dst, ldd, dim, n,
-                                                                         stamps, step, err);
+                                                                         stamps, step, err, flags);
     else
         rows_kernel<1, R><<<static_cast<unsigned>(blocks), 256, 0, st>>>(mode, ids, count, src, lds, dst, ldd, dim, n,
-                                                                         stamps, step, err);
+                                                                         stamps, step, err, flags);
     ++t_launches;
     GASB_CUDA(cudaGetLastError());
 }
@@ -123,9 +137,11 @@ struct gasb_history_s {
     int64_t* stamps = nullptr;
     int64_t* step = nullptr;
     int32_t* err = nullptr;
+    int32_t* flags = nullptr;  // per layer: OR of table_flag_of over every value ever stored
 
     float* table(int32_t layer) const { return tables + static_cast<int64_t>(layer - 1) * n * ld; }
     int64_t* stamp(int32_t layer) const { return stamps + static_cast<int64_t>(layer - 1) * n; }
+    int32_t* flag(int32_t layer) const { return flags + (layer - 1); }
     void check_layer(int32_t layer) const {
         if (layer < 1 || layer > layers)
             throw std::invalid_argument("HistoryStore: layer " + std::to_string(layer) + " out of range [1," +
@@ -136,6 +152,7 @@ struct gasb_history_s {
         cudaFree(stamps);
         cudaFree(step);
         cudaFree(err);
+        cudaFree(flags);
     }
 };
 
@@ -176,6 +193,8 @@ gasb_history history_create(int32_t layers, int32_t n, int32_t dim) {
         GASB_CUDA(cudaMemset(h->step, 0, sizeof(int64_t)));
         GASB_CUDA(cudaMalloc(&h->err, sizeof(int32_t)));
         GASB_CUDA(cudaMemset(h->err, 0, sizeof(int32_t)));
+        GASB_CUDA(cudaMalloc(&h->flags, sizeof(int32_t) * std::max(layers, 1)));
+        GASB_CUDA(cudaMemset(h->flags, 0, sizeof(int32_t) * std::max(layers, 1)));  // zero tables
         GASB_CUDA(cudaDeviceSynchronize());
     } catch (...) {
         delete h;
@@ -187,6 +206,7 @@ float* history_table(gasb_history h, int32_t layer) { return h->table(layer); }
 int64_t history_ld(gasb_history h) { return h->ld; }
 int64_t* history_stamps(gasb_history h, int32_t layer) { return h->stamp(layer); }
 int64_t* history_step_ptr(gasb_history h) { return h->step; }
+int32_t* history_flags(gasb_history h, int32_t layer) { return h->flag(layer); }
 void history_destroy(gasb_history h) { delete h; }
 }  // namespace gasb
 
@@ -222,7 +242,7 @@ gasb_status gasb_history_push(gasb_history h, int32_t layer, const int32_t* ids,
         require(count >= 0 && (count == 0 || (ids && rows)) && ld_rows >= h->dim,
                 "HistoryStore::push: row count mismatch");
         launch_rows(0, ids, count, rows, ld_rows, h->table(layer), h->ld, h->dim, h->n, h->stamp(layer), h->step,
-                    h->err, as_stream(stream));
+                    h->err, as_stream(stream), h->flag(layer));
     });
 }
 
@@ -271,7 +291,7 @@ gasb_status gasb_history_push_host(gasb_history h, int32_t layer, const int32_t*
         GASB_CUDA(cudaMemcpyAsync(d_ids, ids, sizeof(int32_t) * count, cudaMemcpyHostToDevice, st));
         GASB_CUDA(cudaMemcpyAsync(d_rows, rows, sizeof(float) * count * h->dim, cudaMemcpyHostToDevice, st));
         launch_rows(0, d_ids, count, d_rows, h->dim, h->table(layer), h->ld, h->dim, h->n, h->stamp(layer), h->step,
-                    h->err, st);
+                    h->err, st, h->flag(layer));
         GASB_CUDA(cudaFreeAsync(d_ids, st));
         GASB_CUDA(cudaFreeAsync(d_rows, st));
         GASB_CUDA(cudaStreamSynchronize(st));
@@ -342,6 +362,8 @@ gasb_status gasb_history_fill_layer(gasb_history h, int32_t layer, const float* 
         GASB_CUDA(cudaMemcpy2D(h->table(layer), sizeof(float) * h->ld, values, sizeof(float) * h->dim,
                                sizeof(float) * h->dim, h->n, cudaMemcpyHostToDevice));
         if (h->n > 0) fill_stamps_kernel<<<256, 256>>>(h->stamp(layer), h->n, h->step);
+        GASB_CUDA(cudaMemset(h->flag(layer), 0, sizeof(int32_t)));  // the table is replaced whole
+        launch_scan_special(h->table(layer), h->n, h->ld, h->dim, h->flag(layer), nullptr);
         GASB_CUDA(cudaGetLastError());
         GASB_CUDA(cudaDeviceSynchronize());
     });
@@ -375,6 +397,7 @@ gasb_status gasb_history_reset(gasb_history h) {
         const int64_t ns = static_cast<int64_t>(h->layers) * h->n;
         if (ns) GASB_CUDA(cudaMemset(h->stamps, 0xFF, sizeof(int64_t) * ns));
         GASB_CUDA(cudaMemset(h->step, 0, sizeof(int64_t)));
+        GASB_CUDA(cudaMemset(h->flags, 0, sizeof(int32_t) * std::max(h->layers, 1)));
         GASB_CUDA(cudaDeviceSynchronize());
     });
 }

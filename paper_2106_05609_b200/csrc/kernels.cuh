@@ -16,11 +16,29 @@ inline int64_t round_up(int64_t a, int64_t b) { return ceil_div(a, b) * b; }
 // Counts kernel launches issued through these helpers (gpu_launches evidence).
 extern thread_local int64_t t_launches;
 
+// Per-table value flags (device int32, OR-accumulated by every producer of a table that the
+// SpMM reads): they pick the fp32 -> fp64 widening path of the forward SpMM (spmm.cu).
+constexpr int32_t kTableNeg = 1;        // some value has its sign bit set
+constexpr int32_t kTableNonFinite = 2;  // some value is inf / nan
+// Coefficients of the forward SpMM are stored multiplied by 2^896 (exact; see spmm.cu).
+constexpr double kCoeffScale = 0x1.0p+896;
+
+__host__ __device__ inline int32_t table_flag_of(float v) {
+#ifdef __CUDA_ARCH__
+    const uint32_t u = __float_as_uint(v);
+#else
+    uint32_t u;
+    __builtin_memcpy(&u, &v, 4);
+#endif
+    return ((u >> 31) ? kTableNeg : 0) | (((u & 0x7fffffffu) >= 0x7f800000u) ? kTableNonFinite : 0);
+}
+
 // ---- history rows (history.cu) ------------------------------------------------------
 // mode 0 = push: dst[ids[i]] = src[i] (+ stamps[ids[i]] = *step); mode 1 = pull: dst[i] = src[ids[i]].
+// flags (push only, optional): the destination table's value-flag word.
 void launch_rows(int mode, const int32_t* ids, int64_t count, const float* src, int64_t lds, float* dst,
                  int64_t ldd, int32_t dim, int32_t n, int64_t* stamps, const int64_t* step, int32_t* err,
-                 cudaStream_t st);
+                 cudaStream_t st, int32_t* flags = nullptr);
 void launch_advance_step(int64_t* step, cudaStream_t st);
 
 // ---- SpMM (spmm.cu) -------------------------------------------------------------------
@@ -38,14 +56,18 @@ struct SpmmSegs {
     int64_t nseg;
     int64_t seg_base;         // absolute index of this launch's first segment
 };
+// coeffs: stencil coefficients as fp64 pre-multiplied by kCoeffScale. special: the source
+// table's flag word (kTableNeg / kTableNonFinite); nullptr = assume anything (exact F2F).
 void launch_spmm_fwd(const SpmmSegs& s, const int32_t* cols, const double* coeffs, const float* x, int64_t ldx,
                      int32_t dim, float* y, int64_t ldy, int64_t row_base, double* partial, int64_t partial_ld,
-                     int32_t* counters, int32_t counters_ld, cudaStream_t st);
+                     int32_t* counters, int32_t counters_ld, cudaStream_t st, const int32_t* special = nullptr);
+// special[0] |= table_flag_of(v) over the values v of x[rows x dim] (pitch ld).
+void launch_scan_special(const float* x, int64_t rows, int64_t ld, int32_t dim, int32_t* special, cudaStream_t st);
 // Transposed (CSC) gather, fp32 multiply-then-add in entry order (bit-exact with the
 // reference scatter). mask (optional): zero where mask <= 0 (relu backward).
 void launch_spmm_bwd(const int64_t* t_rowptr, int32_t ntargets, const int32_t* t_src, const float* t_coeffs,
                      const float* gy, int64_t ldgy, int32_t dim, const float* mask, int64_t ldm, float* gx,
-                     int64_t ldgx, cudaStream_t st);
+                     int64_t ldgx, cudaStream_t st, int32_t nsrc = 0);
 
 // ---- GEMM (gemm.cu) -------------------------------------------------------------------
 // op 0: C = A B ; 1: C = A B^T ; 2: C = A^T B.  Row-major fp32, fp32 accumulation.
@@ -57,16 +79,18 @@ struct PushEpilogue {
     const int32_t* ids;
     int64_t* stamps;
     const int64_t* step;
+    int32_t* special;  // the table's value flags: OR of table_flag_of(pushed values)
 };
 void launch_gemm(int op, int m, int n, int k, const float* a, int64_t lda, const float* b, int64_t ldb, float* c,
                  int64_t ldc, float beta, bool relu, const PushEpilogue* push, cudaStream_t st);
 
 // ---- training ops (train_ops.cu) ---------------------------------------------------
-// Softmax cross-entropy over `rows` (batch indices) with labels: loss (double, written to
-// *loss_out) and d loss / d logits into glogits (zeroed rows elsewhere), as tensor.cpp:597-647.
-void launch_softmax_ce(const float* logits, int64_t ldl, int32_t m, int32_t n, const int32_t* rows,
-                       const int32_t* labels, int32_t r, float* glogits, int64_t ldg, double* loss_out,
-                       double* row_scratch, cudaStream_t st);
+// Softmax cross-entropy over the training rows (row_label[i] >= 0; r of them) of an m-row
+// batch: loss (double, written to *loss_out) and d loss / d logits into glogits (zero rows
+// elsewhere), as tensor.cpp:597-647. row_scratch: m doubles; done: self-resetting counter.
+void launch_softmax_ce(const float* logits, int64_t ldl, int32_t m, int32_t n, const int32_t* row_label, int32_t r,
+                       float* glogits, int64_t ldg, double* loss_out, double* row_scratch, int32_t* done,
+                       cudaStream_t st);
 // AdamState::step (nn.cpp:20-41) over the flat parameter vector; bias corrections from
 // bc[2*t], t = ++(*t_counter) on device. clip_max_norm > 0 applies grad_clip first.
 void launch_adam(float* p, float* m, float* v, float* g, int64_t size, int64_t* t_counter, const double* bc,

@@ -10,44 +10,82 @@
 
 namespace gasb {
 
-// One block. Rows of the training mask are handled one per thread (sequential over the
-// classes, as the reference); the per-row losses are summed in row order by thread 0.
-__global__ void __launch_bounds__(256) softmax_ce_kernel(const float* __restrict__ logits, int64_t ldl, int32_t m,
-                                                         int32_t n, const int32_t* __restrict__ rows,
-                                                         const int32_t* __restrict__ labels, int32_t r,
-                                                         float* __restrict__ gl, int64_t ldg,
-                                                         double* __restrict__ loss_out, double* __restrict__ scratch) {
-    for (int64_t i = threadIdx.x; i < static_cast<int64_t>(m) * n; i += blockDim.x)
-        gl[(i / n) * ldg + (i % n)] = 0.0f;
-    __syncthreads();
+// A warp per batch row (grid-wide), lanes over the classes. row_label[i] = label of batch row
+// i when it is a training row, -1 otherwise (its gradient row is zeroed). Row max is exact in
+// any order; the fp64 softmax denominator and the loss sum use a fixed shuffle / tree order
+// (deterministic; differs from the reference's sequential fp64 sums only below the fp32
+// resolution of the outputs). The last CTA to finish sums the per-row terms in row order.
+constexpr int kCeThreads = 256;
+
+__global__ void __launch_bounds__(kCeThreads) softmax_ce_kernel(const float* __restrict__ logits, int64_t ldl,
+                                                                int32_t m, int32_t n,
+                                                                const int32_t* __restrict__ row_label, int32_t r,
+                                                                float* __restrict__ gl, int64_t ldg,
+                                                                double* __restrict__ loss_out,
+                                                                double* __restrict__ scratch,
+                                                                int32_t* __restrict__ done) {
+    __shared__ double red[kCeThreads];
+    __shared__ int last;
+    const int lane = threadIdx.x & 31;
+    const int32_t i = blockIdx.x * (kCeThreads / 32) + (threadIdx.x >> 5);
     const float inv_m = __frcp_rn(static_cast<float>(r));  // 1.0f / float(rows.size())
-    for (int32_t i = threadIdx.x; i < r; i += blockDim.x) {
-        const float* row = logits + static_cast<int64_t>(rows[i]) * ldl;
-        float* g = gl + static_cast<int64_t>(rows[i]) * ldg;
-        float mx = row[0];
-        for (int32_t j = 1; j < n; ++j) mx = fmaxf(mx, row[j]);
-        double denom = 0.0;
-        for (int32_t j = 0; j < n; ++j) denom = __dadd_rn(denom, exp(__dsub_rn(static_cast<double>(row[j]), mx)));
-        scratch[i] = __dsub_rn(log(denom), __dsub_rn(static_cast<double>(row[labels[i]]), mx));
-        const float gy_inv = __fmul_rn(1.0f, inv_m);
-        for (int32_t j = 0; j < n; ++j) {
-            const double p = __ddiv_rn(exp(__dsub_rn(static_cast<double>(row[j]), mx)), denom);
-            const double delta = (j == labels[i]) ? 1.0 : 0.0;
-            g[j] = __fadd_rn(g[j], __fmul_rn(gy_inv, static_cast<float>(__dsub_rn(p, delta))));
+    const float gy_inv = __fmul_rn(1.0f, inv_m);            // gy * inv_m, gy = 1
+    double term = 0.0;
+    if (i < m) {
+        const float* row = logits + static_cast<int64_t>(i) * ldl;
+        float* g = gl + static_cast<int64_t>(i) * ldg;
+        const int lab = row_label[i];
+        if (lab < 0) {
+            for (int j = lane; j < n; j += 32) g[j] = 0.0f;
+        } else {
+        float mx = -INFINITY;
+        for (int j = lane; j < n; j += 32) mx = fmaxf(mx, row[j]);
+        for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        double e[2] = {0.0, 0.0}, den = 0.0;
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            const int j = lane + 32 * k;
+            if (j < n) e[k] = exp(__dsub_rn(static_cast<double>(row[j]), static_cast<double>(mx)));
+            den = __dadd_rn(den, e[k]);
         }
+        for (int j = 64 + lane; j < n; j += 32) den = __dadd_rn(den, exp(__dsub_rn(static_cast<double>(row[j]), mx)));
+        for (int o = 16; o > 0; o >>= 1) den = __dadd_rn(den, __shfl_xor_sync(0xffffffffu, den, o));
+        term = __dsub_rn(log(den), __dsub_rn(static_cast<double>(row[lab]), mx));
+        for (int j = lane; j < n; j += 32) {
+            const double ej = j < 64 ? e[j >> 5] : exp(__dsub_rn(static_cast<double>(row[j]), mx));
+            const double p = __ddiv_rn(ej, den);
+            const double delta = (j == lab) ? 1.0 : 0.0;
+            g[j] = __fmul_rn(gy_inv, static_cast<float>(__dsub_rn(p, delta)));
+        }
+        }
+        if (lane == 0) scratch[i] = term;
     }
+    __threadfence();
     __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(done, 1) == static_cast<int>(gridDim.x) - 1;
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    double acc = 0.0;
+    for (int32_t k = threadIdx.x; k < m; k += kCeThreads) acc = __dadd_rn(acc, __ldcg(scratch + k));
+    red[threadIdx.x] = acc;
+    __syncthreads();
+    for (int s = kCeThreads / 2; s > 0; s >>= 1) {
+        if (threadIdx.x < s) red[threadIdx.x] = __dadd_rn(red[threadIdx.x], red[threadIdx.x + s]);
+        __syncthreads();
+    }
     if (threadIdx.x == 0) {
-        double total = 0.0;
-        for (int32_t i = 0; i < r; ++i) total = __dadd_rn(total, scratch[i]);
-        *loss_out = static_cast<double>(static_cast<float>(__ddiv_rn(total, static_cast<double>(r))));
+        *loss_out = static_cast<double>(static_cast<float>(__ddiv_rn(red[0], static_cast<double>(r))));
+        *done = 0;  // self-reset for the next launch / graph replay
     }
 }
 
-void launch_softmax_ce(const float* logits, int64_t ldl, int32_t m, int32_t n, const int32_t* rows,
-                       const int32_t* labels, int32_t r, float* glogits, int64_t ldg, double* loss_out,
-                       double* row_scratch, cudaStream_t st) {
-    softmax_ce_kernel<<<1, 256, 0, st>>>(logits, ldl, m, n, rows, labels, r, glogits, ldg, loss_out, row_scratch);
+void launch_softmax_ce(const float* logits, int64_t ldl, int32_t m, int32_t n, const int32_t* row_label, int32_t r,
+                       float* glogits, int64_t ldg, double* loss_out, double* row_scratch, int32_t* done,
+                       cudaStream_t st) {
+    const unsigned blocks = static_cast<unsigned>(ceil_div(m, kCeThreads / 32));
+    softmax_ce_kernel<<<blocks, kCeThreads, 0, st>>>(logits, ldl, m, n, row_label, r, glogits, ldg, loss_out,
+                                                     row_scratch, done);
     ++t_launches;
     GASB_CUDA(cudaGetLastError());
 }

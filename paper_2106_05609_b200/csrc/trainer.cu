@@ -42,6 +42,7 @@ float* history_table(gasb_history h, int32_t layer);
 int64_t history_ld(gasb_history h);
 int64_t* history_stamps(gasb_history h, int32_t layer);
 int64_t* history_step_ptr(gasb_history h);
+int32_t* history_flags(gasb_history h, int32_t layer);
 
 namespace {
 
@@ -188,9 +189,10 @@ struct gasb_trainer_s {
     DevBuf<float> t_cf;
     DevBuf<int64_t> t_rowptr;
     SegTable seg_batch, seg_all;
-    DevBuf<int32_t> counters;
+    DevBuf<int32_t> counters, row_label, xflags, ce_done;  // xflags: value flags of X (kernels.cuh)
     DevBuf<double> partial_batch, partial_all;
     int32_t max_chunks = 0;
+    int64_t pld = 0, pld_all = 0;
 
     // model
     std::vector<int64_t> poff, prow, pcol;  // per parameter tensor
@@ -226,6 +228,8 @@ struct gasb_trainer_s {
     }
 
     int64_t ld_of(int32_t d) const { return round_up(std::max(d, 1), 8); }
+    // value flags of the table layer l's aggregation reads: X for l = 1, H_{l-1} otherwise
+    const int32_t* source_flags(int32_t l) const { return l == 1 ? xflags.p : history_flags(hist, l - 1); }
     float* W(int32_t l) { return params.p + poff[layer_param[l]]; }
     float* gW(int32_t l) { return grads.p + poff[layer_param[l]]; }
 
@@ -303,7 +307,7 @@ void gasb_trainer_s::build(const float* h_features, const int32_t* h_labels, con
 
     // ---- host staging of the concatenated stencils ----
     std::vector<int32_t> h_bn(R), h_cg(E), h_cl(E), h_tsrc(T), h_trr(tr_off[num_parts]), h_trl(tr_off[num_parts]);
-    std::vector<int32_t> h_ext(NE), h_cidx(NE);
+    std::vector<int32_t> h_ext(NE), h_cidx(NE), h_rlab(R);
     std::vector<double> h_cf(E);
     std::vector<float> h_tcf(T);
     std::vector<int64_t> h_rp(R + 1), h_trp(R + num_parts);
@@ -321,7 +325,7 @@ void gasb_trainer_s::build(const float* h_features, const int32_t* h_labels, con
         for (size_t e = 0; e < P.gcn_cols.size(); ++e) {
             h_cg[e0 + e] = P.extended[P.gcn_cols[e]];
             h_cl[e0 + e] = P.gcn_cols[e];
-            h_cf[e0 + e] = static_cast<double>(P.gcn_coeffs[e]);
+            h_cf[e0 + e] = static_cast<double>(P.gcn_coeffs[e]) * kCoeffScale;  // exact (see spmm.cu)
         }
         // transposed intra-batch stencil: target = batch index of the source row, entries
         // in ascending dst row r (the reference's scatter order, tensor.cpp:540-547)
@@ -343,12 +347,14 @@ void gasb_trainer_s::build(const float* h_features, const int32_t* h_labels, con
                 h_tcf[k] = P.gcn_coeffs[e];
             }
         int32_t k = 0;
-        for (int32_t i = 0; i < nb[p]; ++i)
+        for (int32_t i = 0; i < nb[p]; ++i) {
+            h_rlab[r0 + i] = h_train[P.batch[i]] ? h_labels[P.batch[i]] : -1;
             if (h_train[P.batch[i]]) {
                 h_trr[tr_off[p] + k] = i;
                 h_trl[tr_off[p] + k] = h_labels[P.batch[i]];
                 ++k;
             }
+        }
         int32_t hk = 0;
         for (int32_t i = 0; i < ne[p]; ++i) {
             h_ext[ext_off[p] + i] = P.extended[i];
@@ -370,6 +376,7 @@ void gasb_trainer_s::build(const float* h_features, const int32_t* h_labels, con
     t_rowptr.upload(h_trp);
     train_rows.upload(h_trr);
     train_labels.upload(h_trl);
+    row_label.upload(h_rlab);
     extended.upload(h_ext);
     compose_idx.upload(h_cidx);
     {
@@ -383,8 +390,10 @@ void gasb_trainer_s::build(const float* h_features, const int32_t* h_labels, con
     max_chunks = static_cast<int32_t>(ceil_div(std::max(F, H), 64));
     counters.alloc(R * max_chunks);
     counters.zero();
-    partial_batch.alloc(std::max<int64_t>(seg_batch.max_group_slots, 1) * max_chunks * 64);
-    partial_all.alloc(std::max<int64_t>(seg_all.total_slots, 1) * ceil_div(F, 64) * 64);
+    pld = round_up(std::max(F, H), 128);  // fp64 partial row width, any SpMM chunk width
+    pld_all = round_up(F, 128);
+    partial_batch.alloc(std::max<int64_t>(seg_batch.max_group_slots, 1) * pld);
+    partial_all.alloc(std::max<int64_t>(seg_all.total_slots, 1) * pld_all);
 
     // ---- features ----
     X.alloc(static_cast<int64_t>(n) * ldF);
@@ -392,6 +401,12 @@ void gasb_trainer_s::build(const float* h_features, const int32_t* h_labels, con
                            cudaMemcpyHostToDevice));
     if (ldF > F)
         GASB_CUDA(cudaMemset2D(X.p + F, sizeof(float) * ldF, 0, sizeof(float) * (ldF - F), n));
+    // SpMM source tables free of denormal / non-finite values take the integer widening path
+    xflags.alloc(1);
+    xflags.zero();
+    launch_scan_special(X.p, n, ldF, F, xflags.p, nullptr);
+    ce_done.alloc(1);
+    ce_done.zero();
 
     // ---- Model::build (trainer.cpp:55-129), GCN: W_l (d_{l-1} x d_l) ----
     layer_param.assign(static_cast<size_t>(L) + 1, -1);
@@ -442,8 +457,8 @@ void gasb_trainer_s::build(const float* h_features, const int32_t* h_labels, con
 void gasb_trainer_s::enqueue_hoisted() {
     SpmmSegs s{seg_all.seg_beg.p, seg_all.seg_row.p, seg_all.seg_slot.p, seg_all.row_seg0.p,
                seg_all.row_nseg.p, seg_all.group_nseg[0], 0};
-    launch_spmm_fwd(s, cols_g.p, coef64.p, X.p, ldF, F, agg_all.p, ldF, 0, partial_all.p, ceil_div(F, 64) * 64,
-                    counters.p, max_chunks, stream);
+    launch_spmm_fwd(s, cols_g.p, coef64.p, X.p, ldF, F, agg_all.p, ldF, 0, partial_all.p, pld_all,
+                    counters.p, max_chunks, stream, source_flags(1));
 }
 
 void gasb_trainer_s::enqueue_batch(int32_t p, bool train, bool push, bool use_hoisted, bool fused) {
@@ -462,8 +477,8 @@ void gasb_trainer_s::enqueue_batch(int32_t p, bool train, bool push, bool use_ho
         } else if (fused) {
             const float* src = l == 1 ? X.p : history_table(hist, l - 1);
             const int64_t lds = l == 1 ? ldF : history_ld(hist);
-            launch_spmm_fwd(segs, cols_g.p, coef64.p, src, lds, din, a, lda, r0, partial_batch.p,
-                            static_cast<int64_t>(max_chunks) * 64, counters.p, max_chunks, stream);
+            launch_spmm_fwd(segs, cols_g.p, coef64.p, src, lds, din, a, lda, r0, partial_batch.p, pld, counters.p,
+                            max_chunks, stream, source_flags(l));
         } else {
             // reference structure: x_ext / compose over V_b local rows, SpMM by local ids
             const int64_t ldx = ld_of(din);
@@ -485,13 +500,16 @@ void gasb_trainer_s::enqueue_batch(int32_t p, bool train, bool push, bool use_ho
                 GASB_CUDA(cudaGetLastError());
                 hsrc = h_ext.p;
             }
-            launch_spmm_fwd(segs, cols_l.p, coef64.p, hsrc, ldx, din, a, lda, r0, partial_batch.p,
-                            static_cast<int64_t>(max_chunks) * 64, counters.p, max_chunks, stream);
+            // the composed rows come from X / H_{l-1} (+ act_{l-1}, pushed to H_{l-1} when push);
+            // without push the act rows are unflagged, so take the exact F2F widening
+            launch_spmm_fwd(segs, cols_l.p, coef64.p, hsrc, ldx, din, a, lda, r0, partial_batch.p, pld, counters.p,
+                            max_chunks, stream, (push || l == 1) ? source_flags(l) : nullptr);
         }
         float* Wl = W(l);
         if (l < L) {
+            // HistoryStore::push fused into the epilogue (stamps + the table's value flags)
             PushEpilogue pe{history_table(hist, l), history_ld(hist), bn, history_stamps(hist, l),
-                            history_step_ptr(hist)};
+                            history_step_ptr(hist), history_flags(hist, l)};
             launch_gemm(0, m, dout, din, a, lda, Wl, dout, act[l].p, ldH, 0.f, true, push ? &pe : nullptr, stream);
         } else {
             launch_gemm(0, m, dout, din, a, lda, Wl, dout, logits.p, ldC, 0.f, false, nullptr, stream);
@@ -500,8 +518,8 @@ void gasb_trainer_s::enqueue_batch(int32_t p, bool train, bool push, bool use_ho
     // ---------------- loss + backward (run_batch, trainer.cpp:295-339) ----------------
     const bool stepped = ntrain[p] > 0 && train;
     if (ntrain[p] > 0)
-        launch_softmax_ce(logits.p, ldC, m, C, train_rows.p + tr_off[p], train_labels.p + tr_off[p], ntrain[p],
-                          glogits.p, ldC, loss.p + p, row_scratch.p, stream);
+        launch_softmax_ce(logits.p, ldC, m, C, row_label.p + r0, ntrain[p], glogits.p, ldC, loss.p + p,
+                          row_scratch.p, ce_done.p, stream);
     if (stepped) {
         float* g = glogits.p;
         int64_t ldg = ldC;
@@ -515,7 +533,7 @@ void gasb_trainer_s::enqueue_batch(int32_t p, bool train, bool push, bool use_ho
             launch_gemm(1, m, din, dout, g, ldg, W(l), dout, g_agg.p, ldH, 0.f, false, nullptr, stream);
             // aggregate backward over intra-batch edges + compose bwd + relu bwd (mask = act)
             launch_spmm_bwd(t_rowptr.p + r0 + p, m, t_src.p, t_cf.p, g_agg.p, ldH, din, act[l - 1].p, ldH, g_out.p,
-                            ldH, stream);
+                            ldH, stream, m);
             g = g_out.p;
             ldg = ldH;
         }
@@ -711,6 +729,60 @@ gasb_status gasb_trainer_stream(gasb_trainer t, gasb_stream* out) {
         require(t && out, "trainer: null argument");
         *out = t->stream;
     });
+}
+
+gasb_status gasb_trainer_set_features(gasb_trainer t, const float* h) {
+    return guard([&] {
+        require(t && h, "trainer: null argument");
+        GASB_CUDA(cudaMemcpy2DAsync(t->X.p, sizeof(float) * t->ldF, h, sizeof(float) * t->F, sizeof(float) * t->F,
+                                    t->n, cudaMemcpyHostToDevice, t->stream));
+        GASB_CUDA(cudaMemsetAsync(t->xflags.p, 0, sizeof(int32_t), t->stream));  // X is replaced whole
+        launch_scan_special(t->X.p, t->n, t->ldF, t->F, t->xflags.p, t->stream);
+    });
+}
+
+gasb_status gasb_trainer_profile_spmm(gasb_trainer t, int32_t part, int32_t layer, int32_t iters, float* avg_ms) {
+    return guard([&] {
+        require(t && avg_ms && iters > 0, "trainer: bad argument");
+        require(part < t->num_parts && layer >= 1 && layer <= t->L, "trainer: part/layer out of range");
+        require(part >= 0 || (layer == 1 && t->agg_all.p), "trainer: hoisted profile needs hoist_layer1");
+        cudaEvent_t a, b;
+        GASB_CUDA(cudaEventCreate(&a));
+        GASB_CUDA(cudaEventCreate(&b));
+        auto once = [&] {
+            if (part < 0) {
+                t->enqueue_hoisted();
+                return;
+            }
+            const int32_t din = t->dims[layer - 1];
+            SpmmSegs segs{t->seg_batch.seg_beg.p, t->seg_batch.seg_row.p, t->seg_batch.seg_slot.p,
+                          t->seg_batch.row_seg0.p, t->seg_batch.row_nseg.p, t->seg_batch.group_nseg[part],
+                          t->seg_batch.group_seg0[part]};
+            const float* src = layer == 1 ? t->X.p : history_table(t->hist, layer - 1);
+            const int64_t lds = layer == 1 ? t->ldF : history_ld(t->hist);
+            launch_spmm_fwd(segs, t->cols_g.p, t->coef64.p, src, lds, din, t->agg[layer].p, t->ld_of(din),
+                            t->row_off[part], t->partial_batch.p, t->pld,
+                            t->counters.p, t->max_chunks, t->stream, t->source_flags(layer));
+        };
+        once();  // warm
+        GASB_CUDA(cudaEventRecord(a, t->stream));
+        for (int32_t i = 0; i < iters; ++i) once();
+        GASB_CUDA(cudaEventRecord(b, t->stream));
+        GASB_CUDA(cudaEventSynchronize(b));
+        float ms = 0.f;
+        GASB_CUDA(cudaEventElapsedTime(&ms, a, b));
+        *avg_ms = ms / static_cast<float>(iters);
+        cudaEventDestroy(a);
+        cudaEventDestroy(b);
+    });
+}
+
+gasb_status gasb_host_register(void* h, size_t bytes) {
+    return guard([&] { GASB_CUDA(cudaHostRegister(h, bytes, cudaHostRegisterDefault)); });
+}
+
+gasb_status gasb_host_unregister(void* h) {
+    return guard([&] { GASB_CUDA(cudaHostUnregister(h)); });
 }
 
 gasb_status gasb_trainer_launch_count(gasb_trainer t, int64_t* out) {

@@ -7,7 +7,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from ._native import ModelSpecC, TrainerOptionsC, check, f64, i32, i64, lib, ptr, vp
+from ._native import ModelSpecC, TrainerOptionsC, check, f64, i32, i64, lib, ptr, vp  # noqa: F401
 from .graph import BatchSchedule
 from .history import HistoryStore
 
@@ -119,6 +119,15 @@ class GasTrainer:
         check(lib.gasb_trainer_batch(self._h, int(part), int(epoch), int(train), int(push), ptr(acts) if acts.size else
                                      None, ptr(logits), C.byref(loss), ptr(grads), C.byref(stepped)))
         return acts, logits, loss.value, (grads if stepped.value else None), bool(stepped.value)
+
+    def set_features(self, features: np.ndarray) -> None:
+        x = np.ascontiguousarray(features, dtype=np.float32)
+        check(lib.gasb_trainer_set_features(self._h, ptr(x)))
+
+    def profile_spmm(self, part: int, layer: int, iters: int = 5) -> float:
+        ms = C.c_float()
+        check(lib.gasb_trainer_profile_spmm(self._h, int(part), int(layer), int(iters), C.byref(ms)))
+        return ms.value
 
     def get_params(self) -> np.ndarray:
         out = np.empty(self.num_param_floats, np.float32)

@@ -1,0 +1,138 @@
+"""History store in HBM vs the reference HistoryStore semantics (history.cpp:10-178).
+SPEC.md:364-398 examples: fresh store = zeros, push-then-pull identity, overwrite,
+stamps, layer range errors, prefetch == synchronous pull."""
+import numpy as np
+import pytest
+
+import paper_2106_05609_b200 as gb
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def torch():
+    import torch
+    assert torch.cuda.is_available()
+    return torch
+
+
+def test_fresh_store_is_zero_and_push_pull_identity():
+    h = gb.HistoryStore(2, 50, 7)
+    assert np.array_equal(h.pull(1, [3, 4, 49]), np.zeros((3, 7), np.float32))
+    rows = np.arange(21, dtype=np.float32).reshape(3, 7)
+    h.push(1, [4, 9, 0], rows)
+    assert np.array_equal(h.pull(1, [0, 4, 9]), rows[[2, 0, 1]])
+    h.push(1, [9], rows[:1] + 100)  # second value wins
+    assert np.array_equal(h.pull(1, [9])[0], rows[0] + 100)
+    assert np.array_equal(h.pull(2, [4]), np.zeros((1, 7), np.float32))
+    assert h.pull(1, []).shape == (0, 7)
+
+
+def test_stamps_and_steps(ref):
+    h = gb.HistoryStore(1, 10, 4)
+    r = ref.lib
+    import ctypes as C
+    rh = C.c_void_p()
+    ref.check(r.ref_history_create(1, 10, 4, C.byref(rh)))
+    for step in range(3):
+        ids = np.array([step, step + 3], np.int32)
+        rows = np.full((2, 4), step, np.float32)
+        h.push(1, ids, rows)
+        ref.check(r.ref_history_push(rh, 1, ids.ctypes.data, 2, rows.ctypes.data))
+        h.advance_step()
+        r.ref_history_advance(rh)
+    assert h.step() == 3
+    for v in range(10):
+        s = C.c_int64()
+        ref.check(r.ref_history_stamp(rh, 1, v, C.byref(s)))
+        assert h.last_push_step(1, v) == s.value
+    full = np.zeros((10, 4), np.float32)
+    ref.check(r.ref_history_layer(rh, 1, full.ctypes.data))
+    assert np.array_equal(h.layer_matrix(1), full)
+    h.reset()
+    assert h.step() == 0 and h.last_push_step(1, 0) == -1 and not h.layer_matrix(1).any()
+    r.ref_history_free(rh)
+
+
+def test_errors_match_reference():
+    h = gb.HistoryStore(2, 10, 3)
+    for bad_layer in (0, 3):
+        with pytest.raises(ValueError):
+            h.pull(bad_layer, [1])
+        with pytest.raises(ValueError):
+            h.push(bad_layer, [1], np.zeros((1, 3), np.float32))
+    with pytest.raises(ValueError):
+        h.pull(1, [10])
+    with pytest.raises(ValueError):
+        h.push(1, [1, 2], np.zeros((1, 3), np.float32))  # row count mismatch
+    with pytest.raises(ValueError):
+        h.fill_layer(1, np.zeros((9, 3), np.float32))
+
+
+def test_device_push_pull_large_bit_exact(torch):
+    n, d = 200_000, 256
+    h = gb.HistoryStore(3, n, d)
+    rng = np.random.default_rng(0)
+    ids = np.sort(rng.choice(n, 60_000, replace=False)).astype(np.int32)
+    rows = torch.randn(len(ids), d, device="cuda")
+    d_ids = torch.from_numpy(ids).cuda()
+    h.push_device(2, d_ids, len(ids), rows, d)
+    halo = torch.from_numpy(rng.choice(n, 150_000).astype(np.int32)).cuda()
+    out = torch.empty(len(halo), d, device="cuda")
+    h.pull_device(2, halo, len(halo), out, d)
+    torch.cuda.synchronize()
+    h.check()
+    table = torch.zeros(n, d, device="cuda")
+    table[d_ids.long()] = rows
+    assert torch.equal(out, table[halo.long()])
+
+
+def test_device_bad_id_latches_error(torch):
+    h = gb.HistoryStore(1, 10, 4)
+    ids = torch.tensor([1, 11], dtype=torch.int32, device="cuda")
+    out = torch.zeros(2, 4, device="cuda")
+    h.pull_device(1, ids, 2, out, 4)
+    with pytest.raises(ValueError):
+        h.check()
+    h.check()  # latch cleared
+
+
+def test_odd_dim_scalar_path(torch):
+    h = gb.HistoryStore(1, 100, 47)
+    ids = np.arange(0, 100, 3, dtype=np.int32)
+    rows = np.random.default_rng(1).standard_normal((len(ids), 47)).astype(np.float32)
+    h.push(1, ids, rows)
+    assert np.array_equal(h.pull(1, ids[::-1]), rows[::-1])
+
+
+def test_prefetch_snapshot(torch):
+    n, d = 5000, 64
+    h = gb.HistoryStore(3, n, d)
+    vals = [np.random.default_rng(l).standard_normal((n, d)).astype(np.float32) for l in range(3)]
+    for l in range(3):
+        h.fill_layer(l + 1, vals[l])
+    assert h.last_push_step(2, 17) == 0  # fill_layer stamps every row with the current step
+    pf = gb.Prefetcher(h)
+    halo_np = np.random.default_rng(9).choice(n, 1234).astype(np.int32)
+    halo = torch.from_numpy(halo_np).cuda()
+    s = torch.cuda.Stream()
+    handle = pf.begin(halo, len(halo), s)
+    for l in (1, 2, 3):
+        p, ld = handle.wait(l)
+        s.synchronize()
+        snap = _device_to_numpy(torch, p, len(halo), ld)[:, :d]
+        assert np.array_equal(snap, vals[l - 1][halo_np])
+    with pytest.raises(ValueError):
+        handle.wait(4)
+    pf.begin(halo, len(halo), s)
+    with pytest.raises(RuntimeError):
+        handle.wait(1)  # stale generation -> logic_error
+
+
+def _device_to_numpy(torch, ptr, rows, ld):
+    import ctypes
+    out = np.empty((rows, ld), np.float32)
+    cudart = ctypes.CDLL("/usr/local/cuda/lib64/libcudart.so.12")
+    cudart.cudaMemcpy.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int]
+    assert cudart.cudaMemcpy(out.ctypes.data, ptr, out.nbytes, 2) == 0
+    return out

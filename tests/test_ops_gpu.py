@@ -1,0 +1,130 @@
+"""Message-passing and transform kernels vs the CPU oracle (restating src/tensor.cpp).
+
+aggregate forward: bit-exact in sequential mode (seg_edges=0) and in segmented mode on
+these inputs (fp64 partial combination differs from sequential fp64 only below fp32
+resolution; the test tolerates a vanishing fraction of 1-ulp differences).
+aggregate backward: bit-exact (fp32 multiply-then-add in the reference's scatter order).
+matmul: fp32 accumulation vs the reference's fp64 -> <= 1e-6 normwise (stated tolerance).
+"""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+import paper_2106_05609_b200 as gb
+from paper_2106_05609_b200._native import check, lib
+
+from conftest import normwise
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def torch():
+    import torch
+    assert torch.cuda.is_available()
+    return torch
+
+
+@pytest.fixture(scope="module")
+def hub_plan():
+    """A batch of a power-law graph with hub rows (degree >> segment size)."""
+    edges, comm = gb.synth_pairs(20000, 400_000, 20, 0.3, gamma=2.2, min_weight=1.0, max_weight=400.0, seed=3)
+    g = gb.build_graph(edges, 20000)
+    parts = gb.partition_parts(comm, 20)
+    p = gb.make_batch_plan(g, parts[4], full=False)
+    assert np.diff(p.gcn_row_ptr).max() > 1000
+    return p
+
+
+def _dev(torch, a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+@pytest.mark.parametrize("d", [16, 47, 64, 256, 602])
+@pytest.mark.parametrize("seg", [0, 64])
+def test_aggregate_forward(torch, oracle, hub_plan, d, seg):
+    p = hub_plan
+    rng = np.random.default_rng(d)
+    ne, nb = len(p.extended_nodes), len(p.batch_nodes)
+    x = rng.standard_normal((ne, d)).astype(np.float32)
+    ld = (d + 3) // 4 * 4  # source rows 16 B aligned
+    xp = np.zeros((ne, ld), np.float32)
+    xp[:, :d] = x
+    want = oracle.aggregate(p.gcn_row_ptr, p.gcn_cols, p.gcn_coeffs, x)
+    d_rp = _dev(torch, p.gcn_row_ptr.astype(np.int32))
+    d_cols, d_cf, d_x = _dev(torch, p.gcn_cols), _dev(torch, p.gcn_coeffs), _dev(torch, xp)
+    d_y = torch.zeros(nb, ld, device="cuda")
+    check(lib.gasb_spmm_fwd(d_rp.data_ptr(), nb, d_cols.data_ptr(), d_cf.data_ptr(), d_x.data_ptr(), ne, ld, d,
+                            d_y.data_ptr(), ld, seg, None))
+    got = d_y.cpu().numpy()[:, :d]
+    mism = int((got != want).sum())
+    if seg == 0:
+        assert mism == 0
+    else:
+        assert mism <= max(2, want.size // 100000), mism
+        assert normwise(got, want) < 1e-7
+
+
+@pytest.mark.parametrize("special", [False, True])
+def test_aggregate_forward_zeros_and_denormals(torch, oracle, hub_plan, special):
+    """Sparse (relu-like) inputs take the integer widening path; a table holding a denormal
+    switches to the exact F2F path — bit-exact either way."""
+    p = hub_plan
+    rng = np.random.default_rng(7)
+    ne, nb, d = len(p.extended_nodes), len(p.batch_nodes), 64
+    x = np.maximum(rng.standard_normal((ne, d)), 0).astype(np.float32)
+    x[0, 1] = -0.0
+    if special:
+        x[3, 5] = np.float32(1e-40)  # denormal
+        x[7, 9] = -np.float32(3e-39)
+    want = oracle.aggregate(p.gcn_row_ptr, p.gcn_cols, p.gcn_coeffs, x)
+    d_rp = _dev(torch, p.gcn_row_ptr.astype(np.int32))
+    d_cols, d_cf, d_x = _dev(torch, p.gcn_cols), _dev(torch, p.gcn_coeffs), _dev(torch, x)
+    d_y = torch.zeros(nb, d, device="cuda")
+    check(lib.gasb_spmm_fwd(d_rp.data_ptr(), nb, d_cols.data_ptr(), d_cf.data_ptr(), d_x.data_ptr(), ne, d, d,
+                            d_y.data_ptr(), d, 0, None))
+    assert np.array_equal(d_y.cpu().numpy(), want)
+
+
+@pytest.mark.parametrize("d", [16, 64, 256])
+def test_aggregate_backward_bit_exact(torch, oracle, hub_plan, d):
+    p = hub_plan
+    rng = np.random.default_rng(100 + d)
+    ne, nb = len(p.extended_nodes), len(p.batch_nodes)
+    gy = rng.standard_normal((nb, d)).astype(np.float32)
+    x = np.zeros((ne, d), np.float32)
+    _, want = oracle.aggregate(p.gcn_row_ptr, p.gcn_cols, p.gcn_coeffs, x, gy)
+    # transposed stencil over all V_b targets, entries in ascending dst row (stable sort)
+    rows = np.repeat(np.arange(nb, dtype=np.int32), np.diff(p.gcn_row_ptr))
+    order = np.argsort(p.gcn_cols, kind="stable")
+    t_src, t_cf = rows[order], p.gcn_coeffs[order]
+    t_rp = np.zeros(ne + 1, np.int32)
+    t_rp[1:] = np.cumsum(np.bincount(p.gcn_cols, minlength=ne))
+    d_gy = _dev(torch, gy)
+    d_gx = torch.zeros(ne, d, device="cuda")
+    d_rp, d_src, d_cf = _dev(torch, t_rp), _dev(torch, t_src), _dev(torch, t_cf)  # keep alive across the call
+    check(lib.gasb_spmm_bwd(d_rp.data_ptr(), ne, d_src.data_ptr(), d_cf.data_ptr(), d_gy.data_ptr(), d, nb, d, None, 0,
+                            d_gx.data_ptr(), d, None))
+    assert np.array_equal(d_gx.cpu().numpy(), want)
+
+
+@pytest.mark.parametrize("m,k,n", [(1165, 602, 256), (1165, 256, 41), (271, 1433, 16), (37, 5, 3)])
+def test_matmul_forward_backward(torch, oracle, m, k, n):
+    rng = np.random.default_rng(m + k + n)
+    a = rng.standard_normal((m, k)).astype(np.float32)
+    a[a < -1.5] = 0.0
+    b = (rng.standard_normal((k, n)) * 0.1).astype(np.float32)
+    gy = rng.standard_normal((m, n)).astype(np.float32)
+    y, ga, gbw = oracle.matmul(a, b, gy)
+    da, db, dg = _dev(torch, a), _dev(torch, b), _dev(torch, gy)
+    dy = torch.empty(m, n, device="cuda")
+    dga = torch.empty(m, k, device="cuda")
+    dgb = torch.empty(k, n, device="cuda")
+    check(lib.gasb_gemm(0, m, n, k, da.data_ptr(), k, db.data_ptr(), n, dy.data_ptr(), n, 0.0, None))
+    check(lib.gasb_gemm(1, m, k, n, dg.data_ptr(), n, db.data_ptr(), n, dga.data_ptr(), k, 0.0, None))
+    check(lib.gasb_gemm(2, k, n, m, da.data_ptr(), k, dg.data_ptr(), n, dgb.data_ptr(), n, 0.0, None))
+    torch.cuda.synchronize()
+    assert normwise(dy.cpu().numpy(), y) < 1e-6
+    assert normwise(dga.cpu().numpy(), ga) < 1e-6
+    assert normwise(dgb.cpu().numpy(), gbw) < 1e-6

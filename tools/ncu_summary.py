@@ -1,0 +1,30 @@
+"""Key per-kernel counters from an ncu report: python tools/ncu_summary.py rep.ncu-rep"""
+import csv
+import io
+import subprocess
+import sys
+
+KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum", "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
+        "lts__throughput.avg.pct_of_peak_sustained_elapsed", "l1tex__throughput.avg.pct_of_peak_sustained_active",
+        "sm__throughput.avg.pct_of_peak_sustained_elapsed", "sm__warps_active.avg.pct_of_peak_sustained_active",
+        "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active", "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active",
+        "lts__t_sector_hit_rate.pct", "launch__registers_per_thread", "launch__grid_size", "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
+        "smsp__inst_executed.sum"]
+out = subprocess.run(["ncu", "-i", sys.argv[1], "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+rows = list(csv.reader(io.StringIO(out)))
+hdr, units = rows[0], rows[1]
+for r in rows[2:]:
+    print("==", r[hdr.index("Kernel Name")][:70])
+    for k in KEYS:
+        if k in hdr:
+            print(f"   {k:70s} {r[hdr.index(k)]:>16s} {units[hdr.index(k)]}")
+    stalls = [(h, r[i]) for i, h in enumerate(hdr) if h.startswith("smsp__average_warp_latency_issue_stalled") or
+              h.startswith("smsp__pcsamp_warps_issue_stalled")]
+    vals = []
+    for h, v in stalls:
+        try:
+            vals.append((float(v.replace(",", "")), h))
+        except ValueError:
+            pass
+    for v, h in sorted(vals, reverse=True)[:6]:
+        print(f"   {h:70s} {v:16.1f}")
