@@ -2,6 +2,8 @@
 // between translation units; the kernels live in history.cu, spmm.cu, gemm.cu, train_ops.cu.
 #pragma once
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -53,14 +55,23 @@ struct SpmmSegs {
     const int32_t* seg_slot;  // nseg: partial slot or -1 (single-segment row)
     const int32_t* row_seg0;  // per absolute row: first segment index (only multi-seg rows)
     const int32_t* row_nseg;  // per absolute row: number of segments
-    int64_t nseg;
-    int64_t seg_base;         // absolute index of this launch's first segment
+    const int32_t* range_seg; // nranges + 1 segment boundaries of this launch (split_ranges)
+    int32_t nranges;
 };
+// Host: splits segments [g0, g1) into nranges contiguous ranges of ~equal edges.
+void split_ranges(const int64_t* seg_beg, int64_t g0, int64_t g1, int32_t nranges, int32_t* out);
+// Work ranges per SpMM launch: 8 resident warps per SM (2 CTAs of 4).
+int32_t spmm_ranges_per_launch();
 // coeffs: stencil coefficients as fp64 pre-multiplied by kCoeffScale. special: the source
 // table's flag word (kTableNeg / kTableNonFinite); nullptr = assume anything (exact F2F).
+// tmap (optional): tensor map of x for TMA tile::gather4 staging (make_row_tmap with
+// box_cols = spmm_box_cols()); nullptr = cp.async staging.
 void launch_spmm_fwd(const SpmmSegs& s, const int32_t* cols, const double* coeffs, const float* x, int64_t ldx,
                      int32_t dim, float* y, int64_t ldy, int64_t row_base, double* partial, int64_t partial_ld,
-                     int32_t* counters, int32_t counters_ld, cudaStream_t st, const int32_t* special = nullptr);
+                     int32_t* counters, int32_t counters_ld, cudaStream_t st, const int32_t* special = nullptr,
+                     const CUtensorMap* tmap = nullptr);
+bool make_row_tmap(const float* base, int64_t rows, int32_t dim, int64_t ld, int32_t box_cols, CUtensorMap* out);
+int32_t spmm_box_cols();
 // special[0] |= table_flag_of(v) over the values v of x[rows x dim] (pitch ld).
 void launch_scan_special(const float* x, int64_t rows, int64_t ld, int32_t dim, int32_t* special, cudaStream_t st);
 // Transposed (CSC) gather, fp32 multiply-then-add in entry order (bit-exact with the

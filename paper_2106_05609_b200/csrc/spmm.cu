@@ -77,163 +77,375 @@ struct PipeCfg {
     static constexpr int kEdges = kStageDataBytes / (kCols * 4);  // edges per stage (32 | 16)
     static constexpr int kPieces = kCols / 4;                     // 16 B pieces per row slice
     static constexpr int kRowsPerIssue = 32 / kPieces;            // rows per LDGSTS instruction
-    static constexpr int kStageBytes = kStageDataBytes + kEdges * 8;
+    static constexpr int kHdrBytes = 16;                          // stage descriptor
+    // 128 B aligned: TMA destinations must be 128 B aligned
+    static constexpr int kStageBytes = (kStageDataBytes + kEdges * 8 + kHdrBytes + 127) / 128 * 128;
     static constexpr int kSmem = kPipeWarps * kStages * kStageBytes;
 };
 
-// One stage of FMAs: rows of the stage in CSR order, CPL fp64 accumulators per lane.
+// Stage descriptor (shared memory): edges of ONE segment, so the FMA loop needs no
+// boundary tests; `ends` marks the segment's last stage (then it is finalized).
+struct StageHdr {
+    int32_t cnt, ends, row, slot;
+};
+
+// All KE edges of a stage (predicated on j < cnt, warp-uniform), CSR order, CPL fp64
+// accumulators per lane.
 template <int CPL, int MODE>
-__device__ __forceinline__ void stage_fma(const float* rows, const double* cf, int cnt, double (&acc)[CPL]) {
+__device__ __forceinline__ void edge_fma(const float* rows, const double* cf, int j, double (&acc)[CPL]) {
     constexpr int kCols = 32 * CPL;
-#pragma unroll 8
-    for (int j = 0; j < cnt; ++j) {
-        const double c = cf[j];
-        if constexpr (CPL == 4) {
-            const float4 v = *reinterpret_cast<const float4*>(rows + j * kCols);
-            acc[0] = __fma_rn(c, widen_scaled<MODE>(v.x), acc[0]);
-            acc[1] = __fma_rn(c, widen_scaled<MODE>(v.y), acc[1]);
-            acc[2] = __fma_rn(c, widen_scaled<MODE>(v.z), acc[2]);
-            acc[3] = __fma_rn(c, widen_scaled<MODE>(v.w), acc[3]);
-        } else {
-            const float2 v = *reinterpret_cast<const float2*>(rows + j * kCols);
-            acc[0] = __fma_rn(c, widen_scaled<MODE>(v.x), acc[0]);
-            acc[1] = __fma_rn(c, widen_scaled<MODE>(v.y), acc[1]);
-        }
+    const double c = cf[j];
+    if constexpr (CPL == 4) {
+        const float4 v = *reinterpret_cast<const float4*>(rows + j * kCols);
+        acc[0] = __fma_rn(c, widen_scaled<MODE>(v.x), acc[0]);
+        acc[1] = __fma_rn(c, widen_scaled<MODE>(v.y), acc[1]);
+        acc[2] = __fma_rn(c, widen_scaled<MODE>(v.z), acc[2]);
+        acc[3] = __fma_rn(c, widen_scaled<MODE>(v.w), acc[3]);
+    } else {
+        const float2 v = *reinterpret_cast<const float2*>(rows + j * kCols);
+        acc[0] = __fma_rn(c, widen_scaled<MODE>(v.x), acc[0]);
+        acc[1] = __fma_rn(c, widen_scaled<MODE>(v.y), acc[1]);
     }
 }
 
-// coeffs are the stencil coefficients pre-scaled by 2^896 (see widen_scaled).
-template <int CPL>
+template <int CPL, int MODE, int KE>
+__device__ __forceinline__ void stage_fma(const float* rows, const double* cf, int cnt, double (&acc)[CPL]) {
+    if (cnt == KE) {  // full stage (the common case): straight-line code, loads hoisted freely
+#pragma unroll
+        for (int j = 0; j < KE; ++j) edge_fma<CPL, MODE>(rows, cf, j, acc);
+    } else {
+#pragma unroll 4
+        for (int j = 0; j < cnt; ++j) edge_fma<CPL, MODE>(rows, cf, j, acc);
+    }
+}
+
+// Persistent streaming SpMM. The launch's segments are pre-split (host) into `nranges`
+// contiguous ranges of ~equal edge count (range_seg[r] .. range_seg[r+1]); work item =
+// (chunk, range), chunk-major, handed to warps grid-stride. A warp streams its range as a
+// sequence of stages of <= KE edges of a single segment through the cp.async pipeline
+// (kStages deep, no drain at row boundaries); after a segment's last stage it stores the
+// row, or publishes an fp64 partial and the last-arriving warp of the row combines the
+// partials in segment order. coeffs are pre-scaled by 2^896 (see widen_scaled).
+// ---- TMA (tile::gather4) + mbarrier helpers ----
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+// Bounded wait: a barrier that never completes traps instead of hanging the GPU.
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    for (uint32_t spins = 0;; ++spins) {
+        uint32_t done;
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(done)
+            : "r"(smem_u32(bar)), "r"(parity)
+            : "memory");
+        if (done) return;
+        if (spins > (1u << 26)) __trap();
+    }
+}
+// 4 rows x box-width columns of a 2-D row-major table -> shared memory (rows contiguous);
+// out-of-range rows / columns are zero-filled; completes `bytes` on the mbarrier.
+__device__ __forceinline__ void tma_gather4(void* dst, const CUtensorMap* tm, int32_t c0, int32_t r0, int32_t r1,
+                                            int32_t r2, int32_t r3, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];\n" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(smem_u32(bar))
+        : "memory");
+}
+
+template <int CPL, bool TMA>
 __global__ void __launch_bounds__(kPipeWarps * 32, 2) spmm_fwd_pipe_kernel(
     const int64_t* __restrict__ seg_beg, const int32_t* __restrict__ seg_row, const int32_t* __restrict__ seg_slot,
-    const int32_t* __restrict__ row_seg0, const int32_t* __restrict__ row_nseg, int64_t nseg, int64_t seg_base,
-    const int32_t* __restrict__ cols, const double* __restrict__ coeffs, const float* __restrict__ x, int64_t ldx,
-    int32_t dim, int32_t nchunks, float* __restrict__ y, int64_t ldy, int64_t row_base, double* __restrict__ partial,
-    int64_t pld, int32_t* __restrict__ counters, int32_t cld, const int32_t* __restrict__ table_flags) {
+    const int32_t* __restrict__ row_seg0, const int32_t* __restrict__ row_nseg, const int32_t* __restrict__ range_seg,
+    int32_t nranges, const int32_t* __restrict__ cols, const double* __restrict__ coeffs, const float* __restrict__ x,
+    int64_t ldx, int32_t dim, int32_t nchunks, float* __restrict__ y, int64_t ldy, int64_t row_base,
+    double* __restrict__ partial, int64_t pld, int32_t* __restrict__ counters, int32_t cld,
+    const int32_t* __restrict__ table_flags, const __grid_constant__ CUtensorMap tmap) {
     using Cfg = PipeCfg<CPL>;
     constexpr int KE = Cfg::kEdges;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
+    extern __shared__ __align__(128) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int64_t w = static_cast<int64_t>(blockIdx.x) * kPipeWarps + warp;
-    if (w >= nseg * nchunks) return;  // warps are independent: no block-wide barriers below
+    const int64_t nwarps = static_cast<int64_t>(gridDim.x) * kPipeWarps;
     const int mode = widen_mode(table_flags);
     unsigned char* wbase = smem_raw + static_cast<size_t>(warp) * kStages * Cfg::kStageBytes;
-    const int32_t chunk = static_cast<int32_t>(w / nseg);
-    const int64_t s = seg_base + (w - static_cast<int64_t>(chunk) * nseg);
-    const int32_t col = chunk * Cfg::kCols + lane * CPL;
-    const bool active = col < dim;
-    const int64_t e0 = seg_beg[s], e1 = seg_beg[s + 1];
-    const int nblk = static_cast<int>((e1 - e0 + KE - 1) / KE);
     const int rsub = lane / Cfg::kPieces, q = lane % Cfg::kPieces;
-    const int32_t colq = chunk * Cfg::kCols + q * 4;  // first float of this lane's 16 B piece
-    const bool qok = colq + 4 <= ldx;                 // pieces past the row pitch are zero-filled
-
-    auto issue = [&](int b, int32_t mc, double mf) {
-        unsigned char* st = wbase + (b % kStages) * Cfg::kStageBytes;
-        float* rows = reinterpret_cast<float*>(st);
-        if (lane < KE) reinterpret_cast<double*>(st + kStageDataBytes)[lane] = mf;
-#pragma unroll
-        for (int i = 0; i < KE / Cfg::kRowsPerIssue; ++i) {
-            const int j = i * Cfg::kRowsPerIssue + rsub;
-            const int32_t c = __shfl_sync(0xffffffffu, mc, j);
-            const bool ok = c >= 0 && qok;
-            const float* src = ok ? x + static_cast<int64_t>(c) * ldx + colq : x;
-            cp_async16(rows + j * Cfg::kCols + q * 4, src, ok ? 16 : 0);
+    // TMA: one mbarrier per stage slot (after all stage buffers), phase bit per slot
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + kPipeWarps * kStages * Cfg::kStageBytes) + warp * kStages;
+    uint32_t phases = 0;
+    if constexpr (TMA) {
+        if (lane == 0) {
+            asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
+            for (int k = 0; k < kStages; ++k) mbar_init(bars + k, 1);
+            asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
         }
-    };
-    auto meta = [&](int b, int32_t& mc, double& mf) {
-        const int64_t e = e0 + static_cast<int64_t>(KE) * b + lane;
-        const bool ok = lane < KE && e < e1;
-        mc = ok ? __ldg(cols + e) : -1;
-        mf = ok ? __ldg(coeffs + e) : 0.0;
-    };
-
-    int32_t mc;
-    double mf;
-#pragma unroll
-    for (int b = 0; b < kStages; ++b) {
-        if (b < nblk) {
-            meta(b, mc, mf);
-            issue(b, mc, mf);
-        }
-        cp_async_commit();
+        __syncwarp();
     }
-    int32_t nc = -1;
-    double nf = 0.0;
-    if (kStages < nblk) meta(kStages, nc, nf);
-    double acc[CPL];
+    for (int64_t item = static_cast<int64_t>(blockIdx.x) * kPipeWarps + warp;
+         item < static_cast<int64_t>(nchunks) * nranges; item += nwarps) {
+        const int32_t chunk = static_cast<int32_t>(item / nranges);
+        const int32_t r = static_cast<int32_t>(item - static_cast<int64_t>(chunk) * nranges);
+        const int32_t s_lo = range_seg[r], s_hi = range_seg[r + 1];
+        if (s_lo >= s_hi) continue;
+        const int32_t col = chunk * Cfg::kCols + lane * CPL;
+        const int32_t colq = chunk * Cfg::kCols + q * 4;  // first float of this lane's 16 B piece
+        const bool qok = colq + 4 <= ldx;                 // pieces past the row pitch are zero-filled
+
+        // ---- issue-side cursor over the range's segments (window of 32 segment records)
+        int32_t iseg = s_lo, wbase_seg = s_lo, w_row = 0, w_slot = -1;
+        int64_t ipos = seg_beg[s_lo], w_end = 0;
+        auto load_window = [&](int32_t from) {
+            wbase_seg = from;
+            const int32_t sg = from + lane;
+            w_end = sg < s_hi ? seg_beg[sg + 1] : 0;
+            w_row = sg < s_hi ? seg_row[sg] : 0;
+            w_slot = sg < s_hi ? seg_slot[sg] : -1;
+        };
+        load_window(s_lo);
+        // describe the next stage (edges [ipos, ipos + cnt) of segment iseg) and advance
+        auto next_stage = [&](StageHdr& h, int64_t& e_first) -> bool {
+            if (iseg >= s_hi) return false;
+            if (iseg - wbase_seg >= 32) load_window(iseg);
+            const int k = iseg - wbase_seg;
+            const int64_t end = __shfl_sync(0xffffffffu, w_end, k);
+            const int64_t c = end - ipos < KE ? end - ipos : KE;
+            h.cnt = static_cast<int32_t>(c);
+            h.ends = ipos + c == end;
+            h.row = __shfl_sync(0xffffffffu, w_row, k);
+            h.slot = __shfl_sync(0xffffffffu, w_slot, k);
+            e_first = ipos;
+            ipos += c;
+            if (h.ends) ++iseg;
+            return true;
+        };
+        auto meta = [&](const StageHdr& h, int64_t e_first, int32_t& mc, double& mf) {
+            const bool ok = lane < h.cnt;
+            mc = ok ? __ldg(cols + e_first + lane) : -1;
+            mf = ok ? __ldg(coeffs + e_first + lane) : 0.0;
+        };
+        auto issue = [&](int slot_idx, const StageHdr& h, int32_t mc, double mf) {
+            unsigned char* st = wbase + slot_idx * Cfg::kStageBytes;
+            float* rows = reinterpret_cast<float*>(st);
+            if (lane < KE) reinterpret_cast<double*>(st + kStageDataBytes)[lane] = mf;
+            if (lane == 0) *reinterpret_cast<StageHdr*>(st + kStageDataBytes + KE * 8) = h;
+            if constexpr (TMA) {
+                // rows of stage i go to rows + i*kCols; unused slots (mc = -1) are zero-filled
+                const int ng = (h.cnt + 3) >> 2;
+                if (lane == 0) {
+                    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // after the warp's reads
+                    mbar_expect_tx(bars + slot_idx, static_cast<uint32_t>(ng) * 4u * Cfg::kCols * 4u);
+                }
 #pragma unroll
-    for (int k = 0; k < CPL; ++k) acc[k] = 0.0;
-    for (int b = 0; b < nblk; ++b) {
-        cp_async_wait<kStages - 1>();
-        __syncwarp();
-        const unsigned char* st = wbase + (b % kStages) * Cfg::kStageBytes;
-        const float* rows = reinterpret_cast<const float*>(st) + lane * CPL;
-        const double* cf = reinterpret_cast<const double*>(st + kStageDataBytes);
-        const int64_t rem = e1 - e0 - static_cast<int64_t>(KE) * b;
-        const int cnt = static_cast<int>(rem < KE ? rem : KE);
-        if (active) {
-            if (mode == kWidenNonNeg) stage_fma<CPL, kWidenNonNeg>(rows, cf, cnt, acc);
-            else if (mode == kWidenSigned) stage_fma<CPL, kWidenSigned>(rows, cf, cnt, acc);
-            else stage_fma<CPL, kWidenF2F>(rows, cf, cnt, acc);
+                for (int i = 0; i < KE / 4; ++i) {
+                    if (i < ng) {  // warp-uniform
+                        const int32_t r0 = __shfl_sync(0xffffffffu, mc, 4 * i + 0);
+                        const int32_t r1 = __shfl_sync(0xffffffffu, mc, 4 * i + 1);
+                        const int32_t r2 = __shfl_sync(0xffffffffu, mc, 4 * i + 2);
+                        const int32_t r3 = __shfl_sync(0xffffffffu, mc, 4 * i + 3);
+                        if (lane == 0)
+                            tma_gather4(rows + 4 * i * Cfg::kCols, &tmap, chunk * Cfg::kCols, r0, r1, r2, r3,
+                                        bars + slot_idx);
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int i = 0; i < KE / Cfg::kRowsPerIssue; ++i) {
+                    const int j = i * Cfg::kRowsPerIssue + rsub;
+                    if (i * Cfg::kRowsPerIssue < h.cnt) {  // warp-uniform
+                        const int32_t c = __shfl_sync(0xffffffffu, mc, j);
+                        const bool ok = c >= 0 && qok;
+                        const float* src = ok ? x + static_cast<int64_t>(c) * ldx + colq : x;
+                        cp_async16(rows + j * Cfg::kCols + q * 4, src, ok ? 16 : 0);
+                    }
+                }
+            }
+        };
+
+        // ---- prologue: up to kStages stages in flight, metadata of the next one prefetched
+        int issued = 0;
+        StageHdr nh;
+        int64_t ne_first = 0;
+        int32_t nmc = -1;
+        double nmf = 0.0;
+        bool have_next = next_stage(nh, ne_first);
+        if (have_next) meta(nh, ne_first, nmc, nmf);
+#pragma unroll
+        for (int k = 0; k < kStages; ++k) {
+            if (have_next) {
+                issue(k, nh, nmc, nmf);
+                ++issued;
+                have_next = next_stage(nh, ne_first);
+                if (have_next) meta(nh, ne_first, nmc, nmf);
+            }
+            if constexpr (!TMA) cp_async_commit();
         }
-        __syncwarp();
-        const int bn = b + kStages;
-        if (bn < nblk) issue(bn, nc, nf);
-        cp_async_commit();
-        if (bn + 1 < nblk) meta(bn + 1, nc, nf);
-    }
-    cp_async_wait<0>();
-    const int32_t row = seg_row[s];
-    const int32_t slot = seg_slot[s];
-    float* yr = y + (static_cast<int64_t>(row) - row_base) * ldy;
-    if (slot >= 0) {  // multi-segment row: publish the fp64 partial, last arriving warp combines
-        double* pp = partial + static_cast<int64_t>(slot) * pld + col;
-#pragma unroll
-        for (int k = 0; k < CPL; ++k) pp[k] = acc[k];
-        __threadfence();
-        __syncwarp();
-        int last = 0;
-        const int32_t nk = row_nseg[row];
-        if (lane == 0) last = atomicAdd(counters + static_cast<int64_t>(row) * cld + chunk, 1) == nk - 1;
-        last = __shfl_sync(0xffffffffu, last, 0);
-        if (!last) return;
-        __threadfence();
-        const int32_t s0 = row_seg0[row];
+        double acc[CPL];
 #pragma unroll
         for (int k = 0; k < CPL; ++k) acc[k] = 0.0;
-        for (int32_t i = 0; i < nk; ++i) {
-            const double* q2 = partial + static_cast<int64_t>(seg_slot[s0 + i]) * pld + col;
+        for (int b = 0; b < issued; ++b) {
+            if constexpr (TMA) {
+                const int sl = b % kStages;
+                mbar_wait(bars + sl, (phases >> sl) & 1u);
+                phases ^= 1u << sl;
+            } else {
+                cp_async_wait<kStages - 1>();
+            }
+            __syncwarp();
+            const unsigned char* st = wbase + (b % kStages) * Cfg::kStageBytes;
+            const float* rows = reinterpret_cast<const float*>(st) + lane * CPL;
+            const double* cf = reinterpret_cast<const double*>(st + kStageDataBytes);
+            const StageHdr h = *reinterpret_cast<const StageHdr*>(st + kStageDataBytes + KE * 8);
+            if (mode == kWidenNonNeg) stage_fma<CPL, kWidenNonNeg, KE>(rows, cf, h.cnt, acc);
+            else if (mode == kWidenSigned) stage_fma<CPL, kWidenSigned, KE>(rows, cf, h.cnt, acc);
+            else stage_fma<CPL, kWidenF2F, KE>(rows, cf, h.cnt, acc);
+            __syncwarp();
+            if (have_next) {  // refill the slot just consumed
+                issue(b % kStages, nh, nmc, nmf);
+                ++issued;
+                have_next = next_stage(nh, ne_first);
+                if (have_next) meta(nh, ne_first, nmc, nmf);
+            }
+            if constexpr (!TMA) cp_async_commit();
+            if (h.ends) {  // end of segment: store the row, or publish the partial and combine
+                float* yr = y + (static_cast<int64_t>(h.row) - row_base) * ldy;
+                bool store = true;
+                if (h.slot >= 0) {
+                    double* pp = partial + static_cast<int64_t>(h.slot) * pld + col;
 #pragma unroll
-            for (int k = 0; k < CPL; ++k) acc[k] += __ldcg(q2 + k);
+                    for (int k = 0; k < CPL; ++k) pp[k] = acc[k];
+                    __threadfence();
+                    __syncwarp();
+                    int last = 0;
+                    const int32_t nk = row_nseg[h.row];
+                    if (lane == 0)
+                        last = atomicAdd(counters + static_cast<int64_t>(h.row) * cld + chunk, 1) == nk - 1;
+                    store = __shfl_sync(0xffffffffu, last, 0) != 0;
+                    if (store) {
+                        __threadfence();
+                        const int32_t s0 = row_seg0[h.row];
+#pragma unroll
+                        for (int k = 0; k < CPL; ++k) acc[k] = 0.0;
+                        for (int32_t i = 0; i < nk; ++i) {
+                            const double* q2 = partial + static_cast<int64_t>(seg_slot[s0 + i]) * pld + col;
+#pragma unroll
+                            for (int k = 0; k < CPL; ++k) acc[k] += __ldcg(q2 + k);
+                        }
+                        if (lane == 0) counters[static_cast<int64_t>(h.row) * cld + chunk] = 0;  // self-reset
+                    }
+                }
+                if (store) {
+#pragma unroll
+                    for (int k = 0; k < CPL; ++k)
+                        if (col + k < dim) yr[col + k] = static_cast<float>(acc[k]);
+                }
+#pragma unroll
+                for (int k = 0; k < CPL; ++k) acc[k] = 0.0;
+            }
         }
-        if (lane == 0) counters[static_cast<int64_t>(row) * cld + chunk] = 0;  // self-reset
+        cp_async_wait<0>();
+        __syncwarp();
     }
-#pragma unroll
-    for (int k = 0; k < CPL; ++k)
-        if (col + k < dim) yr[col + k] = static_cast<float>(acc[k]);
 }
 
-static int g_pipe_smem_set[2] = {};
+static int g_pipe_smem_set[2][2] = {};
 
-template <int CPL>
+template <int CPL, bool TMA>
 static void launch_pipe(const SpmmSegs& s, const int32_t* cols, const double* coeffs, const float* x, int64_t ldx,
                         int32_t dim, float* y, int64_t ldy, int64_t row_base, double* partial, int64_t partial_ld,
-                        int32_t* counters, int32_t counters_ld, cudaStream_t st, const int32_t* special) {
+                        int32_t* counters, int32_t counters_ld, cudaStream_t st, const int32_t* special,
+                        const CUtensorMap* tmap) {
     using Cfg = PipeCfg<CPL>;
-    auto kern = spmm_fwd_pipe_kernel<CPL>;
-    int& set = g_pipe_smem_set[CPL == 4];
+    auto kern = spmm_fwd_pipe_kernel<CPL, TMA>;
+    constexpr int kSmem = Cfg::kSmem + kPipeWarps * kStages * 8;  // + mbarriers
+    int& set = g_pipe_smem_set[CPL == 4][TMA];
     if (!set) {
-        GASB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem));
+        GASB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
         set = 1;
     }
+    CUtensorMap tm{};
+    if (tmap) tm = *tmap;
     const int32_t nchunks = static_cast<int32_t>(ceil_div(dim, Cfg::kCols));
     require(nchunks <= counters_ld && static_cast<int64_t>(nchunks) * Cfg::kCols <= partial_ld,
             "spmm_fwd: counters / partials too narrow");
-    const int64_t warps = s.nseg * nchunks;
-    kern<<<static_cast<unsigned>(ceil_div(warps, kPipeWarps)), kPipeWarps * 32, Cfg::kSmem, st>>>(
-        s.seg_beg, s.seg_row, s.seg_slot, s.row_seg0, s.row_nseg, s.nseg, s.seg_base, cols, coeffs, x, ldx, dim,
-        nchunks, y, ldy, row_base, partial, partial_ld, counters, counters_ld, special);
+    // persistent grid: 2 CTAs (8 warps) per SM — the shared-memory bound — over (chunk, range)
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        GASB_CUDA(cudaGetDevice(&dev));
+        GASB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    }
+    const int64_t items = static_cast<int64_t>(nchunks) * s.nranges;
+    const int64_t blocks = std::min<int64_t>(ceil_div(items, kPipeWarps), 2LL * sms);
+    kern<<<static_cast<unsigned>(blocks), kPipeWarps * 32, kSmem, st>>>(
+        s.seg_beg, s.seg_row, s.seg_slot, s.row_seg0, s.row_nseg, s.range_seg, s.nranges, cols, coeffs, x, ldx, dim,
+        nchunks, y, ldy, row_base, partial, partial_ld, counters, counters_ld, special, tm);
+}
+
+// Tensor map of a row-major fp32 table (rows x dim, pitch ld floats) for tile::gather4:
+// box = {box_cols, 1}; columns >= dim and rows outside [0, rows) read as zero.
+bool make_row_tmap(const float* base, int64_t rows, int32_t dim, int64_t ld, int32_t box_cols, CUtensorMap* out) {
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    if (!encode) {
+        cudaDriverEntryPointQueryResult q;
+        void* fn = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess || !fn)
+            return false;
+        encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }
+    if (rows <= 0 || dim <= 0 || (ld * 4) % 16 != 0 || reinterpret_cast<uintptr_t>(base) % 16 != 0) return false;
+    const cuuint64_t gdim[2] = {static_cast<cuuint64_t>(dim), static_cast<cuuint64_t>(rows)};
+    const cuuint64_t gstride[1] = {static_cast<cuuint64_t>(ld) * 4};
+    const cuuint32_t box[2] = {static_cast<cuuint32_t>(box_cols), 1};
+    const cuuint32_t estride[2] = {1, 1};
+    const CUresult r = encode(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), gdim, gstride, box,
+                              estride, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+// SpMM gather engine (tuning knob GASB_SPMM_TMA = 0 | 1, default 1: TMA tile::gather4).
+bool spmm_use_tma() {
+    static int v = [] {
+        const char* e = getenv("GASB_SPMM_TMA");
+        return e ? atoi(e) : 1;
+    }();
+    return v != 0;
+}
+
+int32_t spmm_box_cols() { return 32 * (getenv("GASB_SPMM_CPL") && atoi(getenv("GASB_SPMM_CPL")) == 2 ? 2 : 4); }
+
+int32_t spmm_ranges_per_launch() {
+    static int32_t v = 0;
+    if (!v) {
+        int dev = 0, sms = 0;
+        if (cudaGetDevice(&dev) != cudaSuccess ||
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0)
+            sms = 148;
+        v = 2 * kPipeWarps * sms;
+    }
+    return v;
+}
+
+// Splits segments [g0, g1) (edges seg_beg[g0] .. seg_beg[g1]) into `nranges` contiguous
+// ranges of ~equal edge count; out receives nranges + 1 absolute segment boundaries.
+void split_ranges(const int64_t* seg_beg, int64_t g0, int64_t g1, int32_t nranges, int32_t* out) {
+    const int64_t E0 = seg_beg[g0], E = seg_beg[g1] - E0;
+    int64_t s = g0;
+    out[0] = static_cast<int32_t>(g0);
+    for (int32_t r = 1; r < nranges; ++r) {
+        const int64_t target = E0 + E * r / nranges;
+        while (s < g1 && seg_beg[s] < target) ++s;
+        out[r] = static_cast<int32_t>(s);
+    }
+    out[nranges] = static_cast<int32_t>(g1);
 }
 
 // Columns per lane of the pipelined SpMM (tuning knob GASB_SPMM_CPL = 2 | 4, default 4:
@@ -267,16 +479,23 @@ void launch_scan_special(const float* x, int64_t rows, int64_t ld, int32_t dim, 
 
 void launch_spmm_fwd(const SpmmSegs& s, const int32_t* cols, const double* coeffs, const float* x, int64_t ldx,
                      int32_t dim, float* y, int64_t ldy, int64_t row_base, double* partial, int64_t partial_ld,
-                     int32_t* counters, int32_t counters_ld, cudaStream_t st, const int32_t* special) {
-    if (s.nseg <= 0 || dim <= 0) return;
+                     int32_t* counters, int32_t counters_ld, cudaStream_t st, const int32_t* special,
+                     const CUtensorMap* tmap) {
+    if (s.nranges <= 0 || dim <= 0) return;
     require(ldx % 4 == 0 && reinterpret_cast<uintptr_t>(x) % 16 == 0,
             "spmm_fwd: source rows must be 16 B aligned (ldx % 4 == 0)");
-    if (spmm_cpl() == 2)
-        launch_pipe<2>(s, cols, coeffs, x, ldx, dim, y, ldy, row_base, partial, partial_ld, counters, counters_ld, st,
-                       special);
-    else
-        launch_pipe<4>(s, cols, coeffs, x, ldx, dim, y, ldy, row_base, partial, partial_ld, counters, counters_ld, st,
-                       special);
+    const bool tma = tmap != nullptr && spmm_use_tma();
+#define GASB_PIPE(C, T)                                                                                               \
+    launch_pipe<C, T>(s, cols, coeffs, x, ldx, dim, y, ldy, row_base, partial, partial_ld, counters, counters_ld, st, \
+                      special, tmap)
+    if (spmm_cpl() == 2) {
+        if (tma) GASB_PIPE(2, true);
+        else GASB_PIPE(2, false);
+    } else {
+        if (tma) GASB_PIPE(4, true);
+        else GASB_PIPE(4, false);
+    }
+#undef GASB_PIPE
     ++t_launches;
     GASB_CUDA(cudaGetLastError());
 }
@@ -512,11 +731,20 @@ extern "C" gasb_status gasb_spmm_fwd(const int32_t* d_rowptr, int32_t m, const i
             GASB_CUDA(cudaMallocAsync(&special, sizeof(int32_t), st));
             GASB_CUDA(cudaMemsetAsync(special, 0, sizeof(int32_t), st));
             launch_scan_special(d_x, num_src, ldx, dim, special, st);
-            SpmmSegs segs{z.seg_beg, z.seg_row, z.seg_slot, z.row_seg0, z.row_nseg, nseg, 0};
+            const int32_t nranges = spmm_ranges_per_launch();
+            std::vector<int32_t> rs(static_cast<size_t>(nranges) + 1);
+            split_ranges(sb.data(), 0, nseg, nranges, rs.data());
+            int32_t* d_rs = nullptr;
+            GASB_CUDA(cudaMallocAsync(&d_rs, sizeof(int32_t) * (nranges + 1), st));
+            GASB_CUDA(cudaMemcpyAsync(d_rs, rs.data(), sizeof(int32_t) * (nranges + 1), cudaMemcpyHostToDevice, st));
+            SpmmSegs segs{z.seg_beg, z.seg_row, z.seg_slot, z.row_seg0, z.row_nseg, d_rs, nranges};
+            CUtensorMap tm;
+            const bool have_tm = make_row_tmap(d_x, num_src, dim, ldx, spmm_box_cols(), &tm);
             launch_spmm_fwd(segs, d_cols, coeffs64, d_x, ldx, dim, d_y, ldy, 0, z.partial,
-                            round_up(dim, 128), z.counters, nchunks, st, special);
+                            round_up(dim, 128), z.counters, nchunks, st, special, have_tm ? &tm : nullptr);
             GASB_CUDA(cudaStreamSynchronize(st));
             cudaFreeAsync(special, st);
+            cudaFreeAsync(d_rs, st);
         }
         cudaFreeAsync(z.seg_beg, st);
         cudaFreeAsync(z.seg_row, st);

@@ -103,8 +103,14 @@ struct DevBuf {
 struct SegTable {
     DevBuf<int64_t> seg_beg;
     DevBuf<int32_t> seg_row, seg_slot, row_seg0, row_nseg;
+    DevBuf<int32_t> ranges;  // per group: nranges + 1 work-range boundaries (split_ranges)
+    int32_t nranges = 0;
     std::vector<int64_t> group_seg0, group_nseg;  // per group (batch) range of segments
     int64_t max_group_slots = 0, total_slots = 0;
+    SpmmSegs segs(int64_t g) const {
+        return SpmmSegs{seg_beg.p, seg_row.p, seg_slot.p, row_seg0.p, row_nseg.p, ranges.p + g * (nranges + 1),
+                        nranges};
+    }
 };
 
 // Segments rows [row_lo, row_hi) of the absolute row pointer `rp` into pieces of <= S
@@ -138,6 +144,12 @@ void build_segments(const std::vector<int64_t>& rp, const std::vector<int64_t>& 
     }
     t.total_slots = per_group_slots ? t.max_group_slots : slot;
     sb.push_back(rp[nrows]);
+    t.nranges = spmm_ranges_per_launch();
+    std::vector<int32_t> rs(static_cast<size_t>(ngroups) * (t.nranges + 1));
+    for (int64_t g = 0; g < ngroups; ++g)
+        split_ranges(sb.data(), t.group_seg0[g], t.group_seg0[g] + t.group_nseg[g], t.nranges,
+                     rs.data() + g * (t.nranges + 1));
+    t.ranges.upload(rs);
     t.seg_beg.upload(sb);
     t.seg_row.upload(sr);
     t.seg_slot.upload(ss);
@@ -209,6 +221,25 @@ struct gasb_trainer_s {
     DevBuf<float> agg_all;        // hoisted layer-1 aggregation, n x ldF
     std::vector<DevBuf<float>> agg, act;
     DevBuf<float> logits, glogits, g_agg, g_out, x_ext, h_ext, halo_buf;
+    // TMA tensor maps of the SpMM source tables (tile::gather4 staging, spmm.cu)
+    CUtensorMap tm_x{}, tm_xext{}, tm_hext{};
+    std::vector<CUtensorMap> tm_hist;
+    bool tm_ok[4] = {false, false, false, false};  // x, hist, x_ext, h_ext
+    const CUtensorMap* source_tmap(int32_t l) const {
+        if (l == 1) return tm_ok[0] ? &tm_x : nullptr;
+        return tm_ok[1] ? &tm_hist[l - 2] : nullptr;
+    }
+    void build_tmaps() {
+        const int32_t bc = spmm_box_cols();
+        tm_ok[0] = make_row_tmap(X.p, n, F, ldF, bc, &tm_x);
+        tm_hist.resize(static_cast<size_t>(std::max(0, L - 1)));
+        tm_ok[1] = L >= 2;
+        for (int32_t l = 1; l < L; ++l)
+            tm_ok[1] = tm_ok[1] && make_row_tmap(history_table(hist, l), n, hist_dim, history_ld(hist), bc,
+                                                 &tm_hist[l - 1]);
+        if (x_ext.p) tm_ok[2] = make_row_tmap(x_ext.p, ne_max, F, ldF, bc, &tm_xext);
+        if (h_ext.p) tm_ok[3] = make_row_tmap(h_ext.p, ne_max, H, ldH, bc, &tm_hext);
+    }
     DevBuf<double> loss, row_scratch;
 
     // graphs
@@ -455,17 +486,14 @@ void gasb_trainer_s::build(const float* h_features, const int32_t* h_labels, con
 }
 
 void gasb_trainer_s::enqueue_hoisted() {
-    SpmmSegs s{seg_all.seg_beg.p, seg_all.seg_row.p, seg_all.seg_slot.p, seg_all.row_seg0.p,
-               seg_all.row_nseg.p, seg_all.group_nseg[0], 0};
-    launch_spmm_fwd(s, cols_g.p, coef64.p, X.p, ldF, F, agg_all.p, ldF, 0, partial_all.p, pld_all,
-                    counters.p, max_chunks, stream, source_flags(1));
+    launch_spmm_fwd(seg_all.segs(0), cols_g.p, coef64.p, X.p, ldF, F, agg_all.p, ldF, 0, partial_all.p, pld_all,
+                    counters.p, max_chunks, stream, source_flags(1), source_tmap(1));
 }
 
 void gasb_trainer_s::enqueue_batch(int32_t p, bool train, bool push, bool use_hoisted, bool fused) {
     const int32_t m = nb[p];
     const int64_t r0 = row_off[p];
-    SpmmSegs segs{seg_batch.seg_beg.p, seg_batch.seg_row.p, seg_batch.seg_slot.p, seg_batch.row_seg0.p,
-                  seg_batch.row_nseg.p, seg_batch.group_nseg[p], seg_batch.group_seg0[p]};
+    const SpmmSegs segs = seg_batch.segs(p);
     const int32_t* bn = batch_nodes.p + r0;
     // ---------------- forward (Model::forward, trainer.cpp:174-251) ----------------
     for (int32_t l = 1; l <= L; ++l) {
@@ -478,7 +506,7 @@ void gasb_trainer_s::enqueue_batch(int32_t p, bool train, bool push, bool use_ho
             const float* src = l == 1 ? X.p : history_table(hist, l - 1);
             const int64_t lds = l == 1 ? ldF : history_ld(hist);
             launch_spmm_fwd(segs, cols_g.p, coef64.p, src, lds, din, a, lda, r0, partial_batch.p, pld, counters.p,
-                            max_chunks, stream, source_flags(l));
+                            max_chunks, stream, source_flags(l), source_tmap(l));
         } else {
             // reference structure: x_ext / compose over V_b local rows, SpMM by local ids
             const int64_t ldx = ld_of(din);
@@ -503,7 +531,8 @@ void gasb_trainer_s::enqueue_batch(int32_t p, bool train, bool push, bool use_ho
             // the composed rows come from X / H_{l-1} (+ act_{l-1}, pushed to H_{l-1} when push);
             // without push the act rows are unflagged, so take the exact F2F widening
             launch_spmm_fwd(segs, cols_l.p, coef64.p, hsrc, ldx, din, a, lda, r0, partial_batch.p, pld, counters.p,
-                            max_chunks, stream, (push || l == 1) ? source_flags(l) : nullptr);
+                            max_chunks, stream, (push || l == 1) ? source_flags(l) : nullptr,
+                            l == 1 ? (tm_ok[2] ? &tm_xext : nullptr) : (tm_ok[3] ? &tm_hext : nullptr));
         }
         float* Wl = W(l);
         if (l < L) {
@@ -620,6 +649,7 @@ gasb_status gasb_trainer_create(gasb_schedule s, const float* h_features, int32_
             }
             t->halo_ids.upload(hid);
         }
+        t->build_tmaps();
         *out = t.release();
     });
 }
@@ -755,14 +785,13 @@ gasb_status gasb_trainer_profile_spmm(gasb_trainer t, int32_t part, int32_t laye
                 return;
             }
             const int32_t din = t->dims[layer - 1];
-            SpmmSegs segs{t->seg_batch.seg_beg.p, t->seg_batch.seg_row.p, t->seg_batch.seg_slot.p,
-                          t->seg_batch.row_seg0.p, t->seg_batch.row_nseg.p, t->seg_batch.group_nseg[part],
-                          t->seg_batch.group_seg0[part]};
+            const SpmmSegs segs = t->seg_batch.segs(part);
             const float* src = layer == 1 ? t->X.p : history_table(t->hist, layer - 1);
             const int64_t lds = layer == 1 ? t->ldF : history_ld(t->hist);
             launch_spmm_fwd(segs, t->cols_g.p, t->coef64.p, src, lds, din, t->agg[layer].p, t->ld_of(din),
                             t->row_off[part], t->partial_batch.p, t->pld,
-                            t->counters.p, t->max_chunks, t->stream, t->source_flags(layer));
+                            t->counters.p, t->max_chunks, t->stream, t->source_flags(layer),
+                            t->source_tmap(layer));
         };
         once();  // warm
         GASB_CUDA(cudaEventRecord(a, t->stream));
