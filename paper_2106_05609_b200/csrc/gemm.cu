@@ -1,6 +1,7 @@
-// Dense feature transform (the reference's matmul, src/tensor.cpp:148-204) — FP32 SIMT
-// tiled GEMM with fused epilogues. This is the correctness-first kernel of round 1; the
-// reference accumulates in fp64, fp32 accumulation stays ~1e-7 normwise.
+// Dense feature transform (the reference's matmul, src/tensor.cpp:148-204) — dispatch to the
+// tcgen05 3xTF32 kernel (gemm_tc.cu) and this FP32 SIMT fallback for pitches a TMA tensor map
+// cannot describe (pitch not 16 B aligned or inner extent < 32). The reference accumulates in
+// fp64; both engines stay ~1e-6 normwise, inside the 1e-5 contract.
 //
 // Tile 64x64x16, 256 threads, 4x4 outputs per thread in a strided (16-apart) pattern so
 // that smem reads are conflict-free broadcasts; register double-buffering of the next
@@ -140,9 +141,22 @@ __global__ void __launch_bounds__(256) gemm_kernel(int M, int N, int K, const fl
     }
 }
 
+bool launch_gemm_tc(int op, int m, int n, int k, const float* a, int64_t lda, const float* b, int64_t ldb, float* c,
+                    int64_t ldc, float beta, bool relu, const PushEpilogue* push, cudaStream_t st);
+
+// GEMM engine (tuning knob GASB_GEMM_TC = 1 tcgen05 3xTF32 (default) | 0 FP32 SIMT).
+static bool gemm_use_tc() {
+    static int v = [] {
+        const char* e = getenv("GASB_GEMM_TC");
+        return e ? atoi(e) : 1;
+    }();
+    return v != 0;
+}
+
 void launch_gemm(int op, int m, int n, int k, const float* a, int64_t lda, const float* b, int64_t ldb, float* c,
                  int64_t ldc, float beta, bool relu, const PushEpilogue* push, cudaStream_t st) {
     if (m <= 0 || n <= 0) return;
+    if (gemm_use_tc() && k > 0 && launch_gemm_tc(op, m, n, k, a, lda, b, ldb, c, ldc, beta, relu, push, st)) return;
     PushEpilogue pe{};
     if (push) pe = *push;
     require(op == 0 || !push, "gemm: push epilogue only for op 0");

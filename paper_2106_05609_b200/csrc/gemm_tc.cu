@@ -1,0 +1,375 @@
+// Dense feature transform (the reference's matmul, src/tensor.cpp:148-204) on the 5th-gen
+// tensor cores: tcgen05.mma kind::tf32 with fp32 accumulators in TMEM, operands staged by
+// TMA (128 B swizzle), 3xTF32 split for fp32-level accuracy (the reference accumulates in
+// fp64; plain TF32 misses the 1e-5 normwise bound, 3xTF32 meets it — SURVEY §7.6).
+//
+//   op 0: C[m,n] = A[m,k] B[k,n]    (A K-major, B MN-major)   forward  X·W
+//   op 1: C[m,n] = A[m,k] B[n,k]^T  (A K-major, B K-major)    dgrad    dY·W^T
+//   op 2: C[m,n] = A[k,m]^T B[k,n]  (A MN-major, B MN-major)  wgrad    X^T·dY
+//
+// CTA = one 128 x BN output tile, 6 warps:
+//   warp 4 (1 thread)   TMA producer: fp32 A/B tiles of BK=32 into a 3-stage ring
+//   warps 0-3           split each landed tile in place into hi = tf32(x) and lo = x - hi
+//                       (exact), then the fused epilogue (TMEM -> registers -> global)
+//   warp 5 (1 thread)   MMA issuer: per k-step of 8, D += Ahi.Bhi + Ahi.Blo + Alo.Bhi
+// mbarriers: full (TMA -> split), split (split -> MMA), empty (tcgen05.commit -> TMA),
+// accum (last commit -> epilogue). Waits are bounded (trap instead of hang).
+#include "gasb_internal.hpp"
+#include "kernels.cuh"
+
+namespace gasb {
+namespace tc {
+
+constexpr int BM = 128, BK = 32, kStagesTC = 3;
+constexpr int kThreads = 192;
+// The tensor core's fp32 accumulation truncates, so its error grows linearly with the number
+// of k-steps; k-steps are interleaved over kAcc TMEM accumulators (kAcc * BN <= 512 columns)
+// summed round-to-nearest in the epilogue, cutting that growth kAcc-fold.
+template <int BN>
+struct Acc {
+    static constexpr int kAcc = 512 / BN < 8 ? 512 / BN : 8;
+    static constexpr int kCols = kAcc * BN;  // TMEM allocation (power of two)
+};
+
+__device__ __forceinline__ uint32_t su32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+
+__device__ __forceinline__ void bar_init(uint64_t* b, uint32_t c) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(su32(b)), "r"(c) : "memory");
+}
+__device__ __forceinline__ void bar_expect(uint64_t* b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(su32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bar_arrive(uint64_t* b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(su32(b)) : "memory");
+}
+__device__ __forceinline__ void bar_wait(uint64_t* b, uint32_t parity) {
+    for (uint32_t spins = 0;; ++spins) {
+        uint32_t done;
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(done)
+            : "r"(su32(b)), "r"(parity)
+            : "memory");
+        if (done) return;
+        if (spins > (1u << 26)) __trap();
+    }
+}
+__device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* tm, int32_t c0, int32_t c1, uint64_t* b) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n"
+        ::"r"(su32(dst)), "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(c1), "r"(su32(b))
+        : "memory");
+}
+
+// UMMA shared-memory descriptor, version 1 (sm_100). layout 2 = SWIZZLE_128B (K-major
+// operands); layout 1 = SWIZZLE_128B_BASE32B (32 B atoms), the only smem layout the tensor
+// core accepts for MN-major tf32 operands.
+__device__ __forceinline__ uint64_t smem_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo, uint32_t layout) {
+    uint64_t d = 0;
+    d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFF);
+    d |= static_cast<uint64_t>((lbo >> 4) & 0x3FFF) << 16;
+    d |= static_cast<uint64_t>((sbo >> 4) & 0x3FFF) << 32;
+    d |= 1ull << 46;  // version
+    d |= static_cast<uint64_t>(layout) << 61;
+    return d;
+}
+
+// Instruction descriptor: D f32, A/B tf32, majors, N, M = 128.
+__host__ __device__ constexpr uint32_t instr_desc(int n, bool a_mn, bool b_mn) {
+    return (1u << 4) | (2u << 7) | (2u << 10) | (static_cast<uint32_t>(a_mn) << 15) |
+           (static_cast<uint32_t>(b_mn) << 16) | (static_cast<uint32_t>(n >> 3) << 17) | ((128u >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+        " tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void mma_commit(uint64_t* b) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(su32(b))
+                 : "memory");
+}
+
+// round-to-nearest tf32 (low 13 mantissa bits zero) and the exact remainder
+__device__ __forceinline__ float tf32_hi(float x) {
+    return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
+}
+
+template <int BN, bool A_MN, bool B_MN>
+struct Layout {
+    static constexpr int kTileA = BM * BK * 4;  // bytes (16 KB)
+    static constexpr int kTileB = BN * BK * 4;
+    // stage: A, A_lo, B, B_lo (each 1024 B aligned: SW128 atoms)
+    static constexpr int kStage = 2 * kTileA + 2 * kTileB;
+    static constexpr int kBars = 8 * (3 * kStagesTC + 1);
+    static constexpr int kSmem = 1024 + kStagesTC * kStage + kBars + 16;
+};
+
+template <int BN, bool A_MN, bool B_MN>
+__global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_constant__ CUtensorMap tma_a,
+                                                             const __grid_constant__ CUtensorMap tma_b, int M,
+                                                             int N, int K, float* __restrict__ C, int64_t ldc,
+                                                             float beta, int relu, PushEpilogue push) {
+    using Lay = Layout<BN, A_MN, B_MN>;
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char* base = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~1023ull);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(base + kStagesTC * Lay::kStage);
+    uint64_t* full = bars;
+    uint64_t* split = bars + kStagesTC;
+    uint64_t* empty = bars + 2 * kStagesTC;
+    uint64_t* accum = bars + 3 * kStagesTC;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * kStagesTC + 1);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
+    const int nk = (K + BK - 1) / BK;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kStagesTC; ++s) {
+            bar_init(full + s, 1);
+            bar_init(split + s, 128);
+            bar_init(empty + s, 1);
+        }
+        bar_init(accum, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    if (warp == 0) {  // TMEM: BN fp32 columns x 128 lanes
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(su32(tmem_slot)),
+                     "r"(Acc<BN>::kCols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 4) {
+        // ---------------- TMA producer ----------------
+        if (lane == 0) {
+            for (int kb = 0; kb < nk; ++kb) {
+                const int s = kb % kStagesTC;
+                bar_wait(empty + s, ((kb / kStagesTC) & 1) ^ 1);
+                unsigned char* st = base + s * Lay::kStage;
+                bar_expect(full + s, Lay::kTileA + Lay::kTileB);
+                const int k0 = kb * BK;
+                if (A_MN) {  // A^T tile: K rows x 128 MN cols as 4 boxes of 32 cols
+                    for (int j = 0; j < BM / 32; ++j) tma_2d(st + j * BK * 128, &tma_a, m0 + 32 * j, k0, full + s);
+                } else {
+                    tma_2d(st, &tma_a, k0, m0, full + s);
+                }
+                unsigned char* sb = st + 2 * Lay::kTileA;
+                if (B_MN) {
+                    for (int j = 0; j < BN / 32; ++j) tma_2d(sb + j * BK * 128, &tma_b, n0 + 32 * j, k0, full + s);
+                } else {
+                    tma_2d(sb, &tma_b, k0, n0, full + s);
+                }
+            }
+        }
+    } else if (warp == 5) {
+        // ---------------- MMA issuer ----------------
+        if (lane == 0) {
+            constexpr uint32_t idesc = instr_desc(BN, A_MN, B_MN);
+            for (int kb = 0; kb < nk; ++kb) {
+                const int s = kb % kStagesTC;
+                bar_wait(split + s, (kb / kStagesTC) & 1);
+                asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+                const uint32_t sa = su32(base + s * Lay::kStage);
+                const uint32_t sa_lo = sa + Lay::kTileA;
+                const uint32_t sb = sa + 2 * Lay::kTileA;
+                const uint32_t sb_lo = sb + Lay::kTileB;
+#pragma unroll
+                for (int kk = 0; kk < BK / 8; ++kk) {
+                    // K-major (SW128): +32 B per k-step inside the 128 B swizzle row; LBO unused,
+                    // SBO = 1024 B between 8-row groups.
+                    // MN-major (SW128_32B): +8 K-rows x 128 B per k-step; LBO = stride of the
+                    // 32-column MN blocks (one TMA box each), SBO = 512 B between 4-row atoms.
+                    const uint32_t offa = A_MN ? kk * 1024 : kk * 32;
+                    const uint32_t offb = B_MN ? kk * 1024 : kk * 32;
+                    const uint32_t lboa = A_MN ? BK * 128 : 16, lbob = B_MN ? BK * 128 : 16;
+                    const uint32_t sboa = A_MN ? 512 : 1024, sbob = B_MN ? 512 : 1024;
+                    const uint32_t lya = A_MN ? 1 : 2, lyb = B_MN ? 1 : 2;
+                    const uint64_t ahi = smem_desc(sa + offa, lboa, sboa, lya);
+                    const uint64_t alo = smem_desc(sa_lo + offa, lboa, sboa, lya);
+                    const uint64_t bhi = smem_desc(sb + offb, lbob, sbob, lyb);
+                    const uint64_t blo = smem_desc(sb_lo + offb, lbob, sbob, lyb);
+                    const int g = kb * (BK / 8) + kk;  // global k-step -> accumulator g % kAcc
+                    const uint32_t d = tmem + static_cast<uint32_t>((g % Acc<BN>::kAcc) * BN);
+                    const uint32_t first = g < Acc<BN>::kAcc ? 0u : 1u;
+                    mma_tf32(d, ahi, bhi, idesc, first);
+                    mma_tf32(d, ahi, blo, idesc, 1u);
+                    mma_tf32(d, alo, bhi, idesc, 1u);
+                }
+                mma_commit(empty + s);  // frees the stage once these MMAs have read it
+            }
+            mma_commit(accum);
+        }
+    } else {
+        // ---------------- split (warps 0-3), then epilogue ----------------
+        for (int kb = 0; kb < nk; ++kb) {
+            const int s = kb % kStagesTC;
+            bar_wait(full + s, (kb / kStagesTC) & 1);
+            float4* a = reinterpret_cast<float4*>(base + s * Lay::kStage);
+            float4* alo = a + Lay::kTileA / 16;
+            float4* b = a + 2 * Lay::kTileA / 16;
+            float4* blo = b + Lay::kTileB / 16;
+            // hi = rn_tf32(x), lo = rn_tf32(x - hi): both exactly tf32, so the tensor core's
+            // operand truncation changes nothing; dropped lo*lo term ~2^-22 relative
+            for (int i = threadIdx.x; i < Lay::kTileA / 16; i += 128) {
+                float4 v = a[i], h;
+                h.x = tf32_hi(v.x), h.y = tf32_hi(v.y), h.z = tf32_hi(v.z), h.w = tf32_hi(v.w);
+                a[i] = h;
+                alo[i] = make_float4(tf32_hi(v.x - h.x), tf32_hi(v.y - h.y), tf32_hi(v.z - h.z), tf32_hi(v.w - h.w));
+            }
+            for (int i = threadIdx.x; i < Lay::kTileB / 16; i += 128) {
+                float4 v = b[i], h;
+                h.x = tf32_hi(v.x), h.y = tf32_hi(v.y), h.z = tf32_hi(v.z), h.w = tf32_hi(v.w);
+                b[i] = h;
+                blo[i] = make_float4(tf32_hi(v.x - h.x), tf32_hi(v.y - h.y), tf32_hi(v.z - h.z), tf32_hi(v.w - h.w));
+            }
+            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // generic writes -> tensor core
+            bar_arrive(split + s);
+        }
+        bar_wait(accum, 0);
+        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+        const int row = m0 + warp * 32 + lane;  // TMEM lane == tile row
+        float* crow = row < M ? C + static_cast<int64_t>(row) * ldc : nullptr;
+        float* prow = nullptr;
+        if (crow && push.table) {
+            const int32_t id = push.ids[row];
+            prow = push.table + static_cast<int64_t>(id) * push.ld;
+            if (blockIdx.y == 0 && push.stamps) push.stamps[id] = *push.step;
+        }
+        int32_t flags = 0;
+        const int nsteps = nk * (BK / 8);
+        const int nacc = nsteps < Acc<BN>::kAcc ? nsteps : Acc<BN>::kAcc;  // accumulators written
+#pragma unroll 1
+        for (int c0 = 0; c0 < BN; c0 += 32) {
+            float sum[32];
+#pragma unroll 1
+            for (int q = 0; q < nacc; ++q) {
+                uint32_t v[32];
+                const uint32_t taddr =
+                    tmem + (static_cast<uint32_t>(warp * 32) << 16) + static_cast<uint32_t>(q * BN + c0);
+                asm volatile(
+                    "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+                    "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+                    : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+                      "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+                      "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]),
+                      "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]),
+                      "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+                    : "r"(taddr));
+                asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+                for (int j = 0; j < 32; ++j) sum[j] = q == 0 ? __uint_as_float(v[j]) : __fadd_rn(sum[j], __uint_as_float(v[j]));
+            }
+            if (crow) {
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                    const int col = n0 + c0 + j;
+                    if (col < N) {
+                        float x = sum[j];
+                        if (beta != 0.f) x += beta * crow[col];
+                        if (relu) x = x > 0.f ? x : 0.f;
+                        crow[col] = x;
+                        if (prow) {
+                            prow[col] = x;
+                            flags |= table_flag_of(x);
+                        }
+                    }
+                }
+            }
+        }
+        if (push.special) {
+            flags = __reduce_or_sync(0xffffffffu, flags);
+            if (lane == 0 && flags) atomicOr(push.special, flags);
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    __syncthreads();
+    if (warp == 0) {
+        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(Acc<BN>::kCols));
+    }
+}
+
+// 2-D fp32 tensor map for TMA with 128 B swizzle: contiguous dim `inner` (elements), `outer`
+// rows with pitch `ld` floats; box {32, box_outer}. mn_major selects the 32 B-atom swizzle.
+static bool make_tmap(const float* p, int64_t inner, int64_t outer, int64_t ld, int box_outer, CUtensorMap* out,
+                      bool mn_major) {
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    if (!encode) {
+        cudaDriverEntryPointQueryResult q;
+        void* fn = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess || !fn)
+            return false;
+        encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }
+    // the 32-element box must fit the contiguous dimension (narrower tables read back zeros)
+    if (inner < 32 || outer <= 0 || (ld * 4) % 16 != 0 || reinterpret_cast<uintptr_t>(p) % 16 != 0) return false;
+    const cuuint64_t gdim[2] = {static_cast<cuuint64_t>(inner), static_cast<cuuint64_t>(outer)};
+    const cuuint64_t gstride[1] = {static_cast<cuuint64_t>(ld) * 4};
+    const cuuint32_t box[2] = {32, static_cast<cuuint32_t>(box_outer)};
+    const cuuint32_t es[2] = {1, 1};
+    return encode(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(p), gdim, gstride, box, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  mn_major ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int BN, bool A_MN, bool B_MN>
+static bool launch_tc(int m, int n, int k, const float* a, int64_t lda, const float* b, int64_t ldb, float* c,
+                      int64_t ldc, float beta, bool relu, const PushEpilogue* push, cudaStream_t st) {
+    using Lay = Layout<BN, A_MN, B_MN>;
+    CUtensorMap ta, tb;
+    // A: K-major -> inner K, outer M (box 32 x 128); MN-major -> inner M, outer K (box 32 x 32)
+    const bool ok_a = A_MN ? make_tmap(a, m, k, lda, BK, &ta, true) : make_tmap(a, k, m, lda, BM, &ta, false);
+    const bool ok_b = B_MN ? make_tmap(b, n, k, ldb, BK, &tb, true) : make_tmap(b, k, n, ldb, BN, &tb, false);
+    if (!ok_a || !ok_b) return false;  // pitch not 16 B aligned: caller uses the SIMT kernel
+    static bool attr = false;
+    if (!attr) {
+        GASB_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<BN, A_MN, B_MN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       Lay::kSmem));
+        attr = true;
+    }
+    PushEpilogue pe{};
+    if (push) pe = *push;
+    dim3 grid(static_cast<unsigned>(ceil_div(m, BM)), static_cast<unsigned>(ceil_div(n, BN)));
+    gemm_tc_kernel<BN, A_MN, B_MN><<<grid, kThreads, Lay::kSmem, st>>>(ta, tb, m, n, k, c, ldc, beta, relu ? 1 : 0,
+                                                                        pe);
+    return true;
+}
+
+}  // namespace tc
+
+// Tensor-core path of launch_gemm (gemm.cu) — same contract. Returns false (nothing
+// launched) when an operand's row pitch cannot be described to TMA.
+bool launch_gemm_tc(int op, int m, int n, int k, const float* a, int64_t lda, const float* b, int64_t ldb, float* c,
+                    int64_t ldc, float beta, bool relu, const PushEpilogue* push, cudaStream_t st) {
+    if (m <= 0 || n <= 0) return true;
+    bool ok;
+    // narrow N tiles keep enough CTAs in flight for the ~1K-row batch GEMMs
+    switch (op) {
+        case 0:
+            ok = n <= 32 ? tc::launch_tc<32, false, true>(m, n, k, a, lda, b, ldb, c, ldc, beta, relu, push, st)
+                         : tc::launch_tc<64, false, true>(m, n, k, a, lda, b, ldb, c, ldc, beta, relu, push, st);
+            break;
+        case 1:
+            ok = n <= 32 ? tc::launch_tc<32, false, false>(m, n, k, a, lda, b, ldb, c, ldc, beta, relu, push, st)
+                         : tc::launch_tc<64, false, false>(m, n, k, a, lda, b, ldb, c, ldc, beta, relu, push, st);
+            break;
+        case 2:
+            ok = n <= 32 ? tc::launch_tc<32, true, true>(m, n, k, a, lda, b, ldb, c, ldc, beta, relu, push, st)
+                         : tc::launch_tc<64, true, true>(m, n, k, a, lda, b, ldb, c, ldc, beta, relu, push, st);
+            break;
+        default: throw std::invalid_argument("gemm: op must be 0, 1 or 2");
+    }
+    if (!ok) return false;
+    ++t_launches;
+    GASB_CUDA(cudaGetLastError());
+    return true;
+}
+
+}  // namespace gasb

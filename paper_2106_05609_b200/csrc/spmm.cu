@@ -560,7 +560,7 @@ __global__ void __launch_bounds__(256) spmm_bwd_kernel(const int64_t* __restrict
 // stages the 32-column slice gy[:, chunk] (nsrc x 128 B) in smem once and every target of
 // its range gathers from smem; lane = column, entries in order -> same rounding sequence.
 constexpr int kBwdCW = 32;
-constexpr int kBwdThreads = 512;
+constexpr int kBwdThreads = 1024;
 
 __global__ void __launch_bounds__(kBwdThreads) spmm_bwd_smem_kernel(
     const int64_t* __restrict__ rp, int32_t nt, const int32_t* __restrict__ src, const float* __restrict__ cf,
@@ -604,16 +604,34 @@ __global__ void __launch_bounds__(kBwdThreads) spmm_bwd_smem_kernel(
     for (int32_t t = t_lo + warp; t < t_hi; t += nwarps) {
         const int64_t e0 = rp[t], e1 = rp[t + 1];
         float a = 0.0f;
-        for (int64_t eb = e0; eb < e1; eb += 32) {
-            const int cnt = static_cast<int>((e1 - eb) < 32 ? (e1 - eb) : 32);
-            const int32_t my_r = lane < cnt ? __ldg(src + eb + lane) : 0;
-            const float my_c = lane < cnt ? __ldg(cf + eb + lane) : 0.0f;
-#pragma unroll 8
-            for (int j = 0; j < cnt; ++j) {
-                const int32_t r = __shfl_sync(0xffffffffu, my_r, j);
-                const float c = __shfl_sync(0xffffffffu, my_c, j);
-                a = __fadd_rn(a, __fmul_rn(c, sg[r * kBwdCW + lane]));
+        // metadata of the next 32 entries is loaded while the current 32 are accumulated
+        int64_t eb = e0;
+        int cnt = static_cast<int>((e1 - eb) < 32 ? (e1 - eb) : 32);
+        int32_t my_r = lane < cnt ? __ldg(src + eb + lane) : 0;
+        float my_c = lane < cnt ? __ldg(cf + eb + lane) : 0.0f;
+        while (eb < e1) {
+            const int64_t nb = eb + 32;
+            const int ncnt = static_cast<int>(e1 - nb <= 0 ? 0 : (e1 - nb < 32 ? e1 - nb : 32));
+            const int32_t nr = lane < ncnt ? __ldg(src + nb + lane) : 0;
+            const float nc = lane < ncnt ? __ldg(cf + nb + lane) : 0.0f;
+            if (cnt == 32) {
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                    const int32_t r = __shfl_sync(0xffffffffu, my_r, j);
+                    const float c = __shfl_sync(0xffffffffu, my_c, j);
+                    a = __fadd_rn(a, __fmul_rn(c, sg[r * kBwdCW + lane]));
+                }
+            } else {
+                for (int j = 0; j < cnt; ++j) {
+                    const int32_t r = __shfl_sync(0xffffffffu, my_r, j);
+                    const float c = __shfl_sync(0xffffffffu, my_c, j);
+                    a = __fadd_rn(a, __fmul_rn(c, sg[r * kBwdCW + lane]));
+                }
             }
+            eb = nb;
+            cnt = ncnt;
+            my_r = nr;
+            my_c = nc;
         }
         if (lane < ncol) {
             const int32_t col = col0 + lane;
@@ -637,9 +655,15 @@ void launch_spmm_bwd(const int64_t* t_rowptr, int32_t nt, const int32_t* t_src, 
             g_bwd_smem_set = 1;
         }
         const int32_t nchunks = static_cast<int32_t>(ceil_div(dim, kBwdCW));
-        // ~148 CTAs in total, at least one warp-round of targets each
-        const int32_t splits = static_cast<int32_t>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(148, nchunks),
-                                                                                        ceil_div(nt, 16))));
+        // one CTA per SM (the staged slice fills shared memory): a single wave of <= #SMs CTAs
+        static int sms = 0;
+        if (!sms) {
+            int dev = 0;
+            GASB_CUDA(cudaGetDevice(&dev));
+            GASB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        }
+        const int32_t splits = static_cast<int32_t>(
+            std::max<int64_t>(1, std::min<int64_t>(sms / nchunks, ceil_div(nt, kBwdThreads / 32))));
         const int32_t per = static_cast<int32_t>(ceil_div(nt, splits));
         dim3 grid(static_cast<unsigned>(nchunks), static_cast<unsigned>(ceil_div(nt, per)));
         spmm_bwd_smem_kernel<<<grid, kBwdThreads, smem, st>>>(t_rowptr, nt, t_src, t_coeffs, gy, ldgy, nsrc, dim,
