@@ -546,9 +546,11 @@ static void relu_bwd(const float* x, const float* gy, float* g, int64_t sz) {
 }
 
 /* Model::forward (trainer.cpp:174-251) + run_batch (:295-339) + advance_step (:426). */
-int go_session_batch(go_session* s, int32_t part, int64_t epoch, int train, int push, float* acts_out,
-                     float* logits_out, double* loss_out, float* grads_out, int* stepped) {
-    (void)epoch; /* only seeds dropout, which is not restated (must be 0) */
+/* run_batch (trainer.cpp:295-339) up to, not including, the optimizer: forward (pushes into
+ * the tables when `push`), loss, backward. gflat (nflat floats, zeroed) receives the
+ * pre-clip gradients when *stepped. */
+static int batch_core(go_session* s, int32_t part, int train, int push, float* acts_out, float* logits_out,
+                      double* loss_out, float* gflat, int* stepped) {
     if (part < 0 || part >= s->num_parts) return 1;
     const go_plan* P = &s->plans[part];
     const int32_t L = s->L, nb = P->nb, ne = P->next, F = s->in_dim, H = s->spec.hidden, C = s->num_classes;
@@ -681,7 +683,6 @@ int go_session_batch(go_session* s, int32_t part, int64_t epoch, int train, int 
     *stepped = 0;
     *loss_out = 0.0;
     if (r > 0) {
-        float* gflat = zalloc(s->nflat);
         float loss = go_softmax_ce(logits, nb, C, rows, lab, r, NULL);
         if (train && s->spec.l2_weight > 0.0f) { /* l2_penalty (tensor.cpp:649-678), recorded after CE */
             double acc = 0.0;
@@ -780,18 +781,11 @@ int go_session_batch(go_session* s, int32_t part, int64_t epoch, int train, int 
                 free(g_z1);
                 free(g_h0);
             }
-            if (grads_out) memcpy(grads_out, gflat, sizeof(float) * (size_t)s->nflat);
-            if (s->spec.clip_max_norm > 0.0f) go_grad_clip(gflat, s->nflat, s->spec.clip_max_norm);
-            s->adam_t++;
-            go_adam_cfg cfg = {s->spec.lr, s->spec.beta1, s->spec.beta2, s->spec.eps};
-            go_adam_step(s->flat, s->adam_m, s->adam_v, gflat, s->nflat, s->adam_t, cfg);
             *stepped = 1;
         }
-        free(gflat);
     }
     free(rows);
     free(lab);
-    s->store_step++;
 
     /* cleanup */
     for (int32_t l = 1; l <= L; ++l) {
@@ -805,6 +799,101 @@ int go_session_batch(go_session* s, int32_t part, int64_t epoch, int train, int 
     free(hin); free(agg); free(mix); free(wt); free(outp); free(act); free(din); free(dout);
     free(xe); free(hz1); free(hr1); free(hz2);
     return 0;
+}
+
+/* grad_clip + AdamState::step (trainer.cpp:328-333, nn.cpp:20-63) */
+static void optimizer_step(go_session* s, float* g) {
+    if (s->spec.clip_max_norm > 0.0f) go_grad_clip(g, s->nflat, s->spec.clip_max_norm);
+    s->adam_t++;
+    go_adam_cfg cfg = {s->spec.lr, s->spec.beta1, s->spec.beta2, s->spec.eps};
+    go_adam_step(s->flat, s->adam_m, s->adam_v, g, s->nflat, s->adam_t, cfg);
+}
+
+int go_session_batch(go_session* s, int32_t part, int64_t epoch, int train, int push, float* acts_out,
+                     float* logits_out, double* loss_out, float* grads_out, int* stepped) {
+    (void)epoch; /* only seeds dropout, which is not restated (must be 0) */
+    float* g = zalloc(s->nflat);
+    const int rc = batch_core(s, part, train, push, acts_out, logits_out, loss_out, g, stepped);
+    if (!rc && *stepped) {
+        if (grads_out) memcpy(grads_out, g, sizeof(float) * (size_t)s->nflat);
+        optimizer_step(s, g);
+    }
+    free(g);
+    if (!rc) s->store_step++; /* advance_step once per batch (trainer.cpp:426) */
+    return rc;
+}
+
+/* ---- data-parallel GAS step — no reference counterpart; at k = 1 it IS
+ * gas_epoch. A step takes k consecutive batches of the seeded epoch order (rank j gets the
+ * j-th). Every batch sees the start-of-step parameters and histories (its own rows are
+ * fresh through compose_rows; its pushes are staged and committed after the step, Jacobi
+ * semantics); gradients are summed in rank order, divided by the number of batches that
+ * had training rows, then clipped and applied once. ---- */
+int go_session_dp_batch(go_session* s, int32_t part, float* grads_out, float* acts_out, double* loss, int* stepped) {
+    memset(grads_out, 0, sizeof(float) * (size_t)s->nflat);
+    return batch_core(s, part, 1, 0, acts_out, NULL, loss, grads_out, stepped);
+}
+
+void go_session_dp_commit(go_session* s, int32_t part, const float* acts) {
+    const go_plan* P = &s->plans[part];
+    const int32_t hd = s->hist_dim;
+    for (int32_t l = 1; l < s->L; ++l)
+        for (int32_t i = 0; i < P->nb; ++i)
+            memcpy(s->hist[l - 1] + (int64_t)P->batch[i] * hd, acts + ((int64_t)(l - 1) * P->nb + i) * hd,
+                   sizeof(float) * (size_t)hd);
+}
+
+void go_session_dp_apply(go_session* s, const float* grad_sum, int32_t count, int32_t batches) {
+    if (count > 0) {
+        float* g = zalloc(s->nflat);
+        for (int64_t e = 0; e < s->nflat; ++e) g[e] = grad_sum[e] / (float)count;
+        optimizer_step(s, g);
+        free(g);
+    }
+    s->store_step += batches;
+}
+
+int go_session_dp_epoch(go_session* s, int64_t epoch, int shuffle, int32_t k, double* loss) {
+    if (k < 1) return 1;
+    int32_t* order = malloc(sizeof(int32_t) * (size_t)s->num_parts);
+    if (shuffle) go_epoch_order(s->num_parts, s->spec.seed, epoch, order);
+    else for (int32_t i = 0; i < s->num_parts; ++i) order[i] = i;
+    float* gsum = zalloc(s->nflat);
+    float* g = zalloc(s->nflat);
+    float** acts = calloc((size_t)k, sizeof(float*));
+    double sum = 0.0;
+    int64_t cnt = 0;
+    int rc = 0;
+    for (int32_t s0 = 0; s0 < s->num_parts && !rc; s0 += k) {
+        const int32_t kk = s->num_parts - s0 < k ? s->num_parts - s0 : k;
+        memset(gsum, 0, sizeof(float) * (size_t)s->nflat);
+        int32_t count = 0;
+        for (int32_t j = 0; j < kk && !rc; ++j) {
+            const go_plan* P = &s->plans[order[s0 + j]];
+            acts[j] = zalloc((int64_t)(s->L > 1 ? s->L - 1 : 0) * P->nb * s->hist_dim);
+            double l = 0.0;
+            int stepped = 0;
+            rc = go_session_dp_batch(s, order[s0 + j], g, acts[j], &l, &stepped);
+            if (stepped) {
+                for (int64_t e = 0; e < s->nflat; ++e) gsum[e] += g[e];
+                ++count;
+                sum += l;
+                ++cnt;
+            }
+        }
+        for (int32_t j = 0; j < kk; ++j) {
+            if (!rc) go_session_dp_commit(s, order[s0 + j], acts[j]);
+            free(acts[j]);
+            acts[j] = NULL;
+        }
+        if (!rc) go_session_dp_apply(s, gsum, count, kk);
+    }
+    free(acts);
+    free(gsum);
+    free(g);
+    free(order);
+    *loss = cnt > 0 ? sum / (double)cnt : 0.0;
+    return rc;
 }
 
 int go_session_epoch(go_session* s, int64_t epoch, int shuffle, double* loss) { /* trainer.cpp:386-442 */

@@ -101,6 +101,11 @@ int go_session_batch(go_session* s, int32_t part, int64_t epoch, int train, int 
                      float* logits, double* loss, float* grads, int* stepped);
 /* One gas_epoch; *loss = mean batch loss. */
 int go_session_epoch(go_session* s, int64_t epoch, int shuffle, double* loss);
+/* data-parallel GAS step semantics (gas_oracle.c). k = 1 == go_session_epoch. */
+int go_session_dp_batch(go_session* s, int32_t part, float* grads_out, float* acts_out, double* loss, int* stepped);
+void go_session_dp_commit(go_session* s, int32_t part, const float* acts);
+void go_session_dp_apply(go_session* s, const float* grad_sum, int32_t count, int32_t batches);
+int go_session_dp_epoch(go_session* s, int64_t epoch, int shuffle, int32_t k, double* loss);
 
 #ifdef __cplusplus
 }

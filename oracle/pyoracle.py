@@ -86,6 +86,10 @@ class Oracle:
         L.go_session_set_history.argtypes = [vp, i32, vp]
         L.go_session_batch.argtypes = [vp, i32, i64, C.c_int, C.c_int, vp, vp, P(f64), vp, P(C.c_int)]
         L.go_session_epoch.argtypes = [vp, i64, C.c_int, P(f64)]
+        L.go_session_dp_batch.argtypes = [vp, i32, vp, vp, P(f64), P(C.c_int)]
+        L.go_session_dp_commit.argtypes = [vp, i32, vp]
+        L.go_session_dp_apply.argtypes = [vp, vp, i32, i32]
+        L.go_session_dp_epoch.argtypes = [vp, i64, C.c_int, i32, P(f64)]
 
     def build_graph(self, edges: np.ndarray, n: int, symmetrize=True):
         e = np.ascontiguousarray(np.asarray(edges, np.int32).reshape(-1, 2))
@@ -448,3 +452,32 @@ class Session:
         self.owner.check(self.owner.lib.ref_session_epoch(self.h, epoch, int(shuffle), int(prefetch), C.byref(loss),
                                                           C.byref(secs)))
         return loss.value, secs.value
+
+    # ---- data-parallel step semantics (C restatement only) ----
+    def dp_epoch(self, epoch, k, shuffle=True):
+        """Mean loss of one data-parallel epoch with k batches per step (k = 1: gas_epoch)."""
+        assert self.kind == "go"
+        loss = f64()
+        if self.owner.lib.go_session_dp_epoch(self.h, epoch, int(shuffle), int(k), C.byref(loss)):
+            raise ValueError("go_session_dp_epoch failed")
+        return loss.value
+
+    def dp_batch(self, part, nb):
+        """(grads, acts[(L-1), nb, hd], loss, stepped) against the current params/histories; no push, no step."""
+        assert self.kind == "go"
+        g = np.zeros(self.nparam, np.float32)
+        acts = np.zeros((max(self.spec.num_layers - 1, 0), nb, self.hist_dim), np.float32)
+        loss, st = f64(), C.c_int()
+        if self.owner.lib.go_session_dp_batch(self.h, int(part), _p(g), _p(acts) if acts.size else None,
+                                              C.byref(loss), C.byref(st)):
+            raise ValueError("go_session_dp_batch failed")
+        return g, acts, loss.value, bool(st.value)
+
+    def dp_commit(self, part, acts):
+        a = np.ascontiguousarray(acts, np.float32)
+        self.owner.lib.go_session_dp_commit(self.h, int(part), _p(a) if a.size else None)
+
+    def dp_apply(self, grad_sum, count, batches):
+        g = np.ascontiguousarray(grad_sum, np.float32)
+        self.owner.lib.go_session_dp_apply(self.h, _p(g), int(count), int(batches))
+

@@ -70,7 +70,8 @@ __device__ __forceinline__ void store_b(float (*Bs)[BN + 4], int tid, const floa
 template <int OP>
 __global__ void __launch_bounds__(256) gemm_kernel(int M, int N, int K, const float* __restrict__ A, int64_t lda,
                                                    const float* __restrict__ B, int64_t ldb, float* __restrict__ C,
-                                                   int64_t ldc, float beta, int relu, PushEpilogue push) {
+                                                   int64_t ldc, GemmEpilogue ep) {
+    const PushEpilogue& push = ep.push;
     __shared__ float As[2][BK][BM + 4];
     __shared__ float Bs[2][BK][BN + 4];
     const int tid = threadIdx.x;
@@ -125,9 +126,7 @@ __global__ void __launch_bounds__(256) gemm_kernel(int M, int N, int K, const fl
         for (int j = 0; j < 4; ++j) {
             const int n = n0 + tx + 16 * j;
             if (n >= N) continue;
-            float v = acc[i][j];
-            if (beta != 0.f) v += beta * crow[n];
-            if (relu) v = v > 0.f ? v : 0.f;
+            const float v = gemm_epilogue_value(ep, acc[i][j], crow, n);
             crow[n] = v;
             if (prow) {
                 prow[n] = v;
@@ -142,7 +141,7 @@ __global__ void __launch_bounds__(256) gemm_kernel(int M, int N, int K, const fl
 }
 
 bool launch_gemm_tc(int op, int m, int n, int k, const float* a, int64_t lda, const float* b, int64_t ldb, float* c,
-                    int64_t ldc, float beta, bool relu, const PushEpilogue* push, cudaStream_t st);
+                    int64_t ldc, const GemmEpilogue& ep, cudaStream_t st);
 
 // GEMM engine (tuning knob GASB_GEMM_TC = 1 tcgen05 3xTF32 (default) | 0 FP32 SIMT).
 static bool gemm_use_tc() {
@@ -154,21 +153,28 @@ static bool gemm_use_tc() {
 }
 
 void launch_gemm(int op, int m, int n, int k, const float* a, int64_t lda, const float* b, int64_t ldb, float* c,
-                 int64_t ldc, float beta, bool relu, const PushEpilogue* push, cudaStream_t st) {
+                 int64_t ldc, const GemmEpilogue& ep, cudaStream_t st) {
     if (m <= 0 || n <= 0) return;
-    if (gemm_use_tc() && k > 0 && launch_gemm_tc(op, m, n, k, a, lda, b, ldb, c, ldc, beta, relu, push, st)) return;
-    PushEpilogue pe{};
-    if (push) pe = *push;
-    require(op == 0 || !push, "gemm: push epilogue only for op 0");
+    require(op == 0 || !ep.push.table, "gemm: push epilogue only for op 0");
+    if (gemm_use_tc() && k > 0 && launch_gemm_tc(op, m, n, k, a, lda, b, ldb, c, ldc, ep, st)) return;
     dim3 grid(static_cast<unsigned>(ceil_div(n, BN)), static_cast<unsigned>(ceil_div(m, BM)));
     switch (op) {
-        case 0: gemm_kernel<0><<<grid, 256, 0, st>>>(m, n, k, a, lda, b, ldb, c, ldc, beta, relu, pe); break;
-        case 1: gemm_kernel<1><<<grid, 256, 0, st>>>(m, n, k, a, lda, b, ldb, c, ldc, beta, relu, pe); break;
-        case 2: gemm_kernel<2><<<grid, 256, 0, st>>>(m, n, k, a, lda, b, ldb, c, ldc, beta, relu, pe); break;
+        case 0: gemm_kernel<0><<<grid, 256, 0, st>>>(m, n, k, a, lda, b, ldb, c, ldc, ep); break;
+        case 1: gemm_kernel<1><<<grid, 256, 0, st>>>(m, n, k, a, lda, b, ldb, c, ldc, ep); break;
+        case 2: gemm_kernel<2><<<grid, 256, 0, st>>>(m, n, k, a, lda, b, ldb, c, ldc, ep); break;
         default: throw std::invalid_argument("gemm: op must be 0, 1 or 2");
     }
     ++t_launches;
     GASB_CUDA(cudaGetLastError());
+}
+
+void launch_gemm(int op, int m, int n, int k, const float* a, int64_t lda, const float* b, int64_t ldb, float* c,
+                 int64_t ldc, float beta, bool relu, const PushEpilogue* push, cudaStream_t st) {
+    GemmEpilogue ep;
+    ep.beta = beta;
+    ep.relu = relu ? 1 : 0;
+    if (push) ep.push = *push;
+    launch_gemm(op, m, n, k, a, lda, b, ldb, c, ldc, ep, st);
 }
 
 }  // namespace gasb

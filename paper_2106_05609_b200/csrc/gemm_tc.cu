@@ -110,7 +110,8 @@ template <int BN, bool A_MN, bool B_MN>
 __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_constant__ CUtensorMap tma_a,
                                                              const __grid_constant__ CUtensorMap tma_b, int M,
                                                              int N, int K, float* __restrict__ C, int64_t ldc,
-                                                             float beta, int relu, PushEpilogue push) {
+                                                             GemmEpilogue ep) {
+    const PushEpilogue& push = ep.push;
     using Lay = Layout<BN, A_MN, B_MN>;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* base = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~1023ull);
@@ -269,9 +270,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
                 for (int j = 0; j < 32; ++j) {
                     const int col = n0 + c0 + j;
                     if (col < N) {
-                        float x = sum[j];
-                        if (beta != 0.f) x += beta * crow[col];
-                        if (relu) x = x > 0.f ? x : 0.f;
+                        const float x = gemm_epilogue_value(ep, sum[j], crow, col);
                         crow[col] = x;
                         if (prow) {
                             prow[col] = x;
@@ -321,7 +320,7 @@ static bool make_tmap(const float* p, int64_t inner, int64_t outer, int64_t ld, 
 
 template <int BN, bool A_MN, bool B_MN>
 static bool launch_tc(int m, int n, int k, const float* a, int64_t lda, const float* b, int64_t ldb, float* c,
-                      int64_t ldc, float beta, bool relu, const PushEpilogue* push, cudaStream_t st) {
+                      int64_t ldc, const GemmEpilogue& ep, cudaStream_t st) {
     using Lay = Layout<BN, A_MN, B_MN>;
     CUtensorMap ta, tb;
     // A: K-major -> inner K, outer M (box 32 x 128); MN-major -> inner M, outer K (box 32 x 32)
@@ -334,11 +333,8 @@ static bool launch_tc(int m, int n, int k, const float* a, int64_t lda, const fl
                                        Lay::kSmem));
         attr = true;
     }
-    PushEpilogue pe{};
-    if (push) pe = *push;
     dim3 grid(static_cast<unsigned>(ceil_div(m, BM)), static_cast<unsigned>(ceil_div(n, BN)));
-    gemm_tc_kernel<BN, A_MN, B_MN><<<grid, kThreads, Lay::kSmem, st>>>(ta, tb, m, n, k, c, ldc, beta, relu ? 1 : 0,
-                                                                        pe);
+    gemm_tc_kernel<BN, A_MN, B_MN><<<grid, kThreads, Lay::kSmem, st>>>(ta, tb, m, n, k, c, ldc, ep);
     return true;
 }
 
@@ -347,22 +343,22 @@ static bool launch_tc(int m, int n, int k, const float* a, int64_t lda, const fl
 // Tensor-core path of launch_gemm (gemm.cu) — same contract. Returns false (nothing
 // launched) when an operand's row pitch cannot be described to TMA.
 bool launch_gemm_tc(int op, int m, int n, int k, const float* a, int64_t lda, const float* b, int64_t ldb, float* c,
-                    int64_t ldc, float beta, bool relu, const PushEpilogue* push, cudaStream_t st) {
+                    int64_t ldc, const GemmEpilogue& ep, cudaStream_t st) {
     if (m <= 0 || n <= 0) return true;
     bool ok;
     // narrow N tiles keep enough CTAs in flight for the ~1K-row batch GEMMs
     switch (op) {
         case 0:
-            ok = n <= 32 ? tc::launch_tc<32, false, true>(m, n, k, a, lda, b, ldb, c, ldc, beta, relu, push, st)
-                         : tc::launch_tc<64, false, true>(m, n, k, a, lda, b, ldb, c, ldc, beta, relu, push, st);
+            ok = n <= 32 ? tc::launch_tc<32, false, true>(m, n, k, a, lda, b, ldb, c, ldc, ep, st)
+                         : tc::launch_tc<64, false, true>(m, n, k, a, lda, b, ldb, c, ldc, ep, st);
             break;
         case 1:
-            ok = n <= 32 ? tc::launch_tc<32, false, false>(m, n, k, a, lda, b, ldb, c, ldc, beta, relu, push, st)
-                         : tc::launch_tc<64, false, false>(m, n, k, a, lda, b, ldb, c, ldc, beta, relu, push, st);
+            ok = n <= 32 ? tc::launch_tc<32, false, false>(m, n, k, a, lda, b, ldb, c, ldc, ep, st)
+                         : tc::launch_tc<64, false, false>(m, n, k, a, lda, b, ldb, c, ldc, ep, st);
             break;
         case 2:
-            ok = n <= 32 ? tc::launch_tc<32, true, true>(m, n, k, a, lda, b, ldb, c, ldc, beta, relu, push, st)
-                         : tc::launch_tc<64, true, true>(m, n, k, a, lda, b, ldb, c, ldc, beta, relu, push, st);
+            ok = n <= 32 ? tc::launch_tc<32, true, true>(m, n, k, a, lda, b, ldb, c, ldc, ep, st)
+                         : tc::launch_tc<64, true, true>(m, n, k, a, lda, b, ldb, c, ldc, ep, st);
             break;
         default: throw std::invalid_argument("gemm: op must be 0, 1 or 2");
     }

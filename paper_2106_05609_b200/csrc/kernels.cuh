@@ -76,14 +76,16 @@ int32_t spmm_box_cols();
 void launch_scan_special(const float* x, int64_t rows, int64_t ld, int32_t dim, int32_t* special, cudaStream_t st);
 // Transposed (CSC) gather, fp32 multiply-then-add in entry order (bit-exact with the
 // reference scatter). mask (optional): zero where mask <= 0 (relu backward).
+// accumulate: gx[t] continues from its current value (the reference's `g += c * gy` into
+// a grad buffer that already holds other contributions) instead of starting at 0.
 void launch_spmm_bwd(const int64_t* t_rowptr, int32_t ntargets, const int32_t* t_src, const float* t_coeffs,
                      const float* gy, int64_t ldgy, int32_t dim, const float* mask, int64_t ldm, float* gx,
-                     int64_t ldgx, cudaStream_t st, int32_t nsrc = 0);
+                     int64_t ldgx, cudaStream_t st, int32_t nsrc = 0, bool accumulate = false);
 
 // ---- GEMM (gemm.cu) -------------------------------------------------------------------
 // op 0: C = A B ; 1: C = A B^T ; 2: C = A^T B.  Row-major fp32, fp32 accumulation.
-// Epilogue (op 0 only): relu_push != nullptr -> C = relu(AB) and rows also scattered to
-// relu_push->table[ids[i]] with stamps.
+// History push fused into the epilogue (op 0 only): rows also scattered to
+// table[ids[i]] with stamps and the table's value flags.
 struct PushEpilogue {
     float* table;
     int64_t ld;
@@ -92,8 +94,31 @@ struct PushEpilogue {
     const int64_t* step;
     int32_t* special;  // the table's value flags: OR of table_flag_of(pushed values)
 };
+// Epilogue applied to each rounded fp32 result x, in the reference's op order (each step
+// one fp32 rounding, no contraction):
+//   x = x * post_scale   (scale(), tensor.cpp:254-275; 1 = skip)
+//   x = x + beta * C     (gradient accumulation; beta is 0 or 1)
+//   x = x + bias[col]    (add_rowvec, tensor.cpp:277-307; nullptr = skip)
+//   x = relu(x)          (tensor.cpp:355-372)
+//   C = x; push (table != nullptr)
+struct GemmEpilogue {
+    float beta = 0.f;
+    float post_scale = 1.f;
+    const float* bias = nullptr;
+    int relu = 0;
+    PushEpilogue push{};
+};
+void launch_gemm(int op, int m, int n, int k, const float* a, int64_t lda, const float* b, int64_t ldb, float* c,
+                 int64_t ldc, const GemmEpilogue& ep, cudaStream_t st);
 void launch_gemm(int op, int m, int n, int k, const float* a, int64_t lda, const float* b, int64_t ldb, float* c,
                  int64_t ldc, float beta, bool relu, const PushEpilogue* push, cudaStream_t st);
+__device__ __forceinline__ float gemm_epilogue_value(const GemmEpilogue& ep, float x, const float* crow, int col) {
+    if (ep.post_scale != 1.f) x = __fmul_rn(x, ep.post_scale);
+    if (ep.beta != 0.f) x = __fadd_rn(x, crow[col]);
+    if (ep.bias) x = __fadd_rn(x, ep.bias[col]);
+    if (ep.relu) x = x > 0.f ? x : 0.f;
+    return x;
+}
 
 // ---- training ops (train_ops.cu) ---------------------------------------------------
 // Softmax cross-entropy over the training rows (row_label[i] >= 0; r of them) of an m-row
@@ -108,5 +133,19 @@ void launch_adam(float* p, float* m, float* v, float* g, int64_t size, int64_t* 
                  float lr, float b1, float b2, float eps, float clip_max_norm, double* norm_scratch,
                  cudaStream_t st);
 void launch_zero(float* p, int64_t count, cudaStream_t st);
+
+// ---- residual models: APPNP / GCNII (residual.cu) ---------------------------------------
+// out[i] = alpha * h0[rows[i]] + (1 - alpha) * prop[i]  (+ optional history push of out)
+void launch_mix(const float* h0, int64_t ldh0, const int32_t* rows, const float* prop, int64_t ldp, int32_t m,
+                int32_t d, float alpha, float* out, int64_t ldo, const PushEpilogue* push, cudaStream_t st);
+// wt[l] = (1 - beta) I + beta W[l], l < layers (d x d each, dense)
+void launch_wtilde(const float* w, float* wt, int32_t layers, int32_t d, float beta, cudaStream_t st);
+// dprop = (1 - alpha) dmix ; h0g[rows[i]] += alpha dmix[i]
+void launch_mix_bwd(const float* dmix, int64_t ldd, int32_t m, int32_t d, float alpha, const int32_t* rows,
+                    float* h0g, int64_t ldh, float* dprop, int64_t ldp, cudaStream_t st);
+// out[j] = float(sum_i double(g[i, j]))
+void launch_colsum(const float* g, int64_t ldg, int32_t m, int32_t n, float* out, cudaStream_t st);
+// g = mask > 0 ? g : 0
+void launch_mask(float* g, int64_t ldg, const float* mask, int64_t ldm, int32_t m, int32_t n, cudaStream_t st);
 
 }  // namespace gasb

@@ -504,7 +504,7 @@ __global__ void __launch_bounds__(256) spmm_bwd_kernel(const int64_t* __restrict
                                                        const int32_t* __restrict__ src, const float* __restrict__ cf,
                                                        const float* __restrict__ gy, int64_t ldgy, int32_t dim,
                                                        int32_t nchunks, const float* __restrict__ mask, int64_t ldm,
-                                                       float* __restrict__ gx, int64_t ldgx) {
+                                                       float* __restrict__ gx, int64_t ldgx, int accumulate) {
     const int lane = threadIdx.x & 31;
     const int64_t w = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
     if (w >= static_cast<int64_t>(nt) * nchunks) return;
@@ -514,6 +514,11 @@ __global__ void __launch_bounds__(256) spmm_bwd_kernel(const int64_t* __restrict
     const bool active = col < dim;
     const float* gc = gy + col;
     float a0 = 0.0f, a1 = 0.0f;
+    if (accumulate && active) {
+        const float* o = gx + static_cast<int64_t>(t) * ldgx + col;
+        a0 = o[0];
+        a1 = col + 1 < dim ? o[1] : 0.0f;
+    }
     const int64_t e0 = rp[t], e1 = rp[t + 1];
     for (int64_t eb = e0; eb < e1; eb += 32) {
         const int cnt = static_cast<int>((e1 - eb) < 32 ? (e1 - eb) : 32);
@@ -565,7 +570,7 @@ constexpr int kBwdThreads = 1024;
 __global__ void __launch_bounds__(kBwdThreads) spmm_bwd_smem_kernel(
     const int64_t* __restrict__ rp, int32_t nt, const int32_t* __restrict__ src, const float* __restrict__ cf,
     const float* __restrict__ gy, int64_t ldgy, int32_t nsrc, int32_t dim, const float* __restrict__ mask,
-    int64_t ldm, float* __restrict__ gx, int64_t ldgx, int32_t targets_per_cta) {
+    int64_t ldm, float* __restrict__ gx, int64_t ldgx, int32_t targets_per_cta, int accumulate) {
     extern __shared__ float sg[];  // nsrc x kBwdCW
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
     const int32_t col0 = blockIdx.x * kBwdCW;
@@ -603,7 +608,7 @@ __global__ void __launch_bounds__(kBwdThreads) spmm_bwd_smem_kernel(
     const int32_t t_hi = min(nt, t_lo + targets_per_cta);
     for (int32_t t = t_lo + warp; t < t_hi; t += nwarps) {
         const int64_t e0 = rp[t], e1 = rp[t + 1];
-        float a = 0.0f;
+        float a = (accumulate && lane < ncol) ? gx[static_cast<int64_t>(t) * ldgx + col0 + lane] : 0.0f;
         // metadata of the next 32 entries is loaded while the current 32 are accumulated
         int64_t eb = e0;
         int cnt = static_cast<int>((e1 - eb) < 32 ? (e1 - eb) : 32);
@@ -645,7 +650,7 @@ static int g_bwd_smem_set = 0;
 
 void launch_spmm_bwd(const int64_t* t_rowptr, int32_t nt, const int32_t* t_src, const float* t_coeffs,
                      const float* gy, int64_t ldgy, int32_t dim, const float* mask, int64_t ldm, float* gx,
-                     int64_t ldgx, cudaStream_t st, int32_t nsrc) {
+                     int64_t ldgx, cudaStream_t st, int32_t nsrc, bool accumulate) {
     if (nt <= 0 || dim <= 0) return;
     const int64_t smem = static_cast<int64_t>(nsrc) * kBwdCW * sizeof(float);
     if (nsrc > 0 && smem <= 200 * 1024) {
@@ -667,7 +672,7 @@ void launch_spmm_bwd(const int64_t* t_rowptr, int32_t nt, const int32_t* t_src, 
         const int32_t per = static_cast<int32_t>(ceil_div(nt, splits));
         dim3 grid(static_cast<unsigned>(nchunks), static_cast<unsigned>(ceil_div(nt, per)));
         spmm_bwd_smem_kernel<<<grid, kBwdThreads, smem, st>>>(t_rowptr, nt, t_src, t_coeffs, gy, ldgy, nsrc, dim,
-                                                             mask, ldm, gx, ldgx, per);
+                                                             mask, ldm, gx, ldgx, per, accumulate ? 1 : 0);
         ++t_launches;
         GASB_CUDA(cudaGetLastError());
         return;
@@ -676,7 +681,7 @@ void launch_spmm_bwd(const int64_t* t_rowptr, int32_t nt, const int32_t* t_src, 
     const int32_t nchunks = static_cast<int32_t>(ceil_div(dim, kChunk));
     const int64_t blocks = ceil_div(static_cast<int64_t>(nt) * nchunks, 8);
     spmm_bwd_kernel<<<static_cast<unsigned>(blocks), 256, 0, st>>>(t_rowptr, nt, t_src, t_coeffs, gy, ldgy, dim,
-                                                                   nchunks, mask, ldm, gx, ldgx);
+                                                                   nchunks, mask, ldm, gx, ldgx, accumulate ? 1 : 0);
     ++t_launches;
     GASB_CUDA(cudaGetLastError());
 }

@@ -238,9 +238,38 @@ struct gasb_trainer_s {
             tm_ok[1] = tm_ok[1] && make_row_tmap(history_table(hist, l), n, hist_dim, history_ld(hist), bc,
                                                  &tm_hist[l - 1]);
         if (x_ext.p) tm_ok[2] = make_row_tmap(x_ext.p, ne_max, F, ldF, bc, &tm_xext);
-        if (h_ext.p) tm_ok[3] = make_row_tmap(h_ext.p, ne_max, H, ldH, bc, &tm_hext);
+        const int32_t hdim = residual ? D : H;
+        if (h_ext.p) tm_ok[3] = make_row_tmap(h_ext.p, ne_max, hdim, ld_of(hdim), bc, &tm_hext);
+        if (residual && h0.p) tm_h0_ok = make_row_tmap(h0.p, ne_max, D, ldD, bc, &tm_h0);
     }
     DevBuf<double> loss, row_scratch;
+
+    // ---- residual models: APPNP (kind 2) / GCNII (kind 3) ----
+    bool residual = false;
+    int32_t D = 0;      // width of every propagation layer and of the histories (GCNII: H, APPNP: C)
+    int64_t ldD = 0, ldA = 0;  // ldA: row pitch of act[l] (GCN: ldH)
+    int32_t p_hw1 = -1, p_hb1 = -1, p_hw2 = -1, p_hb2 = -1, p_ow = -1, p_ob = -1;  // param indices
+    DevBuf<int32_t> brow;                  // batch_local_rows per part, at row_off
+    DevBuf<int64_t> a_rowptr;              // CSC over ALL edges of a batch (targets = V_b local rows)
+    DevBuf<int32_t> a_src;                 //   entries: batch row r, ascending r per target
+    DevBuf<float> a_cf;
+    std::vector<int64_t> a_off;            // per part: offset of its ne+1 row pointers
+    DevBuf<float> h0, z, h0g, zg, wt, prop, gmix, dprop, gout;
+    std::vector<DevBuf<float>> mixed;      // GCNII: mixed_l (needed for dW~_l)
+    CUtensorMap tm_h0{};
+    bool tm_h0_ok = false;
+    float* P(int32_t i) { return params.p + poff[i]; }
+    float* G(int32_t i) { return grads.p + poff[i]; }
+    int32_t add_param(int64_t r, int64_t c) {
+        poff.push_back(nparam);
+        prow.push_back(r);
+        pcol.push_back(c);
+        nparam += r * c;
+        return static_cast<int32_t>(poff.size()) - 1;
+    }
+    void build_residual(const std::vector<int64_t>& h_arp, const std::vector<int32_t>& h_asrc,
+                        const std::vector<float>& h_acf, const std::vector<int32_t>& h_brow);
+    void enqueue_batch_res(int32_t p, bool train, bool push, bool fused);
 
     // graphs
     std::vector<cudaGraphExec_t> graphs;
@@ -290,16 +319,22 @@ void gasb_trainer_s::build(const float* h_features, const int32_t* h_labels, con
     num_parts = sched->num_parts;
     L = spec.num_layers;
     H = spec.hidden;
-    require(spec.kind == 0, "trainer: only GCN (kind 0) is implemented on the device path in this build");
+    require(spec.kind == 0 || spec.kind == 2 || spec.kind == 3,
+            "trainer: the device path implements GCN, APPNP and GCNII (GIN is out of scope)");
     require(L >= 1 && H > 0 && F > 0 && C > 0, "trainer: bad model dims");
     require(spec.dropout == 0.0f, "trainer: dropout > 0 is not supported by the device path yet");
-    hist_dim = L >= 2 ? H : 0;
-    dims.assign(static_cast<size_t>(L) + 1, H);
+    require(spec.l2_weight == 0.0f, "trainer: l2_weight > 0 is not supported by the device path yet");
+    residual = spec.kind != 0;
+    D = spec.kind == 2 ? C : H;  // Model::history_dim (trainer.cpp:130-140)
+    hist_dim = L >= 2 ? (residual ? D : H) : 0;
+    dims.assign(static_cast<size_t>(L) + 1, residual ? D : H);
     dims[0] = F;
-    dims[L] = C;
+    if (!residual) dims[L] = C;
     ldF = ld_of(F);
     ldH = ld_of(H);
     ldC = ld_of(C);
+    ldD = ld_of(D);
+    ldA = residual ? ldD : ldH;
 
     // ---- per-part sizes and offsets ----
     nb.resize(num_parts);
@@ -343,6 +378,18 @@ void gasb_trainer_s::build(const float* h_features, const int32_t* h_labels, con
     std::vector<float> h_tcf(T);
     std::vector<int64_t> h_rp(R + 1), h_trp(R + num_parts);
     h_rp[R] = E;
+    // residual models: batch_local_rows, and the all-edge CSC for the layer-1 backward
+    std::vector<int32_t> h_brow, h_asrc;
+    std::vector<float> h_acf;
+    std::vector<int64_t> h_arp;
+    if (residual) {
+        h_brow.resize(R);
+        h_asrc.resize(E);
+        h_acf.resize(E);
+        h_arp.resize(NE + num_parts);
+        a_off.resize(num_parts);
+        for (int32_t p = 0; p < num_parts; ++p) a_off[p] = ext_off[p] + p;
+    }
 #pragma omp parallel for schedule(dynamic, 1)
     for (int32_t p = 0; p < num_parts; ++p) {
         const HostPlan& P = sched->plans[p];
@@ -390,6 +437,22 @@ void gasb_trainer_s::build(const float* h_features, const int32_t* h_labels, con
         for (int32_t i = 0; i < ne[p]; ++i) {
             h_ext[ext_off[p] + i] = P.extended[i];
             h_cidx[ext_off[p] + i] = P.is_halo[i] ? -(hk++) - 1 : local2batch[i];
+        }
+        if (residual) {
+            for (int32_t i = 0; i < nb[p]; ++i) h_brow[r0 + i] = P.batch_local_rows[i];
+            // transposed stencil over every V_b target (tensor.cpp:531-549 writes all rows of
+            // h_in; layer 1 of APPNP/GCNII keeps the halo rows)
+            std::vector<int64_t> ac(static_cast<size_t>(ne[p]) + 1, 0);
+            for (int32_t c : P.gcn_cols) ac[c + 1]++;
+            for (int32_t t = 0; t < ne[p]; ++t) ac[t + 1] += ac[t];
+            int64_t* arp = h_arp.data() + a_off[p];
+            for (int32_t t = 0; t <= ne[p]; ++t) arp[t] = e0 + ac[t];
+            for (int32_t r = 0; r < nb[p]; ++r)
+                for (int64_t e = P.gcn_rowptr[r]; e < P.gcn_rowptr[r + 1]; ++e) {
+                    const int64_t k = e0 + ac[P.gcn_cols[e]]++;
+                    h_asrc[k] = r;
+                    h_acf[k] = P.gcn_coeffs[e];
+                }
         }
     }
     for (int32_t i = 0; i < static_cast<int32_t>(h_trl.size()); ++i)
@@ -439,19 +502,32 @@ void gasb_trainer_s::build(const float* h_features, const int32_t* h_labels, con
     ce_done.alloc(1);
     ce_done.zero();
 
-    // ---- Model::build (trainer.cpp:55-129), GCN: W_l (d_{l-1} x d_l) ----
+    // ---- Model::build (trainer.cpp:55-129); params in Model::params() order ----
     layer_param.assign(static_cast<size_t>(L) + 1, -1);
-    for (int32_t l = 1; l <= L; ++l) {
-        layer_param[l] = static_cast<int32_t>(poff.size());
-        poff.push_back(nparam);
-        prow.push_back(dims[l - 1]);
-        pcol.push_back(dims[l]);
-        nparam += static_cast<int64_t>(dims[l - 1]) * dims[l];
+    if (!residual) {  // GCN: W_l (d_{l-1} x d_l)
+        for (int32_t l = 1; l <= L; ++l) layer_param[l] = add_param(dims[l - 1], dims[l]);
+    } else {  // head_w1, head_b1, [head_w2, head_b2], [W_l], [out_w, out_b]
+        p_hw1 = add_param(F, H);
+        p_hb1 = add_param(1, H);
+        if (spec.kind == 2) {
+            p_hw2 = add_param(H, C);
+            p_hb2 = add_param(1, C);
+        } else {
+            for (int32_t l = 1; l <= L; ++l) layer_param[l] = add_param(H, H);
+            p_ow = add_param(H, C);
+            p_ob = add_param(1, C);
+        }
     }
     h_params_init.assign(static_cast<size_t>(nparam), 0.0f);
+    auto glorot_at = [&](int32_t i, uint64_t seed) {
+        glorot_init(h_params_init.data() + poff[i], prow[i], pcol[i], seed);
+    };
     for (int32_t l = 1; l <= L; ++l)  // Layer::build(cfg, derive_seed(seed,10,l)) -> glorot(derive_seed(.,1))
-        glorot_init(h_params_init.data() + poff[layer_param[l]], dims[l - 1], dims[l],
-                    derive_seed(derive_seed(spec.seed, 10, static_cast<uint64_t>(l)), 1));
+        if (layer_param[l] >= 0)
+            glorot_at(layer_param[l], derive_seed(derive_seed(spec.seed, 10, static_cast<uint64_t>(l)), 1));
+    if (p_hw1 >= 0) glorot_at(p_hw1, derive_seed(spec.seed, 20, 1));  // seed_for(20, 1)
+    if (p_hw2 >= 0) glorot_at(p_hw2, derive_seed(spec.seed, 20, 2));
+    if (p_ow >= 0) glorot_at(p_ow, derive_seed(spec.seed, 30, 1));
     params.upload(h_params_init);
     grads.alloc(nparam);
     grads.zero();
@@ -470,9 +546,13 @@ void gasb_trainer_s::build(const float* h_features, const int32_t* h_labels, con
     // ---- activations ----
     agg.resize(static_cast<size_t>(L) + 1);
     act.resize(static_cast<size_t>(L) + 1);
-    for (int32_t l = 1; l <= L; ++l) agg[l].alloc(static_cast<int64_t>(nb_max) * ld_of(dims[l - 1]));
-    for (int32_t l = 1; l < L; ++l) act[l].alloc(static_cast<int64_t>(nb_max) * ldH);
-    if (opt.hoist_layer1) agg_all.alloc(R * ldF);
+    if (!residual) {
+        for (int32_t l = 1; l <= L; ++l) agg[l].alloc(static_cast<int64_t>(nb_max) * ld_of(dims[l - 1]));
+        for (int32_t l = 1; l < L; ++l) act[l].alloc(static_cast<int64_t>(nb_max) * ldH);
+        if (opt.hoist_layer1) agg_all.alloc(R * ldF);
+    } else {
+        build_residual(h_arp, h_asrc, h_acf, h_brow);
+    }
     logits.alloc(static_cast<int64_t>(nb_max) * ldC);
     glogits.alloc(static_cast<int64_t>(nb_max) * ldC);
     g_agg.alloc(static_cast<int64_t>(nb_max) * std::max(ldH, ldC));
@@ -490,7 +570,164 @@ void gasb_trainer_s::enqueue_hoisted() {
                     counters.p, max_chunks, stream, source_flags(1), source_tmap(1));
 }
 
+void gasb_trainer_s::build_residual(const std::vector<int64_t>& h_arp, const std::vector<int32_t>& h_asrc,
+                                    const std::vector<float>& h_acf, const std::vector<int32_t>& h_brow) {
+    brow.upload(h_brow);
+    a_rowptr.upload(h_arp);
+    a_src.upload(h_asrc);
+    a_cf.upload(h_acf);
+    const int64_t nbm = nb_max, nem = ne_max;
+    h0.alloc(nem * ldD);
+    h0g.alloc(nem * ldD);
+    if (spec.kind == 2) {
+        z.alloc(nem * ldH);
+        zg.alloc(nem * ldH);
+    } else {
+        wt.alloc(static_cast<int64_t>(L) * H * H);
+        mixed.resize(static_cast<size_t>(L) + 1);
+        for (int32_t l = 1; l <= L; ++l) mixed[l].alloc(nbm * ldD);
+    }
+    for (int32_t l = 1; l <= L; ++l)
+        if (l < L || spec.kind == 3) act[l].alloc(nbm * ldD);
+    prop.alloc(nbm * ldD);
+    gmix.alloc(nbm * ldD);
+    dprop.alloc(nbm * ldD);
+    gout.alloc(nbm * ldD);
+}
+
+// APPNP / GCNII batch: Model::forward (trainer.cpp:174-251) with head_forward over all V_b
+// rows (:142-163), appnp/gcnii layers (layers.cpp:150-168), the GCNII output head
+// (:221-227), then run_batch's backward (halo rows of h0 receive the layer-1 aggregation
+// gradient) and Adam.
+void gasb_trainer_s::enqueue_batch_res(int32_t p, bool train, bool push, bool fused) {
+    const int32_t m = nb[p], me = ne[p];
+    const int64_t r0 = row_off[p];
+    const SpmmSegs segs = seg_batch.segs(p);
+    const int32_t* bn = batch_nodes.p + r0;
+    const int32_t* br = brow.p + r0;
+    const bool gcnii = spec.kind == 3;
+    // ---- head_forward over the extended rows: x_ext = X[V_b] (gather_features, trainer.cpp:20-27)
+    launch_rows(1, extended.p + ext_off[p], me, X.p, ldF, x_ext.p, ldF, F, n, nullptr, nullptr, nullptr, stream);
+    {
+        GemmEpilogue e1;
+        e1.bias = P(p_hb1);
+        e1.relu = 1;
+        launch_gemm(0, me, H, F, x_ext.p, ldF, P(p_hw1), H, gcnii ? h0.p : z.p, gcnii ? ldD : ldH, e1, stream);
+        if (!gcnii) {
+            GemmEpilogue e2;
+            e2.bias = P(p_hb2);
+            launch_gemm(0, me, C, H, z.p, ldH, P(p_hw2), C, h0.p, ldD, e2, stream);
+        }
+    }
+    if (gcnii) launch_wtilde(P(layer_param[1]), wt.p, L, H, spec.beta, stream);
+    // ---- propagation layers ----
+    for (int32_t l = 1; l <= L; ++l) {
+        if (l == 1) {  // input = h0 over V_b (local ids)
+            launch_spmm_fwd(segs, cols_l.p, coef64.p, h0.p, ldD, D, prop.p, ldD, r0, partial_batch.p, pld, counters.p,
+                            max_chunks, stream, nullptr, tm_h0_ok ? &tm_h0 : nullptr);
+        } else if (fused) {  // pull-free: H_{l-1} by global id
+            launch_spmm_fwd(segs, cols_g.p, coef64.p, history_table(hist, l - 1), history_ld(hist), D, prop.p, ldD, r0,
+                            partial_batch.p, pld, counters.p, max_chunks, stream, source_flags(l), source_tmap(l));
+        } else {  // pull halos, compose_rows, SpMM over local ids
+            launch_rows(1, halo_ids.p + (ext_off[p] - row_off[p]), nh[p], history_table(hist, l - 1),
+                        history_ld(hist), halo_buf.p, ldD, D, n, nullptr, nullptr, nullptr, stream);
+            const int64_t blocks = ceil_div(static_cast<int64_t>(me) * 32, 256);
+            compose_kernel<<<static_cast<unsigned>(blocks), 256, 0, stream>>>(compose_idx.p + ext_off[p],
+                                                                               act[l - 1].p, ldD, halo_buf.p, ldD, me,
+                                                                               D, h_ext.p, ldD);
+            ++t_launches;
+            GASB_CUDA(cudaGetLastError());
+            launch_spmm_fwd(segs, cols_l.p, coef64.p, h_ext.p, ldD, D, prop.p, ldD, r0, partial_batch.p, pld,
+                            counters.p, max_chunks, stream, push ? source_flags(l) : nullptr,
+                            tm_ok[3] ? &tm_hext : nullptr);
+        }
+        PushEpilogue pe{history_table(hist, l), history_ld(hist), bn, history_stamps(hist, l),
+                        history_step_ptr(hist), history_flags(hist, l)};
+        const bool do_push = push && l < L;
+        if (gcnii) {
+            launch_mix(h0.p, ldD, br, prop.p, ldD, m, D, spec.alpha, mixed[l].p, ldD, nullptr, stream);
+            GemmEpilogue e;  // act_l = relu(mixed_l . W~_l), pushed for l < L
+            e.relu = 1;
+            if (do_push) e.push = pe;
+            launch_gemm(0, m, H, H, mixed[l].p, ldD, wt.p + static_cast<int64_t>(l - 1) * H * H, H, act[l].p, ldD, e,
+                        stream);
+            if (l == L) {  // relu -> out_w, out_b (trainer.cpp:221-227)
+                GemmEpilogue eo;
+                eo.bias = P(p_ob);
+                launch_gemm(0, m, C, H, act[L].p, ldD, P(p_ow), C, logits.p, ldC, eo, stream);
+            }
+        } else {  // APPNP: out = alpha h0[B] + (1 - alpha) prop, pushed raw (no relu)
+            launch_mix(h0.p, ldD, br, prop.p, ldD, m, D, spec.alpha, l < L ? act[l].p : logits.p, l < L ? ldD : ldC,
+                       do_push ? &pe : nullptr, stream);
+        }
+    }
+    // ---- loss + backward ----
+    const bool stepped = ntrain[p] > 0 && train;
+    if (ntrain[p] > 0)
+        launch_softmax_ce(logits.p, ldC, m, C, row_label.p + r0, ntrain[p], glogits.p, ldC, loss.p + p,
+                          row_scratch.p, ce_done.p, stream);
+    if (stepped) {
+        const GemmEpilogue plain;
+        const float* dout = glogits.p;
+        int64_t ldo = ldC;
+        if (gcnii) {  // output head: d out_w, d out_b, then relu backward into d act_L
+            launch_gemm(2, H, C, m, act[L].p, ldD, glogits.p, ldC, G(p_ow), C, plain, stream);
+            launch_colsum(glogits.p, ldC, m, C, G(p_ob), stream);
+            launch_gemm(1, m, H, C, glogits.p, ldC, P(p_ow), C, gout.p, ldD, plain, stream);
+            launch_mask(gout.p, ldD, act[L].p, ldD, m, H, stream);
+            dout = gout.p;
+            ldo = ldD;
+        }
+        launch_zero(h0g.p, static_cast<int64_t>(me) * ldD, stream);
+        for (int32_t l = L; l >= 1; --l) {
+            const float* dmix = dout;
+            int64_t ldm = ldo;
+            if (gcnii) {  // out_l = mixed_l . W~_l
+                GemmEpilogue ew;  // dW_l = beta * (mixed_l^T dout) (scale bwd of W~)
+                ew.post_scale = spec.beta;
+                launch_gemm(2, H, H, m, mixed[l].p, ldD, dout, ldo, G(layer_param[l]), H, ew, stream);
+                launch_gemm(1, m, H, H, dout, ldo, wt.p + static_cast<int64_t>(l - 1) * H * H, H, gmix.p, ldD, plain,
+                            stream);
+                dmix = gmix.p;
+                ldm = ldD;
+            }
+            launch_mix_bwd(dmix, ldm, m, D, spec.alpha, br, h0g.p, ldD, dprop.p, ldD, stream);
+            if (l >= 2) {  // to act_{l-1}'s batch rows (compose bwd), relu mask for GCNII
+                launch_spmm_bwd(t_rowptr.p + r0 + p, m, t_src.p, t_cf.p, dprop.p, ldD, D, gcnii ? act[l - 1].p : nullptr,
+                                ldD, gout.p, ldD, stream, m);
+                dout = gout.p;
+                ldo = ldD;
+            } else {  // layer 1: every V_b row of h0, accumulated onto the residual terms
+                launch_spmm_bwd(a_rowptr.p + a_off[p], me, a_src.p, a_cf.p, dprop.p, ldD, D, nullptr, 0, h0g.p, ldD,
+                                stream, m, true);
+            }
+        }
+        // head backward (x_ext carries no gradient)
+        if (gcnii) {
+            launch_mask(h0g.p, ldD, h0.p, ldD, me, H, stream);
+            launch_colsum(h0g.p, ldD, me, H, G(p_hb1), stream);
+            launch_gemm(2, F, H, me, x_ext.p, ldF, h0g.p, ldD, G(p_hw1), H, plain, stream);
+        } else {
+            launch_colsum(h0g.p, ldD, me, C, G(p_hb2), stream);
+            launch_gemm(2, H, C, me, z.p, ldH, h0g.p, ldD, G(p_hw2), C, plain, stream);
+            launch_gemm(1, me, H, C, h0g.p, ldD, P(p_hw2), C, zg.p, ldH, plain, stream);
+            launch_mask(zg.p, ldH, z.p, ldH, me, H, stream);
+            launch_colsum(zg.p, ldH, me, H, G(p_hb1), stream);
+            launch_gemm(2, F, H, me, x_ext.p, ldF, zg.p, ldH, G(p_hw1), H, plain, stream);
+        }
+        launch_adam(params.p, adam_m.p, adam_v.p, grads.p, nparam, t_counter.p, bc.p, spec.lr, spec.beta1,
+                    spec.beta2, spec.eps, spec.clip_max_norm, norm_scratch.p, stream);
+    }
+    end_batch_kernel<<<1, 1, 0, stream>>>(history_step_ptr(hist), t_counter.p, stepped ? 1 : 0);
+    ++t_launches;
+    GASB_CUDA(cudaGetLastError());
+}
+
 void gasb_trainer_s::enqueue_batch(int32_t p, bool train, bool push, bool use_hoisted, bool fused) {
+    if (residual) {
+        enqueue_batch_res(p, train, push, fused);
+        return;
+    }
     const int32_t m = nb[p];
     const int64_t r0 = row_off[p];
     const SpmmSegs segs = seg_batch.segs(p);
@@ -585,7 +822,7 @@ void gasb_trainer_s::run_epoch(int64_t epoch, bool shuffle) {
     int64_t steps = 0;
     for (int32_t p : order) steps += ntrain[p] > 0 ? 1 : 0;
     ensure_bc(t_host + steps + 2);
-    const bool hoisted = opt.hoist_layer1 && opt.fused;
+    const bool hoisted = opt.hoist_layer1 && opt.fused && !residual;
     const int64_t l0 = t_launches;
     if (hoisted) enqueue_hoisted();
     epoch_launches = t_launches - l0;
@@ -705,11 +942,11 @@ gasb_status gasb_trainer_batch(gasb_trainer t, int32_t part, int64_t epoch, int3
         if (st) t->t_host++;
         GASB_CUDA(cudaStreamSynchronize(t->stream));
         const int32_t m = t->nb[part];
-        if (h_acts)
+        const int32_t hd = t->hist_dim;
+        if (h_acts && hd > 0)
             for (int32_t l = 1; l < t->L; ++l)
-                GASB_CUDA(cudaMemcpy2D(h_acts + static_cast<int64_t>(l - 1) * m * t->H, sizeof(float) * t->H,
-                                       t->act[l].p, sizeof(float) * t->ldH, sizeof(float) * t->H, m,
-                                       cudaMemcpyDeviceToHost));
+                GASB_CUDA(cudaMemcpy2D(h_acts + static_cast<int64_t>(l - 1) * m * hd, sizeof(float) * hd, t->act[l].p,
+                                       sizeof(float) * t->ldA, sizeof(float) * hd, m, cudaMemcpyDeviceToHost));
         if (h_logits)
             GASB_CUDA(cudaMemcpy2D(h_logits, sizeof(float) * t->C, t->logits.p, sizeof(float) * t->ldC,
                                    sizeof(float) * t->C, m, cudaMemcpyDeviceToHost));
@@ -776,6 +1013,7 @@ gasb_status gasb_trainer_profile_spmm(gasb_trainer t, int32_t part, int32_t laye
         require(t && avg_ms && iters > 0, "trainer: bad argument");
         require(part < t->num_parts && layer >= 1 && layer <= t->L, "trainer: part/layer out of range");
         require(part >= 0 || (layer == 1 && t->agg_all.p), "trainer: hoisted profile needs hoist_layer1");
+        require(!t->residual || layer >= 2, "trainer: APPNP/GCNII layer 1 aggregates the per-batch head output");
         cudaEvent_t a, b;
         GASB_CUDA(cudaEventCreate(&a));
         GASB_CUDA(cudaEventCreate(&b));
@@ -788,7 +1026,8 @@ gasb_status gasb_trainer_profile_spmm(gasb_trainer t, int32_t part, int32_t laye
             const SpmmSegs segs = t->seg_batch.segs(part);
             const float* src = layer == 1 ? t->X.p : history_table(t->hist, layer - 1);
             const int64_t lds = layer == 1 ? t->ldF : history_ld(t->hist);
-            launch_spmm_fwd(segs, t->cols_g.p, t->coef64.p, src, lds, din, t->agg[layer].p, t->ld_of(din),
+            float* out = t->residual ? t->prop.p : t->agg[layer].p;
+            launch_spmm_fwd(segs, t->cols_g.p, t->coef64.p, src, lds, din, out, t->ld_of(din),
                             t->row_off[part], t->partial_batch.p, t->pld,
                             t->counters.p, t->max_chunks, t->stream, t->source_flags(layer),
                             t->source_tmap(layer));

@@ -111,7 +111,8 @@ class GasTrainer:
     def batch(self, part: int, epoch: int = 0, train: bool = True, push: bool = True):
         """One batch with capture: (acts[(L-1), nb, hd], logits[nb, C], loss, grads|None, stepped)."""
         nb = int(self.schedule.sizes(part)[0])
-        L, hd = self.spec.num_layers, self.spec.hidden
+        L = self.spec.num_layers
+        hd = self.num_classes if self.spec.kind == "appnp" else self.spec.hidden  # Model::history_dim
         acts = np.zeros((max(L - 1, 0), nb, hd), np.float32)
         logits = np.zeros((nb, self.num_classes), np.float32)
         grads = np.zeros(self.num_param_floats, np.float32)

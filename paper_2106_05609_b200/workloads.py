@@ -43,6 +43,8 @@ WORKLOADS = {
     "pubmed_gcnii": Workload("pubmed_gcnii", 19717, 44700, 8, 0.8, 60.0, 500, 3, "gcnii", 64, 64),
     "reddit": Workload("reddit", 232965, 65_300_000, 200, 0.335, 120.0, 602, 41, "gcn", 4, 256),
     # down-scaled shapes for fast parity runs
+    "cora_appnp": Workload("cora_appnp", 2708, 5570, 10, 0.87, 60.0, 1433, 7, "appnp", 3, 64),
+    "cora_gcnii": Workload("cora_gcnii", 2708, 5570, 10, 0.87, 60.0, 1433, 7, "gcnii", 8, 64),
     "reddit_mini": Workload("reddit_mini", 12000, 1_200_000, 12, 0.4, 60.0, 602, 41, "gcn", 4, 256),
 }
 

@@ -1,0 +1,95 @@
+// C++ shim (include/gasb/gas.hpp) compiled against libgasb.so and run on the host.
+// Host-only parts run everywhere: Graph, BatchSchedule (plans + gcn stencil) and the error
+// mapping. Device parts (HistoryStore, Trainer) run when a GPU is present; without one the
+// constructor must fail with std::runtime_error (CUDA error), never silently.
+//
+// Known answers: SPEC.md:278-279 (GCN on the path P3, W = I, h = 1: node 0 -> 1/2 + 1/sqrt 6).
+#include <cmath>
+#include <cstdio>
+#include <stdexcept>
+#include <vector>
+
+#include "gasb/gas.hpp"
+
+using namespace gas::b200;
+
+static int failures = 0;
+#define EXPECT(c)                                                    \
+    do {                                                             \
+        if (!(c)) {                                                  \
+            std::fprintf(stderr, "FAIL %s:%d: %s\n", __FILE__, __LINE__, #c); \
+            ++failures;                                              \
+        }                                                            \
+    } while (0)
+
+template <class E, class F>
+static bool throws(F&& f) {
+    try {
+        f();
+    } catch (const E&) {
+        return true;
+    } catch (...) {
+        return false;
+    }
+    return false;
+}
+
+int main() {
+    // P3: 0 - 1 - 2 (undirected), symmetrized
+    std::vector<NodeId> src{0, 1}, dst{1, 2};
+    Graph g = Graph::build(src, dst, 3);
+    EXPECT(g.num_nodes() == 3);
+    EXPECT(g.num_edges() == 4);
+    EXPECT(g.row_offsets()[3] == 4);
+
+    // one part -> no halos; stencil of node 0 = [(1, 1/sqrt(2*3)), (0, 1/2)] (self term last)
+    std::vector<std::int32_t> one{0, 0, 0};
+    BatchSchedule s1 = BatchSchedule::build(g, one, 1);
+    BatchPlan p = s1.plan(0);
+    EXPECT(p.halo_nodes.empty());
+    EXPECT(p.gcn_row_ptr.size() == 4 && p.gcn_row_ptr[1] == 2);
+    EXPECT(p.gcn_cols[0] == 1 && p.gcn_cols[1] == 0);
+    EXPECT(p.gcn_coeffs[0] == static_cast<float>(1.0 / (std::sqrt(2.0) * std::sqrt(3.0))));
+    EXPECT(p.gcn_coeffs[1] == static_cast<float>(1.0 / (std::sqrt(2.0) * std::sqrt(2.0))));
+    const double y0 = static_cast<double>(p.gcn_coeffs[0]) + p.gcn_coeffs[1];  // h = 1, W = I
+    EXPECT(std::fabs(y0 - (0.5 + 1.0 / std::sqrt(6.0))) < 1e-7);
+
+    // two parts {0,1} | {2}: part 0 sees node 2 as its halo
+    std::vector<std::int32_t> two{0, 0, 1};
+    BatchSchedule s2 = BatchSchedule::build(g, two, 2);
+    EXPECT(s2.num_parts() == 2);
+    BatchPlan q = s2.plan(0);
+    EXPECT(q.batch_nodes == (std::vector<NodeId>{0, 1}));
+    EXPECT(q.halo_nodes == (std::vector<NodeId>{2}));
+    EXPECT(q.extended_nodes == (std::vector<NodeId>{0, 1, 2}));
+
+    // error mapping (make_batch_plan / build_graph throw std::invalid_argument)
+    std::vector<NodeId> bad_src{0}, bad_dst{7};
+    EXPECT(throws<std::invalid_argument>([&] { Graph::build(bad_src, bad_dst, 3); }));
+    std::vector<std::int32_t> bad_assign{0, 0, 5};
+    EXPECT(throws<std::invalid_argument>([&] { BatchSchedule::build(g, bad_assign, 2); }));
+    EXPECT(throws<std::invalid_argument>([&] { s2.plan(9); }));
+
+    // device part: HistoryStore push -> pull identity, fresh rows are zeros
+    bool have_gpu = true;
+    try {
+        HistoryStore h(3, 3, 4);
+        std::vector<NodeId> ids{2, 0};
+        std::vector<float> rows{1, 2, 3, 4, 5, 6, 7, 8};
+        h.push(1, ids, rows);
+        DenseMatrix got = h.pull(1, std::vector<NodeId>{0, 1, 2});
+        EXPECT(got.row(0)[0] == 5 && got.row(1)[3] == 0 && got.row(2)[3] == 4);
+        EXPECT(h.last_push_step(1, 2) == 0 && h.last_push_step(1, 1) == -1);
+        h.advance_step();
+        EXPECT(h.step() == 1);
+        EXPECT(throws<std::invalid_argument>([&] { h.pull(4, ids); }));  // layer out of [1, 3]
+        EXPECT(throws<std::invalid_argument>([&] { h.pull(0, ids); }));
+        std::vector<NodeId> oob{3};
+        EXPECT(throws<std::invalid_argument>([&] { h.pull(1, oob); }));  // id out of range
+    } catch (const std::runtime_error& e) {
+        have_gpu = false;
+        std::printf("no device: %s\n", e.what());
+    }
+    std::printf("%s %d failures\n", have_gpu ? "gpu" : "host-only", failures);
+    return failures == 0 ? 0 : 1;
+}

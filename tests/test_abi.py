@@ -31,3 +31,22 @@ def test_error_status_maps_to_reference_exception():
     with pytest.raises(ValueError):
         gb.build_graph([[0, 9]], 2)
     assert "out of range" in gb.lib.gasb_last_error().decode()
+
+
+def _build_shim_test(tmp_path):
+    import subprocess
+    exe = tmp_path / "test_shim"
+    cmd = ["g++", "-std=c++20", "-O1", "-Wall", "-Werror", f"-I{ROOT / 'include'}", str(ROOT / "tests" / "cpp" / "test_shim.cpp"),
+           "-o", str(exe), f"-L{gb.LIB_PATH.parent}", "-lgasb", f"-Wl,-rpath,{gb.LIB_PATH.parent}"]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    return exe
+
+
+def test_cpp_shim_host_parts(tmp_path):
+    """include/gasb/gas.hpp compiles -Werror against gasb.h, links libgasb.so, and its host parts
+    (Graph, BatchSchedule, error mapping) pass; device parts fail loudly without a GPU."""
+    import subprocess
+    r = subprocess.run([str(_build_shim_test(tmp_path))], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "0 failures" in r.stdout
