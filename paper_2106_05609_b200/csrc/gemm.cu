@@ -184,6 +184,14 @@ extern "C" gasb_status gasb_gemm(int32_t op, int32_t m, int32_t n, int32_t k, co
     return gasb::guard([&] {
         gasb::require(m >= 0 && n >= 0 && k >= 0, "matmul: negative shape");
         gasb::require(beta == 0.f || beta == 1.f, "matmul: beta must be 0 or 1");
+        // split-K scratch for the standalone entry point (allocated once, never captured)
+        static float* ws = nullptr;
+        constexpr int64_t kWsFloats = 148LL * 128 * 64 + 4096;
+        if (!ws) GASB_CUDA(cudaMalloc(&ws, sizeof(float) * kWsFloats));
+        gasb::set_gemm_workspace(ws, kWsFloats);
+        struct Reset {
+            ~Reset() { gasb::set_gemm_workspace(nullptr, 0); }
+        } reset;
         gasb::launch_gemm(op, m, n, k, a, lda, b, ldb, c, ldc, beta, false, nullptr, gasb::as_stream(stream));
     });
 }

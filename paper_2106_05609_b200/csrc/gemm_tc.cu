@@ -18,6 +18,24 @@
 #include "kernels.cuh"
 
 namespace gasb {
+
+thread_local float* t_gemm_ws = nullptr;
+thread_local int64_t t_gemm_ws_floats = 0;
+void set_gemm_workspace(float* ws, int64_t floats) {
+    t_gemm_ws = ws;
+    t_gemm_ws_floats = ws ? floats : 0;
+}
+
+static int num_sms() {
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        GASB_CUDA(cudaGetDevice(&dev));
+        GASB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    }
+    return sms;
+}
+
 namespace tc {
 
 constexpr int BM = 128, BK = 32, kStagesTC = 3;
@@ -110,7 +128,7 @@ template <int BN, bool A_MN, bool B_MN>
 __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_constant__ CUtensorMap tma_a,
                                                              const __grid_constant__ CUtensorMap tma_b, int M,
                                                              int N, int K, float* __restrict__ C, int64_t ldc,
-                                                             GemmEpilogue ep) {
+                                                             GemmEpilogue ep, int kbs, float* __restrict__ ws) {
     const PushEpilogue& push = ep.push;
     using Lay = Layout<BN, A_MN, B_MN>;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -124,7 +142,10 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
-    const int nk = (K + BK - 1) / BK;
+    // split-K: this CTA covers k-blocks [kb0, kb0 + nk) (blockIdx.z = slice); with ws != nullptr
+    // it writes its raw fp32 sums to ws[slice] and gemm_splitk_reduce applies the epilogue.
+    const int kb0 = blockIdx.z * kbs;
+    const int nk = min((K + BK - 1) / BK - kb0, kbs);
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < kStagesTC; ++s) {
@@ -153,7 +174,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
                 bar_wait(empty + s, ((kb / kStagesTC) & 1) ^ 1);
                 unsigned char* st = base + s * Lay::kStage;
                 bar_expect(full + s, Lay::kTileA + Lay::kTileB);
-                const int k0 = kb * BK;
+                const int k0 = (kb0 + kb) * BK;
                 if (A_MN) {  // A^T tile: K rows x 128 MN cols as 4 boxes of 32 cols
                     for (int j = 0; j < BM / 32; ++j) tma_2d(st + j * BK * 128, &tma_a, m0 + 32 * j, k0, full + s);
                 } else {
@@ -236,7 +257,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
         const int row = m0 + warp * 32 + lane;  // TMEM lane == tile row
         float* crow = row < M ? C + static_cast<int64_t>(row) * ldc : nullptr;
         float* prow = nullptr;
-        if (crow && push.table) {
+        if (crow && push.table && !ws) {
             const int32_t id = push.ids[row];
             prow = push.table + static_cast<int64_t>(id) * push.ld;
             if (blockIdx.y == 0 && push.stamps) push.stamps[id] = *push.step;
@@ -265,7 +286,12 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
 #pragma unroll
                 for (int j = 0; j < 32; ++j) sum[j] = q == 0 ? __uint_as_float(v[j]) : __fadd_rn(sum[j], __uint_as_float(v[j]));
             }
-            if (crow) {
+            if (crow && ws) {
+                float* wrow = ws + (static_cast<int64_t>(blockIdx.z) * M + row) * N;
+#pragma unroll
+                for (int j = 0; j < 32; ++j)
+                    if (n0 + c0 + j < N) wrow[n0 + c0 + j] = sum[j];
+            } else if (crow) {
 #pragma unroll
                 for (int j = 0; j < 32; ++j) {
                     const int col = n0 + c0 + j;
@@ -290,6 +316,33 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
     if (warp == 0) {
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(Acc<BN>::kCols));
+    }
+}
+
+// Split-K finish: C = epilogue(sum over slices in slice order) (+ history push), one
+// thread per output element (fixed order -> deterministic).
+__global__ void __launch_bounds__(256) gemm_splitk_reduce(const float* __restrict__ ws, int S, int M, int N,
+                                                         float* __restrict__ C, int64_t ldc, GemmEpilogue ep) {
+    const int64_t total = static_cast<int64_t>(M) * N;
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    int32_t flags = 0;
+    if (i < total) {
+        const int row = static_cast<int>(i / N), col = static_cast<int>(i - static_cast<int64_t>(row) * N);
+        float v = ws[i];
+        for (int z = 1; z < S; ++z) v = __fadd_rn(v, ws[static_cast<int64_t>(z) * total + i]);
+        float* crow = C + static_cast<int64_t>(row) * ldc;
+        v = gemm_epilogue_value(ep, v, crow, col);
+        crow[col] = v;
+        if (ep.push.table) {
+            const int32_t id = ep.push.ids[row];
+            ep.push.table[static_cast<int64_t>(id) * ep.push.ld + col] = v;
+            if (col == 0 && ep.push.stamps) ep.push.stamps[id] = *ep.push.step;
+            flags = table_flag_of(v);
+        }
+    }
+    if (ep.push.special) {
+        flags = __reduce_or_sync(0xffffffffu, flags);
+        if ((threadIdx.x & 31) == 0 && flags) atomicOr(ep.push.special, flags);
     }
 }
 
@@ -333,8 +386,26 @@ static bool launch_tc(int m, int n, int k, const float* a, int64_t lda, const fl
                                        Lay::kSmem));
         attr = true;
     }
-    dim3 grid(static_cast<unsigned>(ceil_div(m, BM)), static_cast<unsigned>(ceil_div(n, BN)));
-    gemm_tc_kernel<BN, A_MN, B_MN><<<grid, kThreads, Lay::kSmem, st>>>(ta, tb, m, n, k, c, ldc, ep);
+    // split-K over otherwise idle SMs (deterministic: slices reduced in order by a 2nd kernel)
+    const int64_t tiles = ceil_div(m, BM) * ceil_div(n, BN);
+    const int nkb = static_cast<int>(ceil_div(k, BK));
+    int S = 1;
+    if (t_gemm_ws && tiles < num_sms()) {
+        S = static_cast<int>(std::min<int64_t>(num_sms() / tiles, std::max(1, nkb / 2)));
+        while (S > 1 && static_cast<int64_t>(S) * m * n > t_gemm_ws_floats) --S;
+    }
+    const int kbs = static_cast<int>(ceil_div(nkb, S));
+    S = static_cast<int>(ceil_div(nkb, kbs));  // no empty slices
+    dim3 grid(static_cast<unsigned>(ceil_div(m, BM)), static_cast<unsigned>(ceil_div(n, BN)), static_cast<unsigned>(S));
+    gemm_tc_kernel<BN, A_MN, B_MN><<<grid, kThreads, Lay::kSmem, st>>>(ta, tb, m, n, k, c, ldc, ep, kbs,
+                                                                        S > 1 ? t_gemm_ws : nullptr);
+    if (S > 1) {
+        GASB_CUDA(cudaGetLastError());
+        ++t_launches;
+        const int64_t total = static_cast<int64_t>(m) * n;
+        gemm_splitk_reduce<<<static_cast<unsigned>(ceil_div(total, 256)), 256, 0, st>>>(t_gemm_ws, S, m, n, c, ldc,
+                                                                                       ep);
+    }
     return true;
 }
 

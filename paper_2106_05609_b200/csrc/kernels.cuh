@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <vector>
 
 namespace gasb {
 
@@ -60,6 +61,11 @@ struct SpmmSegs {
 };
 // Host: splits segments [g0, g1) into nranges contiguous ranges of ~equal edges.
 void split_ranges(const int64_t* seg_beg, int64_t g0, int64_t g1, int32_t nranges, int32_t* out);
+// Host: segments + nranges+1 work ranges of one launch over rows [r_lo, r_hi) (spmm.cu).
+// Appends to sb/sr/ss (plus a trailing sentinel in sb), fills r0/rn of those rows.
+void segment_launch(const int64_t* rp, int64_t r_lo, int64_t r_hi, bool split, int32_t nranges,
+                    std::vector<int64_t>& sb, std::vector<int32_t>& sr, std::vector<int32_t>& ss, int32_t* r0,
+                    int32_t* rn, int64_t& slot, int32_t* ranges);
 // Work ranges per SpMM launch: 8 resident warps per SM (2 CTAs of 4).
 int32_t spmm_ranges_per_launch();
 // coeffs: stencil coefficients as fp64 pre-multiplied by kCoeffScale. special: the source
@@ -110,6 +116,9 @@ struct GemmEpilogue {
 };
 void launch_gemm(int op, int m, int n, int k, const float* a, int64_t lda, const float* b, int64_t ldb, float* c,
                  int64_t ldc, const GemmEpilogue& ep, cudaStream_t st);
+// Split-K scratch for the tensor-core GEMM on this host thread (nullptr: no split-K). GEMMs
+// enqueued afterwards on ONE stream may share it (they run in order).
+void set_gemm_workspace(float* ws, int64_t floats);
 void launch_gemm(int op, int m, int n, int k, const float* a, int64_t lda, const float* b, int64_t ldb, float* c,
                  int64_t ldc, float beta, bool relu, const PushEpilogue* push, cudaStream_t st);
 __device__ __forceinline__ float gemm_epilogue_value(const GemmEpilogue& ep, float x, const float* crow, int col) {

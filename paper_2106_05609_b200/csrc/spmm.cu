@@ -448,6 +448,51 @@ void split_ranges(const int64_t* seg_beg, int64_t g0, int64_t g1, int32_t nrange
     out[nranges] = static_cast<int32_t>(g1);
 }
 
+// Segments the rows [r_lo, r_hi) of one launch (rp: absolute edge offsets). split = false:
+// one segment per row (the bit-exact sequential mode) and ranges at row boundaries.
+// split = true: the launch's edges are cut into nranges ranges of EXACTLY equal size and a
+// row is split only where a range boundary falls inside it (<= nranges - 1 extra segments
+// per launch, each an fp64 partial); all other rows are one segment with no partial.
+void segment_launch(const int64_t* rp, int64_t r_lo, int64_t r_hi, bool split, int32_t nranges,
+                    std::vector<int64_t>& sb, std::vector<int32_t>& sr, std::vector<int32_t>& ss, int32_t* r0,
+                    int32_t* rn, int64_t& slot, int32_t* ranges) {
+    const int64_t g0 = static_cast<int64_t>(sr.size());
+    const int64_t E0 = rp[r_lo], E = rp[r_hi] - E0;
+    auto bound = [&](int64_t k) { return E0 + E * k / nranges; };
+    int64_t k = 1;  // next interior boundary
+    std::vector<int64_t> cuts;
+    for (int64_t r = r_lo; r < r_hi; ++r) {
+        const int64_t b = rp[r], e = rp[r + 1];
+        while (k < nranges && bound(k) <= b) ++k;
+        cuts.clear();
+        if (split)
+            for (; k < nranges && bound(k) < e; ++k)
+                if (cuts.empty() || cuts.back() != bound(k)) cuts.push_back(bound(k));
+        const int64_t pieces = 1 + static_cast<int64_t>(cuts.size());
+        r0[r] = static_cast<int32_t>(sr.size());
+        rn[r] = static_cast<int32_t>(pieces);
+        for (int64_t i = 0; i < pieces; ++i) {
+            sb.push_back(i == 0 ? b : cuts[static_cast<size_t>(i - 1)]);
+            sr.push_back(static_cast<int32_t>(r));
+            ss.push_back(pieces == 1 ? -1 : static_cast<int32_t>(slot++));
+        }
+    }
+    const int64_t g1 = static_cast<int64_t>(sr.size());
+    sb.push_back(rp[r_hi]);  // sentinel (popped by the caller when appending more launches)
+    if (!split) {
+        split_ranges(sb.data(), g0, g1, nranges, ranges);
+        return;
+    }
+    int64_t s = g0;  // ranges: first segment starting at or after each boundary
+    ranges[0] = static_cast<int32_t>(g0);
+    for (int32_t q = 1; q < nranges; ++q) {
+        const int64_t t = bound(q);
+        while (s < g1 && sb[s] < t) ++s;
+        ranges[q] = static_cast<int32_t>(s);
+    }
+    ranges[nranges] = static_cast<int32_t>(g1);
+}
+
 // Columns per lane of the pipelined SpMM (tuning knob GASB_SPMM_CPL = 2 | 4, default 4:
 // 128-column chunks, measured fastest on the Reddit-shaped workload).
 static int spmm_cpl() {
@@ -712,22 +757,17 @@ extern "C" gasb_status gasb_spmm_fwd(const int32_t* d_rowptr, int32_t m, const i
         GASB_CUDA(cudaMemcpyAsync(rp.data(), d_rowptr, sizeof(int32_t) * (m + 1), cudaMemcpyDeviceToHost, st));
         GASB_CUDA(cudaStreamSynchronize(st));
         const int64_t nnz = rp[m];
-        std::vector<int64_t> sb;
-        std::vector<int32_t> sr, ss, r0(static_cast<size_t>(m)), rn(static_cast<size_t>(m));
-        int32_t slots = 0;
-        for (int32_t r = 0; r < m; ++r) {
-            require(rp[r + 1] >= rp[r], "aggregate: row pointer not monotone");
-            const int64_t deg = rp[r + 1] - rp[r];
-            const int64_t k = (seg_edges == 0 || deg <= seg_edges) ? 1 : ceil_div(deg, seg_edges);
-            r0[r] = static_cast<int32_t>(sr.size());
-            rn[r] = static_cast<int32_t>(k);
-            for (int64_t i = 0; i < k; ++i) {
-                sb.push_back(rp[r] + i * (k == 1 ? 0 : seg_edges));
-                sr.push_back(r);
-                ss.push_back(k == 1 ? -1 : slots++);
-            }
+        std::vector<int64_t> rp64(static_cast<size_t>(m) + 1), sb;
+        for (int32_t r = 0; r <= m; ++r) {
+            require(r == 0 || rp[r] >= rp[r - 1], "aggregate: row pointer not monotone");
+            rp64[r] = rp[r];
         }
-        sb.push_back(nnz);
+        std::vector<int32_t> sr, ss, r0(static_cast<size_t>(m)), rn(static_cast<size_t>(m));
+        const int32_t nranges = spmm_ranges_per_launch();
+        std::vector<int32_t> rs(static_cast<size_t>(nranges) + 1);
+        int64_t slot64 = 0;
+        segment_launch(rp64.data(), 0, m, seg_edges > 0, nranges, sb, sr, ss, r0.data(), rn.data(), slot64, rs.data());
+        const int64_t slots = slot64;
         const int64_t nseg = static_cast<int64_t>(sr.size());
         const int32_t nchunks = static_cast<int32_t>(ceil_div(dim, kChunk));
         SegScratch z;
@@ -760,9 +800,6 @@ extern "C" gasb_status gasb_spmm_fwd(const int32_t* d_rowptr, int32_t m, const i
             GASB_CUDA(cudaMallocAsync(&special, sizeof(int32_t), st));
             GASB_CUDA(cudaMemsetAsync(special, 0, sizeof(int32_t), st));
             launch_scan_special(d_x, num_src, ldx, dim, special, st);
-            const int32_t nranges = spmm_ranges_per_launch();
-            std::vector<int32_t> rs(static_cast<size_t>(nranges) + 1);
-            split_ranges(sb.data(), 0, nseg, nranges, rs.data());
             int32_t* d_rs = nullptr;
             GASB_CUDA(cudaMallocAsync(&d_rs, sizeof(int32_t) * (nranges + 1), st));
             GASB_CUDA(cudaMemcpyAsync(d_rs, rs.data(), sizeof(int32_t) * (nranges + 1), cudaMemcpyHostToDevice, st));

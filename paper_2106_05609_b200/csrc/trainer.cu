@@ -113,9 +113,10 @@ struct SegTable {
     }
 };
 
-// Segments rows [row_lo, row_hi) of the absolute row pointer `rp` into pieces of <= S
-// edges (S == 0: one per row). Slots restart at 0 per group when per_group_slots.
-void build_segments(const std::vector<int64_t>& rp, const std::vector<int64_t>& group_rows, int64_t S,
+// Segments each group (batch) of rows of the absolute row pointer `rp` for one SpMM launch
+// per group (segment_launch, spmm.cu): split = false keeps rows whole (bit-exact mode).
+// Partial slots restart at 0 per group when per_group_slots (one launch at a time).
+void build_segments(const std::vector<int64_t>& rp, const std::vector<int64_t>& group_rows, bool split,
                     bool per_group_slots, SegTable& t) {
     const int64_t ngroups = static_cast<int64_t>(group_rows.size()) - 1;
     const int64_t nrows = group_rows.back();
@@ -123,32 +124,20 @@ void build_segments(const std::vector<int64_t>& rp, const std::vector<int64_t>& 
     std::vector<int32_t> sr, ss, r0(static_cast<size_t>(nrows)), rn(static_cast<size_t>(nrows));
     t.group_seg0.assign(static_cast<size_t>(ngroups), 0);
     t.group_nseg.assign(static_cast<size_t>(ngroups), 0);
+    t.nranges = spmm_ranges_per_launch();
+    std::vector<int32_t> rs(static_cast<size_t>(ngroups) * (t.nranges + 1));
     int64_t slot = 0;
     t.max_group_slots = 0;
     for (int64_t g = 0; g < ngroups; ++g) {
         if (per_group_slots) slot = 0;
         t.group_seg0[g] = static_cast<int64_t>(sr.size());
-        for (int64_t r = group_rows[g]; r < group_rows[g + 1]; ++r) {
-            const int64_t deg = rp[r + 1] - rp[r];
-            const int64_t k = (S == 0 || deg <= S) ? 1 : ceil_div(deg, S);
-            r0[r] = static_cast<int32_t>(sr.size());
-            rn[r] = static_cast<int32_t>(k);
-            for (int64_t i = 0; i < k; ++i) {
-                sb.push_back(rp[r] + i * S);
-                sr.push_back(static_cast<int32_t>(r));
-                ss.push_back(k == 1 ? -1 : static_cast<int32_t>(slot++));
-            }
-        }
+        if (!sb.empty()) sb.pop_back();  // previous group's sentinel
+        segment_launch(rp.data(), group_rows[g], group_rows[g + 1], split, t.nranges, sb, sr, ss, r0.data(),
+                       rn.data(), slot, rs.data() + g * (t.nranges + 1));
         t.group_nseg[g] = static_cast<int64_t>(sr.size()) - t.group_seg0[g];
         t.max_group_slots = std::max(t.max_group_slots, slot);
     }
     t.total_slots = per_group_slots ? t.max_group_slots : slot;
-    sb.push_back(rp[nrows]);
-    t.nranges = spmm_ranges_per_launch();
-    std::vector<int32_t> rs(static_cast<size_t>(ngroups) * (t.nranges + 1));
-    for (int64_t g = 0; g < ngroups; ++g)
-        split_ranges(sb.data(), t.group_seg0[g], t.group_seg0[g] + t.group_nseg[g], t.nranges,
-                     rs.data() + g * (t.nranges + 1));
     t.ranges.upload(rs);
     t.seg_beg.upload(sb);
     t.seg_row.upload(sr);
@@ -243,6 +232,12 @@ struct gasb_trainer_s {
         if (residual && h0.p) tm_h0_ok = make_row_tmap(h0.p, ne_max, D, ldD, bc, &tm_h0);
     }
     DevBuf<double> loss, row_scratch;
+
+    DevBuf<float> gemm_ws;  // split-K scratch of the tensor-core GEMM (gemm_tc.cu)
+    struct WsGuard {        // scopes the thread's GEMM workspace to one enqueue
+        explicit WsGuard(DevBuf<float>& w) { set_gemm_workspace(w.p, w.n); }
+        ~WsGuard() { set_gemm_workspace(nullptr, 0); }
+    };
 
     // ---- residual models: APPNP (kind 2) / GCNII (kind 3) ----
     bool residual = false;
@@ -476,10 +471,9 @@ void gasb_trainer_s::build(const float* h_features, const int32_t* h_labels, con
     {
         std::vector<int64_t> grp(num_parts + 1);
         for (int32_t p = 0; p <= num_parts; ++p) grp[p] = row_off[p];
-        build_segments(h_rp, grp, opt.seg_edges, true, seg_batch);
-        const int64_t S_all = opt.seg_edges == 0 ? 0 : std::max<int64_t>(opt.seg_edges, 2048);
+        build_segments(h_rp, grp, opt.seg_edges > 0, true, seg_batch);
         std::vector<int64_t> one{0, R};
-        build_segments(h_rp, one, S_all, false, seg_all);
+        build_segments(h_rp, one, opt.seg_edges > 0, false, seg_all);
     }
     max_chunks = static_cast<int32_t>(ceil_div(std::max(F, H), 64));
     counters.alloc(R * max_chunks);
@@ -559,6 +553,7 @@ void gasb_trainer_s::build(const float* h_features, const int32_t* h_labels, con
     g_out.alloc(static_cast<int64_t>(nb_max) * ldH);
     loss.alloc(num_parts);
     loss.zero();
+    gemm_ws.alloc(148LL * 128 * 64 + 4096);  // >= slices x M x N of any split (<= #SMs tiles of 128 x 64)
     row_scratch.alloc(nb_max);
     graphs.assign(num_parts, nullptr);
     graph_launches.assign(num_parts, 0);
@@ -724,6 +719,7 @@ void gasb_trainer_s::enqueue_batch_res(int32_t p, bool train, bool push, bool fu
 }
 
 void gasb_trainer_s::enqueue_batch(int32_t p, bool train, bool push, bool use_hoisted, bool fused) {
+    WsGuard ws(gemm_ws);
     if (residual) {
         enqueue_batch_res(p, train, push, fused);
         return;
