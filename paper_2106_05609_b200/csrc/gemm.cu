@@ -186,9 +186,11 @@ extern "C" gasb_status gasb_gemm(int32_t op, int32_t m, int32_t n, int32_t k, co
         gasb::require(beta == 0.f || beta == 1.f, "matmul: beta must be 0 or 1");
         // split-K scratch for the standalone entry point (allocated once, never captured)
         static float* ws = nullptr;
-        constexpr int64_t kWsFloats = 148LL * 128 * 64 + 4096;
-        if (!ws) GASB_CUDA(cudaMalloc(&ws, sizeof(float) * kWsFloats));
-        gasb::set_gemm_workspace(ws, kWsFloats);
+        if (!ws) {
+            GASB_CUDA(cudaMalloc(&ws, sizeof(float) * (gasb::kGemmWsFloats + gasb::kGemmTileCounters)));
+            GASB_CUDA(cudaMemset(ws, 0, sizeof(float) * (gasb::kGemmWsFloats + gasb::kGemmTileCounters)));
+        }
+        gasb::set_gemm_workspace(ws, gasb::kGemmWsFloats);
         struct Reset {
             ~Reset() { gasb::set_gemm_workspace(nullptr, 0); }
         } reset;

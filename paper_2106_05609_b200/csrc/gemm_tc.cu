@@ -19,6 +19,8 @@
 
 namespace gasb {
 
+// Workspace layout: ws_floats floats of slice partials, then kGemmTileCounters ints of
+// per-tile arrival counters (zero-initialised by the owner, self-resetting).
 thread_local float* t_gemm_ws = nullptr;
 thread_local int64_t t_gemm_ws_floats = 0;
 void set_gemm_workspace(float* ws, int64_t floats) {
@@ -124,11 +126,17 @@ struct Layout {
     static constexpr int kSmem = 1024 + kStagesTC * kStage + kBars + 16;
 };
 
+// shared int next to the TMEM slot (after the mbarriers): the split-K "last CTA" flag
+__device__ __forceinline__ int* tmem_slot_flag(uint64_t* bars) {
+    return reinterpret_cast<int*>(bars + 3 * kStagesTC + 1) + 1;
+}
+
 template <int BN, bool A_MN, bool B_MN>
 __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_constant__ CUtensorMap tma_a,
                                                              const __grid_constant__ CUtensorMap tma_b, int M,
                                                              int N, int K, float* __restrict__ C, int64_t ldc,
-                                                             GemmEpilogue ep, int kbs, float* __restrict__ ws) {
+                                                             GemmEpilogue ep, int kbs, float* __restrict__ ws,
+                                                             int64_t ws_floats) {
     const PushEpilogue& push = ep.push;
     using Lay = Layout<BN, A_MN, B_MN>;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -286,11 +294,12 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
 #pragma unroll
                 for (int j = 0; j < 32; ++j) sum[j] = q == 0 ? __uint_as_float(v[j]) : __fadd_rn(sum[j], __uint_as_float(v[j]));
             }
-            if (crow && ws) {
-                float* wrow = ws + (static_cast<int64_t>(blockIdx.z) * M + row) * N;
+            if (crow && ws) {  // slice partial, row pitch Np = N rounded up to 4 (float4 stores)
+                const int Np = (N + 3) & ~3;
+                float4* wrow = reinterpret_cast<float4*>(ws + (static_cast<int64_t>(blockIdx.z) * M + row) * Np);
 #pragma unroll
-                for (int j = 0; j < 32; ++j)
-                    if (n0 + c0 + j < N) wrow[n0 + c0 + j] = sum[j];
+                for (int j = 0; j < 32; j += 4)
+                    if (n0 + c0 + j < Np) wrow[(n0 + c0 + j) >> 2] = make_float4(sum[j], sum[j + 1], sum[j + 2], sum[j + 3]);
             } else if (crow) {
 #pragma unroll
                 for (int j = 0; j < 32; ++j) {
@@ -306,6 +315,64 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
                 }
             }
         }
+        if (ws) {
+            // parallel split-K fixup: every CTA of the tile publishes its slice, frees its TMEM
+            // (a peer CTA may be waiting for it on this SM), waits until all gridDim.z slices of
+            // the tile are in, then reduces its own 1/S of the tile's rows, summing the slices
+            // in slice order (deterministic, independent of arrival order)
+            __threadfence();
+            asm volatile("bar.sync 1, 128;\n" ::: "memory");
+            if (warp == 0) {
+                asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem),
+                             "r"(Acc<BN>::kCols));
+            }
+            const int S = static_cast<int>(gridDim.z);
+            int* arrive = reinterpret_cast<int*>(ws + ws_floats) + 2 * (blockIdx.y * gridDim.x + blockIdx.x);
+            if (threadIdx.x == 0) {
+                atomicAdd(arrive, 1);
+                for (uint32_t spins = 0;; ++spins) {
+                    int v;
+                    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];\n" : "=r"(v) : "l"(arrive) : "memory");
+                    if (v >= S) break;
+                    if (spins > (1u << 28)) __trap();  // grid <= #SMs: all slices are co-resident
+                    __nanosleep(64);
+                }
+            }
+            asm volatile("bar.sync 1, 128;\n" ::: "memory");
+            const int Np = (N + 3) & ~3;
+            const int64_t slice = static_cast<int64_t>(M) * Np;
+            const int rows_per = (BM + S - 1) / S;
+            const int rlo = blockIdx.z * rows_per, rhi = min(BM, rlo + rows_per);
+            constexpr int kQ = BN / 4;  // float4 quads per tile row
+            for (int idx = threadIdx.x; idx < (rhi - rlo) * kQ; idx += 128) {
+                const int r = m0 + rlo + idx / kQ, c = n0 + 4 * (idx % kQ);
+                if (r >= M || c >= N) continue;
+                const float4* wp = reinterpret_cast<const float4*>(ws + static_cast<int64_t>(r) * Np + c);
+                float4 x = __ldcg(wp);
+                for (int z = 1; z < S; ++z) {
+                    const float4 y = __ldcg(wp + z * (slice >> 2));
+                    x = make_float4(__fadd_rn(x.x, y.x), __fadd_rn(x.y, y.y), __fadd_rn(x.z, y.z), __fadd_rn(x.w, y.w));
+                }
+                float* cr = C + static_cast<int64_t>(r) * ldc;
+                float* pr = push.table ? push.table + static_cast<int64_t>(push.ids[r]) * push.ld : nullptr;
+                const float xs[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    if (c + k >= N) break;
+                    const float v = gemm_epilogue_value(ep, xs[k], cr, c + k);
+                    cr[c + k] = v;
+                    if (pr) {
+                        pr[c + k] = v;
+                        flags |= table_flag_of(v);
+                    }
+                }
+                if (pr && c == 0 && push.stamps) push.stamps[push.ids[r]] = *push.step;
+            }
+            if (threadIdx.x == 0 && atomicAdd(arrive + 1, 1) == S - 1) {  // last to leave resets
+                arrive[0] = 0;
+                arrive[1] = 0;
+            }
+        }
         if (push.special) {
             flags = __reduce_or_sync(0xffffffffu, flags);
             if (lane == 0 && flags) atomicOr(push.special, flags);
@@ -313,36 +380,9 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
     }
     asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
     __syncthreads();
-    if (warp == 0) {
+    if (warp == 0 && !ws) {  // (split-K CTAs freed their TMEM before the fixup)
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(Acc<BN>::kCols));
-    }
-}
-
-// Split-K finish: C = epilogue(sum over slices in slice order) (+ history push), one
-// thread per output element (fixed order -> deterministic).
-__global__ void __launch_bounds__(256) gemm_splitk_reduce(const float* __restrict__ ws, int S, int M, int N,
-                                                         float* __restrict__ C, int64_t ldc, GemmEpilogue ep) {
-    const int64_t total = static_cast<int64_t>(M) * N;
-    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    int32_t flags = 0;
-    if (i < total) {
-        const int row = static_cast<int>(i / N), col = static_cast<int>(i - static_cast<int64_t>(row) * N);
-        float v = ws[i];
-        for (int z = 1; z < S; ++z) v = __fadd_rn(v, ws[static_cast<int64_t>(z) * total + i]);
-        float* crow = C + static_cast<int64_t>(row) * ldc;
-        v = gemm_epilogue_value(ep, v, crow, col);
-        crow[col] = v;
-        if (ep.push.table) {
-            const int32_t id = ep.push.ids[row];
-            ep.push.table[static_cast<int64_t>(id) * ep.push.ld + col] = v;
-            if (col == 0 && ep.push.stamps) ep.push.stamps[id] = *ep.push.step;
-            flags = table_flag_of(v);
-        }
-    }
-    if (ep.push.special) {
-        flags = __reduce_or_sync(0xffffffffu, flags);
-        if ((threadIdx.x & 31) == 0 && flags) atomicOr(ep.push.special, flags);
     }
 }
 
@@ -392,20 +432,15 @@ static bool launch_tc(int m, int n, int k, const float* a, int64_t lda, const fl
     int S = 1;
     if (t_gemm_ws && tiles < num_sms()) {
         S = static_cast<int>(std::min<int64_t>(num_sms() / tiles, std::max(1, nkb / 2)));
-        while (S > 1 && static_cast<int64_t>(S) * m * n > t_gemm_ws_floats) --S;
+        while (S > 1 && static_cast<int64_t>(S) * m * round_up(n, 4) > t_gemm_ws_floats) --S;
+        if (2 * tiles > kGemmTileCounters) S = 1;
     }
     const int kbs = static_cast<int>(ceil_div(nkb, S));
     S = static_cast<int>(ceil_div(nkb, kbs));  // no empty slices
     dim3 grid(static_cast<unsigned>(ceil_div(m, BM)), static_cast<unsigned>(ceil_div(n, BN)), static_cast<unsigned>(S));
     gemm_tc_kernel<BN, A_MN, B_MN><<<grid, kThreads, Lay::kSmem, st>>>(ta, tb, m, n, k, c, ldc, ep, kbs,
-                                                                        S > 1 ? t_gemm_ws : nullptr);
-    if (S > 1) {
-        GASB_CUDA(cudaGetLastError());
-        ++t_launches;
-        const int64_t total = static_cast<int64_t>(m) * n;
-        gemm_splitk_reduce<<<static_cast<unsigned>(ceil_div(total, 256)), 256, 0, st>>>(t_gemm_ws, S, m, n, c, ldc,
-                                                                                       ep);
-    }
+                                                                        S > 1 ? t_gemm_ws : nullptr,
+                                                                        t_gemm_ws_floats);
     return true;
 }
 

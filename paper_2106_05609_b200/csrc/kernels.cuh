@@ -117,7 +117,10 @@ struct GemmEpilogue {
 void launch_gemm(int op, int m, int n, int k, const float* a, int64_t lda, const float* b, int64_t ldb, float* c,
                  int64_t ldc, const GemmEpilogue& ep, cudaStream_t st);
 // Split-K scratch for the tensor-core GEMM on this host thread (nullptr: no split-K). GEMMs
-// enqueued afterwards on ONE stream may share it (they run in order).
+// enqueued afterwards on ONE stream may share it (they run in order). The buffer holds
+// `floats` floats followed by kGemmTileCounters ints that must be zero initially.
+constexpr int64_t kGemmTileCounters = 1024;
+constexpr int64_t kGemmWsFloats = 148LL * 128 * 64 + 4096;
 void set_gemm_workspace(float* ws, int64_t floats);
 void launch_gemm(int op, int m, int n, int k, const float* a, int64_t lda, const float* b, int64_t ldb, float* c,
                  int64_t ldc, float beta, bool relu, const PushEpilogue* push, cudaStream_t st);
@@ -147,8 +150,9 @@ void launch_zero(float* p, int64_t count, cudaStream_t st);
 // out[i] = alpha * h0[rows[i]] + (1 - alpha) * prop[i]  (+ optional history push of out)
 void launch_mix(const float* h0, int64_t ldh0, const int32_t* rows, const float* prop, int64_t ldp, int32_t m,
                 int32_t d, float alpha, float* out, int64_t ldo, const PushEpilogue* push, cudaStream_t st);
-// wt[l] = (1 - beta) I + beta W[l], l < layers (d x d each, dense)
-void launch_wtilde(const float* w, float* wt, int32_t layers, int32_t d, float beta, cudaStream_t st);
+// wt[l] = (1 - beta) I + beta W[l], l < layers (d x d each, row pitch `pitch`)
+void launch_wtilde(const float* w, float* wt, int32_t layers, int32_t d, int64_t pitch, float beta,
+                   cudaStream_t st);
 // dprop = (1 - alpha) dmix ; h0g[rows[i]] += alpha dmix[i]
 void launch_mix_bwd(const float* dmix, int64_t ldd, int32_t m, int32_t d, float alpha, const int32_t* rows,
                     float* h0g, int64_t ldh, float* dprop, int64_t ldp, cudaStream_t st);

@@ -42,13 +42,14 @@ __global__ void __launch_bounds__(256) mix_kernel(const float* __restrict__ h0, 
     }
 }
 
-// wt[l] = (1 - beta) * I + beta * W[l] for all layers (gcnii W~, layers.cpp:166)
+// wt[l] = (1 - beta) * I + beta * W[l] for all layers (gcnii W~, layers.cpp:166); d x d
+// matrices with row pitch `pitch` (pad columns are 0 in W and stay 0 in wt)
 __global__ void wtilde_kernel(const float* __restrict__ w, float* __restrict__ wt, int64_t total, int32_t d,
-                              float beta, float one_m_beta) {
+                              int64_t pitch, float beta, float one_m_beta) {
     for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const int64_t e = i % (static_cast<int64_t>(d) * d);
-        const float id = (e / d == e % d) ? 1.0f : 0.0f;
+        const int64_t e = i % (static_cast<int64_t>(d) * pitch);
+        const float id = (e / pitch == e % pitch) ? 1.0f : 0.0f;
         wt[i] = __fadd_rn(__fmul_rn(id, one_m_beta), __fmul_rn(w[i], beta));
     }
 }
@@ -121,10 +122,11 @@ void launch_mix(const float* h0, int64_t ldh0, const int32_t* rows, const float*
     GASB_CUDA(cudaGetLastError());
 }
 
-void launch_wtilde(const float* w, float* wt, int32_t layers, int32_t d, float beta, cudaStream_t st) {
-    const int64_t total = static_cast<int64_t>(layers) * d * d;
+void launch_wtilde(const float* w, float* wt, int32_t layers, int32_t d, int64_t pitch, float beta,
+                   cudaStream_t st) {
+    const int64_t total = static_cast<int64_t>(layers) * d * pitch;
     if (total <= 0) return;
-    wtilde_kernel<<<grid_for(total, 256), 256, 0, st>>>(w, wt, total, d, beta, 1.0f - beta);
+    wtilde_kernel<<<grid_for(total, 256), 256, 0, st>>>(w, wt, total, d, pitch, beta, 1.0f - beta);
     ++t_launches;
     GASB_CUDA(cudaGetLastError());
 }

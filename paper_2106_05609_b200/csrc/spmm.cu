@@ -66,6 +66,14 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(src_bytes));
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_async_ca4(void* smem, const void* gmem) {
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_ca8(void* smem, const void* gmem) {
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
+}
 template <int N>
 __device__ __forceinline__ void cp_async_wait() {
     asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
@@ -82,6 +90,11 @@ struct PipeCfg {
     static constexpr int kStageBytes = (kStageDataBytes + kEdges * 8 + kHdrBytes + 127) / 128 * 128;
     static constexpr int kSmem = kPipeWarps * kStages * kStageBytes;
 };
+// TMA mode: per-warp ring of kMetaWin windows of 32 edges (int32 col + fp64 coeff each),
+// prefetched with cp.async kMetaWin windows ahead of the gather issue, so the row indices a
+// tile::gather4 needs are in shared memory (not a dependent global load) when it is issued.
+constexpr int kMetaWin = 4;
+constexpr int kMetaRingBytes = kMetaWin * 32 * (4 + 8);
 
 // Stage descriptor (shared memory): edges of ONE segment, so the FMA loop needs no
 // boundary tests; `ends` marks the segment's last stage (then it is finalized).
@@ -179,6 +192,10 @@ __global__ void __launch_bounds__(kPipeWarps * 32, 2) spmm_fwd_pipe_kernel(
     const int rsub = lane / Cfg::kPieces, q = lane % Cfg::kPieces;
     // TMA: one mbarrier per stage slot (after all stage buffers), phase bit per slot
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + kPipeWarps * kStages * Cfg::kStageBytes) + warp * kStages;
+    unsigned char* ring = smem_raw + kPipeWarps * kStages * Cfg::kStageBytes + kPipeWarps * kStages * 8 +
+                          warp * kMetaRingBytes;
+    int32_t* ring_c = reinterpret_cast<int32_t*>(ring);
+    double* ring_f = reinterpret_cast<double*>(ring + kMetaWin * 32 * 4);
     uint32_t phases = 0;
     if constexpr (TMA) {
         if (lane == 0) {
@@ -209,6 +226,36 @@ __global__ void __launch_bounds__(kPipeWarps * 32, 2) spmm_fwd_pipe_kernel(
             w_slot = sg < s_hi ? seg_slot[sg] : -1;
         };
         load_window(s_lo);
+        // ---- edge-metadata ring (TMA mode): window q = edges [e_lo + 32q, +32) in slot q % kMetaWin
+        const int64_t e_lo = seg_beg[s_lo], e_hi = seg_beg[s_hi];
+        int w_issued = 0;
+        auto prefetch_win = [&] {
+            const int slot = w_issued % kMetaWin;
+            const int64_t e = e_lo + 32LL * w_issued + lane;
+            if (e < e_hi) {
+                cp_async_ca4(ring_c + slot * 32 + lane, cols + e);
+                cp_async_ca8(ring_f + slot * 32 + lane, coeffs + e);
+            }
+            cp_async_commit();
+            ++w_issued;
+        };
+        // make the windows holding edges [e_first, e_first + c) resident; recycle older slots
+        auto ensure_meta = [&](int64_t e_first, int c) {
+            const int q0 = static_cast<int>((e_first - e_lo) >> 5);
+            const int q1 = static_cast<int>((e_first + c - 1 - e_lo) >> 5);
+            while (w_issued < q0 + kMetaWin && e_lo + 32LL * w_issued < e_hi) prefetch_win();
+            const int allowed = w_issued - (q1 + 1);  // cp.async groups that may stay in flight
+            if (allowed >= 3) cp_async_wait<3>();
+            else if (allowed == 2) cp_async_wait<2>();
+            else if (allowed == 1) cp_async_wait<1>();
+            else cp_async_wait<0>();
+            __syncwarp();
+        };
+        if constexpr (TMA) {
+#pragma unroll
+            for (int k = 0; k < kMetaWin; ++k)
+                if (e_lo + 32LL * w_issued < e_hi) prefetch_win();
+        }
         // describe the next stage (edges [ipos, ipos + cnt) of segment iseg) and advance
         auto next_stage = [&](StageHdr& h, int64_t& e_first) -> bool {
             if (iseg >= s_hi) return false;
@@ -227,8 +274,16 @@ __global__ void __launch_bounds__(kPipeWarps * 32, 2) spmm_fwd_pipe_kernel(
         };
         auto meta = [&](const StageHdr& h, int64_t e_first, int32_t& mc, double& mf) {
             const bool ok = lane < h.cnt;
-            mc = ok ? __ldg(cols + e_first + lane) : -1;
-            mf = ok ? __ldg(coeffs + e_first + lane) : 0.0;
+            if constexpr (TMA) {
+                if (h.cnt > 0) ensure_meta(e_first, h.cnt);
+                const int64_t o = e_first - e_lo + lane;
+                const int idx = static_cast<int>(((o >> 5) % kMetaWin) * 32 + (o & 31));
+                mc = ok ? ring_c[idx] : -1;
+                mf = ok ? ring_f[idx] : 0.0;
+            } else {
+                mc = ok ? __ldg(cols + e_first + lane) : -1;
+                mf = ok ? __ldg(coeffs + e_first + lane) : 0.0;
+            }
         };
         auto issue = [&](int slot_idx, const StageHdr& h, int32_t mc, double mf) {
             unsigned char* st = wbase + slot_idx * Cfg::kStageBytes;
@@ -363,7 +418,7 @@ static void launch_pipe(const SpmmSegs& s, const int32_t* cols, const double* co
                         const CUtensorMap* tmap) {
     using Cfg = PipeCfg<CPL>;
     auto kern = spmm_fwd_pipe_kernel<CPL, TMA>;
-    constexpr int kSmem = Cfg::kSmem + kPipeWarps * kStages * 8;  // + mbarriers
+    constexpr int kSmem = Cfg::kSmem + kPipeWarps * kStages * 8 + (TMA ? kPipeWarps * kMetaRingBytes : 0);
     int& set = g_pipe_smem_set[CPL == 4][TMA];
     if (!set) {
         GASB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));

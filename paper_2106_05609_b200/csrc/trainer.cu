@@ -196,7 +196,10 @@ struct gasb_trainer_s {
     int64_t pld = 0, pld_all = 0;
 
     // model
-    std::vector<int64_t> poff, prow, pcol;  // per parameter tensor
+    // per parameter tensor: device offset, rows, cols, row pitch (cols rounded up to 4 floats
+    // so every weight is a TMA-describable GEMM operand; pads are 0 and stay 0 under Adam)
+    std::vector<int64_t> poff, prow, pcol, ppitch;
+    int64_t nparam_dense = 0;  // Model::params() floats (the API's flat layout)
     std::vector<int32_t> layer_param;       // param index of W_l (GCN) per layer 1..L
     int64_t nparam = 0;
     std::vector<float> h_params_init;
@@ -235,7 +238,7 @@ struct gasb_trainer_s {
 
     DevBuf<float> gemm_ws;  // split-K scratch of the tensor-core GEMM (gemm_tc.cu)
     struct WsGuard {        // scopes the thread's GEMM workspace to one enqueue
-        explicit WsGuard(DevBuf<float>& w) { set_gemm_workspace(w.p, w.n); }
+        explicit WsGuard(DevBuf<float>& w) { set_gemm_workspace(w.p, kGemmWsFloats); }
         ~WsGuard() { set_gemm_workspace(nullptr, 0); }
     };
 
@@ -259,8 +262,28 @@ struct gasb_trainer_s {
         poff.push_back(nparam);
         prow.push_back(r);
         pcol.push_back(c);
-        nparam += r * c;
+        ppitch.push_back(round_up(c, 4));
+        nparam += r * ppitch.back();
+        nparam_dense += r * c;
         return static_cast<int32_t>(poff.size()) - 1;
+    }
+    int64_t pp(int32_t i) const { return ppitch[i]; }
+    // dense (Model::params() order) <-> padded device layout
+    void params_to_dense(const float* dev, float* host) const {
+        int64_t o = 0;
+        for (size_t i = 0; i < poff.size(); ++i) {
+            GASB_CUDA(cudaMemcpy2D(host + o, sizeof(float) * pcol[i], dev + poff[i], sizeof(float) * ppitch[i],
+                                   sizeof(float) * pcol[i], prow[i], cudaMemcpyDeviceToHost));
+            o += prow[i] * pcol[i];
+        }
+    }
+    void params_from_dense(const float* host, float* dev) const {
+        int64_t o = 0;
+        for (size_t i = 0; i < poff.size(); ++i) {
+            GASB_CUDA(cudaMemcpy2D(dev + poff[i], sizeof(float) * ppitch[i], host + o, sizeof(float) * pcol[i],
+                                   sizeof(float) * pcol[i], prow[i], cudaMemcpyHostToDevice));
+            o += prow[i] * pcol[i];
+        }
     }
     void build_residual(const std::vector<int64_t>& h_arp, const std::vector<int32_t>& h_asrc,
                         const std::vector<float>& h_acf, const std::vector<int32_t>& h_brow);
@@ -514,7 +537,11 @@ void gasb_trainer_s::build(const float* h_features, const int32_t* h_labels, con
     }
     h_params_init.assign(static_cast<size_t>(nparam), 0.0f);
     auto glorot_at = [&](int32_t i, uint64_t seed) {
-        glorot_init(h_params_init.data() + poff[i], prow[i], pcol[i], seed);
+        std::vector<float> w(static_cast<size_t>(prow[i] * pcol[i]));
+        glorot_init(w.data(), prow[i], pcol[i], seed);
+        for (int64_t r = 0; r < prow[i]; ++r)
+            std::copy(w.begin() + r * pcol[i], w.begin() + (r + 1) * pcol[i],
+                      h_params_init.begin() + poff[i] + r * ppitch[i]);
     };
     for (int32_t l = 1; l <= L; ++l)  // Layer::build(cfg, derive_seed(seed,10,l)) -> glorot(derive_seed(.,1))
         if (layer_param[l] >= 0)
@@ -553,7 +580,8 @@ void gasb_trainer_s::build(const float* h_features, const int32_t* h_labels, con
     g_out.alloc(static_cast<int64_t>(nb_max) * ldH);
     loss.alloc(num_parts);
     loss.zero();
-    gemm_ws.alloc(148LL * 128 * 64 + 4096);  // >= slices x M x N of any split (<= #SMs tiles of 128 x 64)
+    gemm_ws.alloc(kGemmWsFloats + kGemmTileCounters);  // split-K slices + tile counters
+    gemm_ws.zero();
     row_scratch.alloc(nb_max);
     graphs.assign(num_parts, nullptr);
     graph_launches.assign(num_parts, 0);
@@ -578,7 +606,7 @@ void gasb_trainer_s::build_residual(const std::vector<int64_t>& h_arp, const std
         z.alloc(nem * ldH);
         zg.alloc(nem * ldH);
     } else {
-        wt.alloc(static_cast<int64_t>(L) * H * H);
+        wt.alloc(static_cast<int64_t>(L) * H * round_up(H, 4));
         mixed.resize(static_cast<size_t>(L) + 1);
         for (int32_t l = 1; l <= L; ++l) mixed[l].alloc(nbm * ldD);
     }
@@ -607,14 +635,14 @@ void gasb_trainer_s::enqueue_batch_res(int32_t p, bool train, bool push, bool fu
         GemmEpilogue e1;
         e1.bias = P(p_hb1);
         e1.relu = 1;
-        launch_gemm(0, me, H, F, x_ext.p, ldF, P(p_hw1), H, gcnii ? h0.p : z.p, gcnii ? ldD : ldH, e1, stream);
+        launch_gemm(0, me, H, F, x_ext.p, ldF, P(p_hw1), pp(p_hw1), gcnii ? h0.p : z.p, gcnii ? ldD : ldH, e1, stream);
         if (!gcnii) {
             GemmEpilogue e2;
             e2.bias = P(p_hb2);
-            launch_gemm(0, me, C, H, z.p, ldH, P(p_hw2), C, h0.p, ldD, e2, stream);
+            launch_gemm(0, me, C, H, z.p, ldH, P(p_hw2), pp(p_hw2), h0.p, ldD, e2, stream);
         }
     }
-    if (gcnii) launch_wtilde(P(layer_param[1]), wt.p, L, H, spec.beta, stream);
+    if (gcnii) launch_wtilde(P(layer_param[1]), wt.p, L, H, pp(layer_param[1]), spec.beta, stream);
     // ---- propagation layers ----
     for (int32_t l = 1; l <= L; ++l) {
         if (l == 1) {  // input = h0 over V_b (local ids)
@@ -644,12 +672,13 @@ void gasb_trainer_s::enqueue_batch_res(int32_t p, bool train, bool push, bool fu
             GemmEpilogue e;  // act_l = relu(mixed_l . W~_l), pushed for l < L
             e.relu = 1;
             if (do_push) e.push = pe;
-            launch_gemm(0, m, H, H, mixed[l].p, ldD, wt.p + static_cast<int64_t>(l - 1) * H * H, H, act[l].p, ldD, e,
+            launch_gemm(0, m, H, H, mixed[l].p, ldD, wt.p + static_cast<int64_t>(l - 1) * H * pp(layer_param[1]),
+                        pp(layer_param[1]), act[l].p, ldD, e,
                         stream);
             if (l == L) {  // relu -> out_w, out_b (trainer.cpp:221-227)
                 GemmEpilogue eo;
                 eo.bias = P(p_ob);
-                launch_gemm(0, m, C, H, act[L].p, ldD, P(p_ow), C, logits.p, ldC, eo, stream);
+                launch_gemm(0, m, C, H, act[L].p, ldD, P(p_ow), pp(p_ow), logits.p, ldC, eo, stream);
             }
         } else {  // APPNP: out = alpha h0[B] + (1 - alpha) prop, pushed raw (no relu)
             launch_mix(h0.p, ldD, br, prop.p, ldD, m, D, spec.alpha, l < L ? act[l].p : logits.p, l < L ? ldD : ldC,
@@ -666,9 +695,9 @@ void gasb_trainer_s::enqueue_batch_res(int32_t p, bool train, bool push, bool fu
         const float* dout = glogits.p;
         int64_t ldo = ldC;
         if (gcnii) {  // output head: d out_w, d out_b, then relu backward into d act_L
-            launch_gemm(2, H, C, m, act[L].p, ldD, glogits.p, ldC, G(p_ow), C, plain, stream);
+            launch_gemm(2, H, C, m, act[L].p, ldD, glogits.p, ldC, G(p_ow), pp(p_ow), plain, stream);
             launch_colsum(glogits.p, ldC, m, C, G(p_ob), stream);
-            launch_gemm(1, m, H, C, glogits.p, ldC, P(p_ow), C, gout.p, ldD, plain, stream);
+            launch_gemm(1, m, H, C, glogits.p, ldC, P(p_ow), pp(p_ow), gout.p, ldD, plain, stream);
             launch_mask(gout.p, ldD, act[L].p, ldD, m, H, stream);
             dout = gout.p;
             ldo = ldD;
@@ -680,9 +709,9 @@ void gasb_trainer_s::enqueue_batch_res(int32_t p, bool train, bool push, bool fu
             if (gcnii) {  // out_l = mixed_l . W~_l
                 GemmEpilogue ew;  // dW_l = beta * (mixed_l^T dout) (scale bwd of W~)
                 ew.post_scale = spec.beta;
-                launch_gemm(2, H, H, m, mixed[l].p, ldD, dout, ldo, G(layer_param[l]), H, ew, stream);
-                launch_gemm(1, m, H, H, dout, ldo, wt.p + static_cast<int64_t>(l - 1) * H * H, H, gmix.p, ldD, plain,
-                            stream);
+                launch_gemm(2, H, H, m, mixed[l].p, ldD, dout, ldo, G(layer_param[l]), pp(layer_param[l]), ew, stream);
+                launch_gemm(1, m, H, H, dout, ldo, wt.p + static_cast<int64_t>(l - 1) * H * pp(layer_param[1]),
+                            pp(layer_param[1]), gmix.p, ldD, plain, stream);
                 dmix = gmix.p;
                 ldm = ldD;
             }
@@ -701,14 +730,14 @@ void gasb_trainer_s::enqueue_batch_res(int32_t p, bool train, bool push, bool fu
         if (gcnii) {
             launch_mask(h0g.p, ldD, h0.p, ldD, me, H, stream);
             launch_colsum(h0g.p, ldD, me, H, G(p_hb1), stream);
-            launch_gemm(2, F, H, me, x_ext.p, ldF, h0g.p, ldD, G(p_hw1), H, plain, stream);
+            launch_gemm(2, F, H, me, x_ext.p, ldF, h0g.p, ldD, G(p_hw1), pp(p_hw1), plain, stream);
         } else {
             launch_colsum(h0g.p, ldD, me, C, G(p_hb2), stream);
-            launch_gemm(2, H, C, me, z.p, ldH, h0g.p, ldD, G(p_hw2), C, plain, stream);
-            launch_gemm(1, me, H, C, h0g.p, ldD, P(p_hw2), C, zg.p, ldH, plain, stream);
+            launch_gemm(2, H, C, me, z.p, ldH, h0g.p, ldD, G(p_hw2), pp(p_hw2), plain, stream);
+            launch_gemm(1, me, H, C, h0g.p, ldD, P(p_hw2), pp(p_hw2), zg.p, ldH, plain, stream);
             launch_mask(zg.p, ldH, z.p, ldH, me, H, stream);
             launch_colsum(zg.p, ldH, me, H, G(p_hb1), stream);
-            launch_gemm(2, F, H, me, x_ext.p, ldF, zg.p, ldH, G(p_hw1), H, plain, stream);
+            launch_gemm(2, F, H, me, x_ext.p, ldF, zg.p, ldH, G(p_hw1), pp(p_hw1), plain, stream);
         }
         launch_adam(params.p, adam_m.p, adam_v.p, grads.p, nparam, t_counter.p, bc.p, spec.lr, spec.beta1,
                     spec.beta2, spec.eps, spec.clip_max_norm, norm_scratch.p, stream);
@@ -772,9 +801,10 @@ void gasb_trainer_s::enqueue_batch(int32_t p, bool train, bool push, bool use_ho
             // HistoryStore::push fused into the epilogue (stamps + the table's value flags)
             PushEpilogue pe{history_table(hist, l), history_ld(hist), bn, history_stamps(hist, l),
                             history_step_ptr(hist), history_flags(hist, l)};
-            launch_gemm(0, m, dout, din, a, lda, Wl, dout, act[l].p, ldH, 0.f, true, push ? &pe : nullptr, stream);
+            launch_gemm(0, m, dout, din, a, lda, Wl, pp(layer_param[l]), act[l].p, ldH, 0.f, true, push ? &pe : nullptr,
+                        stream);
         } else {
-            launch_gemm(0, m, dout, din, a, lda, Wl, dout, logits.p, ldC, 0.f, false, nullptr, stream);
+            launch_gemm(0, m, dout, din, a, lda, Wl, pp(layer_param[l]), logits.p, ldC, 0.f, false, nullptr, stream);
         }
     }
     // ---------------- loss + backward (run_batch, trainer.cpp:295-339) ----------------
@@ -790,9 +820,9 @@ void gasb_trainer_s::enqueue_batch(int32_t p, bool train, bool push, bool use_ho
             const int64_t lda = ld_of(din);
             const float* a = (l == 1 && use_hoisted) ? agg_all.p + r0 * ldF : agg[l].p;
             // matmul backward (tensor.cpp:169-204): dW = agg^T g ; dagg = g W^T
-            launch_gemm(2, din, dout, m, a, lda, g, ldg, gW(l), dout, 0.f, false, nullptr, stream);
+            launch_gemm(2, din, dout, m, a, lda, g, ldg, gW(l), pp(layer_param[l]), 0.f, false, nullptr, stream);
             if (l == 1) break;  // x_ext carries no gradient
-            launch_gemm(1, m, din, dout, g, ldg, W(l), dout, g_agg.p, ldH, 0.f, false, nullptr, stream);
+            launch_gemm(1, m, din, dout, g, ldg, W(l), pp(layer_param[l]), g_agg.p, ldH, 0.f, false, nullptr, stream);
             // aggregate backward over intra-batch edges + compose bwd + relu bwd (mask = act)
             launch_spmm_bwd(t_rowptr.p + r0 + p, m, t_src.p, t_cf.p, g_agg.p, ldH, din, act[l - 1].p, ldH, g_out.p,
                             ldH, stream, m);
@@ -952,7 +982,7 @@ gasb_status gasb_trainer_batch(gasb_trainer t, int32_t part, int64_t epoch, int3
             *loss = l;
         }
         if (h_grads && st)
-            GASB_CUDA(cudaMemcpy(h_grads, t->grads.p, sizeof(float) * t->nparam, cudaMemcpyDeviceToHost));
+            t->params_to_dense(t->grads.p, h_grads);
         if (stepped) *stepped = st ? 1 : 0;
     });
 }
@@ -960,7 +990,7 @@ gasb_status gasb_trainer_batch(gasb_trainer t, int32_t part, int64_t epoch, int3
 gasb_status gasb_trainer_num_param_floats(gasb_trainer t, int64_t* out) {
     return guard([&] {
         require(t && out, "trainer: null argument");
-        *out = t->nparam;
+        *out = t->nparam_dense;
     });
 }
 
@@ -968,7 +998,7 @@ gasb_status gasb_trainer_get_params(gasb_trainer t, float* h) {
     return guard([&] {
         require(t && h, "trainer: null argument");
         GASB_CUDA(cudaStreamSynchronize(t->stream));
-        GASB_CUDA(cudaMemcpy(h, t->params.p, sizeof(float) * t->nparam, cudaMemcpyDeviceToHost));
+        t->params_to_dense(t->params.p, h);
     });
 }
 
@@ -976,7 +1006,7 @@ gasb_status gasb_trainer_set_params(gasb_trainer t, const float* h) {
     return guard([&] {
         require(t && h, "trainer: null argument");
         GASB_CUDA(cudaStreamSynchronize(t->stream));
-        GASB_CUDA(cudaMemcpy(t->params.p, h, sizeof(float) * t->nparam, cudaMemcpyHostToDevice));
+        t->params_from_dense(h, t->params.p);
     });
 }
 
