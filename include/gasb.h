@@ -243,6 +243,37 @@ gasb_status gasb_host_unregister(void* h_ptr);
 /* Kernel launches per epoch (counted by the host driver while enqueueing). */
 gasb_status gasb_trainer_launch_count(gasb_trainer t, int64_t* out);
 
+/* ==================================================================================== */
+/* data-parallel training over k GPUs of one node (no reference counterpart: */
+/* the reference is single-process). One process per GPU. A step runs k consecutive      */
+/* batches of gas_epoch's seeded order (trainer.cpp:395-400), rank j the j-th, against    */
+/* start-of-step parameters and histories; pushes are committed to every replica after    */
+/* the step; gradients are summed in rank order over the batches with training rows,      */
+/* divided by their count, clipped and applied once (oracle: go_session_dp_epoch).        */
+/* Exchange over peer memory: each rank exports one HBM region (CUDA IPC handle); peers   */
+/* map it (NVLink P2P) and read gradients and pushed rows directly.                       */
+/* ==================================================================================== */
+#define GASB_DP_HANDLE_BYTES 64
+typedef struct gasb_dp_s* gasb_dp;
+/* Turns a trainer into rank `rank` of `world` (1..8): allocates the exchange region and
+ * makes the trainer's gradient and pushed-row buffers views into it. */
+gasb_status gasb_dp_create(gasb_trainer t, int32_t rank, int32_t world, gasb_dp* out);
+/* This rank's region handle (GASB_DP_HANDLE_BYTES), to be all-gathered by the caller. */
+gasb_status gasb_dp_export(gasb_dp d, uint8_t* h_handle);
+/* Maps every peer's region from the gathered handles (world x GASB_DP_HANDLE_BYTES). */
+gasb_status gasb_dp_connect(gasb_dp d, const uint8_t* h_handles);
+/* Enqueues one data-parallel epoch on the trainer's stream (all ranks must call it). */
+gasb_status gasb_dp_epoch_async(gasb_dp d, int64_t epoch, int32_t shuffle);
+/* Synchronizes; a cross-rank barrier that timed out is a RUNTIME_ERROR. */
+gasb_status gasb_dp_check(gasb_dp d);
+/* Per-part losses of the last epoch for the parts THIS rank ran (0 elsewhere): summing
+ * the arrays over ranks gives every part's loss exactly. Synchronizes. */
+gasb_status gasb_dp_last_losses(gasb_dp d, double* h_losses);
+gasb_status gasb_dp_launch_count(gasb_dp d, int64_t* out);
+gasb_status gasb_dp_destroy(gasb_dp d);
+/* gas_epoch's batch order (trainer.cpp:395-400) for `epoch` (host only). */
+gasb_status gasb_epoch_order(int32_t num_parts, uint64_t seed, int64_t epoch, int32_t shuffle, int32_t* h_order);
+
 #ifdef __cplusplus
 }
 #endif

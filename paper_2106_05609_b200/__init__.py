@@ -10,9 +10,10 @@ from .graph import (BatchPlan, BatchSchedule, Graph, build_graph, graph_from_csr
                     partition_parts, synth_features, synth_pairs)
 from .history import HistoryStore, Prefetcher, PrefetchHandle  # noqa: F401
 from .trainer import AdamConfig, GasTrainer, ModelSpec, TrainerOptions  # noqa: F401
+from .dp import DataParallelTrainer, epoch_order, step_plan  # noqa: F401
 
 __all__ = [
     "Graph", "build_graph", "graph_from_csr", "make_batch_plan", "BatchPlan", "BatchSchedule", "partition_parts",
     "synth_pairs", "synth_features", "HistoryStore", "Prefetcher", "PrefetchHandle", "ModelSpec", "AdamConfig",
-    "TrainerOptions", "GasTrainer",
+    "TrainerOptions", "GasTrainer", "DataParallelTrainer", "epoch_order", "step_plan",
 ]

@@ -116,7 +116,18 @@ _SIGS = {
     "gasb_trainer_profile_spmm": (i32, [vp, i32, i32, i32, P(f32)]),
     "gasb_host_register": (i32, [vp, C.c_size_t]),
     "gasb_host_unregister": (i32, [vp]),
+    "gasb_dp_create": (i32, [vp, i32, i32, P(vp)]),
+    "gasb_dp_export": (i32, [vp, vp]),
+    "gasb_dp_connect": (i32, [vp, vp]),
+    "gasb_dp_epoch_async": (i32, [vp, i64, i32]),
+    "gasb_dp_check": (i32, [vp]),
+    "gasb_dp_last_losses": (i32, [vp, vp]),
+    "gasb_dp_launch_count": (i32, [vp, P(i64)]),
+    "gasb_dp_destroy": (i32, [vp]),
+    "gasb_epoch_order": (i32, [i32, u64, i64, i32, vp]),
 }
+
+DP_HANDLE_BYTES = 64  # GASB_DP_HANDLE_BYTES
 
 for _name, (_res, _args) in _SIGS.items():
     _fn = getattr(lib, _name)

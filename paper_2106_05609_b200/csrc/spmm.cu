@@ -14,6 +14,8 @@
 // Backward (tensor.cpp:531-549): the scatter gx[col_e] += c_e * gy[r] becomes a gather
 // over the transposed stencil, entries of each target in ascending r with fp32
 // multiply-then-add -> bit-exact; relu backward (tensor.cpp:363-369) fused as a mask.
+#include <cstring>
+
 #include "gasb_internal.hpp"
 #include "kernels.cuh"
 
@@ -409,6 +411,189 @@ __global__ void __launch_bounds__(kPipeWarps * 32, 2) spmm_fwd_pipe_kernel(
     }
 }
 
+// ---- direct-load forward (no shared-memory staging) ------------------------------------
+// Same work decomposition, segment tables and fp64 partial protocol as the pipelined
+// kernel, but each lane gathers its 16 B piece of every source row straight into
+// registers (LDG.128, L1 no-allocate): KD independent row loads in flight per warp, no
+// stage bookkeeping, and the edge stream runs across segment (row) boundaries without
+// draining. Small register footprint -> 16 warps per SM hide the L2/HBM latency.
+constexpr int kDirectKD = 8;      // row loads in flight per warp
+constexpr int kDirectWarps = 8;   // warps per CTA (2 CTAs per SM)
+
+__device__ __forceinline__ float4 ldg_row_piece(const float* p) {
+    float4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "l"(p));
+    return v;
+}
+
+// Ends segment `k` of the warp's window: store the row (single-segment row) or publish an
+// fp64 partial, the last-arriving warp of the row summing the partials in segment order.
+__device__ __forceinline__ void direct_finish(double a0, double a1, double a2, double a3, int32_t row, int32_t slot, int lane, int32_t col,
+                                              int32_t chunk, int32_t dim, float* __restrict__ y, int64_t ldy,
+                                              int64_t row_base, double* __restrict__ partial, int64_t pld,
+                                              int32_t* __restrict__ counters, int32_t cld,
+                                              const int32_t* __restrict__ seg_slot,
+                                              const int32_t* __restrict__ row_seg0,
+                                              const int32_t* __restrict__ row_nseg) {
+    double acc[4] = {a0, a1, a2, a3};
+    bool store = true;
+    if (slot >= 0) {
+        double* pp = partial + static_cast<int64_t>(slot) * pld + col;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) pp[k] = acc[k];
+        __threadfence();
+        __syncwarp();
+        int last = 0;
+        const int32_t nk = row_nseg[row];
+        if (lane == 0) last = atomicAdd(counters + static_cast<int64_t>(row) * cld + chunk, 1) == nk - 1;
+        store = __shfl_sync(0xffffffffu, last, 0) != 0;
+        if (store) {
+            __threadfence();
+            const int32_t s0 = row_seg0[row];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) acc[k] = 0.0;
+            for (int32_t i = 0; i < nk; ++i) {
+                const double* q2 = partial + static_cast<int64_t>(seg_slot[s0 + i]) * pld + col;
+#pragma unroll
+                for (int k = 0; k < 4; ++k) acc[k] += __ldcg(q2 + k);
+            }
+            if (lane == 0) counters[static_cast<int64_t>(row) * cld + chunk] = 0;  // self-reset
+        }
+    }
+    if (store) {
+        float* yr = y + (static_cast<int64_t>(row) - row_base) * ldy;
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            if (col + k < dim) yr[col + k] = static_cast<float>(acc[k]);
+    }
+}
+
+template <int MODE>
+__device__ __forceinline__ void direct_items(
+    const int64_t* __restrict__ seg_beg, const int32_t* __restrict__ seg_row, const int32_t* __restrict__ seg_slot,
+    const int32_t* __restrict__ row_seg0, const int32_t* __restrict__ row_nseg, const int32_t* __restrict__ range_seg,
+    int32_t nranges, const int32_t* __restrict__ cols, const double* __restrict__ coeffs, const float* __restrict__ x,
+    int64_t ldx, int32_t dim, int32_t nchunks, float* __restrict__ y, int64_t ldy, int64_t row_base,
+    double* __restrict__ partial, int64_t pld, int32_t* __restrict__ counters, int32_t cld) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nwarps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
+    for (int64_t item = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+         item < static_cast<int64_t>(nchunks) * nranges; item += nwarps) {
+        const int32_t chunk = static_cast<int32_t>(item / nranges);
+        const int32_t r = static_cast<int32_t>(item - static_cast<int64_t>(chunk) * nranges);
+        const int32_t s_lo = range_seg[r], s_hi = range_seg[r + 1];
+        if (s_lo >= s_hi) continue;
+        const int32_t col = chunk * 128 + lane * 4;
+        const bool colok = col < dim;  // col % 4 == 0 and ldx % 4 == 0: the whole piece is inside the pitch
+        const float* xc = x + (colok ? col : 0);
+        // window of 32 segment records (end offset, row, slot), lane k holds segment wseg + k
+        int32_t wseg = s_lo, cur = s_lo;
+        int64_t w_end = 0;
+        int32_t w_row = 0, w_slot = -1;
+        auto load_window = [&](int32_t from) {
+            wseg = from;
+            const int32_t sg = from + lane;
+            w_end = sg < s_hi ? seg_beg[sg + 1] : 0;
+            w_row = sg < s_hi ? seg_row[sg] : 0;
+            w_slot = sg < s_hi ? seg_slot[sg] : -1;
+        };
+        load_window(s_lo);
+        int64_t cur_end = __shfl_sync(0xffffffffu, w_end, 0);
+        double acc[4] = {0.0, 0.0, 0.0, 0.0};
+        auto finish = [&] {
+            const int k = cur - wseg;
+            const int32_t row = __shfl_sync(0xffffffffu, w_row, k);
+            const int32_t slot = __shfl_sync(0xffffffffu, w_slot, k);
+            direct_finish(acc[0], acc[1], acc[2], acc[3], row, slot, lane, col, chunk, dim, y, ldy, row_base, partial, pld, counters, cld,
+                          seg_slot, row_seg0, row_nseg);
+            acc[0] = acc[1] = acc[2] = acc[3] = 0.0;
+            ++cur;
+            if (cur < s_hi) {
+                if (cur - wseg >= 32) load_window(cur);
+                cur_end = __shfl_sync(0xffffffffu, w_end, cur - wseg);
+            }
+        };
+        const int64_t E_lo = seg_beg[s_lo], E_hi = seg_beg[s_hi];
+        for (int64_t e = E_lo; e < E_hi; e += 32) {
+            const int n = static_cast<int>(E_hi - e < 32 ? E_hi - e : 32);
+            const int32_t mc = lane < n ? __ldg(cols + e + lane) : 0;
+            const double mf = lane < n ? __ldg(coeffs + e + lane) : 0.0;
+            for (int j = 0; j < n; j += kDirectKD) {
+                float4 v[kDirectKD];
+#pragma unroll
+                for (int k = 0; k < kDirectKD; ++k) {
+                    const int32_t c = __shfl_sync(0xffffffffu, mc, j + k);
+                    v[k] = (j + k < n && colok) ? ldg_row_piece(xc + static_cast<int64_t>(c) * ldx)
+                                                : make_float4(0.f, 0.f, 0.f, 0.f);
+                }
+#pragma unroll
+                for (int k = 0; k < kDirectKD; ++k) {
+                    const double f = __shfl_sync(0xffffffffu, mf, j + k);
+                    if (j + k < n) {  // warp-uniform
+                        while (e + j + k == cur_end && cur < s_hi) finish();
+                        acc[0] = __fma_rn(f, widen_scaled<MODE>(v[k].x), acc[0]);
+                        acc[1] = __fma_rn(f, widen_scaled<MODE>(v[k].y), acc[1]);
+                        acc[2] = __fma_rn(f, widen_scaled<MODE>(v[k].z), acc[2]);
+                        acc[3] = __fma_rn(f, widen_scaled<MODE>(v[k].w), acc[3]);
+                    }
+                }
+            }
+        }
+        while (cur < s_hi) finish();  // the last segment (and any empty trailing ones)
+    }
+}
+
+__global__ void __launch_bounds__(kDirectWarps * 32, 2) spmm_fwd_direct_kernel(
+    const int64_t* __restrict__ seg_beg, const int32_t* __restrict__ seg_row, const int32_t* __restrict__ seg_slot,
+    const int32_t* __restrict__ row_seg0, const int32_t* __restrict__ row_nseg, const int32_t* __restrict__ range_seg,
+    int32_t nranges, const int32_t* __restrict__ cols, const double* __restrict__ coeffs, const float* __restrict__ x,
+    int64_t ldx, int32_t dim, int32_t nchunks, float* __restrict__ y, int64_t ldy, int64_t row_base,
+    double* __restrict__ partial, int64_t pld, int32_t* __restrict__ counters, int32_t cld,
+    const int32_t* __restrict__ table_flags) {
+    const int mode = widen_mode(table_flags);
+#define GASB_DIRECT(M)                                                                                           \
+    direct_items<M>(seg_beg, seg_row, seg_slot, row_seg0, row_nseg, range_seg, nranges, cols, coeffs, x, ldx, dim, \
+                    nchunks, y, ldy, row_base, partial, pld, counters, cld)
+    if (mode == kWidenNonNeg) GASB_DIRECT(kWidenNonNeg);
+    else if (mode == kWidenSigned) GASB_DIRECT(kWidenSigned);
+    else GASB_DIRECT(kWidenF2F);
+#undef GASB_DIRECT
+}
+
+static void launch_direct(const SpmmSegs& s, const int32_t* cols, const double* coeffs, const float* x, int64_t ldx,
+                          int32_t dim, float* y, int64_t ldy, int64_t row_base, double* partial, int64_t partial_ld,
+                          int32_t* counters, int32_t counters_ld, cudaStream_t st, const int32_t* special) {
+    const int32_t nchunks = static_cast<int32_t>(ceil_div(dim, 128));
+    require(nchunks <= counters_ld && static_cast<int64_t>(nchunks) * 128 <= partial_ld,
+            "spmm_fwd: counters / partials too narrow");
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        GASB_CUDA(cudaGetDevice(&dev));
+        GASB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    }
+    const int64_t items = static_cast<int64_t>(nchunks) * s.nranges;
+    const int64_t blocks = std::min<int64_t>(ceil_div(items, kDirectWarps), 2LL * sms);
+    spmm_fwd_direct_kernel<<<static_cast<unsigned>(blocks), kDirectWarps * 32, 0, st>>>(
+        s.seg_beg, s.seg_row, s.seg_slot, s.row_seg0, s.row_nseg, s.range_seg, s.nranges, cols, coeffs, x, ldx, dim,
+        nchunks, y, ldy, row_base, partial, partial_ld, counters, counters_ld, special);
+}
+
+// SpMM gather engine (GASB_SPMM_ENGINE = tma | cp | direct): TMA tile::gather4 staging,
+// cp.async staging, or direct register loads.
+static int spmm_engine() {
+    static int v = [] {
+        const char* e = getenv("GASB_SPMM_ENGINE");
+        if (!e) return 0;
+        if (!strcmp(e, "direct")) return 2;
+        if (!strcmp(e, "cp")) return 1;
+        return 0;
+    }();
+    return v;
+}
+
 static int g_pipe_smem_set[2][2] = {};
 
 template <int CPL, bool TMA>
@@ -584,7 +769,14 @@ void launch_spmm_fwd(const SpmmSegs& s, const int32_t* cols, const double* coeff
     if (s.nranges <= 0 || dim <= 0) return;
     require(ldx % 4 == 0 && reinterpret_cast<uintptr_t>(x) % 16 == 0,
             "spmm_fwd: source rows must be 16 B aligned (ldx % 4 == 0)");
-    const bool tma = tmap != nullptr && spmm_use_tma();
+    if (spmm_engine() == 2) {
+        launch_direct(s, cols, coeffs, x, ldx, dim, y, ldy, row_base, partial, partial_ld, counters, counters_ld, st,
+                      special);
+        ++t_launches;
+        GASB_CUDA(cudaGetLastError());
+        return;
+    }
+    const bool tma = tmap != nullptr && spmm_use_tma() && spmm_engine() == 0;
 #define GASB_PIPE(C, T)                                                                                               \
     launch_pipe<C, T>(s, cols, coeffs, x, ldx, dim, y, ldy, row_base, partial, partial_ld, counters, counters_ld, st, \
                       special, tmap)

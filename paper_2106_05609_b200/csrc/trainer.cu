@@ -31,19 +31,9 @@
 #include <numeric>
 #include <random>
 
-#include "gasb_internal.hpp"
-#include "kernels.cuh"
+#include "trainer_impl.hpp"
 
 namespace gasb {
-const Schedule& schedule_of(gasb_schedule s);
-gasb_history history_create(int32_t layers, int32_t n, int32_t dim);
-void history_destroy(gasb_history h);
-float* history_table(gasb_history h, int32_t layer);
-int64_t history_ld(gasb_history h);
-int64_t* history_stamps(gasb_history h, int32_t layer);
-int64_t* history_step_ptr(gasb_history h);
-int32_t* history_flags(gasb_history h, int32_t layer);
-
 namespace {
 
 // ---- host RNG exactly as gas::Rng (include/gas/rng.hpp) -------------------------------
@@ -75,43 +65,6 @@ void glorot_init(float* w, int64_t rows, int64_t cols, uint64_t seed) {  // nn.c
     Rng rng(seed);
     for (int64_t i = 0; i < rows * cols; ++i) w[i] = static_cast<float>((rng.next_double() * 2.0 - 1.0) * bound);
 }
-
-template <class T>
-struct DevBuf {
-    T* p = nullptr;
-    int64_t n = 0;
-    void alloc(int64_t count) {
-        free();
-        n = count;
-        GASB_CUDA(cudaMalloc(&p, sizeof(T) * std::max<int64_t>(count, 1)));
-    }
-    void upload(const std::vector<T>& v) {
-        alloc(static_cast<int64_t>(v.size()));
-        if (!v.empty()) GASB_CUDA(cudaMemcpy(p, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice));
-    }
-    void zero() {
-        if (n) GASB_CUDA(cudaMemset(p, 0, sizeof(T) * n));
-    }
-    void free() {
-        if (p) cudaFree(p);
-        p = nullptr;
-        n = 0;
-    }
-    ~DevBuf() { free(); }
-};
-
-struct SegTable {
-    DevBuf<int64_t> seg_beg;
-    DevBuf<int32_t> seg_row, seg_slot, row_seg0, row_nseg;
-    DevBuf<int32_t> ranges;  // per group: nranges + 1 work-range boundaries (split_ranges)
-    int32_t nranges = 0;
-    std::vector<int64_t> group_seg0, group_nseg;  // per group (batch) range of segments
-    int64_t max_group_slots = 0, total_slots = 0;
-    SpmmSegs segs(int64_t g) const {
-        return SpmmSegs{seg_beg.p, seg_row.p, seg_slot.p, row_seg0.p, row_nseg.p, ranges.p + g * (nranges + 1),
-                        nranges};
-    }
-};
 
 // Segments each group (batch) of rows of the absolute row pointer `rp` for one SpMM launch
 // per group (segment_launch, spmm.cu): split = false keeps rows whole (bit-exact mode).
@@ -166,170 +119,7 @@ __global__ void compose_kernel(const int32_t* __restrict__ src_index, const floa
 
 }  // namespace
 }  // namespace gasb
-
 using namespace gasb;
-
-struct gasb_trainer_s {
-    gasb_model_spec spec{};
-    gasb_trainer_options opt{};
-    int32_t n = 0, F = 0, C = 0, L = 0, H = 0, hist_dim = 0, num_parts = 0;
-    int64_t ldF = 0, ldH = 0, ldC = 0;
-    const Schedule* sched = nullptr;
-    cudaStream_t stream = nullptr, side = nullptr;
-    gasb_history hist = nullptr;
-
-    // per part (host)
-    std::vector<int32_t> nb, ne, nh, ntrain;
-    std::vector<int64_t> row_off, edge_off, t_off, tr_off, ext_off;
-    int32_t nb_max = 0, ne_max = 0;
-
-    // device data
-    DevBuf<float> X;
-    DevBuf<int32_t> batch_nodes, cols_g, cols_l, t_src, train_rows, train_labels, extended, compose_idx, halo_ids;
-    DevBuf<double> coef64;
-    DevBuf<float> t_cf;
-    DevBuf<int64_t> t_rowptr;
-    SegTable seg_batch, seg_all;
-    DevBuf<int32_t> counters, row_label, xflags, ce_done;  // xflags: value flags of X (kernels.cuh)
-    DevBuf<double> partial_batch, partial_all;
-    int32_t max_chunks = 0;
-    int64_t pld = 0, pld_all = 0;
-
-    // model
-    // per parameter tensor: device offset, rows, cols, row pitch (cols rounded up to 4 floats
-    // so every weight is a TMA-describable GEMM operand; pads are 0 and stay 0 under Adam)
-    std::vector<int64_t> poff, prow, pcol, ppitch;
-    int64_t nparam_dense = 0;  // Model::params() floats (the API's flat layout)
-    std::vector<int32_t> layer_param;       // param index of W_l (GCN) per layer 1..L
-    int64_t nparam = 0;
-    std::vector<float> h_params_init;
-    DevBuf<float> params, grads, adam_m, adam_v;
-    DevBuf<int64_t> t_counter;
-    DevBuf<double> bc, norm_scratch;
-    int64_t bc_cap = 0, t_host = 0;
-
-    // activations
-    std::vector<int32_t> dims;    // d[0..L]
-    DevBuf<float> agg_all;        // hoisted layer-1 aggregation, n x ldF
-    std::vector<DevBuf<float>> agg, act;
-    DevBuf<float> logits, glogits, g_agg, g_out, x_ext, h_ext, halo_buf;
-    // TMA tensor maps of the SpMM source tables (tile::gather4 staging, spmm.cu)
-    CUtensorMap tm_x{}, tm_xext{}, tm_hext{};
-    std::vector<CUtensorMap> tm_hist;
-    bool tm_ok[4] = {false, false, false, false};  // x, hist, x_ext, h_ext
-    const CUtensorMap* source_tmap(int32_t l) const {
-        if (l == 1) return tm_ok[0] ? &tm_x : nullptr;
-        return tm_ok[1] ? &tm_hist[l - 2] : nullptr;
-    }
-    void build_tmaps() {
-        const int32_t bc = spmm_box_cols();
-        tm_ok[0] = make_row_tmap(X.p, n, F, ldF, bc, &tm_x);
-        tm_hist.resize(static_cast<size_t>(std::max(0, L - 1)));
-        tm_ok[1] = L >= 2;
-        for (int32_t l = 1; l < L; ++l)
-            tm_ok[1] = tm_ok[1] && make_row_tmap(history_table(hist, l), n, hist_dim, history_ld(hist), bc,
-                                                 &tm_hist[l - 1]);
-        if (x_ext.p) tm_ok[2] = make_row_tmap(x_ext.p, ne_max, F, ldF, bc, &tm_xext);
-        const int32_t hdim = residual ? D : H;
-        if (h_ext.p) tm_ok[3] = make_row_tmap(h_ext.p, ne_max, hdim, ld_of(hdim), bc, &tm_hext);
-        if (residual && h0.p) tm_h0_ok = make_row_tmap(h0.p, ne_max, D, ldD, bc, &tm_h0);
-    }
-    DevBuf<double> loss, row_scratch;
-
-    DevBuf<float> gemm_ws;  // split-K scratch of the tensor-core GEMM (gemm_tc.cu)
-    struct WsGuard {        // scopes the thread's GEMM workspace to one enqueue
-        explicit WsGuard(DevBuf<float>& w) { set_gemm_workspace(w.p, kGemmWsFloats); }
-        ~WsGuard() { set_gemm_workspace(nullptr, 0); }
-    };
-
-    // ---- residual models: APPNP (kind 2) / GCNII (kind 3) ----
-    bool residual = false;
-    int32_t D = 0;      // width of every propagation layer and of the histories (GCNII: H, APPNP: C)
-    int64_t ldD = 0, ldA = 0;  // ldA: row pitch of act[l] (GCN: ldH)
-    int32_t p_hw1 = -1, p_hb1 = -1, p_hw2 = -1, p_hb2 = -1, p_ow = -1, p_ob = -1;  // param indices
-    DevBuf<int32_t> brow;                  // batch_local_rows per part, at row_off
-    DevBuf<int64_t> a_rowptr;              // CSC over ALL edges of a batch (targets = V_b local rows)
-    DevBuf<int32_t> a_src;                 //   entries: batch row r, ascending r per target
-    DevBuf<float> a_cf;
-    std::vector<int64_t> a_off;            // per part: offset of its ne+1 row pointers
-    DevBuf<float> h0, z, h0g, zg, wt, prop, gmix, dprop, gout;
-    std::vector<DevBuf<float>> mixed;      // GCNII: mixed_l (needed for dW~_l)
-    CUtensorMap tm_h0{};
-    bool tm_h0_ok = false;
-    float* P(int32_t i) { return params.p + poff[i]; }
-    float* G(int32_t i) { return grads.p + poff[i]; }
-    int32_t add_param(int64_t r, int64_t c) {
-        poff.push_back(nparam);
-        prow.push_back(r);
-        pcol.push_back(c);
-        ppitch.push_back(round_up(c, 4));
-        nparam += r * ppitch.back();
-        nparam_dense += r * c;
-        return static_cast<int32_t>(poff.size()) - 1;
-    }
-    int64_t pp(int32_t i) const { return ppitch[i]; }
-    // dense (Model::params() order) <-> padded device layout
-    void params_to_dense(const float* dev, float* host) const {
-        int64_t o = 0;
-        for (size_t i = 0; i < poff.size(); ++i) {
-            GASB_CUDA(cudaMemcpy2D(host + o, sizeof(float) * pcol[i], dev + poff[i], sizeof(float) * ppitch[i],
-                                   sizeof(float) * pcol[i], prow[i], cudaMemcpyDeviceToHost));
-            o += prow[i] * pcol[i];
-        }
-    }
-    void params_from_dense(const float* host, float* dev) const {
-        int64_t o = 0;
-        for (size_t i = 0; i < poff.size(); ++i) {
-            GASB_CUDA(cudaMemcpy2D(dev + poff[i], sizeof(float) * ppitch[i], host + o, sizeof(float) * pcol[i],
-                                   sizeof(float) * pcol[i], prow[i], cudaMemcpyHostToDevice));
-            o += prow[i] * pcol[i];
-        }
-    }
-    void build_residual(const std::vector<int64_t>& h_arp, const std::vector<int32_t>& h_asrc,
-                        const std::vector<float>& h_acf, const std::vector<int32_t>& h_brow);
-    void enqueue_batch_res(int32_t p, bool train, bool push, bool fused);
-
-    // graphs
-    std::vector<cudaGraphExec_t> graphs;
-    std::vector<int64_t> graph_launches;
-    int64_t epoch_launches = 0;
-    std::vector<int32_t> last_order;
-    std::vector<uint8_t> last_stepped;
-
-    ~gasb_trainer_s() {
-        if (stream) cudaStreamSynchronize(stream);
-        for (auto g : graphs)
-            if (g) cudaGraphExecDestroy(g);
-        if (hist) history_destroy(hist);
-        if (side) cudaStreamDestroy(side);
-        if (stream) cudaStreamDestroy(stream);
-    }
-
-    int64_t ld_of(int32_t d) const { return round_up(std::max(d, 1), 8); }
-    // value flags of the table layer l's aggregation reads: X for l = 1, H_{l-1} otherwise
-    const int32_t* source_flags(int32_t l) const { return l == 1 ? xflags.p : history_flags(hist, l - 1); }
-    float* W(int32_t l) { return params.p + poff[layer_param[l]]; }
-    float* gW(int32_t l) { return grads.p + poff[layer_param[l]]; }
-
-    void ensure_bc(int64_t t_max) {
-        if (t_max < bc_cap) return;
-        int64_t cap = std::max<int64_t>(1024, bc_cap);
-        while (cap <= t_max) cap *= 2;
-        std::vector<double> h(static_cast<size_t>(2 * cap));
-        for (int64_t t = 1; t < cap; ++t) {  // nn.cpp:23-24, host pow (as the reference)
-            h[2 * t] = 1.0 - std::pow(static_cast<double>(spec.beta1), static_cast<double>(t));
-            h[2 * t + 1] = 1.0 - std::pow(static_cast<double>(spec.beta2), static_cast<double>(t));
-        }
-        GASB_CUDA(cudaStreamSynchronize(stream));
-        bc.upload(h);
-        bc_cap = cap;
-    }
-
-    void build(const float* h_features, const int32_t* h_labels, const uint8_t* h_train);
-    void enqueue_batch(int32_t p, bool train, bool push, bool use_hoisted, bool fused);
-    void enqueue_hoisted();
-    void run_epoch(int64_t epoch, bool shuffle);
-};
 
 void gasb_trainer_s::build(const float* h_features, const int32_t* h_labels, const uint8_t* h_train) {
     const Graph& g = *sched->graph;
@@ -622,7 +412,7 @@ void gasb_trainer_s::build_residual(const std::vector<int64_t>& h_arp, const std
 // rows (:142-163), appnp/gcnii layers (layers.cpp:150-168), the GCNII output head
 // (:221-227), then run_batch's backward (halo rows of h0 receive the layer-1 aggregation
 // gradient) and Adam.
-void gasb_trainer_s::enqueue_batch_res(int32_t p, bool train, bool push, bool fused) {
+void gasb_trainer_s::enqueue_batch_res(int32_t p, bool train, bool push, bool fused, bool dp) {
     const int32_t m = nb[p], me = ne[p];
     const int64_t r0 = row_off[p];
     const SpmmSegs segs = seg_batch.segs(p);
@@ -739,18 +529,20 @@ void gasb_trainer_s::enqueue_batch_res(int32_t p, bool train, bool push, bool fu
             launch_colsum(zg.p, ldH, me, H, G(p_hb1), stream);
             launch_gemm(2, F, H, me, x_ext.p, ldF, zg.p, ldH, G(p_hw1), pp(p_hw1), plain, stream);
         }
-        launch_adam(params.p, adam_m.p, adam_v.p, grads.p, nparam, t_counter.p, bc.p, spec.lr, spec.beta1,
-                    spec.beta2, spec.eps, spec.clip_max_norm, norm_scratch.p, stream);
+        if (!dp)  // data-parallel: Adam runs on the cross-rank gradient sum (dp.cu)
+            launch_adam(params.p, adam_m.p, adam_v.p, grads.p, nparam, t_counter.p, bc.p, spec.lr, spec.beta1,
+                        spec.beta2, spec.eps, spec.clip_max_norm, norm_scratch.p, stream);
     }
+    if (dp) return;
     end_batch_kernel<<<1, 1, 0, stream>>>(history_step_ptr(hist), t_counter.p, stepped ? 1 : 0);
     ++t_launches;
     GASB_CUDA(cudaGetLastError());
 }
 
-void gasb_trainer_s::enqueue_batch(int32_t p, bool train, bool push, bool use_hoisted, bool fused) {
+void gasb_trainer_s::enqueue_batch(int32_t p, bool train, bool push, bool use_hoisted, bool fused, bool dp) {
     WsGuard ws(gemm_ws);
     if (residual) {
-        enqueue_batch_res(p, train, push, fused);
+        enqueue_batch_res(p, train, push, fused, dp);
         return;
     }
     const int32_t m = nb[p];
@@ -829,9 +621,11 @@ void gasb_trainer_s::enqueue_batch(int32_t p, bool train, bool push, bool use_ho
             g = g_out.p;
             ldg = ldH;
         }
-        launch_adam(params.p, adam_m.p, adam_v.p, grads.p, nparam, t_counter.p, bc.p, spec.lr, spec.beta1,
-                    spec.beta2, spec.eps, spec.clip_max_norm, norm_scratch.p, stream);
+        if (!dp)  // data-parallel: Adam runs on the cross-rank gradient sum (dp.cu)
+            launch_adam(params.p, adam_m.p, adam_v.p, grads.p, nparam, t_counter.p, bc.p, spec.lr, spec.beta1,
+                        spec.beta2, spec.eps, spec.clip_max_norm, norm_scratch.p, stream);
     }
+    if (dp) return;
     end_batch_kernel<<<1, 1, 0, stream>>>(history_step_ptr(hist), t_counter.p, stepped ? 1 : 0);
     ++t_launches;
     GASB_CUDA(cudaGetLastError());
@@ -852,29 +646,40 @@ void gasb_trainer_s::run_epoch(int64_t epoch, bool shuffle) {
     const int64_t l0 = t_launches;
     if (hoisted) enqueue_hoisted();
     epoch_launches = t_launches - l0;
-    for (int32_t p : order) {
-        if (opt.use_graphs) {
-            if (!graphs[p]) {
-                cudaGraph_t graph;
-                const int64_t c0 = t_launches;
-                GASB_CUDA(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
-                enqueue_batch(p, true, true, hoisted, opt.fused != 0);
-                GASB_CUDA(cudaStreamEndCapture(stream, &graph));
-                graph_launches[p] = t_launches - c0;
-                t_launches = c0;
-                GASB_CUDA(cudaGraphInstantiate(&graphs[p], graph, 0));
-                GASB_CUDA(cudaGraphDestroy(graph));
-            }
-            GASB_CUDA(cudaGraphLaunch(graphs[p], stream));
-            epoch_launches += graph_launches[p];
-        } else {
-            const int64_t c0 = t_launches;
-            enqueue_batch(p, true, true, hoisted, opt.fused != 0);
-            epoch_launches += t_launches - c0;
-        }
-    }
+    for (int32_t p : order) epoch_launches += launch_batch_graph(p, false);
     t_host += steps;
     last_order = order;
+}
+
+// Enqueues one training batch (forward, push, loss, backward; + Adam and the step counters
+// unless dp) on `stream`, through its captured per-part graph when use_graphs. Returns the
+// number of kernels it launches.
+int64_t gasb_trainer_s::launch_batch_graph(int32_t p, bool dp) {
+    const bool hoisted = !dp && opt.hoist_layer1 && opt.fused && !residual;
+    if (!opt.use_graphs) {
+        const int64_t c0 = t_launches;
+        enqueue_batch(p, true, true, hoisted, opt.fused != 0, dp);
+        return t_launches - c0;
+    }
+    std::vector<cudaGraphExec_t>& gs = dp ? graphs_dp : graphs;
+    std::vector<int64_t>& gl = dp ? graph_launches_dp : graph_launches;
+    if (gs.empty()) {
+        gs.assign(num_parts, nullptr);
+        gl.assign(num_parts, 0);
+    }
+    if (!gs[p]) {
+        cudaGraph_t graph;
+        const int64_t c0 = t_launches;
+        GASB_CUDA(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
+        enqueue_batch(p, true, true, hoisted, opt.fused != 0, dp);
+        GASB_CUDA(cudaStreamEndCapture(stream, &graph));
+        gl[p] = t_launches - c0;
+        t_launches = c0;
+        GASB_CUDA(cudaGraphInstantiate(&gs[p], graph, 0));
+        GASB_CUDA(cudaGraphDestroy(graph));
+    }
+    GASB_CUDA(cudaGraphLaunch(gs[p], stream));
+    return gl[p];
 }
 
 extern "C" {

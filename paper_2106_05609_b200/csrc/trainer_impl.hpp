@@ -1,0 +1,238 @@
+// Internal definition of the single-GPU trainer (trainer.cu), shared with the
+// data-parallel exchange (dp.cu).
+#pragma once
+
+#include <algorithm>
+#include <vector>
+
+#include "gasb_internal.hpp"
+#include "kernels.cuh"
+
+namespace gasb {
+const Schedule& schedule_of(gasb_schedule s);
+gasb_history history_create(int32_t layers, int32_t n, int32_t dim);
+void history_destroy(gasb_history h);
+float* history_table(gasb_history h, int32_t layer);
+int64_t history_ld(gasb_history h);
+int64_t* history_stamps(gasb_history h, int32_t layer);
+int64_t* history_step_ptr(gasb_history h);
+int32_t* history_flags(gasb_history h, int32_t layer);
+
+template <class T>
+struct DevBuf {
+    T* p = nullptr;
+    int64_t n = 0;
+    void alloc(int64_t count) {
+        free();
+        n = count;
+        GASB_CUDA(cudaMalloc(&p, sizeof(T) * std::max<int64_t>(count, 1)));
+    }
+    void upload(const std::vector<T>& v) {
+        alloc(static_cast<int64_t>(v.size()));
+        if (!v.empty()) GASB_CUDA(cudaMemcpy(p, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice));
+    }
+    void zero() {
+        if (n) GASB_CUDA(cudaMemset(p, 0, sizeof(T) * n));
+    }
+    bool owned = true;  // false: a view into memory owned elsewhere (the DP exchange region)
+    void adopt(T* q, int64_t count) {
+        free();
+        p = q;
+        n = count;
+        owned = false;
+    }
+    void free() {
+        if (p && owned) cudaFree(p);
+        p = nullptr;
+        n = 0;
+        owned = true;
+    }
+    ~DevBuf() { free(); }
+};
+
+struct SegTable {
+    DevBuf<int64_t> seg_beg;
+    DevBuf<int32_t> seg_row, seg_slot, row_seg0, row_nseg;
+    DevBuf<int32_t> ranges;  // per group: nranges + 1 work-range boundaries (split_ranges)
+    int32_t nranges = 0;
+    std::vector<int64_t> group_seg0, group_nseg;  // per group (batch) range of segments
+    int64_t max_group_slots = 0, total_slots = 0;
+    SpmmSegs segs(int64_t g) const {
+        return SpmmSegs{seg_beg.p, seg_row.p, seg_slot.p, row_seg0.p, row_nseg.p, ranges.p + g * (nranges + 1),
+                        nranges};
+    }
+};
+
+}  // namespace gasb
+
+using namespace gasb;  // internal header: the trainer is written against gasb's helpers
+
+struct gasb_trainer_s {
+    gasb_model_spec spec{};
+    gasb_trainer_options opt{};
+    int32_t n = 0, F = 0, C = 0, L = 0, H = 0, hist_dim = 0, num_parts = 0;
+    int64_t ldF = 0, ldH = 0, ldC = 0;
+    const Schedule* sched = nullptr;
+    cudaStream_t stream = nullptr, side = nullptr;
+    gasb_history hist = nullptr;
+
+    // per part (host)
+    std::vector<int32_t> nb, ne, nh, ntrain;
+    std::vector<int64_t> row_off, edge_off, t_off, tr_off, ext_off;
+    int32_t nb_max = 0, ne_max = 0;
+
+    // device data
+    DevBuf<float> X;
+    DevBuf<int32_t> batch_nodes, cols_g, cols_l, t_src, train_rows, train_labels, extended, compose_idx, halo_ids;
+    DevBuf<double> coef64;
+    DevBuf<float> t_cf;
+    DevBuf<int64_t> t_rowptr;
+    SegTable seg_batch, seg_all;
+    DevBuf<int32_t> counters, row_label, xflags, ce_done;  // xflags: value flags of X (kernels.cuh)
+    DevBuf<double> partial_batch, partial_all;
+    int32_t max_chunks = 0;
+    int64_t pld = 0, pld_all = 0;
+
+    // model
+    // per parameter tensor: device offset, rows, cols, row pitch (cols rounded up to 4 floats
+    // so every weight is a TMA-describable GEMM operand; pads are 0 and stay 0 under Adam)
+    std::vector<int64_t> poff, prow, pcol, ppitch;
+    int64_t nparam_dense = 0;  // Model::params() floats (the API's flat layout)
+    std::vector<int32_t> layer_param;       // param index of W_l (GCN) per layer 1..L
+    int64_t nparam = 0;
+    std::vector<float> h_params_init;
+    DevBuf<float> params, grads, adam_m, adam_v;
+    DevBuf<int64_t> t_counter;
+    DevBuf<double> bc, norm_scratch;
+    int64_t bc_cap = 0, t_host = 0;
+
+    // activations
+    std::vector<int32_t> dims;    // d[0..L]
+    DevBuf<float> agg_all;        // hoisted layer-1 aggregation, n x ldF
+    std::vector<DevBuf<float>> agg, act;
+    DevBuf<float> logits, glogits, g_agg, g_out, x_ext, h_ext, halo_buf;
+    // TMA tensor maps of the SpMM source tables (tile::gather4 staging, spmm.cu)
+    CUtensorMap tm_x{}, tm_xext{}, tm_hext{};
+    std::vector<CUtensorMap> tm_hist;
+    bool tm_ok[4] = {false, false, false, false};  // x, hist, x_ext, h_ext
+    const CUtensorMap* source_tmap(int32_t l) const {
+        if (l == 1) return tm_ok[0] ? &tm_x : nullptr;
+        return tm_ok[1] ? &tm_hist[l - 2] : nullptr;
+    }
+    void build_tmaps() {
+        const int32_t bc = spmm_box_cols();
+        tm_ok[0] = make_row_tmap(X.p, n, F, ldF, bc, &tm_x);
+        tm_hist.resize(static_cast<size_t>(std::max(0, L - 1)));
+        tm_ok[1] = L >= 2;
+        for (int32_t l = 1; l < L; ++l)
+            tm_ok[1] = tm_ok[1] && make_row_tmap(history_table(hist, l), n, hist_dim, history_ld(hist), bc,
+                                                 &tm_hist[l - 1]);
+        if (x_ext.p) tm_ok[2] = make_row_tmap(x_ext.p, ne_max, F, ldF, bc, &tm_xext);
+        const int32_t hdim = residual ? D : H;
+        if (h_ext.p) tm_ok[3] = make_row_tmap(h_ext.p, ne_max, hdim, ld_of(hdim), bc, &tm_hext);
+        if (residual && h0.p) tm_h0_ok = make_row_tmap(h0.p, ne_max, D, ldD, bc, &tm_h0);
+    }
+    DevBuf<double> loss, row_scratch;
+
+    DevBuf<float> gemm_ws;  // split-K scratch of the tensor-core GEMM (gemm_tc.cu)
+    struct WsGuard {        // scopes the thread's GEMM workspace to one enqueue
+        explicit WsGuard(DevBuf<float>& w) { set_gemm_workspace(w.p, kGemmWsFloats); }
+        ~WsGuard() { set_gemm_workspace(nullptr, 0); }
+    };
+
+    // ---- residual models: APPNP (kind 2) / GCNII (kind 3) ----
+    bool residual = false;
+    int32_t D = 0;      // width of every propagation layer and of the histories (GCNII: H, APPNP: C)
+    int64_t ldD = 0, ldA = 0;  // ldA: row pitch of act[l] (GCN: ldH)
+    int32_t p_hw1 = -1, p_hb1 = -1, p_hw2 = -1, p_hb2 = -1, p_ow = -1, p_ob = -1;  // param indices
+    DevBuf<int32_t> brow;                  // batch_local_rows per part, at row_off
+    DevBuf<int64_t> a_rowptr;              // CSC over ALL edges of a batch (targets = V_b local rows)
+    DevBuf<int32_t> a_src;                 //   entries: batch row r, ascending r per target
+    DevBuf<float> a_cf;
+    std::vector<int64_t> a_off;            // per part: offset of its ne+1 row pointers
+    DevBuf<float> h0, z, h0g, zg, wt, prop, gmix, dprop, gout;
+    std::vector<DevBuf<float>> mixed;      // GCNII: mixed_l (needed for dW~_l)
+    CUtensorMap tm_h0{};
+    bool tm_h0_ok = false;
+    float* P(int32_t i) { return params.p + poff[i]; }
+    float* G(int32_t i) { return grads.p + poff[i]; }
+    int32_t add_param(int64_t r, int64_t c) {
+        poff.push_back(nparam);
+        prow.push_back(r);
+        pcol.push_back(c);
+        ppitch.push_back(round_up(c, 4));
+        nparam += r * ppitch.back();
+        nparam_dense += r * c;
+        return static_cast<int32_t>(poff.size()) - 1;
+    }
+    int64_t pp(int32_t i) const { return ppitch[i]; }
+    // dense (Model::params() order) <-> padded device layout
+    void params_to_dense(const float* dev, float* host) const {
+        int64_t o = 0;
+        for (size_t i = 0; i < poff.size(); ++i) {
+            GASB_CUDA(cudaMemcpy2D(host + o, sizeof(float) * pcol[i], dev + poff[i], sizeof(float) * ppitch[i],
+                                   sizeof(float) * pcol[i], prow[i], cudaMemcpyDeviceToHost));
+            o += prow[i] * pcol[i];
+        }
+    }
+    void params_from_dense(const float* host, float* dev) const {
+        int64_t o = 0;
+        for (size_t i = 0; i < poff.size(); ++i) {
+            GASB_CUDA(cudaMemcpy2D(dev + poff[i], sizeof(float) * ppitch[i], host + o, sizeof(float) * pcol[i],
+                                   sizeof(float) * pcol[i], prow[i], cudaMemcpyHostToDevice));
+            o += prow[i] * pcol[i];
+        }
+    }
+    void build_residual(const std::vector<int64_t>& h_arp, const std::vector<int32_t>& h_asrc,
+                        const std::vector<float>& h_acf, const std::vector<int32_t>& h_brow);
+    void enqueue_batch_res(int32_t p, bool train, bool push, bool fused, bool dp = false);
+
+    // graphs
+    std::vector<cudaGraphExec_t> graphs;
+    std::vector<int64_t> graph_launches;
+    int64_t epoch_launches = 0;
+    std::vector<int32_t> last_order;
+    std::vector<uint8_t> last_stepped;
+
+    ~gasb_trainer_s() {
+        if (stream) cudaStreamSynchronize(stream);
+        for (auto g : graphs)
+            if (g) cudaGraphExecDestroy(g);
+        for (auto g : graphs_dp)
+            if (g) cudaGraphExecDestroy(g);
+        if (hist) history_destroy(hist);
+        if (side) cudaStreamDestroy(side);
+        if (stream) cudaStreamDestroy(stream);
+    }
+
+    int64_t ld_of(int32_t d) const { return round_up(std::max(d, 1), 8); }
+    // value flags of the table layer l's aggregation reads: X for l = 1, H_{l-1} otherwise
+    const int32_t* source_flags(int32_t l) const { return l == 1 ? xflags.p : history_flags(hist, l - 1); }
+    float* W(int32_t l) { return params.p + poff[layer_param[l]]; }
+    float* gW(int32_t l) { return grads.p + poff[layer_param[l]]; }
+
+    void ensure_bc(int64_t t_max) {
+        if (t_max < bc_cap) return;
+        int64_t cap = std::max<int64_t>(1024, bc_cap);
+        while (cap <= t_max) cap *= 2;
+        std::vector<double> h(static_cast<size_t>(2 * cap));
+        for (int64_t t = 1; t < cap; ++t) {  // nn.cpp:23-24, host pow (as the reference)
+            h[2 * t] = 1.0 - std::pow(static_cast<double>(spec.beta1), static_cast<double>(t));
+            h[2 * t + 1] = 1.0 - std::pow(static_cast<double>(spec.beta2), static_cast<double>(t));
+        }
+        GASB_CUDA(cudaStreamSynchronize(stream));
+        bc.upload(h);
+        bc_cap = cap;
+    }
+
+    void build(const float* h_features, const int32_t* h_labels, const uint8_t* h_train);
+    void enqueue_batch(int32_t p, bool train, bool push, bool use_hoisted, bool fused, bool dp = false);
+    void enqueue_hoisted();
+    void run_epoch(int64_t epoch, bool shuffle);
+    // data-parallel mode (dp.cu): batches skip Adam and the step counters (applied after
+    // the cross-rank exchange) and have their own per-part graphs
+    std::vector<cudaGraphExec_t> graphs_dp;
+    DevBuf<char> dp_region;  // the DP exchange region (grads and act_l are views into it)
+    std::vector<int64_t> graph_launches_dp;
+    int64_t launch_batch_graph(int32_t p, bool dp);
+};

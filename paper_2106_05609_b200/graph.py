@@ -136,6 +136,14 @@ class BatchSchedule:
         check(lib.gasb_plan_sizes(self._h, int(part), ptr(z)))
         return z
 
+    def batch_nodes(self, part: int) -> np.ndarray:
+        """The part's batch node ids (sorted global ids), without copying its stencils."""
+        nb, ne = (int(x) for x in self.sizes(part)[:2])
+        ext, blr = np.empty(ne, np.int32), np.empty(nb, np.int32)
+        check(lib.gasb_plan_copy(self._h, int(part), ptr(ext) if ne else None, None, None, ptr(blr) if nb else None,
+                                 *([None] * 9)))
+        return ext[blr] if nb else np.empty(0, np.int32)
+
     def plan(self, part: int) -> BatchPlan:
         nb, ne, nh, lnnz, gnnz, snnz = (int(x) for x in self.sizes(part))
         full = lnnz >= 0

@@ -78,6 +78,15 @@ class GasTrainer:
         check(lib.gasb_trainer_history(self._h, C.byref(hh)))
         self.history = HistoryStore(0, 0, 0, _handle=hh.value, _owned=False) if spec.num_layers >= 1 else None
         self.num_classes = num_classes
+        self.train_mask = tm.astype(bool)
+        self._part_train = None
+
+    def part_train_rows(self) -> np.ndarray:
+        """Training rows per part (parts without any take no optimizer step, trainer.cpp:313-317)."""
+        if self._part_train is None:
+            self._part_train = np.array([int(self.train_mask[self.schedule.batch_nodes(p)].sum())
+                                         for p in range(self.schedule.num_parts)], np.int64)
+        return self._part_train
 
     def __del__(self):
         if getattr(self, "_h", None):
