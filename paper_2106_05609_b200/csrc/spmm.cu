@@ -41,9 +41,22 @@ constexpr int kUnroll = 8;  // edges in flight per lane
 // so fma(c * 2^896, D, acc) == acc + c*x rounded once — the reference's `acc += c * src`.
 // A per-table flag word (kTableNeg / kTableNonFinite) selects the path; tables holding
 // inf/nan take F2F (D = double(x) * 2^-896, also exact).
-constexpr int kStages = 3;
-constexpr int kPipeWarps = 4;
-constexpr int kStageDataBytes = 8192;
+#ifndef GASB_SPMM_STAGES
+#define GASB_SPMM_STAGES 2
+#endif
+#ifndef GASB_SPMM_STAGE_BYTES
+#define GASB_SPMM_STAGE_BYTES 8192
+#endif
+#ifndef GASB_SPMM_CTAS
+#define GASB_SPMM_CTAS 3
+#endif
+constexpr int kStages = GASB_SPMM_STAGES;      // stages in flight per warp
+constexpr int kPipeCtas = GASB_SPMM_CTAS;      // resident CTAs per SM (persistent grid)
+#ifndef GASB_SPMM_WARPS
+#define GASB_SPMM_WARPS 4
+#endif
+constexpr int kPipeWarps = GASB_SPMM_WARPS;    // warps per CTA
+constexpr int kStageDataBytes = GASB_SPMM_STAGE_BYTES;
 
 enum WidenMode { kWidenF2F = 0, kWidenSigned = 1, kWidenNonNeg = 2 };
 
@@ -177,7 +190,7 @@ __device__ __forceinline__ void tma_gather4(void* dst, const CUtensorMap* tm, in
 }
 
 template <int CPL, bool TMA>
-__global__ void __launch_bounds__(kPipeWarps * 32, 2) spmm_fwd_pipe_kernel(
+__global__ void __launch_bounds__(kPipeWarps * 32, kPipeCtas) spmm_fwd_pipe_kernel(
     const int64_t* __restrict__ seg_beg, const int32_t* __restrict__ seg_row, const int32_t* __restrict__ seg_slot,
     const int32_t* __restrict__ row_seg0, const int32_t* __restrict__ row_nseg, const int32_t* __restrict__ range_seg,
     int32_t nranges, const int32_t* __restrict__ cols, const double* __restrict__ coeffs, const float* __restrict__ x,
@@ -622,7 +635,7 @@ static void launch_pipe(const SpmmSegs& s, const int32_t* cols, const double* co
         GASB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     }
     const int64_t items = static_cast<int64_t>(nchunks) * s.nranges;
-    const int64_t blocks = std::min<int64_t>(ceil_div(items, kPipeWarps), 2LL * sms);
+    const int64_t blocks = std::min<int64_t>(ceil_div(items, kPipeWarps), static_cast<int64_t>(kPipeCtas) * sms);
     kern<<<static_cast<unsigned>(blocks), kPipeWarps * 32, kSmem, st>>>(
         s.seg_beg, s.seg_row, s.seg_slot, s.row_seg0, s.row_nseg, s.range_seg, s.nranges, cols, coeffs, x, ldx, dim,
         nchunks, y, ldy, row_base, partial, partial_ld, counters, counters_ld, special, tm);
@@ -669,7 +682,7 @@ int32_t spmm_ranges_per_launch() {
         if (cudaGetDevice(&dev) != cudaSuccess ||
             cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0)
             sms = 148;
-        v = 2 * kPipeWarps * sms;
+        v = kPipeCtas * kPipeWarps * sms;
     }
     return v;
 }

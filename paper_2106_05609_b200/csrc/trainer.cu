@@ -372,6 +372,18 @@ void gasb_trainer_s::build(const float* h_features, const int32_t* h_labels, con
     loss.zero();
     gemm_ws.alloc(kGemmWsFloats + kGemmTileCounters);  // split-K slices + tile counters
     gemm_ws.zero();
+    if (!residual) {
+        gemm_ws2.alloc(kGemmWsFloats + kGemmTileCounters);
+        gemm_ws2.zero();
+        g_out2.alloc(static_cast<int64_t>(nb_max) * ldH);
+        ev_fork.assign(static_cast<size_t>(L) + 1, nullptr);
+        ev_wdone.assign(static_cast<size_t>(L) + 1, nullptr);
+        for (int32_t l = 0; l <= L; ++l) {
+            GASB_CUDA(cudaEventCreateWithFlags(&ev_fork[l], cudaEventDisableTiming));
+            GASB_CUDA(cudaEventCreateWithFlags(&ev_wdone[l], cudaEventDisableTiming));
+        }
+        GASB_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
+    }
     row_scratch.alloc(nb_max);
     graphs.assign(num_parts, nullptr);
     graph_launches.assign(num_parts, 0);
@@ -607,20 +619,32 @@ void gasb_trainer_s::enqueue_batch(int32_t p, bool train, bool push, bool use_ho
     if (stepped) {
         float* g = glogits.p;
         int64_t ldg = ldC;
+        float* gbuf[2] = {g_out.p, g_out2.p};
         for (int32_t l = L; l >= 1; --l) {
             const int32_t din = dims[l - 1], dout = dims[l];
             const int64_t lda = ld_of(din);
             const float* a = (l == 1 && use_hoisted) ? agg_all.p + r0 * ldF : agg[l].p;
-            // matmul backward (tensor.cpp:169-204): dW = agg^T g ; dagg = g W^T
-            launch_gemm(2, din, dout, m, a, lda, g, ldg, gW(l), pp(layer_param[l]), 0.f, false, nullptr, stream);
+            // matmul backward (tensor.cpp:169-204): dW = agg^T g on the side stream (fork
+            // after g is complete) ; dagg = g W^T on the main stream
+            GASB_CUDA(cudaEventRecord(ev_fork[l], stream));
+            GASB_CUDA(cudaStreamWaitEvent(side, ev_fork[l], 0));
+            set_gemm_workspace(gemm_ws2.p, kGemmWsFloats);
+            launch_gemm(2, din, dout, m, a, lda, g, ldg, gW(l), pp(layer_param[l]), 0.f, false, nullptr, side);
+            set_gemm_workspace(gemm_ws.p, kGemmWsFloats);
+            GASB_CUDA(cudaEventRecord(ev_wdone[l], side));
             if (l == 1) break;  // x_ext carries no gradient
             launch_gemm(1, m, din, dout, g, ldg, W(l), pp(layer_param[l]), g_agg.p, ldH, 0.f, false, nullptr, stream);
             // aggregate backward over intra-batch edges + compose bwd + relu bwd (mask = act)
-            launch_spmm_bwd(t_rowptr.p + r0 + p, m, t_src.p, t_cf.p, g_agg.p, ldH, din, act[l - 1].p, ldH, g_out.p,
-                            ldH, stream, m);
-            g = g_out.p;
+            // into the buffer the wgrad of layer l + 1 read: wait for it
+            float* go = gbuf[l & 1];
+            if (l + 1 <= L - 1) GASB_CUDA(cudaStreamWaitEvent(stream, ev_wdone[l + 1], 0));
+            launch_spmm_bwd(t_rowptr.p + r0 + p, m, t_src.p, t_cf.p, g_agg.p, ldH, din, act[l - 1].p, ldH, go, ldH,
+                            stream, m);
+            g = go;
             ldg = ldH;
         }
+        GASB_CUDA(cudaEventRecord(ev_join, side));  // every weight gradient is complete
+        GASB_CUDA(cudaStreamWaitEvent(stream, ev_join, 0));
         if (!dp)  // data-parallel: Adam runs on the cross-rank gradient sum (dp.cu)
             launch_adam(params.p, adam_m.p, adam_v.p, grads.p, nparam, t_counter.p, bc.p, spec.lr, spec.beta1,
                         spec.beta2, spec.eps, spec.clip_max_norm, norm_scratch.p, stream);

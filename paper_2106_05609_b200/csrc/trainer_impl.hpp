@@ -135,6 +135,12 @@ struct gasb_trainer_s {
     DevBuf<double> loss, row_scratch;
 
     DevBuf<float> gemm_ws;  // split-K scratch of the tensor-core GEMM (gemm_tc.cu)
+    // GCN backward: the weight-gradient GEMMs run on `side` (own split-K scratch), overlapped
+    // with the dgrad -> SpMM-backward chain; g_out is double-buffered so a wgrad still
+    // reading layer l's gradient never races the SpMM backward of layer l - 1
+    DevBuf<float> gemm_ws2, g_out2;
+    std::vector<cudaEvent_t> ev_fork, ev_wdone;
+    cudaEvent_t ev_join = nullptr;
     struct WsGuard {        // scopes the thread's GEMM workspace to one enqueue
         explicit WsGuard(DevBuf<float>& w) { set_gemm_workspace(w.p, kGemmWsFloats); }
         ~WsGuard() { set_gemm_workspace(nullptr, 0); }
@@ -201,6 +207,9 @@ struct gasb_trainer_s {
         for (auto g : graphs_dp)
             if (g) cudaGraphExecDestroy(g);
         if (hist) history_destroy(hist);
+        for (auto e : ev_fork) cudaEventDestroy(e);
+        for (auto e : ev_wdone) cudaEventDestroy(e);
+        if (ev_join) cudaEventDestroy(ev_join);
         if (side) cudaStreamDestroy(side);
         if (stream) cudaStreamDestroy(stream);
     }

@@ -1,0 +1,2 @@
+python paper_2106_05609_b200/build.py >/dev/null 2>&1
+for e in tma direct cp; do GASB_SPMM_ENGINE=$e timeout 300 python tools/engine_probe.py 2>&1 | tail -1; done
