@@ -141,6 +141,19 @@ gasb_status gasb_history_fill_layer(gasb_history h, int32_t layer, const float* 
 gasb_status gasb_history_read_layer(gasb_history h, int32_t layer, float* h_values);
 gasb_status gasb_history_read_stamps(gasb_history h, int32_t layer, int64_t* h_stamps);
 gasb_status gasb_history_reset(gasb_history h); /* reset() (history.cpp:114-118) */
+/* measure_staleness (history.hpp:51, history.cpp:77-112): per layer l (index l-1), against
+ * the device reference matrix d_reference[l-1] (num_nodes x dim, pitch ld_reference[l-1]):
+ * eps = per-row L2 distance (max, mean), age = steps since the row's last push (never
+ * pushed: step + 1; max, mean). Row norms on the GPU, ordered sums on the host: bit-exact
+ * with the reference. Synchronous. */
+gasb_status gasb_history_staleness(gasb_history h, const float* const* d_reference, const int64_t* ld_reference,
+                                   double* h_eps_max, double* h_eps_mean, int64_t* h_age_max, double* h_age_mean);
+/* save_checkpoint / load_checkpoint (history.hpp:55-56, history.cpp:130-178): the
+ * reference's GASH file format (magic, u32 layers/nodes/dim, dense fp32 tables), so a
+ * checkpoint written by either side loads in the other. load creates a new store with
+ * every stamp 0 and step 0, as the reference. */
+gasb_status gasb_history_save(gasb_history h, const char* path);
+gasb_status gasb_history_load(const char* path, gasb_history* out);
 
 /* Prefetcher / PrefetchHandle (history.hpp:73-111, history.cpp:184-252) as stream work:
  * begin() snapshots all L-1 layers' halo rows on the prefetcher's side stream after an

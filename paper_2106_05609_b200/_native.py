@@ -93,6 +93,9 @@ _SIGS = {
     "gasb_history_read_layer": (i32, [vp, i32, vp]),
     "gasb_history_read_stamps": (i32, [vp, i32, vp]),
     "gasb_history_reset": (i32, [vp]),
+    "gasb_history_staleness": (i32, [vp, vp, vp, vp, vp, vp, vp]),
+    "gasb_history_save": (i32, [vp, C.c_char_p]),
+    "gasb_history_load": (i32, [C.c_char_p, P(vp)]),
     "gasb_prefetcher_create": (i32, [vp, P(vp)]),
     "gasb_prefetcher_destroy": (i32, [vp]),
     "gasb_prefetch_begin": (i32, [vp, vp, i64, vp, P(u64)]),

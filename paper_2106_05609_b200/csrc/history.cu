@@ -6,6 +6,8 @@
 // row starts 16 B aligned and moves as float4), one contiguous allocation; int64 stamps
 // L-1 x num_nodes (-1 = never pushed); int64 step counter in device memory so that pushes
 // captured into CUDA graphs stamp the live step.
+#include <cstdio>
+#include <algorithm>
 #include <cstring>
 #include <vector>
 
@@ -88,6 +90,29 @@ __global__ void fill_stamps_kernel(int64_t* stamps, int64_t n, const int64_t* st
     for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x)
         stamps[i] = s;
+}
+
+// measure_staleness (history.cpp:77-112), per row: norm[v] = sqrt(sum_j (double(a_j) -
+// double(b_j))^2) in column order without contraction (the reference's loop, bit for bit),
+// age[v] = stamp < 0 ? step + 1 : step - stamp. One thread per row: the row sum is
+// sequential by definition; the cross-row sums are done on the host in row order.
+__global__ void __launch_bounds__(256) staleness_rows_kernel(const float* __restrict__ a, int64_t lda,
+                                                             const float* __restrict__ b, int64_t ldb, int32_t n,
+                                                             int32_t dim, const int64_t* __restrict__ stamps,
+                                                             const int64_t* __restrict__ step,
+                                                             double* __restrict__ norm, int64_t* __restrict__ age) {
+    const int64_t v = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (v >= n) return;
+    const float* ra = a + v * lda;
+    const float* rb = b + v * ldb;
+    double acc = 0.0;
+    for (int32_t j = 0; j < dim; ++j) {
+        const double d = __dsub_rn(static_cast<double>(ra[j]), static_cast<double>(rb[j]));
+        acc = __dadd_rn(acc, __dmul_rn(d, d));
+    }
+    norm[v] = __dsqrt_rn(acc);
+    const int64_t st = stamps[v], s = *step;
+    age[v] = st < 0 ? s + 1 : s - st;
 }
 
 static int g_num_sms = 0;
@@ -463,6 +488,125 @@ gasb_status gasb_prefetch_wait(gasb_prefetcher p, uint64_t generation, int32_t l
         GASB_CUDA(cudaStreamWaitEvent(as_stream(compute), p->ready[layer - 1], 0));
         if (rows) *rows = p->bufs[layer - 1];
         if (ld) *ld = p->h->ld;
+    });
+}
+
+/* measure_staleness (history.cpp:77-112). */
+gasb_status gasb_history_staleness(gasb_history h, const float* const* d_reference, const int64_t* ld_reference,
+                                   double* h_eps_max, double* h_eps_mean, int64_t* h_age_max, double* h_age_mean) {
+    return guard([&] {
+        require(h && d_reference && ld_reference, "measure_staleness: null argument");
+        require(h_eps_max && h_eps_mean && h_age_max && h_age_mean, "measure_staleness: null argument");
+        const int64_t n = h->n;
+        double* d_norm = nullptr;
+        int64_t* d_age = nullptr;
+        GASB_CUDA(cudaMalloc(&d_norm, sizeof(double) * std::max<int64_t>(n, 1)));
+        GASB_CUDA(cudaMalloc(&d_age, sizeof(int64_t) * std::max<int64_t>(n, 1)));
+        std::vector<double> norm(static_cast<size_t>(n));
+        std::vector<int64_t> age(static_cast<size_t>(n));
+        try {
+            for (int32_t l = 1; l <= h->layers; ++l) {
+                require(d_reference[l - 1] != nullptr, "measure_staleness: need one reference matrix per layer");
+                require(ld_reference[l - 1] >= h->dim, "measure_staleness: reference shape mismatch");
+                if (n > 0) {
+                    staleness_rows_kernel<<<static_cast<unsigned>(ceil_div(n, 256)), 256>>>(
+                        h->table(l), h->ld, d_reference[l - 1], ld_reference[l - 1], h->n, h->dim, h->stamp(l),
+                        h->step, d_norm, d_age);
+                    ++t_launches;
+                    GASB_CUDA(cudaGetLastError());
+                    GASB_CUDA(cudaMemcpy(norm.data(), d_norm, sizeof(double) * n, cudaMemcpyDeviceToHost));
+                    GASB_CUDA(cudaMemcpy(age.data(), d_age, sizeof(int64_t) * n, cudaMemcpyDeviceToHost));
+                }
+                double sum = 0.0, mx = 0.0, age_sum = 0.0;  // row order, as the reference
+                int64_t age_max = 0;
+                for (int64_t v = 0; v < n; ++v) {
+                    sum += norm[v];
+                    mx = std::max(mx, norm[v]);
+                    age_sum += static_cast<double>(age[v]);
+                    age_max = std::max(age_max, age[v]);
+                }
+                h_eps_max[l - 1] = mx;
+                h_eps_mean[l - 1] = n > 0 ? sum / static_cast<double>(n) : 0.0;
+                h_age_max[l - 1] = age_max;
+                h_age_mean[l - 1] = n > 0 ? age_sum / static_cast<double>(n) : 0.0;
+            }
+        } catch (...) {
+            cudaFree(d_norm);
+            cudaFree(d_age);
+            throw;
+        }
+        cudaFree(d_norm);
+        cudaFree(d_age);
+    });
+}
+
+/* save_checkpoint (history.cpp:130-148): "GASH", u32 layers, u32 nodes, u32 dim, then each
+ * layer's rows x dim fp32 values, row-major, dense (the reference's byte format). */
+gasb_status gasb_history_save(gasb_history h, const char* path) {
+    return guard([&] {
+        require(h && path, "checkpoint: null argument");
+        GASB_CUDA(cudaDeviceSynchronize());
+        std::FILE* f = std::fopen(path, "wb");
+        if (!f) throw std::runtime_error(std::string("checkpoint: cannot open ") + path);
+        std::vector<float> buf(static_cast<size_t>(h->n) * h->dim);
+        try {
+            const uint32_t hdr[3] = {static_cast<uint32_t>(h->layers), static_cast<uint32_t>(h->n),
+                                     static_cast<uint32_t>(h->dim)};
+            if (std::fwrite("GASH", 1, 4, f) != 4 || std::fwrite(hdr, sizeof(uint32_t), 3, f) != 3)
+                throw std::runtime_error("checkpoint: write failed");
+            for (int32_t l = 1; l <= h->layers; ++l) {
+                if (buf.empty()) continue;
+                GASB_CUDA(cudaMemcpy2D(buf.data(), sizeof(float) * h->dim, h->table(l), sizeof(float) * h->ld,
+                                       sizeof(float) * h->dim, h->n, cudaMemcpyDeviceToHost));
+                if (std::fwrite(buf.data(), sizeof(float), buf.size(), f) != buf.size())
+                    throw std::runtime_error("checkpoint: write failed");
+            }
+        } catch (...) {
+            std::fclose(f);
+            throw;
+        }
+        std::fclose(f);
+    });
+}
+
+/* load_checkpoint (history.cpp:150-178): a new store with the file's tables, every stamp 0
+ * and step 0; runtime_error for an unopenable file, bad magic or truncation. */
+gasb_status gasb_history_load(const char* path, gasb_history* out) {
+    return guard([&] {
+        require(path && out, "checkpoint: null argument");
+        std::FILE* f = std::fopen(path, "rb");
+        if (!f) throw std::runtime_error(std::string("checkpoint: cannot open ") + path);
+        gasb_history h = nullptr;
+        try {
+            char magic[4];
+            if (std::fread(magic, 1, 4, f) != 4 || std::memcmp(magic, "GASH", 4) != 0)
+                throw std::runtime_error(std::string("checkpoint: bad magic in ") + path);
+            uint32_t hdr[3];
+            for (int i = 0; i < 3; ++i)
+                if (std::fread(hdr + i, sizeof(uint32_t), 1, f) != 1)
+                    throw std::runtime_error("checkpoint: truncated header");
+            h = history_create(static_cast<int32_t>(hdr[0]), static_cast<int32_t>(hdr[1]),
+                               static_cast<int32_t>(hdr[2]));
+            std::vector<float> buf(static_cast<size_t>(h->n) * h->dim);
+            for (int32_t l = 1; l <= h->layers; ++l) {
+                if (!buf.empty()) {
+                    if (std::fread(buf.data(), sizeof(float), buf.size(), f) != buf.size())
+                        throw std::runtime_error(std::string("checkpoint: truncated matrix in ") + path);
+                    GASB_CUDA(cudaMemcpy2D(h->table(l), sizeof(float) * h->ld, buf.data(), sizeof(float) * h->dim,
+                                           sizeof(float) * h->dim, h->n, cudaMemcpyHostToDevice));
+                    int32_t fl = 0;
+                    for (float v : buf) fl |= table_flag_of(v);
+                    GASB_CUDA(cudaMemcpy(h->flag(l), &fl, sizeof(fl), cudaMemcpyHostToDevice));
+                }
+                if (h->n > 0) GASB_CUDA(cudaMemset(h->stamp(l), 0, sizeof(int64_t) * h->n));
+            }
+        } catch (...) {
+            std::fclose(f);
+            if (h) history_destroy(h);
+            throw;
+        }
+        std::fclose(f);
+        *out = h;
     });
 }
 

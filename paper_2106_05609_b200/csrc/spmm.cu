@@ -102,7 +102,8 @@ struct PipeCfg {
     static constexpr int kRowsPerIssue = 32 / kPieces;            // rows per LDGSTS instruction
     static constexpr int kHdrBytes = 16;                          // stage descriptor
     // 128 B aligned: TMA destinations must be 128 B aligned
-    static constexpr int kStageBytes = (kStageDataBytes + kEdges * 8 + kHdrBytes + 127) / 128 * 128;
+    // data | fp64 coeffs | header | int32 source rows (TMA gather coordinates)
+    static constexpr int kStageBytes = (kStageDataBytes + kEdges * 8 + kHdrBytes + kEdges * 4 + 127) / 128 * 128;
     static constexpr int kSmem = kPipeWarps * kStages * kStageBytes;
 };
 // TMA mode: per-warp ring of kMetaWin windows of 32 edges (int32 col + fp64 coeff each),
@@ -306,22 +307,20 @@ __global__ void __launch_bounds__(kPipeWarps * 32, kPipeCtas) spmm_fwd_pipe_kern
             if (lane < KE) reinterpret_cast<double*>(st + kStageDataBytes)[lane] = mf;
             if (lane == 0) *reinterpret_cast<StageHdr*>(st + kStageDataBytes + KE * 8) = h;
             if constexpr (TMA) {
-                // rows of stage i go to rows + i*kCols; unused slots (mc = -1) are zero-filled
-                const int ng = (h.cnt + 3) >> 2;
+                // rows of stage i go to rows + i*kCols; unused slots (mc = -1) are zero-filled.
+                // The warp parks the stage's source rows in shared memory; lane 0 reads them
+                // back four at a time (one LDS.128 per gather4, no shuffles).
+                int32_t* srow = reinterpret_cast<int32_t*>(st + kStageDataBytes + KE * 8 + Cfg::kHdrBytes);
+                if (lane < KE) srow[lane] = mc;
+                __syncwarp();
                 if (lane == 0) {
+                    const int ng = (h.cnt + 3) >> 2;
                     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // after the warp's reads
                     mbar_expect_tx(bars + slot_idx, static_cast<uint32_t>(ng) * 4u * Cfg::kCols * 4u);
-                }
-#pragma unroll
-                for (int i = 0; i < KE / 4; ++i) {
-                    if (i < ng) {  // warp-uniform
-                        const int32_t r0 = __shfl_sync(0xffffffffu, mc, 4 * i + 0);
-                        const int32_t r1 = __shfl_sync(0xffffffffu, mc, 4 * i + 1);
-                        const int32_t r2 = __shfl_sync(0xffffffffu, mc, 4 * i + 2);
-                        const int32_t r3 = __shfl_sync(0xffffffffu, mc, 4 * i + 3);
-                        if (lane == 0)
-                            tma_gather4(rows + 4 * i * Cfg::kCols, &tmap, chunk * Cfg::kCols, r0, r1, r2, r3,
-                                        bars + slot_idx);
+                    const int32_t c0 = chunk * Cfg::kCols;
+                    for (int i = 0; i < ng; ++i) {
+                        const int4 r = reinterpret_cast<const int4*>(srow)[i];
+                        tma_gather4(rows + 4 * i * Cfg::kCols, &tmap, c0, r.x, r.y, r.z, r.w, bars + slot_idx);
                     }
                 }
             } else {

@@ -112,6 +112,38 @@ class HistoryStore:
     def reset(self) -> None:
         check(lib.gasb_history_reset(self._h))
 
+    def measure_staleness(self, reference) -> list[dict]:
+        """measure_staleness (history.cpp:77-112): one reference matrix per layer (host arrays
+        n x dim, or CUDA tensors); per layer eps_max / eps_mean / age_max / age_mean."""
+        if len(reference) != self._layers:
+            raise ValueError("measure_staleness: need one reference matrix per layer")
+        import torch  # device staging of host references (plumbing)
+        dev = []
+        for r in reference:
+            t = r if hasattr(r, "data_ptr") else torch.from_numpy(np.ascontiguousarray(r, np.float32))
+            if tuple(t.shape) != (self._n, self._dim):
+                raise ValueError("measure_staleness: reference shape mismatch")
+            dev.append(t.cuda().contiguous())
+        L = self._layers
+        ptrs = (C.c_void_p * max(L, 1))(*[t.data_ptr() for t in dev])
+        lds = np.array([self._dim] * max(L, 1), np.int64)
+        emax, emean, amean = (np.zeros(max(L, 1)) for _ in range(3))
+        amax = np.zeros(max(L, 1), np.int64)
+        check(lib.gasb_history_staleness(self._h, ptrs, ptr(lds), ptr(emax), ptr(emean), ptr(amax), ptr(amean)))
+        return [dict(eps_max=float(emax[l]), eps_mean=float(emean[l]), age_max=int(amax[l]),
+                     age_mean=float(amean[l])) for l in range(L)]
+
+    def save_checkpoint(self, path: str) -> None:
+        """save_checkpoint (history.cpp:130-148): the reference's GASH format."""
+        check(lib.gasb_history_save(self._h, str(path).encode()))
+
+    @staticmethod
+    def load_checkpoint(path: str) -> "HistoryStore":
+        """load_checkpoint (history.cpp:150-178): new store, stamps 0, step 0."""
+        h = vp()
+        check(lib.gasb_history_load(str(path).encode(), C.byref(h)))
+        return HistoryStore(0, 0, 0, _handle=h.value)
+
 
 class PrefetchHandle:
     def __init__(self, owner: "Prefetcher", generation: int, stream):

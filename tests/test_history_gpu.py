@@ -136,3 +136,77 @@ def _device_to_numpy(torch, ptr, rows, ld):
     cudart.cudaMemcpy.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int]
     assert cudart.cudaMemcpy(out.ctypes.data, ptr, out.nbytes, 2) == 0
     return out
+
+
+def _ref_store(ref, layers, n, d):
+    import ctypes as C
+    rh = C.c_void_p()
+    ref.check(ref.lib.ref_history_create(layers, n, d, C.byref(rh)))
+    return rh
+
+
+def _drive_both(ref, h, rh, layers, n, d, seed=7):
+    """Same pushes / steps into our store and the compiled reference's."""
+    rng = np.random.default_rng(seed)
+    for step in range(6):
+        for layer in range(1, layers + 1):
+            ids = np.sort(rng.choice(n, size=n // 5, replace=False)).astype(np.int32)
+            rows = rng.standard_normal((len(ids), d)).astype(np.float32)
+            h.push(layer, ids, rows)
+            ref.check(ref.lib.ref_history_push(rh, layer, ids.ctypes.data, len(ids), rows.ctypes.data))
+        h.advance_step()
+        ref.lib.ref_history_advance(rh)
+
+
+def test_measure_staleness_bit_exact(ref):
+    """measure_staleness (history.cpp:77-112): eps (row L2 distances) and push ages."""
+    layers, n, d = 2, 777, 13
+    h = gb.HistoryStore(layers, n, d)
+    rh = _ref_store(ref, layers, n, d)
+    _drive_both(ref, h, rh, layers, n, d)
+    refm = np.random.default_rng(1).standard_normal((layers, n, d)).astype(np.float32)
+    got = h.measure_staleness([refm[l] for l in range(layers)])
+    out = np.zeros(4 * layers)
+    ref.check(ref.lib.ref_history_staleness(rh, refm.ctypes.data, out.ctypes.data))
+    for l in range(layers):
+        exp = out[4 * l:4 * l + 4]
+        g = got[l]
+        assert (g["eps_max"], g["eps_mean"], g["age_max"], g["age_mean"]) == (exp[0], exp[1], int(exp[2]), exp[3])
+    with pytest.raises(ValueError):
+        h.measure_staleness([refm[0]])
+    ref.lib.ref_history_free(rh)
+
+
+def test_gash_checkpoint_interop(ref, tmp_path):
+    """save/load_checkpoint in the reference's GASH format, both directions."""
+    import ctypes as C
+    layers, n, d = 3, 100, 6
+    h = gb.HistoryStore(layers, n, d)
+    rh = _ref_store(ref, layers, n, d)
+    _drive_both(ref, h, rh, layers, n, d, seed=3)
+    ours, theirs = tmp_path / "ours.gash", tmp_path / "theirs.gash"
+    h.save_checkpoint(ours)
+    ref.check(ref.lib.ref_history_save(rh, str(theirs).encode()))
+    assert ours.read_bytes() == theirs.read_bytes()  # byte-identical files
+    loaded = gb.HistoryStore.load_checkpoint(theirs)
+    assert (loaded.num_layers(), loaded.num_nodes(), loaded.dim()) == (layers, n, d)
+    rl = C.c_void_p()
+    ref.check(ref.lib.ref_history_load(str(ours).encode(), C.byref(rl)))
+    for l in range(1, layers + 1):
+        full = np.zeros((n, d), np.float32)
+        ref.check(ref.lib.ref_history_layer(rl, l, full.ctypes.data))
+        assert np.array_equal(loaded.layer_matrix(l), full)
+        assert np.array_equal(loaded.layer_matrix(l), h.layer_matrix(l))
+        assert (loaded.stamps(l) == 0).all()
+    assert loaded.step() == 0
+    bad = tmp_path / "bad.gash"
+    bad.write_bytes(b"GASX" + ours.read_bytes()[4:])
+    with pytest.raises(RuntimeError):
+        gb.HistoryStore.load_checkpoint(bad)
+    bad.write_bytes(ours.read_bytes()[:100])
+    with pytest.raises(RuntimeError):
+        gb.HistoryStore.load_checkpoint(bad)
+    with pytest.raises(RuntimeError):
+        gb.HistoryStore.load_checkpoint(tmp_path / "missing.gash")
+    ref.lib.ref_history_free(rh)
+    ref.lib.ref_history_free(rl)
