@@ -253,6 +253,18 @@ gasb_status gasb_trainer_profile_spmm(gasb_trainer t, int32_t part, int32_t laye
 /* Page-locks host memory for asynchronous copies (cudaHostRegister / Unregister). */
 gasb_status gasb_host_register(void* h_ptr, size_t bytes);
 gasb_status gasb_host_unregister(void* h_ptr);
+/* evaluate (trainer.hpp:131, trainer.cpp:444-464): the model's full-batch forward over
+ * every node (BatchSchedule::full_batch: no halos) with the current parameters; acc3 =
+ * fraction of each mask's nodes (train, val, test; host uint8[n], NULL = 0) whose argmax
+ * logit (first maximum, nn.cpp:117-122) equals the label. GCN; synchronous. */
+gasb_status gasb_trainer_evaluate(gasb_trainer t, const uint8_t* h_train, const uint8_t* h_val, const uint8_t* h_test,
+                                  double* acc3);
+/* Logits (n x C, global node order) of the last evaluate / infer_from_history. */
+gasb_status gasb_trainer_full_logits(gasb_trainer t, float* h_logits);
+/* infer_from_history (trainer.hpp:150, trainer.cpp:501-536): one final-layer application
+ * over the layer-(L-1) histories for every node; predictions (argmax, n) and stale = some
+ * layer-(L-1) row was never pushed. GCN; synchronous. */
+gasb_status gasb_trainer_infer_from_history(gasb_trainer t, int32_t* h_predictions, int32_t* stale);
 /* Kernel launches per epoch (counted by the host driver while enqueueing). */
 gasb_status gasb_trainer_launch_count(gasb_trainer t, int64_t* out);
 

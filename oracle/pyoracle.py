@@ -235,6 +235,8 @@ class RefLib:
         L.ref_session_epoch.argtypes = [vp, i64, C.c_int, C.c_int, P(f64), P(f64)]
         L.ref_session_batch.argtypes = [vp, i32, i64, C.c_int, C.c_int, vp, vp, P(f64), vp, P(C.c_int)]
         L.ref_session_run.argtypes = [vp, i32, i64, P(f64), P(f64)]
+        L.ref_session_evaluate.argtypes = [vp, vp, vp, vp, vp]
+        L.ref_session_infer.argtypes = [vp, vp, P(C.c_int)]
 
     def check(self, rc):
         if rc == 0:
@@ -435,6 +437,22 @@ class Session:
         elif rc:
             raise ValueError("go_session_batch failed")
         return acts, logits, loss.value, (grads if stepped.value else None), bool(stepped.value)
+
+    def evaluate(self, val_mask, test_mask):
+        """Reference only: evaluate (trainer.cpp:444-464) -> ((train, val, test), logits n x C)."""
+        vm = np.ascontiguousarray(val_mask, np.uint8)
+        tm = np.ascontiguousarray(test_mask, np.uint8)
+        acc = np.zeros(3)
+        logits = np.zeros((self.n, self.num_classes), np.float32)
+        self.owner.check(self.owner.lib.ref_session_evaluate(self.h, _p(vm), _p(tm), _p(acc), _p(logits)))
+        return tuple(float(a) for a in acc), logits
+
+    def infer(self):
+        """Reference only: infer_from_history (trainer.cpp:501-536) -> (predictions, stale)."""
+        pred = np.zeros(self.n, np.int32)
+        st = C.c_int()
+        self.owner.check(self.owner.lib.ref_session_infer(self.h, _p(pred), C.byref(st)))
+        return pred, bool(st.value)
 
     def run(self, slot, epoch=0):
         """Reference only: one gas_epoch batch without capture; returns (loss, seconds)."""

@@ -611,4 +611,36 @@ int ref_session_batch(void* sp, std::int32_t slot, std::int64_t epoch, int train
     });
 }
 
+// evaluate (trainer.cpp:444-464) with the session's params: accuracy over the given masks
+// (train mask: the session's) and the full-batch logits (n x C, global order).
+int ref_session_evaluate(void* sp, const std::uint8_t* val_mask, const std::uint8_t* test_mask, double* acc3,
+                         float* logits_out) {
+    return guard([&] {
+        Session* s = static_cast<Session*>(sp);
+        const std::size_t n = static_cast<std::size_t>(s->ds.graph.num_nodes);
+        s->ds.labels.val_mask.assign(val_mask, val_mask + n);
+        s->ds.labels.test_mask.assign(test_mask, test_mask + n);
+        BatchSchedule full = BatchSchedule::full_batch(s->ds.graph);
+        Accuracy a = evaluate(*s->model, s->ds, full);
+        acc3[0] = a.train;
+        acc3[1] = a.val;
+        acc3[2] = a.test;
+        if (logits_out) {
+            Model::ForwardOptions fwd;
+            Tensor lg = s->model->forward(nullptr, s->ds.features, full.plans[0], full.aggs[0], fwd);
+            std::memcpy(logits_out, lg.data(), sizeof(float) * static_cast<std::size_t>(lg.size()));
+        }
+    });
+}
+
+// infer_from_history (trainer.cpp:501-536) over the session's store.
+int ref_session_infer(void* sp, std::int32_t* predictions, int* stale) {
+    return guard([&] {
+        Session* s = static_cast<Session*>(sp);
+        InferenceResult r = infer_from_history(*s->model, s->store, s->ds);
+        std::memcpy(predictions, r.predictions.data(), sizeof(std::int32_t) * r.predictions.size());
+        *stale = r.stale ? 1 : 0;
+    });
+}
+
 }  // extern "C"

@@ -119,6 +119,9 @@ _SIGS = {
     "gasb_trainer_profile_spmm": (i32, [vp, i32, i32, i32, P(f32)]),
     "gasb_host_register": (i32, [vp, C.c_size_t]),
     "gasb_host_unregister": (i32, [vp]),
+    "gasb_trainer_evaluate": (i32, [vp, vp, vp, vp, vp]),
+    "gasb_trainer_full_logits": (i32, [vp, vp]),
+    "gasb_trainer_infer_from_history": (i32, [vp, vp, P(i32)]),
     "gasb_dp_create": (i32, [vp, i32, i32, P(vp)]),
     "gasb_dp_export": (i32, [vp, vp]),
     "gasb_dp_connect": (i32, [vp, vp]),

@@ -117,6 +117,37 @@ __global__ void compose_kernel(const int32_t* __restrict__ src_index, const floa
     for (int c = lane; c < dim; c += 32) out[w * ldo + c] = src[c];
 }
 
+// evaluate's count (trainer.cpp:449-462): row i (part order) is node v = nodes[i]; its
+// prediction is argmax_row (nn.cpp:117-122: first maximum, strict >) of logits row i.
+// counts[2k] = rows in mask k, counts[2k+1] = correct rows; preds[v] = prediction.
+__global__ void __launch_bounds__(256) argmax_count_kernel(const float* __restrict__ logits, int64_t ldl,
+                                                           int64_t rows, int32_t C, const int32_t* __restrict__ nodes,
+                                                           const int32_t* __restrict__ labels,
+                                                           const uint8_t* __restrict__ masks, int64_t n,
+                                                           unsigned long long* __restrict__ counts,
+                                                           int32_t* __restrict__ preds) {
+    __shared__ unsigned long long sc[6];
+    if (threadIdx.x < 6) sc[threadIdx.x] = 0;
+    __syncthreads();
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < rows) {
+        const float* r = logits + i * ldl;
+        int32_t best = 0;
+        for (int32_t j = 1; j < C; ++j)
+            if (r[j] > r[best]) best = j;
+        const int32_t v = nodes[i];
+        if (preds) preds[v] = best;
+        if (masks)
+            for (int k = 0; k < 3; ++k)
+                if (masks[k * n + v]) {
+                    atomicAdd(&sc[2 * k], 1ull);
+                    if (best == labels[v]) atomicAdd(&sc[2 * k + 1], 1ull);
+                }
+    }
+    __syncthreads();
+    if (threadIdx.x < 6 && sc[threadIdx.x]) atomicAdd(&counts[threadIdx.x], sc[threadIdx.x]);
+}
+
 }  // namespace
 }  // namespace gasb
 using namespace gasb;
@@ -279,6 +310,7 @@ void gasb_trainer_s::build(const float* h_features, const int32_t* h_labels, con
     train_rows.upload(h_trr);
     train_labels.upload(h_trl);
     row_label.upload(h_rlab);
+    labels_all.upload(std::vector<int32_t>(h_labels, h_labels + n));
     extended.upload(h_ext);
     compose_idx.upload(h_cidx);
     {
@@ -706,7 +738,132 @@ int64_t gasb_trainer_s::launch_batch_graph(int32_t p, bool dp) {
     return gl[p];
 }
 
+void gasb_trainer_s::ensure_eval() {
+    if (eval_agg.p) return;
+    require(!residual, "evaluate: the device path implements the full-graph forward for GCN");
+    const int64_t R = row_off[num_parts];
+    eval_agg.alloc(R * ld_of(std::max(F, H)));
+    eval_act.alloc(R * ldH);
+    for (auto& b : eval_tab) {
+        b.alloc(static_cast<int64_t>(n) * ldH);
+        b.zero();
+    }
+    eval_logits.alloc(R * ldC);
+    eval_flags.alloc(2);
+    eval_flags.zero();
+    eval_masks.alloc(3LL * n);
+    eval_counts.alloc(6);
+    eval_pld = round_up(std::max(F, H), 128);
+    eval_partial.alloc(std::max<int64_t>(seg_all.total_slots, 1) * eval_pld);
+}
+
+// Model::forward over BatchSchedule::full_batch (every node, no halos): the whole-graph
+// stencil is the concatenation of the parts' stencils (each row's coefficients depend only
+// on global degrees), so the layer-l SpMM is one launch over the whole-epoch segment table
+// gathering the previous layer's table by global id. first_layer = L: infer_from_history's
+// final layer over H_{L-1} (trainer.cpp:512-520).
+void gasb_trainer_s::enqueue_full_forward(int32_t first_layer) {
+    WsGuard ws(gemm_ws);
+    const SpmmSegs segs = seg_all.segs(0);
+    const int64_t R = row_off[num_parts];
+    GASB_CUDA(cudaMemsetAsync(eval_flags.p, 0, 2 * sizeof(int32_t), stream));
+    for (int32_t l = first_layer; l <= L; ++l) {
+        const int32_t din = dims[l - 1], dout = dims[l];
+        const int64_t lda = ld_of(din);
+        const float* src;
+        int64_t lds;
+        const int32_t* flags;
+        const CUtensorMap* tm = nullptr;
+        if (l == 1) {
+            src = X.p, lds = ldF, flags = xflags.p, tm = source_tmap(1);
+        } else if (l == first_layer) {  // pulled layer-(L-1) histories
+            src = history_table(hist, l - 1), lds = history_ld(hist), flags = source_flags(l), tm = source_tmap(l);
+        } else {
+            src = eval_tab[(l - 1) & 1].p, lds = ldH, flags = eval_flags.p + ((l - 1) & 1);
+        }
+        launch_spmm_fwd(segs, cols_g.p, coef64.p, src, lds, din, eval_agg.p, lda, 0, eval_partial.p, eval_pld,
+                        counters.p, max_chunks, stream, flags, tm);
+        if (l < L) {
+            PushEpilogue pe{eval_tab[l & 1].p, ldH, batch_nodes.p, nullptr, nullptr, eval_flags.p + (l & 1)};
+            launch_gemm(0, static_cast<int>(R), dout, din, eval_agg.p, lda, W(l), pp(layer_param[l]), eval_act.p, ldH,
+                        0.f, true, &pe, stream);
+        } else {
+            launch_gemm(0, static_cast<int>(R), dout, din, eval_agg.p, lda, W(l), pp(layer_param[l]), eval_logits.p,
+                        ldC, 0.f, false, nullptr, stream);
+        }
+    }
+}
+
 extern "C" {
+
+gasb_status gasb_trainer_evaluate(gasb_trainer t, const uint8_t* h_train, const uint8_t* h_val, const uint8_t* h_test,
+                                  double* acc3) {
+    return guard([&] {
+        require(t && acc3, "evaluate: null argument");
+        GASB_CUDA(cudaSetDevice(t->opt.device));
+        t->ensure_eval();
+        const int64_t n = t->n;
+        const uint8_t* hm[3] = {h_train, h_val, h_test};
+        for (int k = 0; k < 3; ++k) {
+            if (hm[k]) GASB_CUDA(cudaMemcpyAsync(t->eval_masks.p + k * n, hm[k], n, cudaMemcpyHostToDevice, t->stream));
+            else GASB_CUDA(cudaMemsetAsync(t->eval_masks.p + k * n, 0, n, t->stream));
+        }
+        GASB_CUDA(cudaMemsetAsync(t->eval_counts.p, 0, 6 * sizeof(int64_t), t->stream));
+        t->enqueue_full_forward(1);
+        const int64_t R = t->row_off[t->num_parts];
+        argmax_count_kernel<<<static_cast<unsigned>(ceil_div(R, 256)), 256, 0, t->stream>>>(
+            t->eval_logits.p, t->ldC, R, t->C, t->batch_nodes.p, t->labels_all.p, t->eval_masks.p, n,
+            reinterpret_cast<unsigned long long*>(t->eval_counts.p), nullptr);
+        GASB_CUDA(cudaGetLastError());
+        int64_t c[6];
+        GASB_CUDA(cudaMemcpyAsync(c, t->eval_counts.p, sizeof(c), cudaMemcpyDeviceToHost, t->stream));
+        GASB_CUDA(cudaStreamSynchronize(t->stream));
+        for (int k = 0; k < 3; ++k)
+            acc3[k] = c[2 * k] == 0 ? 0.0 : static_cast<double>(c[2 * k + 1]) / static_cast<double>(c[2 * k]);
+    });
+}
+
+gasb_status gasb_trainer_full_logits(gasb_trainer t, float* h_logits) {
+    return guard([&] {
+        require(t && h_logits, "full_logits: null argument");
+        if (!t->eval_logits.p) throw std::logic_error("full_logits: no evaluate / infer has run");
+        GASB_CUDA(cudaStreamSynchronize(t->stream));
+        const int64_t R = t->row_off[t->num_parts];
+        std::vector<float> rows(static_cast<size_t>(R) * t->C);
+        std::vector<int32_t> nodes(static_cast<size_t>(R));
+        GASB_CUDA(cudaMemcpy2D(rows.data(), sizeof(float) * t->C, t->eval_logits.p, sizeof(float) * t->ldC,
+                               sizeof(float) * t->C, R, cudaMemcpyDeviceToHost));
+        GASB_CUDA(cudaMemcpy(nodes.data(), t->batch_nodes.p, sizeof(int32_t) * R, cudaMemcpyDeviceToHost));
+        for (int64_t i = 0; i < R; ++i)
+            std::copy(rows.begin() + i * t->C, rows.begin() + (i + 1) * t->C,
+                      h_logits + static_cast<int64_t>(nodes[i]) * t->C);
+    });
+}
+
+gasb_status gasb_trainer_infer_from_history(gasb_trainer t, int32_t* h_predictions, int32_t* stale) {
+    return guard([&] {
+        require(t && h_predictions && stale, "infer_from_history: null argument");
+        GASB_CUDA(cudaSetDevice(t->opt.device));
+        t->ensure_eval();
+        const int64_t n = t->n;
+        t->enqueue_full_forward(t->L >= 2 ? t->L : 1);
+        const int64_t R = t->row_off[t->num_parts];
+        DevBuf<int32_t> preds;
+        preds.alloc(n);
+        argmax_count_kernel<<<static_cast<unsigned>(ceil_div(R, 256)), 256, 0, t->stream>>>(
+            t->eval_logits.p, t->ldC, R, t->C, t->batch_nodes.p, t->labels_all.p, nullptr, n, nullptr, preds.p);
+        GASB_CUDA(cudaGetLastError());
+        GASB_CUDA(cudaStreamSynchronize(t->stream));
+        GASB_CUDA(cudaMemcpy(h_predictions, preds.p, sizeof(int32_t) * n, cudaMemcpyDeviceToHost));
+        *stale = 0;
+        if (t->L >= 2) {  // some layer-(L-1) row never pushed (trainer.cpp:521-525)
+            std::vector<int64_t> st(static_cast<size_t>(n));
+            GASB_CUDA(cudaMemcpy(st.data(), history_stamps(t->hist, t->L - 1), sizeof(int64_t) * n,
+                                 cudaMemcpyDeviceToHost));
+            for (int64_t v = 0; v < n && !*stale; ++v) *stale = st[v] < 0;
+        }
+    });
+}
 
 gasb_status gasb_trainer_create(gasb_schedule s, const float* h_features, int32_t in_dim, const int32_t* h_labels,
                                 const uint8_t* h_train_mask, int32_t num_classes, const gasb_model_spec* spec,

@@ -241,7 +241,18 @@ struct gasb_trainer_s {
     // data-parallel mode (dp.cu): batches skip Adam and the step counters (applied after
     // the cross-rank exchange) and have their own per-part graphs
     std::vector<cudaGraphExec_t> graphs_dp;
-    DevBuf<char> dp_region;  // the DP exchange region (grads and act_l are views into it)
+    DevBuf<char> dp_region;
+    // full-graph forward (evaluate / infer_from_history, trainer.cpp:444-536): every row of
+    // every part in one launch per layer over the whole-epoch segment table; layer outputs
+    // scattered by global id into ping-pong tables the next layer gathers in place
+    DevBuf<int32_t> labels_all, eval_flags;
+    DevBuf<uint8_t> eval_masks;
+    DevBuf<int64_t> eval_counts;
+    DevBuf<float> eval_agg, eval_act, eval_tab[2], eval_logits;
+    DevBuf<double> eval_partial;
+    int64_t eval_pld = 0;
+    void ensure_eval();
+    void enqueue_full_forward(int32_t first_layer);  // the DP exchange region (grads and act_l are views into it)
     std::vector<int64_t> graph_launches_dp;
     int64_t launch_batch_graph(int32_t p, bool dp);
 };

@@ -139,6 +139,28 @@ class GasTrainer:
         check(lib.gasb_trainer_profile_spmm(self._h, int(part), int(layer), int(iters), C.byref(ms)))
         return ms.value
 
+    def evaluate(self, train_mask=None, val_mask=None, test_mask=None) -> tuple[float, float, float]:
+        """evaluate (trainer.cpp:444-464): full-batch accuracy (train, val, test); the train
+        mask defaults to the trainer's."""
+        masks = [np.ascontiguousarray(m, np.uint8) if m is not None else None
+                 for m in (self.train_mask if train_mask is None else train_mask, val_mask, test_mask)]
+        acc = np.zeros(3)
+        check(lib.gasb_trainer_evaluate(self._h, *[ptr(m) for m in masks], ptr(acc)))
+        return float(acc[0]), float(acc[1]), float(acc[2])
+
+    def full_logits(self) -> np.ndarray:
+        """Logits (n x C, global order) of the last evaluate / infer_from_history."""
+        out = np.empty((len(self.train_mask), self.num_classes), np.float32)
+        check(lib.gasb_trainer_full_logits(self._h, ptr(out)))
+        return out
+
+    def infer_from_history(self) -> tuple[np.ndarray, bool]:
+        """infer_from_history (trainer.cpp:501-536): (predictions, stale)."""
+        pred = np.empty(len(self.train_mask), np.int32)
+        st = i32()
+        check(lib.gasb_trainer_infer_from_history(self._h, ptr(pred), C.byref(st)))
+        return pred, bool(st.value)
+
     def get_params(self) -> np.ndarray:
         out = np.empty(self.num_param_floats, np.float32)
         check(lib.gasb_trainer_get_params(self._h, ptr(out)))
