@@ -182,6 +182,7 @@ class HistoryStore {
         check(gasb_history_create(num_layers, num_nodes, dim, &h));
         h_ = Handle<gasb_history, gasb_history_destroy>(h);
     }
+    explicit HistoryStore(gasb_history adopted) { h_ = Handle<gasb_history, gasb_history_destroy>(adopted); }
     std::int32_t num_layers() const { return info().l; }
     NodeId num_nodes() const { return info().n; }
     std::int32_t dim() const { return info().d; }
@@ -237,6 +238,32 @@ class HistoryStore {
         return s;
     }
     void reset() { check(gasb_history_reset(h_.get())); }
+    // measure_staleness (history.cpp:77-112) against device reference tables, one per layer
+    struct LayerStats {
+        double eps_max = 0.0, eps_mean = 0.0;
+        std::int64_t age_max = 0;
+        double age_mean = 0.0;
+    };
+    std::vector<LayerStats> measure_staleness(std::span<const float* const> d_reference,
+                                              std::span<const std::int64_t> ld_reference) const {
+        const std::int32_t L = num_layers();
+        if (static_cast<std::int32_t>(d_reference.size()) != L || ld_reference.size() != d_reference.size())
+            throw std::invalid_argument("measure_staleness: need one reference matrix per layer");
+        std::vector<double> emax(L), emean(L), amean(L);
+        std::vector<std::int64_t> amax(L);
+        check(gasb_history_staleness(h_.get(), d_reference.data(), ld_reference.data(), emax.data(), emean.data(),
+                                     amax.data(), amean.data()));
+        std::vector<LayerStats> r(static_cast<std::size_t>(L));
+        for (std::int32_t l = 0; l < L; ++l) r[l] = {emax[l], emean[l], amax[l], amean[l]};
+        return r;
+    }
+    // save_checkpoint / load_checkpoint (history.cpp:130-178), the reference's GASH format
+    void save_checkpoint(const std::string& path) const { check(gasb_history_save(h_.get(), path.c_str())); }
+    static HistoryStore load_checkpoint(const std::string& path) {
+        gasb_history h = nullptr;
+        check(gasb_history_load(path.c_str(), &h));
+        return HistoryStore(h);
+    }
     gasb_history raw() const { return h_.get(); }
 
   private:
@@ -353,6 +380,29 @@ class Trainer {
         return p;
     }
     void set_params(std::span<const float> p) { check(gasb_trainer_set_params(h_.get(), p.data())); }
+    // evaluate (trainer.cpp:444-464): full-batch accuracy over host masks (nullptr = 0)
+    struct Accuracy {
+        double train = 0.0, val = 0.0, test = 0.0;
+    };
+    Accuracy evaluate(const std::uint8_t* train_mask, const std::uint8_t* val_mask,
+                      const std::uint8_t* test_mask) {
+        double a[3] = {0.0, 0.0, 0.0};
+        check(gasb_trainer_evaluate(h_.get(), train_mask, val_mask, test_mask, a));
+        return {a[0], a[1], a[2]};
+    }
+    // infer_from_history (trainer.cpp:501-536)
+    struct InferenceResult {
+        std::vector<std::int32_t> predictions;
+        bool stale = false;
+    };
+    InferenceResult infer_from_history(NodeId num_nodes) {
+        InferenceResult r;
+        r.predictions.resize(static_cast<std::size_t>(num_nodes));
+        std::int32_t st = 0;
+        check(gasb_trainer_infer_from_history(h_.get(), r.predictions.data(), &st));
+        r.stale = st != 0;
+        return r;
+    }
     gasb_trainer raw() const { return h_.get(); }
 
   private:

@@ -593,17 +593,219 @@ static void launch_direct(const SpmmSegs& s, const int32_t* cols, const double* 
         nchunks, y, ldy, row_base, partial, partial_ld, counters, counters_ld, special);
 }
 
-// SpMM gather engine (GASB_SPMM_ENGINE = tma | cp | direct): TMA tile::gather4 staging,
-// cp.async staging, or direct register loads.
+// SpMM gather engine (GASB_SPMM_ENGINE = flat | tma | cp | direct; default flat): the
+// flat-stream TMA kernel, the segment-staged TMA / cp.async pipeline, or direct register
+// loads. All produce identical values (same segments and accumulation order).
 static int spmm_engine() {
     static int v = [] {
         const char* e = getenv("GASB_SPMM_ENGINE");
-        if (!e) return 0;
+        if (!e) return 3;
         if (!strcmp(e, "direct")) return 2;
         if (!strcmp(e, "cp")) return 1;
+        if (!strcmp(e, "flat")) return 3;
         return 0;
     }();
     return v;
+}
+
+// ---- flat-stream forward (TMA tile::gather4) -------------------------------------------
+// The pipelined kernel above cuts stages at segment boundaries, so every row costs at least
+// one (often short) stage and each stage walks the segment cursor. Here a stage is a fixed
+// 16-edge slice of the work range's flat edge stream: the edge metadata arrives in 32-edge
+// windows (cp.async ring, kMetaWin ahead), a stage is exactly half a window, and segment
+// (row) ends are handled inside the FMA loop — a stage with no segment end (the common
+// case: rows average hundreds of edges) runs the 16 FMAs straight. Same segments, ranges,
+// fp64 partials and accumulation order as the pipelined kernel (bit-identical results).
+template <int MODE>
+__device__ __forceinline__ void flat_items(
+    const int64_t* __restrict__ seg_beg, const int32_t* __restrict__ seg_row, const int32_t* __restrict__ seg_slot,
+    const int32_t* __restrict__ row_seg0, const int32_t* __restrict__ row_nseg, const int32_t* __restrict__ range_seg,
+    int32_t nranges, const int32_t* __restrict__ cols, const double* __restrict__ coeffs, int32_t dim,
+    int32_t nchunks, float* __restrict__ y, int64_t ldy, int64_t row_base, double* __restrict__ partial, int64_t pld,
+    int32_t* __restrict__ counters, int32_t cld, const CUtensorMap* tmap, unsigned char* wbase, uint64_t* bars,
+    int32_t* ring_c, double* ring_f) {
+    using Cfg = PipeCfg<4>;
+    constexpr int KE = Cfg::kEdges;
+    static_assert(KE == 16, "a flat stage is half a 32-edge metadata window");
+    const int lane = threadIdx.x & 31;
+    const int64_t nwarps = static_cast<int64_t>(gridDim.x) * kPipeWarps;
+    uint32_t phases = 0;
+    for (int64_t item = static_cast<int64_t>(blockIdx.x) * kPipeWarps + (threadIdx.x >> 5);
+         item < static_cast<int64_t>(nchunks) * nranges; item += nwarps) {
+        const int32_t chunk = static_cast<int32_t>(item / nranges);
+        const int32_t r = static_cast<int32_t>(item - static_cast<int64_t>(chunk) * nranges);
+        const int32_t s_lo = range_seg[r], s_hi = range_seg[r + 1];
+        if (s_lo >= s_hi) continue;
+        const int32_t col = chunk * Cfg::kCols + lane * 4;
+        const int64_t e_lo = seg_beg[s_lo], e_hi = seg_beg[s_hi];
+        const int32_t nst = static_cast<int32_t>((e_hi - e_lo + KE - 1) / KE);
+        // consumer-side window of 32 segment records (end offset, row, slot)
+        int32_t wseg = s_lo, cur = s_lo;
+        int64_t w_end = 0;
+        int32_t w_row = 0, w_slot = -1;
+        auto load_window = [&](int32_t from) {
+            wseg = from;
+            const int32_t sg = from + lane;
+            w_end = sg < s_hi ? seg_beg[sg + 1] : 0;
+            w_row = sg < s_hi ? seg_row[sg] : 0;
+            w_slot = sg < s_hi ? seg_slot[sg] : -1;
+        };
+        load_window(s_lo);
+        int64_t cur_end = __shfl_sync(0xffffffffu, w_end, 0);
+        // edge-metadata ring: window q = edges [e_lo + 32q, +32) in ring slot q % kMetaWin
+        int w_issued = 0;
+        auto prefetch_win = [&] {
+            const int slot = w_issued % kMetaWin;
+            const int64_t e = e_lo + 32LL * w_issued + lane;
+            if (e < e_hi) {
+                cp_async_ca4(ring_c + slot * 32 + lane, cols + e);
+                cp_async_ca8(ring_f + slot * 32 + lane, coeffs + e);
+            }
+            cp_async_commit();
+            ++w_issued;
+        };
+#pragma unroll
+        for (int k = 0; k < kMetaWin; ++k)
+            if (e_lo + 32LL * w_issued < e_hi) prefetch_win();
+        auto issue = [&](int32_t k, int slot_idx) {
+            const int q = k >> 1;
+            while (w_issued < q + kMetaWin && e_lo + 32LL * w_issued < e_hi) prefetch_win();
+            const int allowed = w_issued - (q + 1);  // groups that may stay in flight
+            if (allowed >= 3) cp_async_wait<3>();
+            else if (allowed == 2) cp_async_wait<2>();
+            else if (allowed == 1) cp_async_wait<1>();
+            else cp_async_wait<0>();
+            __syncwarp();
+            const int64_t e0 = e_lo + static_cast<int64_t>(k) * KE;
+            const int cnt = static_cast<int>(e_hi - e0 < KE ? e_hi - e0 : KE);
+            unsigned char* st = wbase + slot_idx * Cfg::kStageBytes;
+            int32_t* srow = reinterpret_cast<int32_t*>(st + kStageDataBytes + KE * 8 + Cfg::kHdrBytes);
+            if (lane < KE) {
+                const int ridx = (q % kMetaWin) * 32 + (k & 1) * KE + lane;
+                const bool ok = lane < cnt;
+                reinterpret_cast<double*>(st + kStageDataBytes)[lane] = ok ? ring_f[ridx] : 0.0;
+                srow[lane] = ok ? ring_c[ridx] : -1;  // row -1: zero-filled by TMA
+            }
+            __syncwarp();
+            if (lane == 0) {
+                const int ng = (cnt + 3) >> 2;
+                float* rows = reinterpret_cast<float*>(st);
+                asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // after the warp's reads
+                mbar_expect_tx(bars + slot_idx, static_cast<uint32_t>(ng) * 4u * Cfg::kCols * 4u);
+                const int32_t c0 = chunk * Cfg::kCols;
+                for (int i = 0; i < ng; ++i) {
+                    const int4 rr = reinterpret_cast<const int4*>(srow)[i];
+                    tma_gather4(rows + 4 * i * Cfg::kCols, tmap, c0, rr.x, rr.y, rr.z, rr.w, bars + slot_idx);
+                }
+            }
+        };
+        double acc[4] = {0.0, 0.0, 0.0, 0.0};
+        auto finish = [&] {
+            const int kk = cur - wseg;
+            const int32_t row = __shfl_sync(0xffffffffu, w_row, kk);
+            const int32_t slot = __shfl_sync(0xffffffffu, w_slot, kk);
+            direct_finish(acc[0], acc[1], acc[2], acc[3], row, slot, lane, col, chunk, dim, y, ldy, row_base, partial,
+                          pld, counters, cld, seg_slot, row_seg0, row_nseg);
+            acc[0] = acc[1] = acc[2] = acc[3] = 0.0;
+            ++cur;
+            if (cur < s_hi) {
+                if (cur - wseg >= 32) load_window(cur);
+                cur_end = __shfl_sync(0xffffffffu, w_end, cur - wseg);
+            }
+        };
+        int32_t issued = 0;
+#pragma unroll
+        for (int k = 0; k < kStages; ++k)
+            if (issued < nst) {
+                issue(issued, k);
+                ++issued;
+            }
+        for (int32_t b = 0; b < nst; ++b) {
+            const int sl = b % kStages;
+            mbar_wait(bars + sl, (phases >> sl) & 1u);
+            phases ^= 1u << sl;
+            const unsigned char* st = wbase + sl * Cfg::kStageBytes;
+            const float* rows = reinterpret_cast<const float*>(st) + lane * 4;
+            const double* cf = reinterpret_cast<const double*>(st + kStageDataBytes);
+            const int64_t eb = e_lo + static_cast<int64_t>(b) * KE;
+            const int cnt = static_cast<int>(e_hi - eb < KE ? e_hi - eb : KE);
+            if (cnt == KE && cur_end >= eb + KE) {  // no segment ends inside: straight FMAs
+#pragma unroll
+                for (int j = 0; j < KE; ++j) edge_fma<4, MODE>(rows, cf, j, acc);
+            } else {
+                for (int j = 0; j < cnt; ++j) {
+                    while (eb + j == cur_end && cur < s_hi) finish();
+                    edge_fma<4, MODE>(rows, cf, j, acc);
+                }
+            }
+            __syncwarp();
+            if (issued < nst) {  // refill the slot just consumed
+                issue(issued, sl);
+                ++issued;
+            }
+        }
+        while (cur < s_hi) finish();
+        cp_async_wait<0>();
+        __syncwarp();
+    }
+}
+
+__global__ void __launch_bounds__(kPipeWarps * 32, kPipeCtas) spmm_fwd_flat_kernel(
+    const int64_t* __restrict__ seg_beg, const int32_t* __restrict__ seg_row, const int32_t* __restrict__ seg_slot,
+    const int32_t* __restrict__ row_seg0, const int32_t* __restrict__ row_nseg, const int32_t* __restrict__ range_seg,
+    int32_t nranges, const int32_t* __restrict__ cols, const double* __restrict__ coeffs, int32_t dim,
+    int32_t nchunks, float* __restrict__ y, int64_t ldy, int64_t row_base, double* __restrict__ partial, int64_t pld,
+    int32_t* __restrict__ counters, int32_t cld, const int32_t* __restrict__ table_flags,
+    const __grid_constant__ CUtensorMap tmap) {
+    using Cfg = PipeCfg<4>;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    unsigned char* wbase = smem_raw + static_cast<size_t>(warp) * kStages * Cfg::kStageBytes;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + kPipeWarps * kStages * Cfg::kStageBytes) + warp * kStages;
+    unsigned char* ring = smem_raw + kPipeWarps * kStages * Cfg::kStageBytes + kPipeWarps * kStages * 8 +
+                          warp * kMetaRingBytes;
+    int32_t* ring_c = reinterpret_cast<int32_t*>(ring);
+    double* ring_f = reinterpret_cast<double*>(ring + kMetaWin * 32 * 4);
+    if (lane == 0) {
+        asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
+        for (int k = 0; k < kStages; ++k) mbar_init(bars + k, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncwarp();
+    const int mode = widen_mode(table_flags);
+#define GASB_FLAT(M)                                                                                              \
+    flat_items<M>(seg_beg, seg_row, seg_slot, row_seg0, row_nseg, range_seg, nranges, cols, coeffs, dim, nchunks, \
+                  y, ldy, row_base, partial, pld, counters, cld, &tmap, wbase, bars, ring_c, ring_f)
+    if (mode == kWidenNonNeg) GASB_FLAT(kWidenNonNeg);
+    else if (mode == kWidenSigned) GASB_FLAT(kWidenSigned);
+    else GASB_FLAT(kWidenF2F);
+#undef GASB_FLAT
+}
+
+static void launch_flat(const SpmmSegs& s, const int32_t* cols, const double* coeffs, int32_t dim, float* y,
+                        int64_t ldy, int64_t row_base, double* partial, int64_t partial_ld, int32_t* counters,
+                        int32_t counters_ld, cudaStream_t st, const int32_t* special, const CUtensorMap* tmap) {
+    using Cfg = PipeCfg<4>;
+    constexpr int kSmem = Cfg::kSmem + kPipeWarps * kStages * 8 + kPipeWarps * kMetaRingBytes;
+    static int set = 0;
+    if (!set) {
+        GASB_CUDA(cudaFuncSetAttribute(spmm_fwd_flat_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
+        set = 1;
+    }
+    const int32_t nchunks = static_cast<int32_t>(ceil_div(dim, Cfg::kCols));
+    require(nchunks <= counters_ld && static_cast<int64_t>(nchunks) * Cfg::kCols <= partial_ld,
+            "spmm_fwd: counters / partials too narrow");
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        GASB_CUDA(cudaGetDevice(&dev));
+        GASB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    }
+    const int64_t items = static_cast<int64_t>(nchunks) * s.nranges;
+    const int64_t blocks = std::min<int64_t>(ceil_div(items, kPipeWarps), static_cast<int64_t>(kPipeCtas) * sms);
+    spmm_fwd_flat_kernel<<<static_cast<unsigned>(blocks), kPipeWarps * 32, kSmem, st>>>(
+        s.seg_beg, s.seg_row, s.seg_slot, s.row_seg0, s.row_nseg, s.range_seg, s.nranges, cols, coeffs, dim, nchunks,
+        y, ldy, row_base, partial, partial_ld, counters, counters_ld, special, *tmap);
 }
 
 static int g_pipe_smem_set[2][2] = {};
@@ -781,6 +983,13 @@ void launch_spmm_fwd(const SpmmSegs& s, const int32_t* cols, const double* coeff
     if (s.nranges <= 0 || dim <= 0) return;
     require(ldx % 4 == 0 && reinterpret_cast<uintptr_t>(x) % 16 == 0,
             "spmm_fwd: source rows must be 16 B aligned (ldx % 4 == 0)");
+    if (spmm_engine() == 3 && tmap && spmm_use_tma() && spmm_cpl() == 4) {
+        launch_flat(s, cols, coeffs, dim, y, ldy, row_base, partial, partial_ld, counters, counters_ld, st, special,
+                    tmap);
+        ++t_launches;
+        GASB_CUDA(cudaGetLastError());
+        return;
+    }
     if (spmm_engine() == 2) {
         launch_direct(s, cols, coeffs, x, ldx, dim, y, ldy, row_base, partial, partial_ld, counters, counters_ld, st,
                       special);

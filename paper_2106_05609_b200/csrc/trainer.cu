@@ -740,13 +740,18 @@ int64_t gasb_trainer_s::launch_batch_graph(int32_t p, bool dp) {
 
 void gasb_trainer_s::ensure_eval() {
     if (eval_agg.p) return;
-    require(!residual, "evaluate: the device path implements the full-graph forward for GCN");
     const int64_t R = row_off[num_parts];
-    eval_agg.alloc(R * ld_of(std::max(F, H)));
-    eval_act.alloc(R * ldH);
+    const int64_t ldT = residual ? ldD : ldH;  // width of the layer tables
+    eval_agg.alloc(R * ld_of(std::max(F, residual ? D : H)));
+    eval_act.alloc(R * ldT);
     for (auto& b : eval_tab) {
-        b.alloc(static_cast<int64_t>(n) * ldH);
+        b.alloc(static_cast<int64_t>(n) * ldT);
         b.zero();
+    }
+    if (residual) {
+        eval_h0.alloc(static_cast<int64_t>(n) * ldD);
+        if (spec.kind == 2) eval_z.alloc(static_cast<int64_t>(n) * ldH);
+        else eval_mixed.alloc(R * ldD);
     }
     eval_logits.alloc(R * ldC);
     eval_flags.alloc(2);
@@ -794,6 +799,72 @@ void gasb_trainer_s::enqueue_full_forward(int32_t first_layer) {
     }
 }
 
+// APPNP / GCNII over the full graph: head MLP over every node in global order (the h0
+// table the layer-1 SpMM gathers by global id), then per layer SpMM -> alpha-mixing with
+// h0[v] (-> GCNII: relu(mixed . W~_l)) -> scatter into the next layer's table; GCNII's
+// output head on the last layer (trainer.cpp:142-163, :221-227; layers.cpp:150-168).
+void gasb_trainer_s::enqueue_full_forward_res(int32_t first_layer) {
+    WsGuard ws(gemm_ws);
+    const SpmmSegs segs = seg_all.segs(0);
+    const int64_t R = row_off[num_parts];
+    const bool gcnii = spec.kind == 3;
+    GASB_CUDA(cudaMemsetAsync(eval_flags.p, 0, 2 * sizeof(int32_t), stream));
+    {  // head over all n nodes (X in global order)
+        GemmEpilogue e1;
+        e1.bias = P(p_hb1);
+        e1.relu = 1;
+        launch_gemm(0, n, H, F, X.p, ldF, P(p_hw1), pp(p_hw1), gcnii ? eval_h0.p : eval_z.p, gcnii ? ldD : ldH, e1,
+                    stream);
+        if (!gcnii) {
+            GemmEpilogue e2;
+            e2.bias = P(p_hb2);
+            launch_gemm(0, n, C, H, eval_z.p, ldH, P(p_hw2), pp(p_hw2), eval_h0.p, ldD, e2, stream);
+        }
+    }
+    if (gcnii) launch_wtilde(P(layer_param[1]), wt.p, L, H, pp(layer_param[1]), spec.beta, stream);
+    // the h0 table's value flags (the SpMM widening path): unknown sign, finite
+    int32_t* h0_flags = eval_flags.p;  // reuse slot 0 for layer 1's source, reset below
+    GASB_CUDA(cudaMemsetAsync(h0_flags, 0, sizeof(int32_t), stream));
+    launch_scan_special(eval_h0.p, n, ldD, D, h0_flags, stream);
+    for (int32_t l = first_layer; l <= L; ++l) {
+        const float* src;
+        int64_t lds;
+        const int32_t* flags;
+        const CUtensorMap* tm = nullptr;
+        if (l == 1) {
+            src = eval_h0.p, lds = ldD, flags = h0_flags;
+        } else if (l == first_layer) {
+            src = history_table(hist, l - 1), lds = history_ld(hist), flags = source_flags(l), tm = source_tmap(l);
+        } else {
+            src = eval_tab[(l - 1) & 1].p, lds = ldD, flags = eval_flags.p + ((l - 1) & 1);
+        }
+        launch_spmm_fwd(segs, cols_g.p, coef64.p, src, lds, D, eval_agg.p, ldD, 0, eval_partial.p, eval_pld,
+                        counters.p, max_chunks, stream, flags, tm);
+        int32_t* out_flags = eval_flags.p + (l & 1);
+        if (l < L) GASB_CUDA(cudaMemsetAsync(out_flags, 0, sizeof(int32_t), stream));
+        PushEpilogue pe{eval_tab[l & 1].p, ldD, batch_nodes.p, nullptr, nullptr, out_flags};
+        if (gcnii) {
+            launch_mix(eval_h0.p, ldD, batch_nodes.p, eval_agg.p, ldD, static_cast<int32_t>(R), D, spec.alpha,
+                       eval_mixed.p, ldD, nullptr, stream);
+            GemmEpilogue e;
+            e.relu = 1;
+            if (l < L) e.push = pe;
+            launch_gemm(0, static_cast<int>(R), H, H, eval_mixed.p, ldD,
+                        wt.p + static_cast<int64_t>(l - 1) * H * pp(layer_param[1]), pp(layer_param[1]), eval_act.p,
+                        ldD, e, stream);
+            if (l == L) {
+                GemmEpilogue eo;
+                eo.bias = P(p_ob);
+                launch_gemm(0, static_cast<int>(R), C, H, eval_act.p, ldD, P(p_ow), pp(p_ow), eval_logits.p, ldC, eo,
+                            stream);
+            }
+        } else {
+            launch_mix(eval_h0.p, ldD, batch_nodes.p, eval_agg.p, ldD, static_cast<int32_t>(R), D, spec.alpha,
+                       l < L ? eval_act.p : eval_logits.p, l < L ? ldD : ldC, l < L ? &pe : nullptr, stream);
+        }
+    }
+}
+
 extern "C" {
 
 gasb_status gasb_trainer_evaluate(gasb_trainer t, const uint8_t* h_train, const uint8_t* h_val, const uint8_t* h_test,
@@ -809,7 +880,8 @@ gasb_status gasb_trainer_evaluate(gasb_trainer t, const uint8_t* h_train, const 
             else GASB_CUDA(cudaMemsetAsync(t->eval_masks.p + k * n, 0, n, t->stream));
         }
         GASB_CUDA(cudaMemsetAsync(t->eval_counts.p, 0, 6 * sizeof(int64_t), t->stream));
-        t->enqueue_full_forward(1);
+        if (t->residual) t->enqueue_full_forward_res(1);
+        else t->enqueue_full_forward(1);
         const int64_t R = t->row_off[t->num_parts];
         argmax_count_kernel<<<static_cast<unsigned>(ceil_div(R, 256)), 256, 0, t->stream>>>(
             t->eval_logits.p, t->ldC, R, t->C, t->batch_nodes.p, t->labels_all.p, t->eval_masks.p, n,
@@ -846,7 +918,8 @@ gasb_status gasb_trainer_infer_from_history(gasb_trainer t, int32_t* h_predictio
         GASB_CUDA(cudaSetDevice(t->opt.device));
         t->ensure_eval();
         const int64_t n = t->n;
-        t->enqueue_full_forward(t->L >= 2 ? t->L : 1);
+        if (t->residual) t->enqueue_full_forward_res(t->L >= 2 ? t->L : 1);
+        else t->enqueue_full_forward(t->L >= 2 ? t->L : 1);
         const int64_t R = t->row_off[t->num_parts];
         DevBuf<int32_t> preds;
         preds.alloc(n);

@@ -248,11 +248,12 @@ struct gasb_trainer_s {
     DevBuf<int32_t> labels_all, eval_flags;
     DevBuf<uint8_t> eval_masks;
     DevBuf<int64_t> eval_counts;
-    DevBuf<float> eval_agg, eval_act, eval_tab[2], eval_logits;
+    DevBuf<float> eval_agg, eval_act, eval_tab[2], eval_logits, eval_h0, eval_z, eval_mixed;
     DevBuf<double> eval_partial;
     int64_t eval_pld = 0;
     void ensure_eval();
-    void enqueue_full_forward(int32_t first_layer);  // the DP exchange region (grads and act_l are views into it)
+    void enqueue_full_forward(int32_t first_layer);
+    void enqueue_full_forward_res(int32_t first_layer);  // the DP exchange region (grads and act_l are views into it)
     std::vector<int64_t> graph_launches_dp;
     int64_t launch_batch_graph(int32_t p, bool dp);
 };

@@ -7,6 +7,7 @@
 #include <cmath>
 #include <cstdio>
 #include <stdexcept>
+#include <string>
 #include <vector>
 
 #include "gasb/gas.hpp"
@@ -86,6 +87,16 @@ int main() {
         EXPECT(throws<std::invalid_argument>([&] { h.pull(0, ids); }));
         std::vector<NodeId> oob{3};
         EXPECT(throws<std::invalid_argument>([&] { h.pull(1, oob); }));  // id out of range
+        // GASH checkpoint round trip (history.cpp:130-178): tables kept, stamps 0, step 0
+        const std::string path = "/tmp/gasb_shim_test.gash";
+        h.save_checkpoint(path);
+        HistoryStore back = HistoryStore::load_checkpoint(path);
+        EXPECT(back.num_layers() == 3 && back.num_nodes() == 3 && back.dim() == 4);
+        DenseMatrix b0 = back.pull(1, std::vector<NodeId>{0, 2});
+        EXPECT(b0.row(0)[0] == 5 && b0.row(1)[3] == 4);
+        EXPECT(back.step() == 0 && back.last_push_step(1, 1) == 0);
+        EXPECT(throws<std::runtime_error>([&] { HistoryStore::load_checkpoint("/nonexistent/x.gash"); }));
+        std::remove(path.c_str());
     } catch (const std::runtime_error& e) {
         have_gpu = false;
         std::printf("no device: %s\n", e.what());

@@ -22,7 +22,7 @@ def _pair(ref, name):
     spec = gb.ModelSpec(kind=w.kind, num_layers=w.num_layers, hidden=w.hidden, seed=3)
     tr = gb.GasTrainer(sched, ds.features, ds.labels, ds.train_mask, w.num_classes, spec)
     rs = ref.session(ds.row_offsets, ds.cols, ds.features, ds.labels, ds.train_mask, w.num_classes, ds.assignment,
-                     w.parts, make_spec(kind=0, num_layers=w.num_layers, hidden=w.hidden, seed=3))
+                     w.parts, make_spec(kind=gb.trainer.KINDS[w.kind], num_layers=w.num_layers, hidden=w.hidden, seed=3))
     return ds, tr, rs
 
 
@@ -31,7 +31,7 @@ def _ambiguous(logits, tol=1e-4):
     return (top2[:, 1] - top2[:, 0]) <= tol * np.maximum(1.0, np.abs(top2[:, 1]))
 
 
-@pytest.mark.parametrize("name", ["cora", "reddit_mini"])
+@pytest.mark.parametrize("name", ["cora", "reddit_mini", "cora_appnp", "cora_gcnii"])
 def test_evaluate_matches_reference(ref, name):
     ds, tr, rs = _pair(ref, name)
     for e in range(2):
@@ -51,8 +51,9 @@ def test_evaluate_matches_reference(ref, name):
     assert 0.0 < acc[0] <= 1.0
 
 
-def test_infer_from_history_matches_reference(ref):
-    ds, tr, rs = _pair(ref, "cora")
+@pytest.mark.parametrize("name", ["cora", "cora_appnp", "cora_gcnii"])
+def test_infer_from_history_matches_reference(ref, name):
+    ds, tr, rs = _pair(ref, name)
     pred, stale = tr.infer_from_history()
     rpred, rstale = rs.infer()
     assert stale and rstale  # nothing pushed yet
