@@ -1084,7 +1084,9 @@ __global__ void __launch_bounds__(kBwdThreads) spmm_bwd_smem_kernel(
     const int64_t* __restrict__ rp, int32_t nt, const int32_t* __restrict__ src, const float* __restrict__ cf,
     const float* __restrict__ gy, int64_t ldgy, int32_t nsrc, int32_t dim, const float* __restrict__ mask,
     int64_t ldm, float* __restrict__ gx, int64_t ldgx, int32_t targets_per_cta, int accumulate) {
-    extern __shared__ float sg[];  // nsrc x kBwdCW
+    extern __shared__ float sg[];  // nsrc x kBwdCW, then 32 (offset, coeff) pairs per warp
+    __shared__ int32_t s_next;
+    if (threadIdx.x == 0) s_next = 0;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
     const int32_t col0 = blockIdx.x * kBwdCW;
     const int32_t ncol = min(kBwdCW, dim - col0);
@@ -1117,33 +1119,42 @@ __global__ void __launch_bounds__(kBwdThreads) spmm_bwd_smem_kernel(
         }
     }
     __syncthreads();
-    const int32_t t_lo = blockIdx.y * targets_per_cta;
-    const int32_t t_hi = min(nt, t_lo + targets_per_cta);
-    for (int32_t t = t_lo + warp; t < t_hi; t += nwarps) {
+    // targets t = blockIdx.y + splits * k; warps claim k dynamically (power-law in-degrees)
+    const int32_t splits = targets_per_cta;
+    int2* wbuf = reinterpret_cast<int2*>(sg + static_cast<int64_t>(nsrc) * kBwdCW) + warp * 32;
+    for (;;) {
+        int32_t k = 0;
+        if (lane == 0) k = atomicAdd(&s_next, 1);
+        const int32_t t = static_cast<int32_t>(blockIdx.y) + splits * __shfl_sync(0xffffffffu, k, 0);
+        if (t >= nt) break;
         const int64_t e0 = rp[t], e1 = rp[t + 1];
         float a = (accumulate && lane < ncol) ? gx[static_cast<int64_t>(t) * ldgx + col0 + lane] : 0.0f;
-        // metadata of the next 32 entries is loaded while the current 32 are accumulated
+        // metadata of the next 32 entries is loaded while the current 32 are accumulated; the
+        // current window is parked in shared memory as (row offset, coeff) pairs read back by
+        // broadcast LDS.64 (one shared-memory op per entry instead of two shuffles)
         int64_t eb = e0;
         int cnt = static_cast<int>((e1 - eb) < 32 ? (e1 - eb) : 32);
         int32_t my_r = lane < cnt ? __ldg(src + eb + lane) : 0;
         float my_c = lane < cnt ? __ldg(cf + eb + lane) : 0.0f;
+        const float* sgl = sg + lane;
         while (eb < e1) {
             const int64_t nb = eb + 32;
             const int ncnt = static_cast<int>(e1 - nb <= 0 ? 0 : (e1 - nb < 32 ? e1 - nb : 32));
             const int32_t nr = lane < ncnt ? __ldg(src + nb + lane) : 0;
             const float nc = lane < ncnt ? __ldg(cf + nb + lane) : 0.0f;
+            __syncwarp();
+            wbuf[lane] = make_int2(my_r * kBwdCW, __float_as_int(my_c));
+            __syncwarp();
             if (cnt == 32) {
 #pragma unroll
                 for (int j = 0; j < 32; ++j) {
-                    const int32_t r = __shfl_sync(0xffffffffu, my_r, j);
-                    const float c = __shfl_sync(0xffffffffu, my_c, j);
-                    a = __fadd_rn(a, __fmul_rn(c, sg[r * kBwdCW + lane]));
+                    const int2 rc = wbuf[j];
+                    a = __fadd_rn(a, __fmul_rn(__int_as_float(rc.y), sgl[rc.x]));
                 }
             } else {
                 for (int j = 0; j < cnt; ++j) {
-                    const int32_t r = __shfl_sync(0xffffffffu, my_r, j);
-                    const float c = __shfl_sync(0xffffffffu, my_c, j);
-                    a = __fadd_rn(a, __fmul_rn(c, sg[r * kBwdCW + lane]));
+                    const int2 rc = wbuf[j];
+                    a = __fadd_rn(a, __fmul_rn(__int_as_float(rc.y), sgl[rc.x]));
                 }
             }
             eb = nb;
@@ -1165,11 +1176,11 @@ void launch_spmm_bwd(const int64_t* t_rowptr, int32_t nt, const int32_t* t_src, 
                      const float* gy, int64_t ldgy, int32_t dim, const float* mask, int64_t ldm, float* gx,
                      int64_t ldgx, cudaStream_t st, int32_t nsrc, bool accumulate) {
     if (nt <= 0 || dim <= 0) return;
-    const int64_t smem = static_cast<int64_t>(nsrc) * kBwdCW * sizeof(float);
-    if (nsrc > 0 && smem <= 200 * 1024) {
+    const int64_t smem = static_cast<int64_t>(nsrc) * kBwdCW * sizeof(float) + (kBwdThreads / 32) * 32 * 8;
+    if (nsrc > 0 && smem <= 216 * 1024) {
         if (!g_bwd_smem_set) {
             GASB_CUDA(cudaFuncSetAttribute(spmm_bwd_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           200 * 1024));
+                                           216 * 1024));
             g_bwd_smem_set = 1;
         }
         const int32_t nchunks = static_cast<int32_t>(ceil_div(dim, kBwdCW));
@@ -1182,10 +1193,9 @@ void launch_spmm_bwd(const int64_t* t_rowptr, int32_t nt, const int32_t* t_src, 
         }
         const int32_t splits = static_cast<int32_t>(
             std::max<int64_t>(1, std::min<int64_t>(sms / nchunks, ceil_div(nt, kBwdThreads / 32))));
-        const int32_t per = static_cast<int32_t>(ceil_div(nt, splits));
-        dim3 grid(static_cast<unsigned>(nchunks), static_cast<unsigned>(ceil_div(nt, per)));
+        dim3 grid(static_cast<unsigned>(nchunks), static_cast<unsigned>(splits));
         spmm_bwd_smem_kernel<<<grid, kBwdThreads, smem, st>>>(t_rowptr, nt, t_src, t_coeffs, gy, ldgy, nsrc, dim,
-                                                             mask, ldm, gx, ldgx, per, accumulate ? 1 : 0);
+                                                             mask, ldm, gx, ldgx, splits, accumulate ? 1 : 0);
         ++t_launches;
         GASB_CUDA(cudaGetLastError());
         return;
