@@ -442,6 +442,48 @@ __device__ __forceinline__ float4 ldg_row_piece(const float* p) {
 
 // Ends segment `k` of the warp's window: store the row (single-segment row) or publish an
 // fp64 partial, the last-arriving warp of the row summing the partials in segment order.
+template <int CPL>
+__device__ __forceinline__ void seg_finish(double (&acc)[CPL], int32_t row, int32_t slot, int lane, int32_t col,
+                                           int32_t chunk, int32_t dim, float* __restrict__ y, int64_t ldy,
+                                           int64_t row_base, double* __restrict__ partial, int64_t pld,
+                                           int32_t* __restrict__ counters, int32_t cld,
+                                           const int32_t* __restrict__ seg_slot,
+                                           const int32_t* __restrict__ row_seg0,
+                                           const int32_t* __restrict__ row_nseg) {
+    bool store = true;
+    if (slot >= 0) {
+        double* pp = partial + static_cast<int64_t>(slot) * pld + col;
+#pragma unroll
+        for (int k = 0; k < CPL; ++k) pp[k] = acc[k];
+        __threadfence();
+        __syncwarp();
+        int last = 0;
+        const int32_t nk = row_nseg[row];
+        if (lane == 0) last = atomicAdd(counters + static_cast<int64_t>(row) * cld + chunk, 1) == nk - 1;
+        store = __shfl_sync(0xffffffffu, last, 0) != 0;
+        if (store) {
+            __threadfence();
+            const int32_t s0 = row_seg0[row];
+#pragma unroll
+            for (int k = 0; k < CPL; ++k) acc[k] = 0.0;
+            for (int32_t i = 0; i < nk; ++i) {
+                const double* q2 = partial + static_cast<int64_t>(seg_slot[s0 + i]) * pld + col;
+#pragma unroll
+                for (int k = 0; k < CPL; ++k) acc[k] += __ldcg(q2 + k);
+            }
+            if (lane == 0) counters[static_cast<int64_t>(row) * cld + chunk] = 0;  // self-reset
+        }
+    }
+    if (store) {
+        float* yr = y + (static_cast<int64_t>(row) - row_base) * ldy;
+#pragma unroll
+        for (int k = 0; k < CPL; ++k)
+            if (col + k < dim) yr[col + k] = static_cast<float>(acc[k]);
+    }
+#pragma unroll
+    for (int k = 0; k < CPL; ++k) acc[k] = 0.0;
+}
+
 __device__ __forceinline__ void direct_finish(double a0, double a1, double a2, double a3, int32_t row, int32_t slot, int lane, int32_t col,
                                               int32_t chunk, int32_t dim, float* __restrict__ y, int64_t ldy,
                                               int64_t row_base, double* __restrict__ partial, int64_t pld,
@@ -616,7 +658,7 @@ static int spmm_engine() {
 // (row) ends are handled inside the FMA loop — a stage with no segment end (the common
 // case: rows average hundreds of edges) runs the 16 FMAs straight. Same segments, ranges,
 // fp64 partials and accumulation order as the pipelined kernel (bit-identical results).
-template <int MODE>
+template <int CPL, int MODE>
 __device__ __forceinline__ void flat_items(
     const int64_t* __restrict__ seg_beg, const int32_t* __restrict__ seg_row, const int32_t* __restrict__ seg_slot,
     const int32_t* __restrict__ row_seg0, const int32_t* __restrict__ row_nseg, const int32_t* __restrict__ range_seg,
@@ -624,9 +666,9 @@ __device__ __forceinline__ void flat_items(
     int32_t nchunks, float* __restrict__ y, int64_t ldy, int64_t row_base, double* __restrict__ partial, int64_t pld,
     int32_t* __restrict__ counters, int32_t cld, const CUtensorMap* tmap, unsigned char* wbase, uint64_t* bars,
     int32_t* ring_c, double* ring_f) {
-    using Cfg = PipeCfg<4>;
+    using Cfg = PipeCfg<CPL>;
     constexpr int KE = Cfg::kEdges;
-    static_assert(KE == 16, "a flat stage is half a 32-edge metadata window");
+    static_assert(KE == 16 || KE == 32, "a flat stage is half or all of a 32-edge metadata window");
     const int lane = threadIdx.x & 31;
     const int64_t nwarps = static_cast<int64_t>(gridDim.x) * kPipeWarps;
     uint32_t phases = 0;
@@ -636,7 +678,7 @@ __device__ __forceinline__ void flat_items(
         const int32_t r = static_cast<int32_t>(item - static_cast<int64_t>(chunk) * nranges);
         const int32_t s_lo = range_seg[r], s_hi = range_seg[r + 1];
         if (s_lo >= s_hi) continue;
-        const int32_t col = chunk * Cfg::kCols + lane * 4;
+        const int32_t col = chunk * Cfg::kCols + lane * CPL;
         const int64_t e_lo = seg_beg[s_lo], e_hi = seg_beg[s_hi];
         const int32_t nst = static_cast<int32_t>((e_hi - e_lo + KE - 1) / KE);
         // consumer-side window of 32 segment records (end offset, row, slot)
@@ -668,7 +710,7 @@ __device__ __forceinline__ void flat_items(
         for (int k = 0; k < kMetaWin; ++k)
             if (e_lo + 32LL * w_issued < e_hi) prefetch_win();
         auto issue = [&](int32_t k, int slot_idx) {
-            const int q = k >> 1;
+            const int q = (k * KE) >> 5;  // metadata window of this stage
             while (w_issued < q + kMetaWin && e_lo + 32LL * w_issued < e_hi) prefetch_win();
             const int allowed = w_issued - (q + 1);  // groups that may stay in flight
             if (allowed >= 3) cp_async_wait<3>();
@@ -681,7 +723,7 @@ __device__ __forceinline__ void flat_items(
             unsigned char* st = wbase + slot_idx * Cfg::kStageBytes;
             int32_t* srow = reinterpret_cast<int32_t*>(st + kStageDataBytes + KE * 8 + Cfg::kHdrBytes);
             if (lane < KE) {
-                const int ridx = (q % kMetaWin) * 32 + (k & 1) * KE + lane;
+                const int ridx = (q % kMetaWin) * 32 + ((k * KE) & 31) + lane;
                 const bool ok = lane < cnt;
                 reinterpret_cast<double*>(st + kStageDataBytes)[lane] = ok ? ring_f[ridx] : 0.0;
                 srow[lane] = ok ? ring_c[ridx] : -1;  // row -1: zero-filled by TMA
@@ -699,14 +741,15 @@ __device__ __forceinline__ void flat_items(
                 }
             }
         };
-        double acc[4] = {0.0, 0.0, 0.0, 0.0};
+        double acc[CPL];
+#pragma unroll
+        for (int k = 0; k < CPL; ++k) acc[k] = 0.0;
         auto finish = [&] {
             const int kk = cur - wseg;
             const int32_t row = __shfl_sync(0xffffffffu, w_row, kk);
             const int32_t slot = __shfl_sync(0xffffffffu, w_slot, kk);
-            direct_finish(acc[0], acc[1], acc[2], acc[3], row, slot, lane, col, chunk, dim, y, ldy, row_base, partial,
-                          pld, counters, cld, seg_slot, row_seg0, row_nseg);
-            acc[0] = acc[1] = acc[2] = acc[3] = 0.0;
+            seg_finish<CPL>(acc, row, slot, lane, col, chunk, dim, y, ldy, row_base, partial, pld, counters, cld,
+                            seg_slot, row_seg0, row_nseg);
             ++cur;
             if (cur < s_hi) {
                 if (cur - wseg >= 32) load_window(cur);
@@ -725,17 +768,17 @@ __device__ __forceinline__ void flat_items(
             mbar_wait(bars + sl, (phases >> sl) & 1u);
             phases ^= 1u << sl;
             const unsigned char* st = wbase + sl * Cfg::kStageBytes;
-            const float* rows = reinterpret_cast<const float*>(st) + lane * 4;
+            const float* rows = reinterpret_cast<const float*>(st) + lane * CPL;
             const double* cf = reinterpret_cast<const double*>(st + kStageDataBytes);
             const int64_t eb = e_lo + static_cast<int64_t>(b) * KE;
             const int cnt = static_cast<int>(e_hi - eb < KE ? e_hi - eb : KE);
             if (cnt == KE && cur_end >= eb + KE) {  // no segment ends inside: straight FMAs
 #pragma unroll
-                for (int j = 0; j < KE; ++j) edge_fma<4, MODE>(rows, cf, j, acc);
+                for (int j = 0; j < KE; ++j) edge_fma<CPL, MODE>(rows, cf, j, acc);
             } else {
                 for (int j = 0; j < cnt; ++j) {
                     while (eb + j == cur_end && cur < s_hi) finish();
-                    edge_fma<4, MODE>(rows, cf, j, acc);
+                    edge_fma<CPL, MODE>(rows, cf, j, acc);
                 }
             }
             __syncwarp();
@@ -750,6 +793,7 @@ __device__ __forceinline__ void flat_items(
     }
 }
 
+template <int CPL>
 __global__ void __launch_bounds__(kPipeWarps * 32, kPipeCtas) spmm_fwd_flat_kernel(
     const int64_t* __restrict__ seg_beg, const int32_t* __restrict__ seg_row, const int32_t* __restrict__ seg_slot,
     const int32_t* __restrict__ row_seg0, const int32_t* __restrict__ row_nseg, const int32_t* __restrict__ range_seg,
@@ -757,7 +801,7 @@ __global__ void __launch_bounds__(kPipeWarps * 32, kPipeCtas) spmm_fwd_flat_kern
     int32_t nchunks, float* __restrict__ y, int64_t ldy, int64_t row_base, double* __restrict__ partial, int64_t pld,
     int32_t* __restrict__ counters, int32_t cld, const int32_t* __restrict__ table_flags,
     const __grid_constant__ CUtensorMap tmap) {
-    using Cfg = PipeCfg<4>;
+    using Cfg = PipeCfg<CPL>;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     unsigned char* wbase = smem_raw + static_cast<size_t>(warp) * kStages * Cfg::kStageBytes;
@@ -774,7 +818,7 @@ __global__ void __launch_bounds__(kPipeWarps * 32, kPipeCtas) spmm_fwd_flat_kern
     __syncwarp();
     const int mode = widen_mode(table_flags);
 #define GASB_FLAT(M)                                                                                              \
-    flat_items<M>(seg_beg, seg_row, seg_slot, row_seg0, row_nseg, range_seg, nranges, cols, coeffs, dim, nchunks, \
+    flat_items<CPL, M>(seg_beg, seg_row, seg_slot, row_seg0, row_nseg, range_seg, nranges, cols, coeffs, dim, nchunks, \
                   y, ldy, row_base, partial, pld, counters, cld, &tmap, wbase, bars, ring_c, ring_f)
     if (mode == kWidenNonNeg) GASB_FLAT(kWidenNonNeg);
     else if (mode == kWidenSigned) GASB_FLAT(kWidenSigned);
@@ -782,14 +826,15 @@ __global__ void __launch_bounds__(kPipeWarps * 32, kPipeCtas) spmm_fwd_flat_kern
 #undef GASB_FLAT
 }
 
+template <int CPL>
 static void launch_flat(const SpmmSegs& s, const int32_t* cols, const double* coeffs, int32_t dim, float* y,
                         int64_t ldy, int64_t row_base, double* partial, int64_t partial_ld, int32_t* counters,
                         int32_t counters_ld, cudaStream_t st, const int32_t* special, const CUtensorMap* tmap) {
-    using Cfg = PipeCfg<4>;
+    using Cfg = PipeCfg<CPL>;
     constexpr int kSmem = Cfg::kSmem + kPipeWarps * kStages * 8 + kPipeWarps * kMetaRingBytes;
     static int set = 0;
     if (!set) {
-        GASB_CUDA(cudaFuncSetAttribute(spmm_fwd_flat_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
+        GASB_CUDA(cudaFuncSetAttribute(spmm_fwd_flat_kernel<CPL>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
         set = 1;
     }
     const int32_t nchunks = static_cast<int32_t>(ceil_div(dim, Cfg::kCols));
@@ -803,7 +848,7 @@ static void launch_flat(const SpmmSegs& s, const int32_t* cols, const double* co
     }
     const int64_t items = static_cast<int64_t>(nchunks) * s.nranges;
     const int64_t blocks = std::min<int64_t>(ceil_div(items, kPipeWarps), static_cast<int64_t>(kPipeCtas) * sms);
-    spmm_fwd_flat_kernel<<<static_cast<unsigned>(blocks), kPipeWarps * 32, kSmem, st>>>(
+    spmm_fwd_flat_kernel<CPL><<<static_cast<unsigned>(blocks), kPipeWarps * 32, kSmem, st>>>(
         s.seg_beg, s.seg_row, s.seg_slot, s.row_seg0, s.row_nseg, s.range_seg, s.nranges, cols, coeffs, dim, nchunks,
         y, ldy, row_base, partial, partial_ld, counters, counters_ld, special, *tmap);
 }
@@ -983,9 +1028,13 @@ void launch_spmm_fwd(const SpmmSegs& s, const int32_t* cols, const double* coeff
     if (s.nranges <= 0 || dim <= 0) return;
     require(ldx % 4 == 0 && reinterpret_cast<uintptr_t>(x) % 16 == 0,
             "spmm_fwd: source rows must be 16 B aligned (ldx % 4 == 0)");
-    if (spmm_engine() == 3 && tmap && spmm_use_tma() && spmm_cpl() == 4) {
-        launch_flat(s, cols, coeffs, dim, y, ldy, row_base, partial, partial_ld, counters, counters_ld, st, special,
-                    tmap);
+    if (spmm_engine() == 3 && tmap && spmm_use_tma()) {
+        if (spmm_cpl() == 2)
+            launch_flat<2>(s, cols, coeffs, dim, y, ldy, row_base, partial, partial_ld, counters, counters_ld, st,
+                           special, tmap);
+        else
+            launch_flat<4>(s, cols, coeffs, dim, y, ldy, row_base, partial, partial_ld, counters, counters_ld, st,
+                           special, tmap);
         ++t_launches;
         GASB_CUDA(cudaGetLastError());
         return;

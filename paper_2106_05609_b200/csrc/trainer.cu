@@ -148,6 +148,31 @@ __global__ void __launch_bounds__(256) argmax_count_kernel(const float* __restri
     if (threadIdx.x < 6 && sc[threadIdx.x]) atomicAdd(&counts[threadIdx.x], sc[threadIdx.x]);
 }
 
+// X[r, :F] = dense[r, :] (row pitch F -> ldF) and flags |= table_flag_of over the values:
+// one warp per row, one atomic per CTA.
+__global__ void __launch_bounds__(256) repitch_flags_kernel(const float* __restrict__ dense, int64_t rows, int32_t F,
+                                                            float* __restrict__ X, int64_t ldF, int32_t* flags) {
+    __shared__ int32_t sf;
+    if (threadIdx.x == 0) sf = 0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    int32_t f = 0;
+    for (int64_t r = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; r < rows;
+         r += (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5) {
+        const float* src = dense + r * F;
+        float* dst = X + r * ldF;
+        for (int32_t c = lane; c < F; c += 32) {
+            const float v = src[c];
+            dst[c] = v;
+            f |= table_flag_of(v);
+        }
+    }
+    f = __reduce_or_sync(0xffffffffu, f);
+    if (lane == 0 && f) atomicOr(&sf, f);
+    __syncthreads();
+    if (threadIdx.x == 0 && sf) atomicOr(flags, sf);
+}
+
 }  // namespace
 }  // namespace gasb
 using namespace gasb;
@@ -1086,10 +1111,15 @@ gasb_status gasb_trainer_stream(gasb_trainer t, gasb_stream* out) {
 gasb_status gasb_trainer_set_features(gasb_trainer t, const float* h) {
     return guard([&] {
         require(t && h, "trainer: null argument");
-        GASB_CUDA(cudaMemcpy2DAsync(t->X.p, sizeof(float) * t->ldF, h, sizeof(float) * t->F, sizeof(float) * t->F,
-                                    t->n, cudaMemcpyHostToDevice, t->stream));
-        GASB_CUDA(cudaMemsetAsync(t->xflags.p, 0, sizeof(int32_t), t->stream));  // X is replaced whole
-        launch_scan_special(t->X.p, t->n, t->ldF, t->F, t->xflags.p, t->stream);
+        // one contiguous DMA at full link rate into a dense staging copy, then one device pass
+        // re-pitches the rows into X and rebuilds X's value flags (X is replaced whole)
+        const int64_t cnt = static_cast<int64_t>(t->n) * t->F;
+        if (t->x_stage.n < cnt) t->x_stage.alloc(cnt);
+        GASB_CUDA(cudaMemcpyAsync(t->x_stage.p, h, sizeof(float) * cnt, cudaMemcpyHostToDevice, t->stream));
+        GASB_CUDA(cudaMemsetAsync(t->xflags.p, 0, sizeof(int32_t), t->stream));
+        repitch_flags_kernel<<<1184, 256, 0, t->stream>>>(t->x_stage.p, t->n, t->F, t->X.p, t->ldF, t->xflags.p);
+        ++t_launches;
+        GASB_CUDA(cudaGetLastError());
     });
 }
 

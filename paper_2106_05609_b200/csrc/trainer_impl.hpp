@@ -82,7 +82,7 @@ struct gasb_trainer_s {
     int32_t nb_max = 0, ne_max = 0;
 
     // device data
-    DevBuf<float> X;
+    DevBuf<float> X, x_stage;  // x_stage: dense host-layout copy for set_features
     DevBuf<int32_t> batch_nodes, cols_g, cols_l, t_src, train_rows, train_labels, extended, compose_idx, halo_ids;
     DevBuf<double> coef64;
     DevBuf<float> t_cf;
