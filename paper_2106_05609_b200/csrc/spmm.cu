@@ -60,14 +60,24 @@ constexpr int kStageDataBytes = GASB_SPMM_STAGE_BYTES;
 
 enum WidenMode { kWidenF2F = 0, kWidenSigned = 1, kWidenNonNeg = 2 };
 
+// The bit pattern {hi = u >> 3, lo = u << 29} is the 64-bit product u * 2^29: one
+// IMAD.WIDE.U32. For a negative x the product carries the sign at bit 28 of hi; adding
+// s * 0x70000000 (s = sign) moves it to bit 31 (carry through bits 28..30): one more IMAD.
+__device__ __forceinline__ uint64_t mul_wide_2p29(uint32_t u) {
+    uint64_t d;
+    asm("mul.wide.u32 %0, %1, 536870912;" : "=l"(d) : "r"(u));
+    return d;
+}
+
 template <int MODE>
 __device__ __forceinline__ double widen_scaled(float f) {
     const uint32_t u = __float_as_uint(f);
-    if (MODE == kWidenNonNeg)
-        return __hiloint2double(static_cast<int>(u >> 3), static_cast<int>(u << 29));
-    if (MODE == kWidenSigned)
-        return __hiloint2double(static_cast<int>(((u & 0x7fffffffu) >> 3) | (u & 0x80000000u)),
-                                static_cast<int>(u << 29));
+    if (MODE == kWidenNonNeg) return __longlong_as_double(static_cast<long long>(mul_wide_2p29(u)));
+    if (MODE == kWidenSigned) {
+        const uint64_t d = mul_wide_2p29(u);
+        const uint32_t hi = static_cast<uint32_t>(d >> 32) + (u >> 31) * 0x70000000u;
+        return __hiloint2double(static_cast<int>(hi), static_cast<int>(static_cast<uint32_t>(d)));
+    }
     return __dmul_rn(static_cast<double>(f), 0x1.0p-896);
 }
 
@@ -668,7 +678,7 @@ __device__ __forceinline__ void flat_items(
     int32_t* ring_c, double* ring_f) {
     using Cfg = PipeCfg<CPL>;
     constexpr int KE = Cfg::kEdges;
-    static_assert(KE == 16 || KE == 32, "a flat stage is half or all of a 32-edge metadata window");
+    static_assert(KE == 8 || KE == 16 || KE == 32, "a flat stage is a quarter, half or all of a 32-edge window");
     const int lane = threadIdx.x & 31;
     const int64_t nwarps = static_cast<int64_t>(gridDim.x) * kPipeWarps;
     uint32_t phases = 0;
