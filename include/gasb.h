@@ -103,6 +103,13 @@ gasb_status gasb_plan_copy(gasb_schedule s, int32_t part, int32_t* extended, int
                            int32_t* local_cols, int64_t* gcn_rowptr, int32_t* gcn_cols, float* gcn_coeffs,
                            int64_t* sum_rowptr, int32_t* sum_cols, float* sum_coeffs);
 gasb_status gasb_schedule_destroy(gasb_schedule s);
+/* save_partition / load_partition (io.hpp:40-41, io.cpp:187-217): the reference's
+ * "node part" text format (# comments, blank lines); load validates as
+ * partition_from_assignment (partition.cpp:314-328) and reports num_parts = max part + 1. */
+gasb_status gasb_partition_save(const char* path, const int32_t* h_assignment, int32_t num_nodes);
+gasb_status gasb_partition_load(const char* path, int32_t num_nodes, int32_t* h_assignment, int32_t* num_parts);
+/* random_partition (partition.hpp:23, partition.cpp:330-342), bit-exact (seeded shuffle). */
+gasb_status gasb_random_partition(int32_t num_nodes, int32_t num_parts, uint64_t seed, int32_t* h_assignment);
 
 /* ==================================================================================== */
 /* history-store: HistoryStore (include/gas/history.hpp:29-66, src/history.cpp:10-178)   */

@@ -195,6 +195,8 @@ class RefLib:
         L.ref_plan_free.argtypes = [vp]
         L.ref_cluster_partition.argtypes = [vp, i32, u64, vp]
         L.ref_random_partition.argtypes = [vp, i32, u64, vp]
+        L.ref_partition_save.argtypes = [C.c_char_p, vp, i32, i32]
+        L.ref_partition_load.argtypes = [C.c_char_p, i32, vp, P(i32)]
         L.ref_inter_intra_ratio.argtypes = [vp, vp, i32]
         L.ref_inter_intra_ratio.restype = f64
         L.ref_aggregate.argtypes = [vp, i64, vp, vp, vp, i64, i64, vp, vp, vp]

@@ -223,6 +223,21 @@ int ref_random_partition(const void* gp, std::int32_t parts, std::uint64_t seed,
     });
 }
 
+// io.cpp:187-217 partition files
+int ref_partition_save(const char* path, const std::int32_t* assignment, std::int32_t n, std::int32_t parts) {
+    return guard([&] {
+        std::vector<std::int32_t> a(assignment, assignment + n);
+        save_partition(path, partition_from_assignment(a, parts));
+    });
+}
+int ref_partition_load(const char* path, std::int32_t n, std::int32_t* assignment, std::int32_t* parts) {
+    return guard([&] {
+        Partitioning p = load_partition(path, n);
+        std::memcpy(assignment, p.assignment.data(), sizeof(std::int32_t) * p.assignment.size());
+        *parts = p.num_parts;
+    });
+}
+
 double ref_inter_intra_ratio(const void* gp, const std::int32_t* assignment, std::int32_t parts) {
     const Graph& g = *static_cast<const Graph*>(gp);
     std::vector<std::int32_t> a(assignment, assignment + g.num_nodes);

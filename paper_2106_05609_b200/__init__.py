@@ -7,13 +7,14 @@ loudly when it has not been built.
 """
 from ._native import LIB_PATH, lib  # noqa: F401  (raises ImportError when unbuilt)
 from .graph import (BatchPlan, BatchSchedule, Graph, build_graph, graph_from_csr, make_batch_plan,  # noqa: F401
-                    partition_parts, synth_features, synth_pairs)
+                    load_partition, partition_parts, random_partition, save_partition, synth_features,
+                    synth_pairs)
 from .history import HistoryStore, Prefetcher, PrefetchHandle  # noqa: F401
 from .trainer import AdamConfig, GasTrainer, ModelSpec, TrainerOptions  # noqa: F401
 from .dp import DataParallelTrainer, epoch_order, step_plan  # noqa: F401
 
 __all__ = [
     "Graph", "build_graph", "graph_from_csr", "make_batch_plan", "BatchPlan", "BatchSchedule", "partition_parts",
-    "synth_pairs", "synth_features", "HistoryStore", "Prefetcher", "PrefetchHandle", "ModelSpec", "AdamConfig",
+    "synth_pairs", "synth_features", "save_partition", "load_partition", "random_partition", "HistoryStore", "Prefetcher", "PrefetchHandle", "ModelSpec", "AdamConfig",
     "TrainerOptions", "GasTrainer", "DataParallelTrainer", "epoch_order", "step_plan",
 ]

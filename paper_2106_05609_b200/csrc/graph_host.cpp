@@ -10,6 +10,11 @@
 // produced by exactly one thread in a fixed order.
 #include <omp.h>
 
+#include <cerrno>
+#include <cstdio>
+#include <cstdlib>
+#include <random>
+#include <string>
 #include <algorithm>
 #include <atomic>
 #include <cmath>
@@ -456,6 +461,90 @@ gasb_status gasb_plan_copy(gasb_schedule s, int32_t part, int32_t* extended, int
 gasb_status gasb_schedule_destroy(gasb_schedule s) {
     delete s;
     return GASB_OK;
+}
+
+/* save_partition (io.cpp:187-192): one "node part" line per node, node order. */
+gasb_status gasb_partition_save(const char* path, const int32_t* assignment, int32_t num_nodes) {
+    return guard([&] {
+        require(path && (assignment || num_nodes == 0), "save_partition: null argument");
+        std::FILE* f = std::fopen(path, "w");
+        if (!f) throw std::runtime_error(std::string("cannot write partition file: ") + path);
+        for (int32_t v = 0; v < num_nodes; ++v) std::fprintf(f, "%d %d\n", v, assignment[v]);
+        std::fclose(f);
+    });
+}
+
+/* load_partition (io.cpp:194-217): '#' comments and blank lines skipped, "node part" per
+ * line (later lines win), then partition_from_assignment (partition.cpp:314-328).
+ * runtime_error: unopenable file, malformed line, node out of range, negative part,
+ * unassigned node; invalid_argument: an empty part. */
+gasb_status gasb_partition_load(const char* path, int32_t num_nodes, int32_t* assignment, int32_t* num_parts) {
+    return guard([&] {
+        require(path && num_parts && (assignment || num_nodes == 0), "load_partition: null argument");
+        std::FILE* f = std::fopen(path, "r");
+        if (!f) throw std::runtime_error(std::string("cannot open partition file: ") + path);
+        std::vector<int32_t> a(static_cast<size_t>(num_nodes), -1);
+        int32_t max_part = -1;
+        std::string line;
+        size_t lineno = 0;
+        auto fail = [&](const char* what) {
+            std::fclose(f);
+            throw std::runtime_error(std::string(path) + ":" + std::to_string(lineno) + ": " + what);
+        };
+        char buf[4096];
+        while (std::fgets(buf, sizeof(buf), f)) {
+            line.assign(buf);
+            while (!line.empty() && line.back() != '\n' && std::fgets(buf, sizeof(buf), f)) line += buf;
+            ++lineno;
+            const size_t hash = line.find('#');
+            std::string body = hash == std::string::npos ? line : line.substr(0, hash);
+            if (body.find_first_not_of(" \t\r\n") == std::string::npos) continue;
+            long long node = 0, part = 0;
+            char* end = nullptr;
+            const char* p0 = body.c_str();
+            errno = 0;
+            node = std::strtoll(p0, &end, 10);
+            if (end == p0 || errno) fail("expected 'node_id part_id'");
+            const char* p1 = end;
+            part = std::strtoll(p1, &end, 10);
+            if (end == p1 || errno) fail("expected 'node_id part_id'");
+            if (node < 0 || node >= num_nodes) fail("node id out of range");
+            if (part < 0) fail("negative part id");
+            a[static_cast<size_t>(node)] = static_cast<int32_t>(part);
+            max_part = std::max(max_part, static_cast<int32_t>(part));
+        }
+        std::fclose(f);
+        for (int32_t v = 0; v < num_nodes; ++v)
+            if (a[v] < 0) throw std::runtime_error(std::string(path) + ": node " + std::to_string(v) + " unassigned");
+        std::vector<int64_t> count(static_cast<size_t>(max_part + 1), 0);
+        for (int32_t v : a) ++count[v];
+        for (int64_t c : count) require(c > 0, "partition_from_assignment: empty part");
+        std::copy(a.begin(), a.end(), assignment);
+        *num_parts = max_part + 1;
+    });
+}
+
+/* random_partition (partition.cpp:330-342): node order shuffled by Rng(derive_seed(seed,
+ * "rand")) (rng.hpp shuffle), node order[i] -> part i % num_parts. Bit-exact. */
+gasb_status gasb_random_partition(int32_t num_nodes, int32_t num_parts, uint64_t seed, int32_t* assignment) {
+    return guard([&] {
+        require(num_parts > 0, "random_partition: num_parts must be positive");
+        require(num_parts <= num_nodes, "random_partition: more parts than nodes");
+        require(assignment != nullptr, "random_partition: null argument");
+        std::vector<int32_t> order(static_cast<size_t>(num_nodes));
+        std::iota(order.begin(), order.end(), 0);
+        const uint64_t s = mix64(mix64(mix64(seed ^ mix64(0x72616e64ull)) ^ mix64(0)) ^ mix64(0));
+        std::mt19937_64 gen(s);
+        for (size_t i = order.size(); i > 1; --i) {  // Rng::shuffle / next_below (rng.hpp:40-61)
+            const uint64_t n = i, limit = ~uint64_t{0} - (~uint64_t{0} % n);
+            uint64_t x;
+            do {
+                x = gen();
+            } while (x >= limit);
+            std::swap(order[i - 1], order[x % n]);
+        }
+        for (size_t i = 0; i < order.size(); ++i) assignment[order[i]] = static_cast<int32_t>(i % num_parts);
+    });
 }
 
 }  // extern "C"

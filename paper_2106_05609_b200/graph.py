@@ -183,3 +183,24 @@ def partition_parts(assignment: np.ndarray, num_parts: int) -> list[np.ndarray]:
     order = np.argsort(a, kind="stable")
     bounds = np.searchsorted(a[order], np.arange(num_parts + 1))
     return [order[bounds[p]:bounds[p + 1]].astype(np.int32) for p in range(num_parts)]
+
+
+def save_partition(path: str, assignment) -> None:
+    """save_partition (io.cpp:187-192)."""
+    a = np.ascontiguousarray(assignment, dtype=np.int32)
+    check(lib.gasb_partition_save(str(path).encode(), ptr(a) if len(a) else None, len(a)))
+
+
+def load_partition(path: str, num_nodes: int) -> tuple[np.ndarray, int]:
+    """load_partition (io.cpp:194-217): (assignment, num_parts)."""
+    a = np.empty(num_nodes, np.int32)
+    k = i32()
+    check(lib.gasb_partition_load(str(path).encode(), int(num_nodes), ptr(a) if num_nodes else None, C.byref(k)))
+    return a, k.value
+
+
+def random_partition(num_nodes: int, num_parts: int, seed: int = 0) -> np.ndarray:
+    """random_partition (partition.cpp:330-342), bit-exact with the reference."""
+    a = np.empty(num_nodes, np.int32)
+    check(lib.gasb_random_partition(int(num_nodes), int(num_parts), int(seed), ptr(a)))
+    return a
