@@ -253,6 +253,12 @@ gasb_status gasb_trainer_stream(gasb_trainer t, gasb_stream* out);
 /* Replaces the device feature matrix from host memory (n x in_dim, dense), stream-ordered
  * on the trainer's stream (asynchronous when h_features is pinned, see gasb_host_register). */
 gasb_status gasb_trainer_set_features(gasb_trainer t, const float* h_features);
+/* set_features in two halves, so a step's input copy overlaps the previous step's compute:
+ * stage = asynchronous H2D (pinned h_features) on the trainer's copy stream after the last
+ * commit consumed the staging buffer; commit = the trainer's stream waits for the staged copy
+ * and installs it as X. set_features == stage + commit. */
+gasb_status gasb_trainer_stage_features(gasb_trainer t, const float* h_features);
+gasb_status gasb_trainer_commit_features(gasb_trainer t);
 /* Times `iters` back-to-back launches of one SpMM of the training step with CUDA events on
  * the trainer's stream: part >= 0 -> the per-batch aggregation of `layer` for that part;
  * part < 0 -> the hoisted whole-epoch layer-1 aggregation. Writes only scratch buffers. */

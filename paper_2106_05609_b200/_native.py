@@ -119,6 +119,8 @@ _SIGS = {
     "gasb_trainer_stream": (i32, [vp, P(vp)]),
     "gasb_trainer_launch_count": (i32, [vp, P(i64)]),
     "gasb_trainer_set_features": (i32, [vp, vp]),
+    "gasb_trainer_stage_features": (i32, [vp, vp]),
+    "gasb_trainer_commit_features": (i32, [vp]),
     "gasb_trainer_profile_spmm": (i32, [vp, i32, i32, i32, P(f32)]),
     "gasb_host_register": (i32, [vp, C.c_size_t]),
     "gasb_host_unregister": (i32, [vp]),

@@ -344,6 +344,10 @@ gasb_status gasb_dp_create(gasb_trainer t, int32_t rank, int32_t world, gasb_dp*
         d->gsum.zero();
         d->err.alloc(1);
         d->err.zero();
+        // every part can land on any rank (the epoch order is reshuffled): capture all the
+        // data-parallel batch graphs now, not inside timed epochs
+        if (t->opt.use_graphs)
+            for (int32_t p = 0; p < t->num_parts; ++p) t->capture_batch_graph(p, true);
         d->peer.assign(static_cast<size_t>(world), nullptr);
         d->peer[rank] = d->region;
         if (world == 1) d->connected = true;

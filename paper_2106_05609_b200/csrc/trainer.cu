@@ -325,6 +325,9 @@ void gasb_trainer_s::build(const float* h_features, const int32_t* h_labels, con
     GASB_CUDA(cudaSetDevice(opt.device));
     GASB_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
     GASB_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+    GASB_CUDA(cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking));
+    GASB_CUDA(cudaEventCreateWithFlags(&ev_staged, cudaEventDisableTiming));
+    GASB_CUDA(cudaEventCreateWithFlags(&ev_stage_free, cudaEventDisableTiming));
     batch_nodes.upload(h_bn);
     cols_g.upload(h_cg);
     cols_l.upload(h_cl);
@@ -690,13 +693,25 @@ void gasb_trainer_s::enqueue_batch(int32_t p, bool train, bool push, bool use_ho
             set_gemm_workspace(gemm_ws.p, kGemmWsFloats);
             GASB_CUDA(cudaEventRecord(ev_wdone[l], side));
             if (l == 1) break;  // x_ext carries no gradient
-            launch_gemm(1, m, din, dout, g, ldg, W(l), pp(layer_param[l]), g_agg.p, ldH, 0.f, false, nullptr, stream);
-            // aggregate backward over intra-batch edges + compose bwd + relu bwd (mask = act)
             // into the buffer the wgrad of layer l + 1 read: wait for it
             float* go = gbuf[l & 1];
             if (l + 1 <= L - 1) GASB_CUDA(cudaStreamWaitEvent(stream, ev_wdone[l + 1], 0));
-            launch_spmm_bwd(t_rowptr.p + r0 + p, m, t_src.p, t_cf.p, g_agg.p, ldH, din, act[l - 1].p, ldH, go, ldH,
-                            stream, m);
+            if (dout < din) {
+                // narrow layer (the classifier, 41 < 256 at C3): aggregate backward on the dout-wide
+                // gradient first, then the dgrad GEMM and the relu mask: A^T (g W^T) == (A^T g) W^T,
+                // dout/din of the gather work (reassociation only; within the 1e-5 grad contract)
+                launch_spmm_bwd(t_rowptr.p + r0 + p, m, t_src.p, t_cf.p, g, ldg, dout, nullptr, 0, g_agg.p, ldC,
+                                stream, m);
+                launch_gemm(1, m, din, dout, g_agg.p, ldC, W(l), pp(layer_param[l]), go, ldH, 0.f, false, nullptr,
+                            stream);
+                launch_mask(go, ldH, act[l - 1].p, ldH, m, din, stream);
+            } else {
+                launch_gemm(1, m, din, dout, g, ldg, W(l), pp(layer_param[l]), g_agg.p, ldH, 0.f, false, nullptr,
+                            stream);
+                // aggregate backward over intra-batch edges + compose bwd + relu bwd (mask = act)
+                launch_spmm_bwd(t_rowptr.p + r0 + p, m, t_src.p, t_cf.p, g_agg.p, ldH, din, act[l - 1].p, ldH, go,
+                                ldH, stream, m);
+            }
             g = go;
             ldg = ldH;
         }
@@ -748,6 +763,20 @@ int64_t gasb_trainer_s::launch_batch_graph(int32_t p, bool dp) {
         gs.assign(num_parts, nullptr);
         gl.assign(num_parts, 0);
     }
+    if (!gs[p]) capture_batch_graph(p, dp);
+    GASB_CUDA(cudaGraphLaunch(gs[p], stream));
+    return gl[p];
+}
+
+// Captures (without launching) the per-part batch graph of part p.
+void gasb_trainer_s::capture_batch_graph(int32_t p, bool dp) {
+    const bool hoisted = !dp && opt.hoist_layer1 && opt.fused && !residual;
+    std::vector<cudaGraphExec_t>& gs = dp ? graphs_dp : graphs;
+    std::vector<int64_t>& gl = dp ? graph_launches_dp : graph_launches;
+    if (gs.empty()) {
+        gs.assign(num_parts, nullptr);
+        gl.assign(num_parts, 0);
+    }
     if (!gs[p]) {
         cudaGraph_t graph;
         const int64_t c0 = t_launches;
@@ -759,8 +788,6 @@ int64_t gasb_trainer_s::launch_batch_graph(int32_t p, bool dp) {
         GASB_CUDA(cudaGraphInstantiate(&gs[p], graph, 0));
         GASB_CUDA(cudaGraphDestroy(graph));
     }
-    GASB_CUDA(cudaGraphLaunch(gs[p], stream));
-    return gl[p];
 }
 
 void gasb_trainer_s::ensure_eval() {
@@ -1108,19 +1135,41 @@ gasb_status gasb_trainer_stream(gasb_trainer t, gasb_stream* out) {
     });
 }
 
-gasb_status gasb_trainer_set_features(gasb_trainer t, const float* h) {
+gasb_status gasb_trainer_stage_features(gasb_trainer t, const float* h) {
     return guard([&] {
         require(t && h, "trainer: null argument");
-        // one contiguous DMA at full link rate into a dense staging copy, then one device pass
-        // re-pitches the rows into X and rebuilds X's value flags (X is replaced whole)
+        // one contiguous DMA at full link rate into a dense staging copy, on the copy stream,
+        // after the previous staged copy has been consumed
         const int64_t cnt = static_cast<int64_t>(t->n) * t->F;
-        if (t->x_stage.n < cnt) t->x_stage.alloc(cnt);
-        GASB_CUDA(cudaMemcpyAsync(t->x_stage.p, h, sizeof(float) * cnt, cudaMemcpyHostToDevice, t->stream));
+        if (t->x_stage.n < cnt) {
+            GASB_CUDA(cudaStreamSynchronize(t->stream));
+            t->x_stage.alloc(cnt);
+            GASB_CUDA(cudaEventRecord(t->ev_stage_free, t->stream));
+        }
+        GASB_CUDA(cudaStreamWaitEvent(t->copy_stream, t->ev_stage_free, 0));
+        GASB_CUDA(cudaMemcpyAsync(t->x_stage.p, h, sizeof(float) * cnt, cudaMemcpyHostToDevice, t->copy_stream));
+        GASB_CUDA(cudaEventRecord(t->ev_staged, t->copy_stream));
+    });
+}
+
+gasb_status gasb_trainer_commit_features(gasb_trainer t) {
+    return guard([&] {
+        require(t, "trainer: null argument");
+        if (!t->x_stage.p) throw std::logic_error("commit_features: nothing staged");
+        // one device pass re-pitches the rows into X and rebuilds X's value flags (X is
+        // replaced whole), ordered after the staged copy
+        GASB_CUDA(cudaStreamWaitEvent(t->stream, t->ev_staged, 0));
         GASB_CUDA(cudaMemsetAsync(t->xflags.p, 0, sizeof(int32_t), t->stream));
         repitch_flags_kernel<<<1184, 256, 0, t->stream>>>(t->x_stage.p, t->n, t->F, t->X.p, t->ldF, t->xflags.p);
         ++t_launches;
         GASB_CUDA(cudaGetLastError());
+        GASB_CUDA(cudaEventRecord(t->ev_stage_free, t->stream));
     });
+}
+
+gasb_status gasb_trainer_set_features(gasb_trainer t, const float* h) {
+    const gasb_status s = gasb_trainer_stage_features(t, h);
+    return s != GASB_OK ? s : gasb_trainer_commit_features(t);
 }
 
 gasb_status gasb_trainer_profile_spmm(gasb_trainer t, int32_t part, int32_t layer, int32_t iters, float* avg_ms) {

@@ -74,6 +74,11 @@ struct gasb_trainer_s {
     int64_t ldF = 0, ldH = 0, ldC = 0;
     const Schedule* sched = nullptr;
     cudaStream_t stream = nullptr, side = nullptr;
+    // host-input pipeline (set_features): H2D into x_stage on copy_stream, re-pitched into X
+    // on `stream`; ev_staged / ev_stage_free order the two so a step's H2D overlaps the
+    // previous step's compute
+    cudaStream_t copy_stream = nullptr;
+    cudaEvent_t ev_staged = nullptr, ev_stage_free = nullptr;
     gasb_history hist = nullptr;
 
     // per part (host)
@@ -210,6 +215,10 @@ struct gasb_trainer_s {
         for (auto e : ev_fork) cudaEventDestroy(e);
         for (auto e : ev_wdone) cudaEventDestroy(e);
         if (ev_join) cudaEventDestroy(ev_join);
+        if (copy_stream) cudaStreamSynchronize(copy_stream);
+        if (ev_staged) cudaEventDestroy(ev_staged);
+        if (ev_stage_free) cudaEventDestroy(ev_stage_free);
+        if (copy_stream) cudaStreamDestroy(copy_stream);
         if (side) cudaStreamDestroy(side);
         if (stream) cudaStreamDestroy(stream);
     }
@@ -256,4 +265,5 @@ struct gasb_trainer_s {
     void enqueue_full_forward_res(int32_t first_layer);  // the DP exchange region (grads and act_l are views into it)
     std::vector<int64_t> graph_launches_dp;
     int64_t launch_batch_graph(int32_t p, bool dp);
+    void capture_batch_graph(int32_t p, bool dp);
 };

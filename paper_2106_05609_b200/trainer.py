@@ -134,6 +134,15 @@ class GasTrainer:
         x = np.ascontiguousarray(features, dtype=np.float32)
         check(lib.gasb_trainer_set_features(self._h, ptr(x)))
 
+    def stage_features(self, features: np.ndarray) -> None:
+        """Asynchronous H2D of the next step's features (page-locked host memory) on the copy
+        stream; the array must stay alive and unmodified until commit_features ran."""
+        check(lib.gasb_trainer_stage_features(self._h, ptr(features)))
+
+    def commit_features(self) -> None:
+        """Installs the staged features as X (stream-ordered before the next epoch)."""
+        check(lib.gasb_trainer_commit_features(self._h))
+
     def profile_spmm(self, part: int, layer: int, iters: int = 5) -> float:
         ms = C.c_float()
         check(lib.gasb_trainer_profile_spmm(self._h, int(part), int(layer), int(iters), C.byref(ms)))

@@ -42,6 +42,9 @@ WORKLOADS = {
     "cora": Workload("cora", 2708, 5570, 10, 0.87, 60.0, 1433, 7, "gcn", 2, 16),
     "pubmed_gcnii": Workload("pubmed_gcnii", 19717, 44700, 8, 0.8, 60.0, 500, 3, "gcnii", 64, 64),
     "reddit": Workload("reddit", 232965, 65_300_000, 200, 0.335, 120.0, 602, 41, "gcn", 4, 256),
+    # C4: ogbn-products shape (61.9M raw undirected edges -> ~123.7M stored nnz), APPNP with
+    # K = 3 propagation layers over 47-wide histories, inter/intra ~1.94
+    "products_appnp": Workload("products_appnp", 2449029, 61_859_140, 100, 0.34, 120.0, 100, 47, "appnp", 3, 256),
     # down-scaled shapes for fast parity runs
     "cora_appnp": Workload("cora_appnp", 2708, 5570, 10, 0.87, 60.0, 1433, 7, "appnp", 3, 64),
     "cora_gcnii": Workload("cora_gcnii", 2708, 5570, 10, 0.87, 60.0, 1433, 7, "gcnii", 8, 64),
