@@ -45,11 +45,19 @@ constexpr int kThreads = 192;
 // The tensor core's fp32 accumulation truncates, so its error grows linearly with the number
 // of k-steps; k-steps are interleaved over kAcc TMEM accumulators (kAcc * BN <= 512 columns)
 // summed round-to-nearest in the epilogue, cutting that growth kAcc-fold.
-template <int BN>
+// TALL variant (many output tiles, short K: e.g. the APPNP/GCNII heads over every V_b row):
+// 2 stages and 4 accumulators so two CTAs share an SM (shared memory and TMEM), overlapping
+// one CTA's epilogue with the other's mainloop.
+template <int BN, bool TALL = false>
 struct Acc {
-    static constexpr int kAcc = 512 / BN < 8 ? 512 / BN : 8;
+    static constexpr int kMax = TALL ? 4 : 8;
+    static constexpr int kAcc = 512 / BN < kMax ? 512 / BN : kMax;
     static constexpr int kCols = kAcc * BN;  // TMEM allocation (power of two)
 };
+template <bool TALL>
+constexpr int stages_of() {
+    return TALL ? 2 : kStagesTC;
+}
 
 __device__ __forceinline__ uint32_t su32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
 
@@ -116,29 +124,26 @@ __device__ __forceinline__ float tf32_hi(float x) {
     return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
 }
 
-template <int BN, bool A_MN, bool B_MN>
+template <int BN, bool A_MN, bool B_MN, bool TALL = false>
 struct Layout {
+    static constexpr int kStages = stages_of<TALL>();
     static constexpr int kTileA = BM * BK * 4;  // bytes (16 KB)
     static constexpr int kTileB = BN * BK * 4;
     // stage: A, A_lo, B, B_lo (each 1024 B aligned: SW128 atoms)
     static constexpr int kStage = 2 * kTileA + 2 * kTileB;
-    static constexpr int kBars = 8 * (3 * kStagesTC + 1);
-    static constexpr int kSmem = 1024 + kStagesTC * kStage + kBars + 16;
+    static constexpr int kBars = 8 * (3 * kStages + 1);
+    static constexpr int kSmem = 1024 + kStages * kStage + kBars + 16;
 };
 
-// shared int next to the TMEM slot (after the mbarriers): the split-K "last CTA" flag
-__device__ __forceinline__ int* tmem_slot_flag(uint64_t* bars) {
-    return reinterpret_cast<int*>(bars + 3 * kStagesTC + 1) + 1;
-}
-
-template <int BN, bool A_MN, bool B_MN>
-__global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_constant__ CUtensorMap tma_a,
+template <int BN, bool A_MN, bool B_MN, bool TALL>
+__global__ void __launch_bounds__(kThreads, TALL ? 2 : 1) gemm_tc_kernel(const __grid_constant__ CUtensorMap tma_a,
                                                              const __grid_constant__ CUtensorMap tma_b, int M,
                                                              int N, int K, float* __restrict__ C, int64_t ldc,
                                                              GemmEpilogue ep, int kbs, float* __restrict__ ws,
                                                              int64_t ws_floats) {
     const PushEpilogue& push = ep.push;
-    using Lay = Layout<BN, A_MN, B_MN>;
+    using Lay = Layout<BN, A_MN, B_MN, TALL>;
+    constexpr int kStagesTC = Lay::kStages;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* base = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~1023ull);
     uint64_t* bars = reinterpret_cast<uint64_t*>(base + kStagesTC * Lay::kStage);
@@ -166,7 +171,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
     }
     if (warp == 0) {  // TMEM: BN fp32 columns x 128 lanes
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(su32(tmem_slot)),
-                     "r"(Acc<BN>::kCols));
+                     "r"(Acc<BN, TALL>::kCols));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
     }
     asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
@@ -224,8 +229,8 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
                     const uint64_t bhi = smem_desc(sb + offb, lbob, sbob, lyb);
                     const uint64_t blo = smem_desc(sb_lo + offb, lbob, sbob, lyb);
                     const int g = kb * (BK / 8) + kk;  // global k-step -> accumulator g % kAcc
-                    const uint32_t d = tmem + static_cast<uint32_t>((g % Acc<BN>::kAcc) * BN);
-                    const uint32_t first = g < Acc<BN>::kAcc ? 0u : 1u;
+                    const uint32_t d = tmem + static_cast<uint32_t>((g % Acc<BN, TALL>::kAcc) * BN);
+                    const uint32_t first = g < Acc<BN, TALL>::kAcc ? 0u : 1u;
                     mma_tf32(d, ahi, bhi, idesc, first);
                     mma_tf32(d, ahi, blo, idesc, 1u);
                     mma_tf32(d, alo, bhi, idesc, 1u);
@@ -272,7 +277,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
         }
         int32_t flags = 0;
         const int nsteps = nk * (BK / 8);
-        const int nacc = nsteps < Acc<BN>::kAcc ? nsteps : Acc<BN>::kAcc;  // accumulators written
+        const int nacc = nsteps < Acc<BN, TALL>::kAcc ? nsteps : Acc<BN, TALL>::kAcc;  // accumulators written
 #pragma unroll 1
         for (int c0 = 0; c0 < BN; c0 += 32) {
             float sum[32];
@@ -301,15 +306,35 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
                 for (int j = 0; j < 32; j += 4)
                     if (n0 + c0 + j < Np) wrow[(n0 + c0 + j) >> 2] = make_float4(sum[j], sum[j + 1], sum[j + 2], sum[j + 3]);
             } else if (crow) {
+                // 16 B stores where the row pitch allows (a thread owns one output row: scalar
+                // stores would cost one instruction per 4 B)
+                const bool v4 = ((ldc & 3) == 0) && ((reinterpret_cast<uintptr_t>(C) & 15) == 0) &&
+                                (!prow || ((push.ld & 3) == 0 && (reinterpret_cast<uintptr_t>(push.table) & 15) == 0));
 #pragma unroll
-                for (int j = 0; j < 32; ++j) {
+                for (int j = 0; j < 32; j += 4) {
                     const int col = n0 + c0 + j;
-                    if (col < N) {
-                        const float x = gemm_epilogue_value(ep, sum[j], crow, col);
-                        crow[col] = x;
+                    if (v4 && col + 3 < N) {
+                        float4 x;
+                        x.x = gemm_epilogue_value(ep, sum[j], crow, col);
+                        x.y = gemm_epilogue_value(ep, sum[j + 1], crow, col + 1);
+                        x.z = gemm_epilogue_value(ep, sum[j + 2], crow, col + 2);
+                        x.w = gemm_epilogue_value(ep, sum[j + 3], crow, col + 3);
+                        *reinterpret_cast<float4*>(crow + col) = x;
                         if (prow) {
-                            prow[col] = x;
-                            flags |= table_flag_of(x);
+                            *reinterpret_cast<float4*>(prow + col) = x;
+                            flags |= table_flag_of(x.x) | table_flag_of(x.y) | table_flag_of(x.z) | table_flag_of(x.w);
+                        }
+                        continue;
+                    }
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        if (col + q < N) {
+                            const float x = gemm_epilogue_value(ep, sum[j + q], crow, col + q);
+                            crow[col + q] = x;
+                            if (prow) {
+                                prow[col + q] = x;
+                                flags |= table_flag_of(x);
+                            }
                         }
                     }
                 }
@@ -324,7 +349,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
             asm volatile("bar.sync 1, 128;\n" ::: "memory");
             if (warp == 0) {
                 asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem),
-                             "r"(Acc<BN>::kCols));
+                             "r"(Acc<BN, TALL>::kCols));
             }
             const int S = static_cast<int>(gridDim.z);
             int* arrive = reinterpret_cast<int*>(ws + ws_floats) + 2 * (blockIdx.y * gridDim.x + blockIdx.x);
@@ -382,7 +407,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
     __syncthreads();
     if (warp == 0 && !ws) {  // (split-K CTAs freed their TMEM before the fixup)
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(Acc<BN>::kCols));
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(Acc<BN, TALL>::kCols));
     }
 }
 
@@ -411,10 +436,10 @@ static bool make_tmap(const float* p, int64_t inner, int64_t outer, int64_t ld, 
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int BN, bool A_MN, bool B_MN>
+template <int BN, bool A_MN, bool B_MN, bool TALL = false>
 static bool launch_tc(int m, int n, int k, const float* a, int64_t lda, const float* b, int64_t ldb, float* c,
                       int64_t ldc, const GemmEpilogue& ep, cudaStream_t st) {
-    using Lay = Layout<BN, A_MN, B_MN>;
+    using Lay = Layout<BN, A_MN, B_MN, TALL>;
     CUtensorMap ta, tb;
     // A: K-major -> inner K, outer M (box 32 x 128); MN-major -> inner M, outer K (box 32 x 32)
     const bool ok_a = A_MN ? make_tmap(a, m, k, lda, BK, &ta, true) : make_tmap(a, k, m, lda, BM, &ta, false);
@@ -422,7 +447,7 @@ static bool launch_tc(int m, int n, int k, const float* a, int64_t lda, const fl
     if (!ok_a || !ok_b) return false;  // pitch not 16 B aligned: caller uses the SIMT kernel
     static bool attr = false;
     if (!attr) {
-        GASB_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<BN, A_MN, B_MN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        GASB_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<BN, A_MN, B_MN, TALL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        Lay::kSmem));
         attr = true;
     }
@@ -430,7 +455,7 @@ static bool launch_tc(int m, int n, int k, const float* a, int64_t lda, const fl
     const int64_t tiles = ceil_div(m, BM) * ceil_div(n, BN);
     const int nkb = static_cast<int>(ceil_div(k, BK));
     int S = 1;
-    if (t_gemm_ws && tiles < num_sms()) {
+    if (!TALL && t_gemm_ws && tiles < num_sms()) {
         S = static_cast<int>(std::min<int64_t>(num_sms() / tiles, std::max(1, nkb / 2)));
         while (S > 1 && static_cast<int64_t>(S) * m * round_up(n, 4) > t_gemm_ws_floats) --S;
         if (2 * tiles > kGemmTileCounters) S = 1;
@@ -438,7 +463,7 @@ static bool launch_tc(int m, int n, int k, const float* a, int64_t lda, const fl
     const int kbs = static_cast<int>(ceil_div(nkb, S));
     S = static_cast<int>(ceil_div(nkb, kbs));  // no empty slices
     dim3 grid(static_cast<unsigned>(ceil_div(m, BM)), static_cast<unsigned>(ceil_div(n, BN)), static_cast<unsigned>(S));
-    gemm_tc_kernel<BN, A_MN, B_MN><<<grid, kThreads, Lay::kSmem, st>>>(ta, tb, m, n, k, c, ldc, ep, kbs,
+    gemm_tc_kernel<BN, A_MN, B_MN, TALL><<<grid, kThreads, Lay::kSmem, st>>>(ta, tb, m, n, k, c, ldc, ep, kbs,
                                                                         S > 1 ? t_gemm_ws : nullptr,
                                                                         t_gemm_ws_floats);
     return true;
@@ -452,6 +477,20 @@ bool launch_gemm_tc(int op, int m, int n, int k, const float* a, int64_t lda, co
                     int64_t ldc, const GemmEpilogue& ep, cudaStream_t st) {
     if (m <= 0 || n <= 0) return true;
     bool ok;
+    // many tiles with a short K (the residual heads over every V_b row): two CTAs per SM
+    const bool tall = ceil_div(m, tc::BM) * ceil_div(n, 64) >= 2LL * num_sms() && k <= 16 * tc::BK;
+    if (tall && n > 32) {
+        switch (op) {
+            case 0: ok = tc::launch_tc<64, false, true, true>(m, n, k, a, lda, b, ldb, c, ldc, ep, st); break;
+            case 1: ok = tc::launch_tc<64, false, false, true>(m, n, k, a, lda, b, ldb, c, ldc, ep, st); break;
+            case 2: ok = tc::launch_tc<64, true, true, true>(m, n, k, a, lda, b, ldb, c, ldc, ep, st); break;
+            default: throw std::invalid_argument("gemm: op must be 0, 1 or 2");
+        }
+        if (!ok) return false;
+        ++t_launches;
+        GASB_CUDA(cudaGetLastError());
+        return true;
+    }
     // narrow N tiles keep enough CTAs in flight for the ~1K-row batch GEMMs
     switch (op) {
         case 0:

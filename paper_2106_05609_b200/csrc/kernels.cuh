@@ -158,6 +158,9 @@ void launch_mix_bwd(const float* dmix, int64_t ldd, int32_t m, int32_t d, float 
                     float* h0g, int64_t ldh, float* dprop, int64_t ldp, cudaStream_t st);
 // out[j] = float(sum_i double(g[i, j]))
 void launch_colsum(const float* g, int64_t ldg, int32_t m, int32_t n, float* out, cudaStream_t st);
+// fp64 row-block partials for launch_colsum on this host thread (nullptr: single-level sum)
+void set_colsum_workspace(double* ws, int64_t doubles);
+constexpr int64_t kColsumWsDoubles = 148LL * 8 * 1024;
 // g = mask > 0 ? g : 0
 void launch_mask(float* g, int64_t ldg, const float* mask, int64_t ldm, int32_t m, int32_t n, cudaStream_t st);
 

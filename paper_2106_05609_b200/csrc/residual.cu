@@ -96,12 +96,12 @@ __global__ void __launch_bounds__(256) colsum_kernel(const float* __restrict__ g
 // g = mask > 0 ? g : 0 (relu backward, tensor.cpp:363-369), in place.
 __global__ void mask_kernel(float* __restrict__ g, int64_t ldg, const float* __restrict__ mask, int64_t ldm,
                             int32_t m, int32_t n) {
-    const int64_t total = static_cast<int64_t>(m) * n;
-    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
-         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const int64_t r = i / n, c = i - r * n;
-        if (!(mask[r * ldm + c] > 0.0f)) g[r * ldg + c] = 0.0f;
-    }
+    // one warp per row (grid-stride), lanes across the columns: no per-element division
+    const int lane = threadIdx.x & 31;
+    for (int64_t r = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; r < m;
+         r += (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5)
+        for (int32_t c = lane; c < n; c += 32)
+            if (!(mask[r * ldm + c] > 0.0f)) g[r * ldg + c] = 0.0f;
 }
 
 unsigned grid_for(int64_t work, int threads) {
@@ -140,10 +140,60 @@ void launch_mix_bwd(const float* dmix, int64_t ldd, int32_t m, int32_t d, float 
     GASB_CUDA(cudaGetLastError());
 }
 
+// Two-level column sum for tall inputs (APPNP/GCNII heads run over every V_b row: 585K rows
+// at C4): CTA (x, y) sums rows y, y + R, ... of its 32 columns in fp64 (8 warps, fixed order),
+// then one thread per column adds the R row-block partials in order. Deterministic.
+__global__ void __launch_bounds__(256) colsum_partial_kernel(const float* __restrict__ g, int64_t ldg, int32_t m,
+                                                             int32_t n, double* __restrict__ part) {
+    __shared__ double sp[8][33];
+    const int cx = threadIdx.x & 31, ry = threadIdx.x >> 5;
+    const int32_t col = blockIdx.x * 32 + cx;
+    const int32_t R = gridDim.y;
+    double acc = 0.0;
+    if (col < n)
+        for (int64_t i = static_cast<int64_t>(blockIdx.y) + static_cast<int64_t>(ry) * R; i < m;
+             i += static_cast<int64_t>(8) * R)
+            acc += static_cast<double>(g[i * ldg + col]);
+    sp[ry][cx] = acc;
+    __syncthreads();
+    if (ry == 0 && col < n) {
+        double s = sp[0][cx];
+        for (int k = 1; k < 8; ++k) s += sp[k][cx];
+        part[static_cast<int64_t>(blockIdx.y) * n + col] = s;
+    }
+}
+
+__global__ void colsum_finish_kernel(const double* __restrict__ part, int32_t R, int32_t n, float* __restrict__ out) {
+    const int32_t col = blockIdx.x * blockDim.x + threadIdx.x;
+    if (col >= n) return;
+    double s = 0.0;
+    for (int32_t r = 0; r < R; ++r) s += part[static_cast<int64_t>(r) * n + col];
+    out[col] = static_cast<float>(s);
+}
+
+thread_local double* t_colsum_ws = nullptr;
+thread_local int64_t t_colsum_ws_doubles = 0;
+void set_colsum_workspace(double* ws, int64_t doubles) {
+    t_colsum_ws = ws;
+    t_colsum_ws_doubles = ws ? doubles : 0;
+}
+
 void launch_colsum(const float* g, int64_t ldg, int32_t m, int32_t n, float* out, cudaStream_t st) {
     if (n <= 0) return;
-    colsum_kernel<<<static_cast<unsigned>(ceil_div(n, 32)), 256, 0, st>>>(g, ldg, m, n, out);
-    ++t_launches;
+    const int64_t cb = ceil_div(n, 32);
+    int64_t R = std::min<int64_t>(ceil_div(m, 2048), std::max<int64_t>(1, 148 * 8 / cb));
+    if (t_colsum_ws) R = std::min<int64_t>(R, t_colsum_ws_doubles / n);
+    if (R <= 1 || !t_colsum_ws) {
+        colsum_kernel<<<static_cast<unsigned>(cb), 256, 0, st>>>(g, ldg, m, n, out);
+        ++t_launches;
+        GASB_CUDA(cudaGetLastError());
+        return;
+    }
+    colsum_partial_kernel<<<dim3(static_cast<unsigned>(cb), static_cast<unsigned>(R)), 256, 0, st>>>(g, ldg, m, n,
+                                                                                                  t_colsum_ws);
+    colsum_finish_kernel<<<static_cast<unsigned>(ceil_div(n, 128)), 128, 0, st>>>(t_colsum_ws,
+                                                                                 static_cast<int32_t>(R), n, out);
+    t_launches += 2;
     GASB_CUDA(cudaGetLastError());
 }
 

@@ -430,6 +430,7 @@ void gasb_trainer_s::build(const float* h_features, const int32_t* h_labels, con
     g_out.alloc(static_cast<int64_t>(nb_max) * ldH);
     loss.alloc(num_parts);
     loss.zero();
+    if (residual) colsum_ws.alloc(kColsumWsDoubles);
     gemm_ws.alloc(kGemmWsFloats + kGemmTileCounters);  // split-K slices + tile counters
     gemm_ws.zero();
     if (!residual) {
@@ -612,7 +613,7 @@ void gasb_trainer_s::enqueue_batch_res(int32_t p, bool train, bool push, bool fu
 }
 
 void gasb_trainer_s::enqueue_batch(int32_t p, bool train, bool push, bool use_hoisted, bool fused, bool dp) {
-    WsGuard ws(gemm_ws);
+    WsGuard ws(gemm_ws, &colsum_ws);
     if (residual) {
         enqueue_batch_res(p, train, push, fused, dp);
         return;
@@ -820,7 +821,7 @@ void gasb_trainer_s::ensure_eval() {
 // gathering the previous layer's table by global id. first_layer = L: infer_from_history's
 // final layer over H_{L-1} (trainer.cpp:512-520).
 void gasb_trainer_s::enqueue_full_forward(int32_t first_layer) {
-    WsGuard ws(gemm_ws);
+    WsGuard ws(gemm_ws, &colsum_ws);
     const SpmmSegs segs = seg_all.segs(0);
     const int64_t R = row_off[num_parts];
     GASB_CUDA(cudaMemsetAsync(eval_flags.p, 0, 2 * sizeof(int32_t), stream));
@@ -856,7 +857,7 @@ void gasb_trainer_s::enqueue_full_forward(int32_t first_layer) {
 // h0[v] (-> GCNII: relu(mixed . W~_l)) -> scatter into the next layer's table; GCNII's
 // output head on the last layer (trainer.cpp:142-163, :221-227; layers.cpp:150-168).
 void gasb_trainer_s::enqueue_full_forward_res(int32_t first_layer) {
-    WsGuard ws(gemm_ws);
+    WsGuard ws(gemm_ws, &colsum_ws);
     const SpmmSegs segs = seg_all.segs(0);
     const int64_t R = row_off[num_parts];
     const bool gcnii = spec.kind == 3;

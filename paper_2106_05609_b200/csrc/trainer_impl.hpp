@@ -146,9 +146,16 @@ struct gasb_trainer_s {
     DevBuf<float> gemm_ws2, g_out2;
     std::vector<cudaEvent_t> ev_fork, ev_wdone;
     cudaEvent_t ev_join = nullptr;
-    struct WsGuard {        // scopes the thread's GEMM workspace to one enqueue
-        explicit WsGuard(DevBuf<float>& w) { set_gemm_workspace(w.p, kGemmWsFloats); }
-        ~WsGuard() { set_gemm_workspace(nullptr, 0); }
+    DevBuf<double> colsum_ws;  // row-block partials of the bias-gradient column sums
+    struct WsGuard {        // scopes the thread's GEMM / column-sum workspaces to one enqueue
+        explicit WsGuard(DevBuf<float>& w, DevBuf<double>* c = nullptr) {
+            set_gemm_workspace(w.p, kGemmWsFloats);
+            if (c && c->p) set_colsum_workspace(c->p, c->n);
+        }
+        ~WsGuard() {
+            set_gemm_workspace(nullptr, 0);
+            set_colsum_workspace(nullptr, 0);
+        }
     };
 
     // ---- residual models: APPNP (kind 2) / GCNII (kind 3) ----

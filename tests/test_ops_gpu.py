@@ -118,7 +118,8 @@ def _padded(torch, a, ld):
 
 
 @pytest.mark.parametrize("pad", [False, True])
-@pytest.mark.parametrize("m,k,n", [(1165, 602, 256), (1165, 256, 41), (271, 1433, 16), (37, 5, 3), (300, 64, 96)])
+@pytest.mark.parametrize("m,k,n", [(1165, 602, 256), (1165, 256, 41), (271, 1433, 16), (37, 5, 3), (300, 64, 96),
+                                   (60000, 100, 256), (60000, 256, 47)])  # last two: TALL tiles, split-K wgrad
 def test_matmul_forward_backward(torch, oracle, m, k, n, pad):
     rng = np.random.default_rng(m + k + n)
     a = rng.standard_normal((m, k)).astype(np.float32)
