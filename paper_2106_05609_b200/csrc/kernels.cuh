@@ -58,6 +58,10 @@ struct SpmmSegs {
     const int32_t* row_nseg;  // per absolute row: number of segments
     const int32_t* range_seg; // nranges + 1 segment boundaries of this launch (split_ranges)
     int32_t nranges;
+    // 1: one fp64 chain per column in CSR order (the bit-exact sequential mode); 0: rows may
+    // be split anyway, so each row also runs two interleaved chains (even / odd edges of the
+    // stage) added at the row end — twice the independent DFMAs, same fp64 accuracy class
+    int32_t exact = 1;
 };
 // Host: splits segments [g0, g1) into nranges contiguous ranges of ~equal edges.
 void split_ranges(const int64_t* seg_beg, int64_t g0, int64_t g1, int32_t nranges, int32_t* out);

@@ -668,7 +668,7 @@ static int spmm_engine() {
 // (row) ends are handled inside the FMA loop — a stage with no segment end (the common
 // case: rows average hundreds of edges) runs the 16 FMAs straight. Same segments, ranges,
 // fp64 partials and accumulation order as the pipelined kernel (bit-identical results).
-template <int CPL, int MODE>
+template <int CPL, int MODE, bool DUAL>
 __device__ __forceinline__ void flat_items(
     const int64_t* __restrict__ seg_beg, const int32_t* __restrict__ seg_row, const int32_t* __restrict__ seg_slot,
     const int32_t* __restrict__ row_seg0, const int32_t* __restrict__ row_nseg, const int32_t* __restrict__ range_seg,
@@ -751,13 +751,20 @@ __device__ __forceinline__ void flat_items(
                 }
             }
         };
-        double acc[CPL];
+        double acc[CPL], acc2[CPL];  // acc2: odd stage edges when DUAL (added at the row end)
 #pragma unroll
-        for (int k = 0; k < CPL; ++k) acc[k] = 0.0;
+        for (int k = 0; k < CPL; ++k) acc[k] = acc2[k] = 0.0;
         auto finish = [&] {
             const int kk = cur - wseg;
             const int32_t row = __shfl_sync(0xffffffffu, w_row, kk);
             const int32_t slot = __shfl_sync(0xffffffffu, w_slot, kk);
+            if constexpr (DUAL) {
+#pragma unroll
+                for (int k = 0; k < CPL; ++k) {
+                    acc[k] = __dadd_rn(acc[k], acc2[k]);
+                    acc2[k] = 0.0;
+                }
+            }
             seg_finish<CPL>(acc, row, slot, lane, col, chunk, dim, y, ldy, row_base, partial, pld, counters, cld,
                             seg_slot, row_seg0, row_nseg);
             ++cur;
@@ -783,12 +790,21 @@ __device__ __forceinline__ void flat_items(
             const int64_t eb = e_lo + static_cast<int64_t>(b) * KE;
             const int cnt = static_cast<int>(e_hi - eb < KE ? e_hi - eb : KE);
             if (cnt == KE && cur_end >= eb + KE) {  // no segment ends inside: straight FMAs
+                if constexpr (DUAL) {
 #pragma unroll
-                for (int j = 0; j < KE; ++j) edge_fma<CPL, MODE>(rows, cf, j, acc);
+                    for (int j = 0; j < KE; j += 2) {
+                        edge_fma<CPL, MODE>(rows, cf, j, acc);
+                        edge_fma<CPL, MODE>(rows, cf, j + 1, acc2);
+                    }
+                } else {
+#pragma unroll
+                    for (int j = 0; j < KE; ++j) edge_fma<CPL, MODE>(rows, cf, j, acc);
+                }
             } else {
                 for (int j = 0; j < cnt; ++j) {
                     while (eb + j == cur_end && cur < s_hi) finish();
-                    edge_fma<CPL, MODE>(rows, cf, j, acc);
+                    if (DUAL && (j & 1)) edge_fma<CPL, MODE>(rows, cf, j, acc2);
+                    else edge_fma<CPL, MODE>(rows, cf, j, acc);
                 }
             }
             __syncwarp();
@@ -803,7 +819,7 @@ __device__ __forceinline__ void flat_items(
     }
 }
 
-template <int CPL>
+template <int CPL, bool DUAL>
 __global__ void __launch_bounds__(kPipeWarps * 32, kPipeCtas) spmm_fwd_flat_kernel(
     const int64_t* __restrict__ seg_beg, const int32_t* __restrict__ seg_row, const int32_t* __restrict__ seg_slot,
     const int32_t* __restrict__ row_seg0, const int32_t* __restrict__ row_nseg, const int32_t* __restrict__ range_seg,
@@ -828,7 +844,7 @@ __global__ void __launch_bounds__(kPipeWarps * 32, kPipeCtas) spmm_fwd_flat_kern
     __syncwarp();
     const int mode = widen_mode(table_flags);
 #define GASB_FLAT(M)                                                                                              \
-    flat_items<CPL, M>(seg_beg, seg_row, seg_slot, row_seg0, row_nseg, range_seg, nranges, cols, coeffs, dim, nchunks, \
+    flat_items<CPL, M, DUAL>(seg_beg, seg_row, seg_slot, row_seg0, row_nseg, range_seg, nranges, cols, coeffs, dim, nchunks, \
                   y, ldy, row_base, partial, pld, counters, cld, &tmap, wbase, bars, ring_c, ring_f)
     if (mode == kWidenNonNeg) GASB_FLAT(kWidenNonNeg);
     else if (mode == kWidenSigned) GASB_FLAT(kWidenSigned);
@@ -836,7 +852,7 @@ __global__ void __launch_bounds__(kPipeWarps * 32, kPipeCtas) spmm_fwd_flat_kern
 #undef GASB_FLAT
 }
 
-template <int CPL>
+template <int CPL, bool DUAL>
 static void launch_flat(const SpmmSegs& s, const int32_t* cols, const double* coeffs, int32_t dim, float* y,
                         int64_t ldy, int64_t row_base, double* partial, int64_t partial_ld, int32_t* counters,
                         int32_t counters_ld, cudaStream_t st, const int32_t* special, const CUtensorMap* tmap) {
@@ -844,7 +860,8 @@ static void launch_flat(const SpmmSegs& s, const int32_t* cols, const double* co
     constexpr int kSmem = Cfg::kSmem + kPipeWarps * kStages * 8 + kPipeWarps * kMetaRingBytes;
     static int set = 0;
     if (!set) {
-        GASB_CUDA(cudaFuncSetAttribute(spmm_fwd_flat_kernel<CPL>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
+        GASB_CUDA(cudaFuncSetAttribute(spmm_fwd_flat_kernel<CPL, DUAL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       kSmem));
         set = 1;
     }
     const int32_t nchunks = static_cast<int32_t>(ceil_div(dim, Cfg::kCols));
@@ -858,7 +875,7 @@ static void launch_flat(const SpmmSegs& s, const int32_t* cols, const double* co
     }
     const int64_t items = static_cast<int64_t>(nchunks) * s.nranges;
     const int64_t blocks = std::min<int64_t>(ceil_div(items, kPipeWarps), static_cast<int64_t>(kPipeCtas) * sms);
-    spmm_fwd_flat_kernel<CPL><<<static_cast<unsigned>(blocks), kPipeWarps * 32, kSmem, st>>>(
+    spmm_fwd_flat_kernel<CPL, DUAL><<<static_cast<unsigned>(blocks), kPipeWarps * 32, kSmem, st>>>(
         s.seg_beg, s.seg_row, s.seg_slot, s.row_seg0, s.row_nseg, s.range_seg, s.nranges, cols, coeffs, dim, nchunks,
         y, ldy, row_base, partial, partial_ld, counters, counters_ld, special, *tmap);
 }
@@ -1004,6 +1021,16 @@ void segment_launch(const int64_t* rp, int64_t r_lo, int64_t r_hi, bool split, i
 
 // Columns per lane of the pipelined SpMM (tuning knob GASB_SPMM_CPL = 2 | 4, default 4:
 // 128-column chunks, measured fastest on the Reddit-shaped workload).
+// Two interleaved fp64 chains per column in the segmented (non-exact) mode (GASB_SPMM_DUAL
+// = 1 enables; measured no faster at C3, so off by default).
+static bool spmm_dual() {
+    static int v = [] {
+        const char* e = getenv("GASB_SPMM_DUAL");
+        return e ? atoi(e) : 0;
+    }();
+    return v != 0;
+}
+
 static int spmm_cpl() {
     static int v = [] {
         const char* e = getenv("GASB_SPMM_CPL");
@@ -1039,12 +1066,17 @@ void launch_spmm_fwd(const SpmmSegs& s, const int32_t* cols, const double* coeff
     require(ldx % 4 == 0 && reinterpret_cast<uintptr_t>(x) % 16 == 0,
             "spmm_fwd: source rows must be 16 B aligned (ldx % 4 == 0)");
     if (spmm_engine() == 3 && tmap && spmm_use_tma()) {
-        if (spmm_cpl() == 2)
-            launch_flat<2>(s, cols, coeffs, dim, y, ldy, row_base, partial, partial_ld, counters, counters_ld, st,
-                           special, tmap);
-        else
-            launch_flat<4>(s, cols, coeffs, dim, y, ldy, row_base, partial, partial_ld, counters, counters_ld, st,
-                           special, tmap);
+#define GASB_FLAT_LAUNCH(C, D) \
+    launch_flat<C, D>(s, cols, coeffs, dim, y, ldy, row_base, partial, partial_ld, counters, counters_ld, st, special, tmap)
+        const bool dual = !s.exact && spmm_dual();
+        if (spmm_cpl() == 2) {
+            if (dual) GASB_FLAT_LAUNCH(2, true);
+            else GASB_FLAT_LAUNCH(2, false);
+        } else {
+            if (dual) GASB_FLAT_LAUNCH(4, true);
+            else GASB_FLAT_LAUNCH(4, false);
+        }
+#undef GASB_FLAT_LAUNCH
         ++t_launches;
         GASB_CUDA(cudaGetLastError());
         return;

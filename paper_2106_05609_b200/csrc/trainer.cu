@@ -78,6 +78,7 @@ void build_segments(const std::vector<int64_t>& rp, const std::vector<int64_t>& 
     t.group_seg0.assign(static_cast<size_t>(ngroups), 0);
     t.group_nseg.assign(static_cast<size_t>(ngroups), 0);
     t.nranges = spmm_ranges_per_launch();
+    t.split = split;
     std::vector<int32_t> rs(static_cast<size_t>(ngroups) * (t.nranges + 1));
     int64_t slot = 0;
     t.max_group_slots = 0;

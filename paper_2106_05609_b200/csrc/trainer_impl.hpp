@@ -55,11 +55,13 @@ struct SegTable {
     DevBuf<int32_t> seg_row, seg_slot, row_seg0, row_nseg;
     DevBuf<int32_t> ranges;  // per group: nranges + 1 work-range boundaries (split_ranges)
     int32_t nranges = 0;
+    bool split = false;  // rows cut at range boundaries (not the bit-exact sequential mode)
     std::vector<int64_t> group_seg0, group_nseg;  // per group (batch) range of segments
     int64_t max_group_slots = 0, total_slots = 0;
     SpmmSegs segs(int64_t g) const {
         return SpmmSegs{seg_beg.p, seg_row.p, seg_slot.p, row_seg0.p, row_nseg.p, ranges.p + g * (nranges + 1),
-                        nranges};
+                        nranges,
+                        split ? 0 : 1};
     }
 };
 

@@ -1,6 +1,3 @@
 python paper_2106_05609_b200/build.py >/dev/null 2>&1
-timeout 900 python -m pytest tests/test_ops_gpu.py tests/test_trainer_gpu.py tests/test_eval_gpu.py -x -q 2>&1 | tail -3
-timeout 900 python tools/workload_bench.py products_appnp 2>&1 | tail -1
-timeout 300 python tools/engine_probe.py 2>&1 | tail -1
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --profile-from-start off --csv --log-file gpurun_out/launches_products.csv python tools/profile_epoch.py --workload products_appnp > gpurun_out/launches_products.log 2>&1
-python tools/launches.py gpurun_out/launches_products.csv
+for d in 1 0; do GASB_SPMM_DUAL=$d timeout 300 python tools/engine_probe.py 2>&1 | tail -1; done
+timeout 900 python -m pytest tests/test_ops_gpu.py tests/test_trainer_gpu.py tests/test_dp_gpu.py -x -q 2>&1 | tail -3
