@@ -83,6 +83,59 @@ __global__ void __launch_bounds__(256) rows_kernel(int mode, const int32_t* __re
     }
 }
 
+// Narrow rows (dim <= 64 floats, float4-aligned): a warp splits into 32 / LPR lane groups of
+// LPR lanes, one row per group, so all 32 lanes move data (a 16-float row would otherwise
+// leave 28 lanes idle).
+template <int LPR, int R>
+__global__ void __launch_bounds__(256) rows_narrow_kernel(int mode, const int32_t* __restrict__ ids, int64_t count,
+                                                          const float* __restrict__ src, int64_t lds,
+                                                          float* __restrict__ dst, int64_t ldd, int32_t dim, int32_t n,
+                                                          int64_t* __restrict__ stamps,
+                                                          const int64_t* __restrict__ step, int32_t* __restrict__ err,
+                                                          int32_t* __restrict__ flags) {
+    constexpr int G = 32 / LPR;  // rows per warp instruction
+    const int lane = threadIdx.x & 31, grp = lane / LPR, sub = lane % LPR;
+    const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+    const int64_t stamp = (mode == 0 && stamps) ? *step : 0;
+    int32_t fl = 0;
+    for (int64_t base = warp * R * G; base < count; base += nwarps * R * G) {
+        int64_t srow[R], drow[R];
+        bool ok[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const int64_t i = base + r * G + grp;
+            ok[r] = i < count;
+            const int32_t id = ok[r] ? __ldg(ids + i) : 0;
+            if (ok[r] && (id < 0 || id >= n)) {
+                if (sub == 0) atomicAdd(err, 1);
+                ok[r] = false;
+            }
+            srow[r] = mode == 0 ? i : id;
+            drow[r] = mode == 0 ? id : i;
+            if (ok[r] && mode == 0 && stamps && sub == 0) stamps[id] = stamp;
+        }
+        for (int c = sub * 4; c < dim; c += LPR * 4) {
+            float4 v[R];
+#pragma unroll
+            for (int r = 0; r < R; ++r)
+                if (ok[r]) v[r] = __ldg(reinterpret_cast<const float4*>(src + srow[r] * lds + c));
+#pragma unroll
+            for (int r = 0; r < R; ++r)
+                if (ok[r]) {
+                    *reinterpret_cast<float4*>(dst + drow[r] * ldd + c) = v[r];
+                    if (flags)
+                        fl |= table_flag_of(v[r].x) | table_flag_of(v[r].y) | table_flag_of(v[r].z) |
+                              table_flag_of(v[r].w);
+                }
+        }
+    }
+    if (flags) {
+        fl = __reduce_or_sync(0xffffffffu, fl);
+        if (lane == 0 && fl) atomicOr(flags, fl);
+    }
+}
+
 __global__ void advance_step_kernel(int64_t* step) { *step += 1; }
 
 __global__ void fill_stamps_kernel(int64_t* stamps, int64_t n, const int64_t* step) {
@@ -133,6 +186,21 @@ void launch_rows(int mode, const int32_t* ids, int64_t count, const float* src, 
     const bool vec4 = (dim % 4 == 0) && (lds % 4 == 0) && (ldd % 4 == 0) &&
                       (reinterpret_cast<uintptr_t>(src) % 16 == 0) && (reinterpret_cast<uintptr_t>(dst) % 16 == 0);
     constexpr int R = 4;
+    if (vec4 && dim <= 64) {
+        const int lpr = dim <= 16 ? 4 : dim <= 32 ? 8 : 16;  // lanes per row (float4 each)
+        const int64_t warps_needed = ceil_div(count, static_cast<int64_t>(R) * (32 / lpr));
+        const int64_t blocks = std::min<int64_t>(ceil_div(warps_needed, 8), static_cast<int64_t>(num_sms()) * 8);
+#define GASB_NARROW(L)                                                                                            \
+    rows_narrow_kernel<L, R><<<static_cast<unsigned>(blocks), 256, 0, st>>>(mode, ids, count, src, lds, dst, ldd, \
+                                                                            dim, n, stamps, step, err, flags)
+        if (lpr == 4) GASB_NARROW(4);
+        else if (lpr == 8) GASB_NARROW(8);
+        else GASB_NARROW(16);
+#undef GASB_NARROW
+        ++t_launches;
+        GASB_CUDA(cudaGetLastError());
+        return;
+    }
     const int64_t warps_needed = ceil_div(count, R);
     const int64_t blocks = std::min<int64_t>(ceil_div(warps_needed, 8), static_cast<int64_t>(num_sms()) * 8);
     if (vec4)

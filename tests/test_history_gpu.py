@@ -210,3 +210,22 @@ def test_gash_checkpoint_interop(ref, tmp_path):
         gb.HistoryStore.load_checkpoint(tmp_path / "missing.gash")
     ref.lib.ref_history_free(rh)
     ref.lib.ref_history_free(rl)
+
+
+@pytest.mark.parametrize("d", [4, 16, 32, 48, 64, 68, 256])
+def test_push_pull_widths(d):
+    """Every row-kernel variant (narrow lane groups for d <= 64, float4, scalar) moves rows
+    exactly; stamps follow the pushes."""
+    n = 5000
+    h = gb.HistoryStore(1, n, d)
+    rng = np.random.default_rng(d)
+    ids = np.sort(rng.choice(n, size=1777, replace=False)).astype(np.int32)
+    rows = rng.standard_normal((len(ids), d)).astype(np.float32)
+    h.push(1, ids, rows)
+    want = np.zeros((n, d), np.float32)
+    want[ids] = rows
+    assert np.array_equal(h.layer_matrix(1), want)
+    q = rng.permutation(n)[:999].astype(np.int32)
+    assert np.array_equal(h.pull(1, q), want[q])
+    st = h.stamps(1)
+    assert (st[ids] == 0).all() and (np.delete(st, ids) == -1).all()
