@@ -482,6 +482,17 @@ void gasb_trainer_s::build_residual(const std::vector<int64_t>& h_arp, const std
     gout.alloc(nbm * ldD);
 }
 
+void gasb_trainer_s::enqueue_prefetch(int32_t p) {
+    GASB_CUDA(cudaEventRecord(ev_pf_start, stream));  // after the previous batch's pushes
+    GASB_CUDA(cudaStreamWaitEvent(side, ev_pf_start, 0));
+    for (int32_t l = 1; l < L; ++l) {
+        launch_rows(1, halo_ids.p + (ext_off[p] - row_off[p]), nh[p], history_table(hist, l), history_ld(hist),
+                    halo_pf.p + static_cast<int64_t>(l - 1) * halo_pf_rows * halo_pf_ld, halo_pf_ld, hist_dim, n,
+                    nullptr, nullptr, nullptr, side);
+        GASB_CUDA(cudaEventRecord(ev_pf[l], side));
+    }
+}
+
 // APPNP / GCNII batch: Model::forward (trainer.cpp:174-251) with head_forward over all V_b
 // rows (:142-163), appnp/gcnii layers (layers.cpp:150-168), the GCNII output head
 // (:221-227), then run_batch's backward (halo rows of h0 receive the layer-1 aggregation
@@ -493,6 +504,7 @@ void gasb_trainer_s::enqueue_batch_res(int32_t p, bool train, bool push, bool fu
     const int32_t* bn = batch_nodes.p + r0;
     const int32_t* br = brow.p + r0;
     const bool gcnii = spec.kind == 3;
+    if (!fused && halo_pf.p) enqueue_prefetch(p);
     // ---- head_forward over the extended rows: x_ext = X[V_b] (gather_features, trainer.cpp:20-27)
     launch_rows(1, extended.p + ext_off[p], me, X.p, ldF, x_ext.p, ldF, F, n, nullptr, nullptr, nullptr, stream);
     {
@@ -515,12 +527,20 @@ void gasb_trainer_s::enqueue_batch_res(int32_t p, bool train, bool push, bool fu
         } else if (fused) {  // pull-free: H_{l-1} by global id
             launch_spmm_fwd(segs, cols_g.p, coef64.p, history_table(hist, l - 1), history_ld(hist), D, prop.p, ldD, r0,
                             partial_batch.p, pld, counters.p, max_chunks, stream, source_flags(l), source_tmap(l));
-        } else {  // pull halos, compose_rows, SpMM over local ids
-            launch_rows(1, halo_ids.p + (ext_off[p] - row_off[p]), nh[p], history_table(hist, l - 1),
-                        history_ld(hist), halo_buf.p, ldD, D, n, nullptr, nullptr, nullptr, stream);
+        } else {  // pull halos (or wait for the prefetched copy), compose_rows, SpMM over local ids
+            const float* halo = halo_buf.p;
+            int64_t ldh = ldD;
+            if (halo_pf.p) {
+                GASB_CUDA(cudaStreamWaitEvent(stream, ev_pf[l - 1], 0));
+                halo = halo_pf.p + static_cast<int64_t>(l - 2) * halo_pf_rows * halo_pf_ld;
+                ldh = halo_pf_ld;
+            } else {
+                launch_rows(1, halo_ids.p + (ext_off[p] - row_off[p]), nh[p], history_table(hist, l - 1),
+                            history_ld(hist), halo_buf.p, ldD, D, n, nullptr, nullptr, nullptr, stream);
+            }
             const int64_t blocks = ceil_div(static_cast<int64_t>(me) * 32, 256);
             compose_kernel<<<static_cast<unsigned>(blocks), 256, 0, stream>>>(compose_idx.p + ext_off[p],
-                                                                               act[l - 1].p, ldD, halo_buf.p, ldD, me,
+                                                                               act[l - 1].p, ldD, halo, ldh, me,
                                                                                D, h_ext.p, ldD);
             ++t_launches;
             GASB_CUDA(cudaGetLastError());
@@ -623,6 +643,7 @@ void gasb_trainer_s::enqueue_batch(int32_t p, bool train, bool push, bool use_ho
     const int64_t r0 = row_off[p];
     const SpmmSegs segs = seg_batch.segs(p);
     const int32_t* bn = batch_nodes.p + r0;
+    if (!fused && halo_pf.p) enqueue_prefetch(p);
     // ---------------- forward (Model::forward, trainer.cpp:174-251) ----------------
     for (int32_t l = 1; l <= L; ++l) {
         const int32_t din = dims[l - 1], dout = dims[l];
@@ -645,13 +666,19 @@ void gasb_trainer_s::enqueue_batch(int32_t p, bool train, bool push, bool use_ho
                 hsrc = x_ext.p;
             } else {
                 // HistoryStore::pull of the halo rows, then compose_rows (tensor.cpp:459-512)
-                const HostPlan& P = sched->plans[p];
-                (void)P;
-                launch_rows(1, halo_ids.p + (ext_off[p] - row_off[p]), nh[p], history_table(hist, l - 1),
-                            history_ld(hist), halo_buf.p, ldx, din, n, nullptr, nullptr, nullptr, stream);
+                const float* halo = halo_buf.p;
+                int64_t ldh = ldx;
+                if (halo_pf.p) {  // Prefetcher::wait(l - 1): the side-stream copy of this layer
+                    GASB_CUDA(cudaStreamWaitEvent(stream, ev_pf[l - 1], 0));
+                    halo = halo_pf.p + static_cast<int64_t>(l - 2) * halo_pf_rows * halo_pf_ld;
+                    ldh = halo_pf_ld;
+                } else {
+                    launch_rows(1, halo_ids.p + (ext_off[p] - row_off[p]), nh[p], history_table(hist, l - 1),
+                                history_ld(hist), halo_buf.p, ldx, din, n, nullptr, nullptr, nullptr, stream);
+                }
                 const int64_t blocks = ceil_div(static_cast<int64_t>(ne[p]) * 32, 256);
                 compose_kernel<<<static_cast<unsigned>(blocks), 256, 0, stream>>>(
-                    compose_idx.p + ext_off[p], act[l - 1].p, ldH, halo_buf.p, ldx, ne[p], din, h_ext.p, ldx);
+                    compose_idx.p + ext_off[p], act[l - 1].p, ldH, halo, ldh, ne[p], din, h_ext.p, ldx);
                 ++t_launches;
                 GASB_CUDA(cudaGetLastError());
                 hsrc = h_ext.p;
@@ -1024,6 +1051,16 @@ gasb_status gasb_trainer_create(gasb_schedule s, const float* h_features, int32_
                 std::copy(P.halo.begin(), P.halo.end(), hid.begin() + (t->ext_off[p] - t->row_off[p]));
             }
             t->halo_ids.upload(hid);
+        }
+        if (!t->opt.fused && t->opt.prefetch && t->L >= 2) {
+            int64_t nh_max = 0;
+            for (int32_t p = 0; p < t->num_parts; ++p) nh_max = std::max<int64_t>(nh_max, t->nh[p]);
+            t->halo_pf_ld = t->ld_of(t->hist_dim);
+            t->halo_pf_rows = std::max<int64_t>(nh_max, 1);
+            t->halo_pf.alloc(static_cast<int64_t>(t->L - 1) * t->halo_pf_rows * t->halo_pf_ld);
+            GASB_CUDA(cudaEventCreateWithFlags(&t->ev_pf_start, cudaEventDisableTiming));
+            t->ev_pf.assign(static_cast<size_t>(t->L), nullptr);
+            for (auto& e : t->ev_pf) GASB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         }
         t->build_tmaps();
         *out = t.release();

@@ -148,6 +148,15 @@ struct gasb_trainer_s {
     DevBuf<float> gemm_ws2, g_out2;
     std::vector<cudaEvent_t> ev_fork, ev_wdone;
     cudaEvent_t ev_join = nullptr;
+    // reference-structured mode with opt.prefetch (the Prefetcher, history.cpp:184-252, and
+    // the paper's concurrent execution): every history layer's halo rows of the batch are
+    // pulled on `side` at batch start, overlapped with layer-1 compute; layer l waits only
+    // for its own copy (the batch's pushes never touch its halo rows)
+    DevBuf<float> halo_pf;
+    int64_t halo_pf_ld = 0, halo_pf_rows = 0;
+    cudaEvent_t ev_pf_start = nullptr;
+    std::vector<cudaEvent_t> ev_pf;
+    void enqueue_prefetch(int32_t p);
     DevBuf<double> colsum_ws;  // row-block partials of the bias-gradient column sums
     struct WsGuard {        // scopes the thread's GEMM / column-sum workspaces to one enqueue
         explicit WsGuard(DevBuf<float>& w, DevBuf<double>* c = nullptr) {
@@ -224,6 +233,8 @@ struct gasb_trainer_s {
         for (auto e : ev_fork) cudaEventDestroy(e);
         for (auto e : ev_wdone) cudaEventDestroy(e);
         if (ev_join) cudaEventDestroy(ev_join);
+        if (ev_pf_start) cudaEventDestroy(ev_pf_start);
+        for (auto e : ev_pf) cudaEventDestroy(e);
         if (copy_stream) cudaStreamSynchronize(copy_stream);
         if (ev_staged) cudaEventDestroy(ev_staged);
         if (ev_stage_free) cudaEventDestroy(ev_stage_free);

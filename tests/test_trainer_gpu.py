@@ -76,7 +76,8 @@ def test_fused_equals_materialized_and_hoisting_is_exact(oracle):
     params = []
     for opt in (dict(fused=True, hoist_layer1=True, use_graphs=True, seg_edges=0),
                 dict(fused=False, hoist_layer1=False, use_graphs=True, seg_edges=0),
-                dict(fused=True, hoist_layer1=False, use_graphs=False, seg_edges=0)):
+                dict(fused=True, hoist_layer1=False, use_graphs=False, seg_edges=0),
+                dict(fused=False, prefetch=True, use_graphs=True, seg_edges=0)):  # side-stream halo prefetch
         _, _, tr, _ = _setup(oracle, "cora", **opt)
         for ep in range(2):
             tr.gas_epoch(ep)
@@ -84,6 +85,7 @@ def test_fused_equals_materialized_and_hoisting_is_exact(oracle):
         params.append(tr.history.layer_matrix(1))
     assert np.array_equal(params[0], params[2]) and np.array_equal(params[0], params[4])
     assert np.array_equal(params[1], params[3]) and np.array_equal(params[1], params[5])
+    assert np.array_equal(params[0], params[6]) and np.array_equal(params[1], params[7])
 
 
 def test_push_false_leaves_history_untouched(oracle):
@@ -115,14 +117,15 @@ def test_residual_free_running_epochs(oracle, name):
 @pytest.mark.parametrize("name", ["cora_appnp", "cora_gcnii"])
 def test_residual_fused_equals_materialized(oracle, name):
     params = []
-    for opt in (dict(fused=True, use_graphs=True, seg_edges=0), dict(fused=False, use_graphs=False, seg_edges=0)):
+    for opt in (dict(fused=True, use_graphs=True, seg_edges=0), dict(fused=False, use_graphs=False, seg_edges=0),
+                dict(fused=False, prefetch=True, use_graphs=True, seg_edges=0)):
         _, _, tr, _ = _setup(oracle, name, **opt)
         for ep in range(2):
             tr.gas_epoch(ep)
         params.append(tr.get_params())
         params.append(tr.history.layer_matrix(1))
-    assert np.array_equal(params[0], params[2])
-    assert np.array_equal(params[1], params[3])
+    assert np.array_equal(params[0], params[2]) and np.array_equal(params[0], params[4])
+    assert np.array_equal(params[1], params[3]) and np.array_equal(params[1], params[5])
 
 
 @pytest.mark.parametrize("clip", [0.05, 1.0])
