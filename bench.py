@@ -181,9 +181,9 @@ def run_ours(args):
     w = ds.workload
     sched = gb.BatchSchedule.build(ds.graph, ds.assignment, w.parts)
     spec = gb.ModelSpec(kind=w.kind, num_layers=w.num_layers, hidden=w.hidden, seed=3)
-    # N > 1: data-parallel epochs (dp.cu: k batches per step, exchange over peer memory); the
-    # layer-1 hoist covers a whole epoch's batches, so it is a single-GPU option
-    opts = gb.TrainerOptions(seg_edges=args.seg_edges, device=local, hoist_layer1=not args.no_hoist and ws == 1)
+    # N > 1: data-parallel epochs (dp.cu: k batches per step, exchange over peer memory); each
+    # rank hoists layer 1 over its own batches of the epoch
+    opts = gb.TrainerOptions(seg_edges=args.seg_edges, device=local, hoist_layer1=not args.no_hoist)
     tr = gb.GasTrainer(sched, ds.features, ds.labels, ds.train_mask, w.num_classes, spec, opts)
     runner = tr
     if ws > 1:

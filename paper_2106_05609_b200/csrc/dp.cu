@@ -395,9 +395,15 @@ gasb_status gasb_dp_epoch_async(gasb_dp d, int64_t epoch, int32_t shuffle) {
         T.ensure_bc(T.t_host + steps + 2);
         d->epoch_launches = 0;
         d->last_parts.clear();
+        for (int32_t s0 = 0; s0 < T.num_parts; s0 += d->world)
+            if (d->rank < std::min(d->world, T.num_parts - s0)) d->last_parts.push_back(order[s0 + d->rank]);
+        if (T.opt.hoist_layer1 && T.opt.fused && !T.residual && T.agg_all.p) {
+            const int64_t c0 = t_launches;  // layer 1 of this rank's batches, one launch
+            T.enqueue_hoisted_parts(d->last_parts);
+            d->epoch_launches += t_launches - c0;
+        }
         for (int32_t s0 = 0; s0 < T.num_parts; s0 += d->world) {
             const int32_t kk = std::min(d->world, T.num_parts - s0);
-            if (d->rank < kk) d->last_parts.push_back(order[s0 + d->rank]);
             d->epoch_launches += d->step(order.data() + s0, kk);
         }
         d->last_order = order;

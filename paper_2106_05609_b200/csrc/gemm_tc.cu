@@ -14,6 +14,8 @@
 //   warp 5 (1 thread)   MMA issuer: per k-step of 8, D += Ahi.Bhi + Ahi.Blo + Alo.Bhi
 // mbarriers: full (TMA -> split), split (split -> MMA), empty (tcgen05.commit -> TMA),
 // accum (last commit -> epilogue). Waits are bounded (trap instead of hang).
+#include <cstdlib>
+
 #include "gasb_internal.hpp"
 #include "kernels.cuh"
 
@@ -455,8 +457,12 @@ static bool launch_tc(int m, int n, int k, const float* a, int64_t lda, const fl
     const int64_t tiles = ceil_div(m, BM) * ceil_div(n, BN);
     const int nkb = static_cast<int>(ceil_div(k, BK));
     int S = 1;
-    if (!TALL && t_gemm_ws && tiles < num_sms()) {
-        S = static_cast<int>(std::min<int64_t>(num_sms() / tiles, std::max(1, nkb / 2)));
+    static const int split_div = [] {  // GASB_GEMM_SPLITK_DIV: min k-blocks per split-K slice (0 = off)
+        const char* e = getenv("GASB_GEMM_SPLITK_DIV");
+        return e ? atoi(e) : 8;  // measured: fewer, longer slices beat more fixups at C3 sizes
+    }();
+    if (!TALL && split_div > 0 && t_gemm_ws && tiles < num_sms()) {
+        S = static_cast<int>(std::min<int64_t>(num_sms() / tiles, std::max(1, nkb / split_div)));
         while (S > 1 && static_cast<int64_t>(S) * m * round_up(n, 4) > t_gemm_ws_floats) --S;
         if (2 * tiles > kGemmTileCounters) S = 1;
     }

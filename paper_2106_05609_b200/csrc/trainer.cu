@@ -30,6 +30,7 @@
 #include <memory>
 #include <numeric>
 #include <random>
+#include <type_traits>
 
 #include "trainer_impl.hpp"
 
@@ -346,6 +347,7 @@ void gasb_trainer_s::build(const float* h_features, const int32_t* h_labels, con
         std::vector<int64_t> grp(num_parts + 1);
         for (int32_t p = 0; p <= num_parts; ++p) grp[p] = row_off[p];
         build_segments(h_rp, grp, opt.seg_edges > 0, true, seg_batch);
+        h_rowptr = h_rp;
         std::vector<int64_t> one{0, R};
         build_segments(h_rp, one, opt.seg_edges > 0, false, seg_all);
     }
@@ -450,6 +452,93 @@ void gasb_trainer_s::build(const float* h_features, const int32_t* h_labels, con
     graphs.assign(num_parts, nullptr);
     graph_launches.assign(num_parts, 0);
     GASB_CUDA(cudaDeviceSynchronize());
+}
+
+// Layer 1 hoisted over a subset of parts (one data-parallel rank's batches of an epoch):
+// the parts' edges are copied into one contiguous stream, segments / ranges are built on the
+// host over that stream (rows keep their absolute ids, so the output lands in agg_all where
+// the per-part graphs read it), and one chunk-major launch aggregates them all.
+void gasb_trainer_s::enqueue_hoisted_parts(const std::vector<int32_t>& parts) {
+    std::vector<int64_t> vrp(1, 0);  // virtual (contiguous) row pointers
+    std::vector<int32_t> vrow;       // virtual row -> absolute row
+    int64_t E = 0;
+    for (int32_t p : parts) {
+        for (int64_t r = row_off[p]; r < row_off[p + 1]; ++r) {
+            E += h_rowptr[r + 1] - h_rowptr[r];
+            vrp.push_back(E);
+            vrow.push_back(static_cast<int32_t>(r));
+        }
+    }
+    const int64_t R = row_off[num_parts], rows = static_cast<int64_t>(vrow.size());
+    if (rows == 0) return;
+    hs_beg.clear();
+    hs_row.clear();
+    hs_slot.clear();
+    std::vector<int32_t> r0(static_cast<size_t>(rows)), rn(static_cast<size_t>(rows));
+    const int32_t nr = spmm_ranges_per_launch();
+    hs_ranges.assign(static_cast<size_t>(nr) + 1, 0);
+    int64_t slot = 0;
+    segment_launch(vrp.data(), 0, rows, opt.seg_edges > 0, nr, hs_beg, hs_row, hs_slot, r0.data(), rn.data(), slot,
+                   hs_ranges.data());
+    for (auto& r : hs_row) r = vrow[r];  // segments name absolute rows
+    hs_r0.assign(static_cast<size_t>(R), 0);
+    hs_rn.assign(static_cast<size_t>(R), 0);
+    for (int64_t v = 0; v < rows; ++v) {
+        hs_r0[vrow[v]] = r0[v];
+        hs_rn[vrow[v]] = rn[v];
+    }
+    if (sub_cols.n < E) {
+        GASB_CUDA(cudaStreamSynchronize(stream));
+        sub_cols.alloc(E);
+        sub_coef.alloc(E);
+    }
+    int64_t off = 0;
+    for (int32_t p : parts) {
+        const int64_t e0 = h_rowptr[row_off[p]], e1 = h_rowptr[row_off[p + 1]];
+        GASB_CUDA(cudaMemcpyAsync(sub_cols.p + off, cols_g.p + e0, sizeof(int32_t) * (e1 - e0),
+                                  cudaMemcpyDeviceToDevice, stream));
+        GASB_CUDA(cudaMemcpyAsync(sub_coef.p + off, coef64.p + e0, sizeof(double) * (e1 - e0),
+                                  cudaMemcpyDeviceToDevice, stream));
+        off += e1 - e0;
+    }
+    // tables -> page-locked staging -> device, all stream-ordered (no host synchronisation)
+    auto bytes_of = [](const auto& v) { return (sizeof(v[0]) * v.size() + 255) / 256 * 256; };
+    const size_t total = bytes_of(hs_beg) + bytes_of(hs_row) + bytes_of(hs_slot) + bytes_of(hs_r0) + bytes_of(hs_rn) +
+                         bytes_of(hs_ranges);
+    if (!ev_sub_uploaded) GASB_CUDA(cudaEventCreateWithFlags(&ev_sub_uploaded, cudaEventDisableTiming));
+    GASB_CUDA(cudaEventSynchronize(ev_sub_uploaded));  // the previous epoch's copies (long done)
+    if (sub_pinned_bytes < total) {
+        if (sub_pinned) GASB_CUDA(cudaFreeHost(sub_pinned));
+        GASB_CUDA(cudaHostAlloc(&sub_pinned, total, cudaHostAllocDefault));
+        sub_pinned_bytes = total;
+    }
+    size_t po = 0;
+    auto stage = [&](auto& dev, const auto& v) {
+        using T = std::decay_t<decltype(v[0])>;
+        if (dev.n < static_cast<int64_t>(v.size())) {
+            GASB_CUDA(cudaStreamSynchronize(stream));
+            dev.alloc(static_cast<int64_t>(v.size()));
+        }
+        std::memcpy(sub_pinned + po, v.data(), sizeof(T) * v.size());
+        GASB_CUDA(cudaMemcpyAsync(dev.p, sub_pinned + po, sizeof(T) * v.size(), cudaMemcpyHostToDevice, stream));
+        po += bytes_of(v);
+    };
+    stage(sub_seg_beg, hs_beg);
+    stage(sub_seg_row, hs_row);
+    stage(sub_seg_slot, hs_slot);
+    stage(sub_row_seg0, hs_r0);
+    stage(sub_row_nseg, hs_rn);
+    stage(sub_ranges, hs_ranges);
+    GASB_CUDA(cudaEventRecord(ev_sub_uploaded, stream));
+    const int64_t need = std::max<int64_t>(slot, 1) * pld_all;
+    if (sub_partial.n < need) {
+        GASB_CUDA(cudaStreamSynchronize(stream));
+        sub_partial.alloc(need);
+    }
+    SpmmSegs segs{sub_seg_beg.p, sub_seg_row.p, sub_seg_slot.p, sub_row_seg0.p, sub_row_nseg.p, sub_ranges.p, nr,
+                  opt.seg_edges > 0 ? 0 : 1};
+    launch_spmm_fwd(segs, sub_cols.p, sub_coef.p, X.p, ldF, F, agg_all.p, ldF, 0, sub_partial.p, pld_all, counters.p,
+                    max_chunks, stream, source_flags(1), source_tmap(1));
 }
 
 void gasb_trainer_s::enqueue_hoisted() {
@@ -780,7 +869,7 @@ void gasb_trainer_s::run_epoch(int64_t epoch, bool shuffle) {
 // unless dp) on `stream`, through its captured per-part graph when use_graphs. Returns the
 // number of kernels it launches.
 int64_t gasb_trainer_s::launch_batch_graph(int32_t p, bool dp) {
-    const bool hoisted = !dp && opt.hoist_layer1 && opt.fused && !residual;
+    const bool hoisted = opt.hoist_layer1 && opt.fused && !residual;
     if (!opt.use_graphs) {
         const int64_t c0 = t_launches;
         enqueue_batch(p, true, true, hoisted, opt.fused != 0, dp);
@@ -799,7 +888,7 @@ int64_t gasb_trainer_s::launch_batch_graph(int32_t p, bool dp) {
 
 // Captures (without launching) the per-part batch graph of part p.
 void gasb_trainer_s::capture_batch_graph(int32_t p, bool dp) {
-    const bool hoisted = !dp && opt.hoist_layer1 && opt.fused && !residual;
+    const bool hoisted = opt.hoist_layer1 && opt.fused && !residual;
     std::vector<cudaGraphExec_t>& gs = dp ? graphs_dp : graphs;
     std::vector<int64_t>& gl = dp ? graph_launches_dp : graph_launches;
     if (gs.empty()) {

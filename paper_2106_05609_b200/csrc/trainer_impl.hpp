@@ -31,6 +31,15 @@ struct DevBuf {
         alloc(static_cast<int64_t>(v.size()));
         if (!v.empty()) GASB_CUDA(cudaMemcpy(p, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice));
     }
+    // stream-ordered upload that reallocates only to grow (per-epoch tables); the host
+    // vector must stay alive until the copy ran (the caller keeps it as a member)
+    void upload_async(const std::vector<T>& v, cudaStream_t st) {
+        if (n < static_cast<int64_t>(v.size())) {
+            GASB_CUDA(cudaStreamSynchronize(st));
+            alloc(static_cast<int64_t>(v.size()));
+        }
+        if (!v.empty()) GASB_CUDA(cudaMemcpyAsync(p, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice, st));
+    }
     void zero() {
         if (n) GASB_CUDA(cudaMemset(p, 0, sizeof(T) * n));
     }
@@ -234,6 +243,8 @@ struct gasb_trainer_s {
         for (auto e : ev_wdone) cudaEventDestroy(e);
         if (ev_join) cudaEventDestroy(ev_join);
         if (ev_pf_start) cudaEventDestroy(ev_pf_start);
+        if (ev_sub_uploaded) cudaEventDestroy(ev_sub_uploaded);
+        if (sub_pinned) cudaFreeHost(sub_pinned);
         for (auto e : ev_pf) cudaEventDestroy(e);
         if (copy_stream) cudaStreamSynchronize(copy_stream);
         if (ev_staged) cudaEventDestroy(ev_staged);
@@ -271,6 +282,22 @@ struct gasb_trainer_s {
     // the cross-rank exchange) and have their own per-part graphs
     std::vector<cudaGraphExec_t> graphs_dp;
     DevBuf<char> dp_region;
+    // data-parallel layer-1 hoisting over this rank's parts of the epoch (enqueue_hoisted_parts):
+    // the parts' stencils are copied contiguously, their segment tables rebuilt per epoch
+    std::vector<int64_t> h_rowptr;  // absolute row pointers of the concatenated stencils (R + 1)
+    DevBuf<int32_t> sub_cols;
+    DevBuf<double> sub_coef;
+    DevBuf<int64_t> sub_seg_beg;
+    DevBuf<int32_t> sub_seg_row, sub_seg_slot, sub_row_seg0, sub_row_nseg, sub_ranges;
+    DevBuf<double> sub_partial;
+    std::vector<int64_t> hs_beg;
+    std::vector<int32_t> hs_row, hs_slot, hs_r0, hs_rn, hs_ranges;
+    // page-locked staging of those tables (asynchronous H2D; reused once the previous
+    // epoch's copies, which ran first in that epoch, are done)
+    char* sub_pinned = nullptr;
+    size_t sub_pinned_bytes = 0;
+    cudaEvent_t ev_sub_uploaded = nullptr;
+    void enqueue_hoisted_parts(const std::vector<int32_t>& parts);
     // full-graph forward (evaluate / infer_from_history, trainer.cpp:444-536): every row of
     // every part in one launch per layer over the whole-epoch segment table; layer outputs
     // scattered by global id into ping-pong tables the next layer gathers in place

@@ -26,7 +26,7 @@ w = ds.workload
 sched = gb.BatchSchedule.build(ds.graph, ds.assignment, w.parts)
 spec = gb.ModelSpec(kind=w.kind, num_layers=w.num_layers, hidden=w.hidden, seed=3)
 tr = gb.GasTrainer(sched, ds.features, ds.labels, ds.train_mask, w.num_classes, spec,
-                   gb.TrainerOptions(device=dev, hoist_layer1=False))
+                   gb.TrainerOptions(device=dev, hoist_layer1=len(sys.argv) > 5 and sys.argv[5] == "hoist"))
 dp = gb.DataParallelTrainer(tr, rank, world, group=dist.group.WORLD)
 losses = [dp.gas_epoch(e) for e in range(epochs)]
 hist = {f"hist{l}": tr.history.layer_matrix(l) for l in range(1, w.num_layers)}

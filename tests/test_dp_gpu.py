@@ -49,13 +49,26 @@ def test_dp_world1_is_gas_epoch(name):
     assert a.history.step() == b.history.step()
 
 
-@pytest.mark.parametrize("name,world", [("cora", 2), ("cora", 3), ("cora_appnp", 2)])
-def test_dp_ranks_share_one_gpu(oracle, tmp_path, name, world):
+def test_dp_world1_hoisted_layer1_is_gas_epoch():
+    """Per-rank layer-1 hoisting (the rank's batches of the epoch in one launch) == gas_epoch,
+    bit for bit in the sequential (exact) SpMM mode."""
+    ds = make_dataset("reddit_mini")
+    a = _trainer(ds, seg_edges=0)
+    b = _trainer(ds, seg_edges=0)
+    dp = gb.DataParallelTrainer(b, 0, 1)
+    for e in range(3):
+        assert a.gas_epoch(e) == dp.gas_epoch(e)
+    assert np.array_equal(a.get_params(), b.get_params())
+
+
+@pytest.mark.parametrize("name,world,hoist", [("cora", 2, ""), ("cora", 3, ""), ("cora_appnp", 2, ""),
+                                              ("reddit_mini", 2, "hoist")])
+def test_dp_ranks_share_one_gpu(oracle, tmp_path, name, world, hoist):
     epochs = 2
     env = dict(os.environ, MASTER_ADDR="127.0.0.1", MASTER_PORT=str(29600 + (os.getpid() + world) % 1000),
                WORLD_SIZE=str(world))
     procs = [subprocess.Popen([sys.executable, str(HERE / "helpers" / "dp_gpu_rank.py"), str(tmp_path), name,
-                               str(world), str(epochs)], env=dict(env, RANK=str(r)), stdout=subprocess.PIPE,
+                               str(world), str(epochs), hoist], env=dict(env, RANK=str(r)), stdout=subprocess.PIPE,
                               stderr=subprocess.STDOUT, text=True) for r in range(world)]
     try:
         outs = [p.communicate(timeout=600)[0] for p in procs]
