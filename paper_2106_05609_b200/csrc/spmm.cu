@@ -1213,13 +1213,25 @@ __global__ void __launch_bounds__(kBwdThreads) spmm_bwd_smem_kernel(
     // targets t = blockIdx.y + splits * k; warps claim k dynamically (power-law in-degrees)
     const int32_t splits = targets_per_cta;
     int2* wbuf = reinterpret_cast<int2*>(sg + static_cast<int64_t>(nsrc) * kBwdCW) + warp * 32;
-    for (;;) {
+    auto claim = [&]() -> int32_t {
         int32_t k = 0;
         if (lane == 0) k = atomicAdd(&s_next, 1);
-        const int32_t t = static_cast<int32_t>(blockIdx.y) + splits * __shfl_sync(0xffffffffu, k, 0);
+        return static_cast<int32_t>(blockIdx.y) + splits * __shfl_sync(0xffffffffu, k, 0);
+    };
+    // software-pipelined over targets: the next target is claimed and its row pointers loaded
+    // while the current one accumulates
+    int32_t t = claim();
+    int64_t e0n = t < nt ? rp[t] : 0, e1n = t < nt ? rp[t + 1] : 0;
+    for (;;) {
         if (t >= nt) break;
-        const int64_t e0 = rp[t], e1 = rp[t + 1];
+        const int64_t e0 = e0n, e1 = e1n;
+        const bool keep = !mask || lane >= ncol || mask[static_cast<int64_t>(t) * ldm + col0 + lane] > 0.0f;
         float a = (accumulate && lane < ncol) ? gx[static_cast<int64_t>(t) * ldgx + col0 + lane] : 0.0f;
+        const int32_t tn = claim();
+        if (tn < nt) {
+            e0n = rp[tn];
+            e1n = rp[tn + 1];
+        }
         // metadata of the next 32 entries is loaded while the current 32 are accumulated; the
         // current window is parked in shared memory as (row offset, coeff) pairs read back by
         // broadcast LDS.64 (one shared-memory op per entry instead of two shuffles)
@@ -1253,11 +1265,8 @@ __global__ void __launch_bounds__(kBwdThreads) spmm_bwd_smem_kernel(
             my_r = nr;
             my_c = nc;
         }
-        if (lane < ncol) {
-            const int32_t col = col0 + lane;
-            if (mask && !(mask[static_cast<int64_t>(t) * ldm + col] > 0.0f)) a = 0.0f;
-            gx[static_cast<int64_t>(t) * ldgx + col] = a;
-        }
+        if (lane < ncol) gx[static_cast<int64_t>(t) * ldgx + col0 + lane] = keep ? a : 0.0f;
+        t = tn;
     }
 }
 
