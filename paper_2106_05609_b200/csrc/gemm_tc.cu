@@ -43,7 +43,9 @@ static int num_sms() {
 namespace tc {
 
 constexpr int BM = 128, BK = 32, kStagesTC = 3;
-constexpr int kThreads = 192;
+constexpr int kSplitHelpers = 4;                      // extra warps that only split tiles
+constexpr int kSplitThreads = 128 + 32 * kSplitHelpers;  // warps 0-3 + helpers
+constexpr int kThreads = 192 + 32 * kSplitHelpers;
 // The tensor core's fp32 accumulation truncates, so its error grows linearly with the number
 // of k-steps; k-steps are interleaved over kAcc TMEM accumulators (kAcc * BN <= 512 columns)
 // summed round-to-nearest in the epilogue, cutting that growth kAcc-fold.
@@ -165,7 +167,7 @@ __global__ void __launch_bounds__(kThreads, TALL ? 2 : 1) gemm_tc_kernel(const _
     if (threadIdx.x == 0) {
         for (int s = 0; s < kStagesTC; ++s) {
             bar_init(full + s, 1);
-            bar_init(split + s, 128);
+            bar_init(split + s, kSplitThreads);
             bar_init(empty + s, 1);
         }
         bar_init(accum, 1);
@@ -242,7 +244,8 @@ __global__ void __launch_bounds__(kThreads, TALL ? 2 : 1) gemm_tc_kernel(const _
             mma_commit(accum);
         }
     } else {
-        // ---------------- split (warps 0-3), then epilogue ----------------
+        // ---------------- split (warps 0-3 and the helper warps 6+), then epilogue (0-3) ----------------
+        const int sid = warp < 4 ? threadIdx.x : threadIdx.x - 64;  // 0 .. kSplitThreads-1
         for (int kb = 0; kb < nk; ++kb) {
             const int s = kb % kStagesTC;
             bar_wait(full + s, (kb / kStagesTC) & 1);
@@ -252,13 +255,13 @@ __global__ void __launch_bounds__(kThreads, TALL ? 2 : 1) gemm_tc_kernel(const _
             float4* blo = b + Lay::kTileB / 16;
             // hi = rn_tf32(x), lo = rn_tf32(x - hi): both exactly tf32, so the tensor core's
             // operand truncation changes nothing; dropped lo*lo term ~2^-22 relative
-            for (int i = threadIdx.x; i < Lay::kTileA / 16; i += 128) {
+            for (int i = sid; i < Lay::kTileA / 16; i += kSplitThreads) {
                 float4 v = a[i], h;
                 h.x = tf32_hi(v.x), h.y = tf32_hi(v.y), h.z = tf32_hi(v.z), h.w = tf32_hi(v.w);
                 a[i] = h;
                 alo[i] = make_float4(tf32_hi(v.x - h.x), tf32_hi(v.y - h.y), tf32_hi(v.z - h.z), tf32_hi(v.w - h.w));
             }
-            for (int i = threadIdx.x; i < Lay::kTileB / 16; i += 128) {
+            for (int i = sid; i < Lay::kTileB / 16; i += kSplitThreads) {
                 float4 v = b[i], h;
                 h.x = tf32_hi(v.x), h.y = tf32_hi(v.y), h.z = tf32_hi(v.z), h.w = tf32_hi(v.w);
                 b[i] = h;
@@ -267,142 +270,144 @@ __global__ void __launch_bounds__(kThreads, TALL ? 2 : 1) gemm_tc_kernel(const _
             asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // generic writes -> tensor core
             bar_arrive(split + s);
         }
-        bar_wait(accum, 0);
-        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-        const int row = m0 + warp * 32 + lane;  // TMEM lane == tile row
-        float* crow = row < M ? C + static_cast<int64_t>(row) * ldc : nullptr;
-        float* prow = nullptr;
-        if (crow && push.table && !ws) {
-            const int32_t id = push.ids[row];
-            prow = push.table + static_cast<int64_t>(id) * push.ld;
-            if (blockIdx.y == 0 && push.stamps) push.stamps[id] = *push.step;
-        }
-        int32_t flags = 0;
-        const int nsteps = nk * (BK / 8);
-        const int nacc = nsteps < Acc<BN, TALL>::kAcc ? nsteps : Acc<BN, TALL>::kAcc;  // accumulators written
-#pragma unroll 1
-        for (int c0 = 0; c0 < BN; c0 += 32) {
-            float sum[32];
-#pragma unroll 1
-            for (int q = 0; q < nacc; ++q) {
-                uint32_t v[32];
-                const uint32_t taddr =
-                    tmem + (static_cast<uint32_t>(warp * 32) << 16) + static_cast<uint32_t>(q * BN + c0);
-                asm volatile(
-                    "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-                    "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
-                    : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
-                      "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
-                      "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]),
-                      "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]),
-                      "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
-                    : "r"(taddr));
-                asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-#pragma unroll
-                for (int j = 0; j < 32; ++j) sum[j] = q == 0 ? __uint_as_float(v[j]) : __fadd_rn(sum[j], __uint_as_float(v[j]));
+        if (warp < 4) {  // epilogue: TMEM lane == tile row
+            bar_wait(accum, 0);
+            asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+            const int row = m0 + warp * 32 + lane;  // TMEM lane == tile row
+            float* crow = row < M ? C + static_cast<int64_t>(row) * ldc : nullptr;
+            float* prow = nullptr;
+            if (crow && push.table && !ws) {
+                const int32_t id = push.ids[row];
+                prow = push.table + static_cast<int64_t>(id) * push.ld;
+                if (blockIdx.y == 0 && push.stamps) push.stamps[id] = *push.step;
             }
-            if (crow && ws) {  // slice partial, row pitch Np = N rounded up to 4 (float4 stores)
-                const int Np = (N + 3) & ~3;
-                float4* wrow = reinterpret_cast<float4*>(ws + (static_cast<int64_t>(blockIdx.z) * M + row) * Np);
-#pragma unroll
-                for (int j = 0; j < 32; j += 4)
-                    if (n0 + c0 + j < Np) wrow[(n0 + c0 + j) >> 2] = make_float4(sum[j], sum[j + 1], sum[j + 2], sum[j + 3]);
-            } else if (crow) {
-                // 16 B stores where the row pitch allows (a thread owns one output row: scalar
-                // stores would cost one instruction per 4 B)
-                const bool v4 = ((ldc & 3) == 0) && ((reinterpret_cast<uintptr_t>(C) & 15) == 0) &&
-                                (!prow || ((push.ld & 3) == 0 && (reinterpret_cast<uintptr_t>(push.table) & 15) == 0));
-#pragma unroll
-                for (int j = 0; j < 32; j += 4) {
-                    const int col = n0 + c0 + j;
-                    if (v4 && col + 3 < N) {
-                        float4 x;
-                        x.x = gemm_epilogue_value(ep, sum[j], crow, col);
-                        x.y = gemm_epilogue_value(ep, sum[j + 1], crow, col + 1);
-                        x.z = gemm_epilogue_value(ep, sum[j + 2], crow, col + 2);
-                        x.w = gemm_epilogue_value(ep, sum[j + 3], crow, col + 3);
-                        *reinterpret_cast<float4*>(crow + col) = x;
-                        if (prow) {
-                            *reinterpret_cast<float4*>(prow + col) = x;
-                            flags |= table_flag_of(x.x) | table_flag_of(x.y) | table_flag_of(x.z) | table_flag_of(x.w);
-                        }
-                        continue;
-                    }
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        if (col + q < N) {
-                            const float x = gemm_epilogue_value(ep, sum[j + q], crow, col + q);
-                            crow[col + q] = x;
+            int32_t flags = 0;
+            const int nsteps = nk * (BK / 8);
+            const int nacc = nsteps < Acc<BN, TALL>::kAcc ? nsteps : Acc<BN, TALL>::kAcc;  // accumulators written
+    #pragma unroll 1
+            for (int c0 = 0; c0 < BN; c0 += 32) {
+                float sum[32];
+    #pragma unroll 1
+                for (int q = 0; q < nacc; ++q) {
+                    uint32_t v[32];
+                    const uint32_t taddr =
+                        tmem + (static_cast<uint32_t>(warp * 32) << 16) + static_cast<uint32_t>(q * BN + c0);
+                    asm volatile(
+                        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+                        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+                        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+                          "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+                          "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]),
+                          "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]),
+                          "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+                        : "r"(taddr));
+                    asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+    #pragma unroll
+                    for (int j = 0; j < 32; ++j) sum[j] = q == 0 ? __uint_as_float(v[j]) : __fadd_rn(sum[j], __uint_as_float(v[j]));
+                }
+                if (crow && ws) {  // slice partial, row pitch Np = N rounded up to 4 (float4 stores)
+                    const int Np = (N + 3) & ~3;
+                    float4* wrow = reinterpret_cast<float4*>(ws + (static_cast<int64_t>(blockIdx.z) * M + row) * Np);
+    #pragma unroll
+                    for (int j = 0; j < 32; j += 4)
+                        if (n0 + c0 + j < Np) wrow[(n0 + c0 + j) >> 2] = make_float4(sum[j], sum[j + 1], sum[j + 2], sum[j + 3]);
+                } else if (crow) {
+                    // 16 B stores where the row pitch allows (a thread owns one output row: scalar
+                    // stores would cost one instruction per 4 B)
+                    const bool v4 = ((ldc & 3) == 0) && ((reinterpret_cast<uintptr_t>(C) & 15) == 0) &&
+                                    (!prow || ((push.ld & 3) == 0 && (reinterpret_cast<uintptr_t>(push.table) & 15) == 0));
+    #pragma unroll
+                    for (int j = 0; j < 32; j += 4) {
+                        const int col = n0 + c0 + j;
+                        if (v4 && col + 3 < N) {
+                            float4 x;
+                            x.x = gemm_epilogue_value(ep, sum[j], crow, col);
+                            x.y = gemm_epilogue_value(ep, sum[j + 1], crow, col + 1);
+                            x.z = gemm_epilogue_value(ep, sum[j + 2], crow, col + 2);
+                            x.w = gemm_epilogue_value(ep, sum[j + 3], crow, col + 3);
+                            *reinterpret_cast<float4*>(crow + col) = x;
                             if (prow) {
-                                prow[col + q] = x;
-                                flags |= table_flag_of(x);
+                                *reinterpret_cast<float4*>(prow + col) = x;
+                                flags |= table_flag_of(x.x) | table_flag_of(x.y) | table_flag_of(x.z) | table_flag_of(x.w);
+                            }
+                            continue;
+                        }
+    #pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            if (col + q < N) {
+                                const float x = gemm_epilogue_value(ep, sum[j + q], crow, col + q);
+                                crow[col + q] = x;
+                                if (prow) {
+                                    prow[col + q] = x;
+                                    flags |= table_flag_of(x);
+                                }
                             }
                         }
                     }
                 }
             }
-        }
-        if (ws) {
-            // parallel split-K fixup: every CTA of the tile publishes its slice, frees its TMEM
-            // (a peer CTA may be waiting for it on this SM), waits until all gridDim.z slices of
-            // the tile are in, then reduces its own 1/S of the tile's rows, summing the slices
-            // in slice order (deterministic, independent of arrival order)
-            __threadfence();
-            asm volatile("bar.sync 1, 128;\n" ::: "memory");
-            if (warp == 0) {
-                asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem),
-                             "r"(Acc<BN, TALL>::kCols));
-            }
-            const int S = static_cast<int>(gridDim.z);
-            int* arrive = reinterpret_cast<int*>(ws + ws_floats) + 2 * (blockIdx.y * gridDim.x + blockIdx.x);
-            if (threadIdx.x == 0) {
-                atomicAdd(arrive, 1);
-                for (uint32_t spins = 0;; ++spins) {
-                    int v;
-                    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];\n" : "=r"(v) : "l"(arrive) : "memory");
-                    if (v >= S) break;
-                    if (spins > (1u << 28)) __trap();  // grid <= #SMs: all slices are co-resident
-                    __nanosleep(64);
+            if (ws) {
+                // parallel split-K fixup: every CTA of the tile publishes its slice, frees its TMEM
+                // (a peer CTA may be waiting for it on this SM), waits until all gridDim.z slices of
+                // the tile are in, then reduces its own 1/S of the tile's rows, summing the slices
+                // in slice order (deterministic, independent of arrival order)
+                __threadfence();
+                asm volatile("bar.sync 1, 128;\n" ::: "memory");
+                if (warp == 0) {
+                    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem),
+                                 "r"(Acc<BN, TALL>::kCols));
                 }
-            }
-            asm volatile("bar.sync 1, 128;\n" ::: "memory");
-            const int Np = (N + 3) & ~3;
-            const int64_t slice = static_cast<int64_t>(M) * Np;
-            const int rows_per = (BM + S - 1) / S;
-            const int rlo = blockIdx.z * rows_per, rhi = min(BM, rlo + rows_per);
-            constexpr int kQ = BN / 4;  // float4 quads per tile row
-            for (int idx = threadIdx.x; idx < (rhi - rlo) * kQ; idx += 128) {
-                const int r = m0 + rlo + idx / kQ, c = n0 + 4 * (idx % kQ);
-                if (r >= M || c >= N) continue;
-                const float4* wp = reinterpret_cast<const float4*>(ws + static_cast<int64_t>(r) * Np + c);
-                float4 x = __ldcg(wp);
-                for (int z = 1; z < S; ++z) {
-                    const float4 y = __ldcg(wp + z * (slice >> 2));
-                    x = make_float4(__fadd_rn(x.x, y.x), __fadd_rn(x.y, y.y), __fadd_rn(x.z, y.z), __fadd_rn(x.w, y.w));
-                }
-                float* cr = C + static_cast<int64_t>(r) * ldc;
-                float* pr = push.table ? push.table + static_cast<int64_t>(push.ids[r]) * push.ld : nullptr;
-                const float xs[4] = {x.x, x.y, x.z, x.w};
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    if (c + k >= N) break;
-                    const float v = gemm_epilogue_value(ep, xs[k], cr, c + k);
-                    cr[c + k] = v;
-                    if (pr) {
-                        pr[c + k] = v;
-                        flags |= table_flag_of(v);
+                const int S = static_cast<int>(gridDim.z);
+                int* arrive = reinterpret_cast<int*>(ws + ws_floats) + 2 * (blockIdx.y * gridDim.x + blockIdx.x);
+                if (threadIdx.x == 0) {
+                    atomicAdd(arrive, 1);
+                    for (uint32_t spins = 0;; ++spins) {
+                        int v;
+                        asm volatile("ld.acquire.gpu.global.b32 %0, [%1];\n" : "=r"(v) : "l"(arrive) : "memory");
+                        if (v >= S) break;
+                        if (spins > (1u << 28)) __trap();  // grid <= #SMs: all slices are co-resident
+                        __nanosleep(64);
                     }
                 }
-                if (pr && c == 0 && push.stamps) push.stamps[push.ids[r]] = *push.step;
+                asm volatile("bar.sync 1, 128;\n" ::: "memory");
+                const int Np = (N + 3) & ~3;
+                const int64_t slice = static_cast<int64_t>(M) * Np;
+                const int rows_per = (BM + S - 1) / S;
+                const int rlo = blockIdx.z * rows_per, rhi = min(BM, rlo + rows_per);
+                constexpr int kQ = BN / 4;  // float4 quads per tile row
+                for (int idx = threadIdx.x; idx < (rhi - rlo) * kQ; idx += 128) {
+                    const int r = m0 + rlo + idx / kQ, c = n0 + 4 * (idx % kQ);
+                    if (r >= M || c >= N) continue;
+                    const float4* wp = reinterpret_cast<const float4*>(ws + static_cast<int64_t>(r) * Np + c);
+                    float4 x = __ldcg(wp);
+                    for (int z = 1; z < S; ++z) {
+                        const float4 y = __ldcg(wp + z * (slice >> 2));
+                        x = make_float4(__fadd_rn(x.x, y.x), __fadd_rn(x.y, y.y), __fadd_rn(x.z, y.z), __fadd_rn(x.w, y.w));
+                    }
+                    float* cr = C + static_cast<int64_t>(r) * ldc;
+                    float* pr = push.table ? push.table + static_cast<int64_t>(push.ids[r]) * push.ld : nullptr;
+                    const float xs[4] = {x.x, x.y, x.z, x.w};
+    #pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        if (c + k >= N) break;
+                        const float v = gemm_epilogue_value(ep, xs[k], cr, c + k);
+                        cr[c + k] = v;
+                        if (pr) {
+                            pr[c + k] = v;
+                            flags |= table_flag_of(v);
+                        }
+                    }
+                    if (pr && c == 0 && push.stamps) push.stamps[push.ids[r]] = *push.step;
+                }
+                if (threadIdx.x == 0 && atomicAdd(arrive + 1, 1) == S - 1) {  // last to leave resets
+                    arrive[0] = 0;
+                    arrive[1] = 0;
+                }
             }
-            if (threadIdx.x == 0 && atomicAdd(arrive + 1, 1) == S - 1) {  // last to leave resets
-                arrive[0] = 0;
-                arrive[1] = 0;
+            if (push.special) {
+                flags = __reduce_or_sync(0xffffffffu, flags);
+                if (lane == 0 && flags) atomicOr(push.special, flags);
             }
-        }
-        if (push.special) {
-            flags = __reduce_or_sync(0xffffffffu, flags);
-            if (lane == 0 && flags) atomicOr(push.special, flags);
         }
     }
     asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
