@@ -1124,11 +1124,8 @@ gasb_status gasb_trainer_create(gasb_schedule s, const float* h_features, int32_
         t->sched = &schedule_of(s);
         t->F = in_dim;
         t->C = num_classes;
-        if (!t->opt.fused) {
-            t->x_ext.alloc(0);
-        }
         t->build(h_features, h_labels, h_train_mask);
-        if (!t->opt.fused || true) {  // buffers for the reference-structured path (also used by push=0)
+        {  // V_b-row buffers: the reference-structured path, push = 0 batches and the residual heads
             const int64_t ldmax = t->ld_of(std::max(t->F, t->H));
             t->x_ext.alloc(static_cast<int64_t>(t->ne_max) * ldmax);
             t->h_ext.alloc(static_cast<int64_t>(t->ne_max) * ldmax);
