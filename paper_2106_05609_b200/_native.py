@@ -14,7 +14,7 @@ LIB_PATH = Path(os.environ.get("GASB_LIB", _PKG / "libgasb.so"))
 
 if not LIB_PATH.exists():
     raise ImportError(
-        f"libgasb.so not found at {LIB_PATH}: build it with `python -m paper_2106_05609_b200.build` "
+        f"libgasb.so not found at {LIB_PATH}: build it with `python paper_2106_05609_b200/build.py` "
         "(nvcc, sm_100a). There is no fallback implementation."
     )
 

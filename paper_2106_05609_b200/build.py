@@ -1,6 +1,6 @@
 """Builds libgasb.so in-tree with nvcc for sm_100a (cross-compiles without a GPU).
 
-    python -m paper_2106_05609_b200.build          # incremental (per-source objects)
+    python paper_2106_05609_b200/build.py          # incremental (per-source objects)
 """
 from __future__ import annotations
 
