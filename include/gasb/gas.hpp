@@ -409,6 +409,36 @@ class Trainer {
     Handle<gasb_trainer, gasb_trainer_destroy> h_;
 };
 
+// Data-parallel epochs over the GPUs of one node (no reference counterpart; csrc/dp.cu):
+// one process per GPU; the caller all-gathers export() from every rank (any transport)
+// and passes the concatenation to connect(). Replicas stay bit-identical.
+class DataParallel {
+  public:
+    DataParallel(Trainer& t, std::int32_t rank, std::int32_t world) {
+        gasb_dp d = nullptr;
+        check(gasb_dp_create(t.raw(), rank, world, &d));
+        h_ = Handle<gasb_dp, gasb_dp_destroy>(d);
+    }
+    std::vector<std::uint8_t> export_handle() const {
+        std::vector<std::uint8_t> h(GASB_DP_HANDLE_BYTES);
+        check(gasb_dp_export(h_.get(), h.data()));
+        return h;
+    }
+    void connect(std::span<const std::uint8_t> all_handles) { check(gasb_dp_connect(h_.get(), all_handles.data())); }
+    // enqueues one epoch (every rank calls it); check() synchronizes and reports barrier timeouts
+    void epoch_async(std::int64_t epoch, bool shuffle = true) { check(gasb_dp_epoch_async(h_.get(), epoch, shuffle)); }
+    void check_done() const { check(gasb_dp_check(h_.get())); }
+    // per-part losses of the parts this rank ran (0 elsewhere): sum over ranks for all parts
+    std::vector<double> part_losses(std::int32_t num_parts) const {
+        std::vector<double> l(static_cast<std::size_t>(num_parts));
+        check(gasb_dp_last_losses(h_.get(), l.data()));
+        return l;
+    }
+
+  private:
+    Handle<gasb_dp, gasb_dp_destroy> h_;
+};
+
 }  // namespace gas::b200
 
 #endif  // GASB_GAS_HPP

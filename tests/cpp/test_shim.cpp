@@ -97,6 +97,23 @@ int main() {
         EXPECT(back.step() == 0 && back.last_push_step(1, 1) == 0);
         EXPECT(throws<std::runtime_error>([&] { HistoryStore::load_checkpoint("/nonexistent/x.gash"); }));
         std::remove(path.c_str());
+        // a world-1 data-parallel trainer over the P3 graph: one epoch, both parts' losses
+        std::vector<float> feats{1.f, 0.f, 0.f, 1.f, 1.f, 1.f};
+        std::vector<std::int32_t> labels{0, 1, 0};
+        std::vector<std::uint8_t> mask{1, 1, 1};
+        ModelSpec spec;
+        spec.num_layers = 2;
+        spec.hidden = 4;
+        TrainerOptions topt;
+        topt.use_graphs = 0;
+        Trainer tr(s2, feats, 2, labels, mask, 2, spec, topt);
+        DataParallel dp(tr, 0, 1);
+        EXPECT(dp.export_handle().size() == GASB_DP_HANDLE_BYTES);
+        dp.epoch_async(0);
+        dp.check_done();
+        const std::vector<double> pl = dp.part_losses(2);
+        EXPECT(pl.size() == 2 && pl[0] > 0.0 && pl[1] > 0.0);
+        EXPECT(throws<std::invalid_argument>([&] { DataParallel bad(tr, 1, 1); }));
     } catch (const std::runtime_error& e) {
         have_gpu = false;
         std::printf("no device: %s\n", e.what());
