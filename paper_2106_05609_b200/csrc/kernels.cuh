@@ -149,6 +149,10 @@ void launch_adam(float* p, float* m, float* v, float* g, int64_t size, int64_t* 
                  float lr, float b1, float b2, float eps, float clip_max_norm, double* norm_scratch,
                  cudaStream_t st);
 void launch_zero(float* p, int64_t count, cudaStream_t st);
+// l2_penalty (tensor.cpp:649-678): g += 2 w p (before clip / Adam), *loss = float(*loss) + float(w sum p^2).
+// scratch: kNormBlocks doubles.
+void launch_l2_penalty(const float* p, float* g, int64_t size, float w, double* loss, double* scratch,
+                       cudaStream_t st);
 
 // ---- residual models: APPNP / GCNII (residual.cu) ---------------------------------------
 // out[i] = alpha * h0[rows[i]] + (1 - alpha) * prop[i]  (+ optional history push of out)

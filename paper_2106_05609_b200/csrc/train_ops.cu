@@ -162,6 +162,34 @@ void launch_adam(float* p, float* m, float* v, float* g, int64_t size, int64_t* 
     GASB_CUDA(cudaGetLastError());
 }
 
+// l2_penalty (tensor.cpp:649-678) as the reference's run_batch applies it (trainer.cpp:322-323):
+// its backward closure runs first, so every parameter gradient is g = (2 w v) + (data
+// gradient) — one fp32 rounding each, as `g[i] += gy * 2.0f * weight * v[i]` with gy = 1 —
+// and the loss becomes float(ce) + float(w * sum double(v)^2).
+__global__ void __launch_bounds__(256) l2_grad_kernel(const float* __restrict__ p, float* __restrict__ g,
+                                                      int64_t size, float two_w) {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < size;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        g[i] = __fadd_rn(__fmul_rn(two_w, p[i]), g[i]);
+}
+
+__global__ void l2_loss_kernel(const double* partial, int nparts, float w, double* loss) {
+    double acc = 0.0;
+    for (int i = 0; i < nparts; ++i) acc = __dadd_rn(acc, partial[i]);
+    const float pen = static_cast<float>(__dmul_rn(static_cast<double>(w), acc));
+    *loss = static_cast<double>(__fadd_rn(static_cast<float>(*loss), pen));
+}
+
+void launch_l2_penalty(const float* p, float* g, int64_t size, float w, double* loss, double* scratch,
+                       cudaStream_t st) {
+    sumsq_kernel<<<kNormBlocks, 256, 0, st>>>(p, size, scratch);
+    l2_loss_kernel<<<1, 1, 0, st>>>(scratch, kNormBlocks, w, loss);
+    const int64_t blocks = std::min<int64_t>(ceil_div(size, 256), 4 * 148);
+    l2_grad_kernel<<<static_cast<unsigned>(blocks), 256, 0, st>>>(p, g, size, 2.0f * w);  // exact
+    t_launches += 3;
+    GASB_CUDA(cudaGetLastError());
+}
+
 __global__ void zero_kernel(float* p, int64_t n) {
     for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x)

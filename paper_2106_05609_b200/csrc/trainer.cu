@@ -189,7 +189,7 @@ void gasb_trainer_s::build(const float* h_features, const int32_t* h_labels, con
             "trainer: the device path implements GCN, APPNP and GCNII (GIN is out of scope)");
     require(L >= 1 && H > 0 && F > 0 && C > 0, "trainer: bad model dims");
     require(spec.dropout == 0.0f, "trainer: dropout > 0 is not supported by the device path yet");
-    require(spec.l2_weight == 0.0f, "trainer: l2_weight > 0 is not supported by the device path yet");
+    require(spec.l2_weight >= 0.0f, "l2_penalty: negative weight");
     residual = spec.kind != 0;
     D = spec.kind == 2 ? C : H;  // Model::history_dim (trainer.cpp:130-140)
     hist_dim = L >= 2 ? (residual ? D : H) : 0;
@@ -411,7 +411,7 @@ void gasb_trainer_s::build(const float* h_features, const int32_t* h_labels, con
     adam_v.zero();
     t_counter.alloc(1);
     t_counter.zero();
-    norm_scratch.alloc(256);
+    norm_scratch.alloc(512);  // [0, 256): clip norm, [256, 512): l2 penalty
     ensure_bc(4096);
 
     // ---- HistoryStore(L-1, n, H) ----
@@ -712,6 +712,8 @@ void gasb_trainer_s::enqueue_batch_res(int32_t p, bool train, bool push, bool fu
             launch_colsum(zg.p, ldH, me, H, G(p_hb1), stream);
             launch_gemm(2, F, H, me, x_ext.p, ldF, zg.p, ldH, G(p_hw1), pp(p_hw1), plain, stream);
         }
+        if (spec.l2_weight > 0.0f)  // l2_penalty (tensor.cpp:649-678): loss term + 2 w p on every gradient
+            launch_l2_penalty(params.p, grads.p, nparam, spec.l2_weight, loss.p + p, norm_scratch.p + 256, stream);
         if (!dp)  // data-parallel: Adam runs on the cross-rank gradient sum (dp.cu)
             launch_adam(params.p, adam_m.p, adam_v.p, grads.p, nparam, t_counter.p, bc.p, spec.lr, spec.beta1,
                         spec.beta2, spec.eps, spec.clip_max_norm, norm_scratch.p, stream);
@@ -835,6 +837,8 @@ void gasb_trainer_s::enqueue_batch(int32_t p, bool train, bool push, bool use_ho
         }
         GASB_CUDA(cudaEventRecord(ev_join, side));  // every weight gradient is complete
         GASB_CUDA(cudaStreamWaitEvent(stream, ev_join, 0));
+        if (spec.l2_weight > 0.0f)  // l2_penalty (tensor.cpp:649-678): loss term + 2 w p on every gradient
+            launch_l2_penalty(params.p, grads.p, nparam, spec.l2_weight, loss.p + p, norm_scratch.p + 256, stream);
         if (!dp)  // data-parallel: Adam runs on the cross-rank gradient sum (dp.cu)
             launch_adam(params.p, adam_m.p, adam_v.p, grads.p, nparam, t_counter.p, bc.p, spec.lr, spec.beta1,
                         spec.beta2, spec.eps, spec.clip_max_norm, norm_scratch.p, stream);

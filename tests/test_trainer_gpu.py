@@ -181,3 +181,29 @@ def test_staged_features_pipeline_equals_set_features(oracle):
         out.append(tr.get_params())
     check(lib.gasb_host_unregister(C.c_void_p(x2.ctypes.data)))
     assert np.array_equal(out[0], out[1])
+
+
+@pytest.mark.parametrize("name", ["cora", "cora_gcnii"])
+def test_l2_penalty_teacher_forced(ref, name):
+    """l2_penalty (tensor.cpp:649-678, added to the loss in run_batch, trainer.cpp:322-323):
+    loss and parameter gradients against the compiled reference, teacher-forced."""
+    ds = make_dataset(name)
+    w = ds.workload
+    sched = gb.BatchSchedule.build(ds.graph, ds.assignment, w.parts)
+    spec = ModelSpec(kind=w.kind, num_layers=w.num_layers, hidden=w.hidden, seed=3, l2_weight=5e-3)
+    tr = GasTrainer(sched, ds.features, ds.labels, ds.train_mask, w.num_classes, spec,
+                    TrainerOptions(use_graphs=False))
+    rs = ref.session(ds.row_offsets, ds.cols, ds.features, ds.labels, ds.train_mask, w.num_classes, ds.assignment,
+                     w.parts, make_spec(kind=gb.trainer.KINDS[w.kind], num_layers=w.num_layers, hidden=w.hidden,
+                                        seed=3, l2_weight=5e-3))
+    for slot, p in enumerate([int(x) for x in ref.epoch_order(w.parts, 3, 0)[:4]]):
+        rs.set_params(tr.get_params())
+        for l in range(1, w.num_layers):
+            rs.set_history(l, tr.history.layer_matrix(l))
+        nb = int(sched.sizes(p)[0])
+        _, lg, lossg, gg, stg = tr.batch(p)
+        _, lo, losso, go, sto = rs.batch(p, 0, nb=nb)
+        assert stg == sto
+        if sto:
+            assert abs(lossg - losso) / abs(losso) <= TOL
+            assert normwise(gg, go) <= TOL

@@ -1,2 +1,2 @@
 python paper_2106_05609_b200/build.py >/dev/null 2>&1
-timeout 900 python -m pytest tests/test_shim_gpu.py tests/test_abi.py -x -q 2>&1 | tail -3
+timeout 900 python -m pytest tests/test_trainer_gpu.py -x -q 2>&1 | tail -3
