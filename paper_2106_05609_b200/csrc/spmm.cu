@@ -1169,6 +1169,7 @@ __global__ void __launch_bounds__(256) spmm_bwd_kernel(const int64_t* __restrict
 // stages the 32-column slice gy[:, chunk] (nsrc x 128 B) in smem once and every target of
 // its range gathers from smem; lane = column, entries in order -> same rounding sequence.
 constexpr int kBwdCW = 32;
+constexpr int kBwdRing = 8;  // metadata windows in flight per warp (spmm_bwd_smem_kernel)
 constexpr int kBwdThreads = 1024;
 
 __global__ void __launch_bounds__(kBwdThreads) spmm_bwd_smem_kernel(
@@ -1212,7 +1213,11 @@ __global__ void __launch_bounds__(kBwdThreads) spmm_bwd_smem_kernel(
     __syncthreads();
     // targets t = blockIdx.y + splits * k; warps claim k dynamically (power-law in-degrees)
     const int32_t splits = targets_per_cta;
-    int2* wbuf = reinterpret_cast<int2*>(sg + static_cast<int64_t>(nsrc) * kBwdCW) + warp * 32;
+    // per-warp ring of kBwdRing 32-entry windows of (source row, coeff), filled by cp.async
+    // kBwdRing windows ahead: a hub target (~1,100 intra-batch entries at C3) costs one
+    // metadata latency, not one per window
+    int32_t* ring_r = reinterpret_cast<int32_t*>(sg + static_cast<int64_t>(nsrc) * kBwdCW) + warp * kBwdRing * 64;
+    float* ring_c = reinterpret_cast<float*>(ring_r + kBwdRing * 32);
     auto claim = [&]() -> int32_t {
         int32_t k = 0;
         if (lane == 0) k = atomicAdd(&s_next, 1);
@@ -1232,38 +1237,46 @@ __global__ void __launch_bounds__(kBwdThreads) spmm_bwd_smem_kernel(
             e0n = rp[tn];
             e1n = rp[tn + 1];
         }
-        // metadata of the next 32 entries is loaded while the current 32 are accumulated; the
-        // current window is parked in shared memory as (row offset, coeff) pairs read back by
-        // broadcast LDS.64 (one shared-memory op per entry instead of two shuffles)
-        int64_t eb = e0;
-        int cnt = static_cast<int>((e1 - eb) < 32 ? (e1 - eb) : 32);
-        int32_t my_r = lane < cnt ? __ldg(src + eb + lane) : 0;
-        float my_c = lane < cnt ? __ldg(cf + eb + lane) : 0.0f;
+        const int32_t nw = static_cast<int32_t>((e1 - e0 + 31) >> 5);
+        int32_t issued = 0;
+        auto prefetch = [&] {
+            const int slot = issued % kBwdRing;
+            const int64_t e = e0 + 32LL * issued + lane;
+            if (e < e1) {
+                cp_async_ca4(ring_r + slot * 32 + lane, src + e);
+                cp_async_ca4(ring_c + slot * 32 + lane, cf + e);
+            }
+            cp_async_commit();
+            ++issued;
+        };
+#pragma unroll
+        for (int k = 0; k < kBwdRing; ++k)
+            if (issued < nw) prefetch();
         const float* sgl = sg + lane;
-        while (eb < e1) {
-            const int64_t nb = eb + 32;
-            const int ncnt = static_cast<int>(e1 - nb <= 0 ? 0 : (e1 - nb < 32 ? e1 - nb : 32));
-            const int32_t nr = lane < ncnt ? __ldg(src + nb + lane) : 0;
-            const float nc = lane < ncnt ? __ldg(cf + nb + lane) : 0.0f;
+        for (int32_t q = 0; q < nw; ++q) {
+            const int pending = issued - q - 1;  // windows after q that may still be in flight
+            if (pending >= 7) cp_async_wait<7>();
+            else if (pending == 6) cp_async_wait<6>();
+            else if (pending == 5) cp_async_wait<5>();
+            else if (pending == 4) cp_async_wait<4>();
+            else if (pending == 3) cp_async_wait<3>();
+            else if (pending == 2) cp_async_wait<2>();
+            else if (pending == 1) cp_async_wait<1>();
+            else cp_async_wait<0>();
             __syncwarp();
-            wbuf[lane] = make_int2(my_r * kBwdCW, __float_as_int(my_c));
-            __syncwarp();
+            const int slot = q % kBwdRing;
+            const int32_t* wr = ring_r + slot * 32;
+            const float* wc = ring_c + slot * 32;
+            const int64_t eb = e0 + 32LL * q;
+            const int cnt = static_cast<int>(e1 - eb < 32 ? e1 - eb : 32);
             if (cnt == 32) {
 #pragma unroll
-                for (int j = 0; j < 32; ++j) {
-                    const int2 rc = wbuf[j];
-                    a = __fadd_rn(a, __fmul_rn(__int_as_float(rc.y), sgl[rc.x]));
-                }
+                for (int j = 0; j < 32; ++j) a = __fadd_rn(a, __fmul_rn(wc[j], sgl[wr[j] * kBwdCW]));
             } else {
-                for (int j = 0; j < cnt; ++j) {
-                    const int2 rc = wbuf[j];
-                    a = __fadd_rn(a, __fmul_rn(__int_as_float(rc.y), sgl[rc.x]));
-                }
+                for (int j = 0; j < cnt; ++j) a = __fadd_rn(a, __fmul_rn(wc[j], sgl[wr[j] * kBwdCW]));
             }
-            eb = nb;
-            cnt = ncnt;
-            my_r = nr;
-            my_c = nc;
+            __syncwarp();  // the slot is free again
+            if (issued < nw) prefetch();
         }
         if (lane < ncol) gx[static_cast<int64_t>(t) * ldgx + col0 + lane] = keep ? a : 0.0f;
         t = tn;
@@ -1276,7 +1289,7 @@ void launch_spmm_bwd(const int64_t* t_rowptr, int32_t nt, const int32_t* t_src, 
                      const float* gy, int64_t ldgy, int32_t dim, const float* mask, int64_t ldm, float* gx,
                      int64_t ldgx, cudaStream_t st, int32_t nsrc, bool accumulate) {
     if (nt <= 0 || dim <= 0) return;
-    const int64_t smem = static_cast<int64_t>(nsrc) * kBwdCW * sizeof(float) + (kBwdThreads / 32) * 32 * 8;
+    const int64_t smem = static_cast<int64_t>(nsrc) * kBwdCW * sizeof(float) + (kBwdThreads / 32) * kBwdRing * 32 * 8;
     if (nsrc > 0 && smem <= 216 * 1024) {
         if (!g_bwd_smem_set) {
             GASB_CUDA(cudaFuncSetAttribute(spmm_bwd_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
