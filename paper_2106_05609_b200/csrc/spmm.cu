@@ -1175,7 +1175,7 @@ constexpr int kBwdThreads = 1024;
 __global__ void __launch_bounds__(kBwdThreads) spmm_bwd_smem_kernel(
     const int64_t* __restrict__ rp, int32_t nt, const int32_t* __restrict__ src, const float* __restrict__ cf,
     const float* __restrict__ gy, int64_t ldgy, int32_t nsrc, int32_t dim, const float* __restrict__ mask,
-    int64_t ldm, float* __restrict__ gx, int64_t ldgx, int32_t targets_per_cta, int accumulate) {
+    int64_t ldm, float* __restrict__ gx, int64_t ldgx, int32_t targets_per_cta, int accumulate, const int32_t* __restrict__ order) {
     extern __shared__ float sg[];  // nsrc x kBwdCW, then 32 (offset, coeff) pairs per warp
     __shared__ int32_t s_next;
     if (threadIdx.x == 0) s_next = 0;
@@ -1216,12 +1216,13 @@ __global__ void __launch_bounds__(kBwdThreads) spmm_bwd_smem_kernel(
     // per-warp ring of kBwdRing 32-entry windows of (source row, coeff), filled by cp.async
     // kBwdRing windows ahead: a hub target (~1,100 intra-batch entries at C3) costs one
     // metadata latency, not one per window
-    int32_t* ring_r = reinterpret_cast<int32_t*>(sg + static_cast<int64_t>(nsrc) * kBwdCW) + warp * kBwdRing * 64;
-    float* ring_c = reinterpret_cast<float*>(ring_r + kBwdRing * 32);
+    // (row, coeff) pairs interleaved so an entry is one broadcast LDS.64
+    int2* ring = reinterpret_cast<int2*>(sg + static_cast<int64_t>(nsrc) * kBwdCW) + warp * kBwdRing * 32;
     auto claim = [&]() -> int32_t {
         int32_t k = 0;
         if (lane == 0) k = atomicAdd(&s_next, 1);
-        return static_cast<int32_t>(blockIdx.y) + splits * __shfl_sync(0xffffffffu, k, 0);
+        const int32_t i = static_cast<int32_t>(blockIdx.y) + splits * __shfl_sync(0xffffffffu, k, 0);
+        return (order && i < nt) ? __ldg(order + i) : i;
     };
     // software-pipelined over targets: the next target is claimed and its row pointers loaded
     // while the current one accumulates
@@ -1243,8 +1244,9 @@ __global__ void __launch_bounds__(kBwdThreads) spmm_bwd_smem_kernel(
             const int slot = issued % kBwdRing;
             const int64_t e = e0 + 32LL * issued + lane;
             if (e < e1) {
-                cp_async_ca4(ring_r + slot * 32 + lane, src + e);
-                cp_async_ca4(ring_c + slot * 32 + lane, cf + e);
+                int2* dst = ring + slot * 32 + lane;
+                cp_async_ca4(&dst->x, src + e);
+                cp_async_ca4(&dst->y, cf + e);
             }
             cp_async_commit();
             ++issued;
@@ -1265,15 +1267,20 @@ __global__ void __launch_bounds__(kBwdThreads) spmm_bwd_smem_kernel(
             else cp_async_wait<0>();
             __syncwarp();
             const int slot = q % kBwdRing;
-            const int32_t* wr = ring_r + slot * 32;
-            const float* wc = ring_c + slot * 32;
+            const int2* w = ring + slot * 32;
             const int64_t eb = e0 + 32LL * q;
             const int cnt = static_cast<int>(e1 - eb < 32 ? e1 - eb : 32);
             if (cnt == 32) {
 #pragma unroll
-                for (int j = 0; j < 32; ++j) a = __fadd_rn(a, __fmul_rn(wc[j], sgl[wr[j] * kBwdCW]));
+                for (int j = 0; j < 32; ++j) {
+                    const int2 rc = w[j];
+                    a = __fadd_rn(a, __fmul_rn(__int_as_float(rc.y), sgl[rc.x * kBwdCW]));
+                }
             } else {
-                for (int j = 0; j < cnt; ++j) a = __fadd_rn(a, __fmul_rn(wc[j], sgl[wr[j] * kBwdCW]));
+                for (int j = 0; j < cnt; ++j) {
+                    const int2 rc = w[j];
+                    a = __fadd_rn(a, __fmul_rn(__int_as_float(rc.y), sgl[rc.x * kBwdCW]));
+                }
             }
             __syncwarp();  // the slot is free again
             if (issued < nw) prefetch();
@@ -1287,7 +1294,7 @@ static int g_bwd_smem_set = 0;
 
 void launch_spmm_bwd(const int64_t* t_rowptr, int32_t nt, const int32_t* t_src, const float* t_coeffs,
                      const float* gy, int64_t ldgy, int32_t dim, const float* mask, int64_t ldm, float* gx,
-                     int64_t ldgx, cudaStream_t st, int32_t nsrc, bool accumulate) {
+                     int64_t ldgx, cudaStream_t st, int32_t nsrc, bool accumulate, const int32_t* order) {
     if (nt <= 0 || dim <= 0) return;
     const int64_t smem = static_cast<int64_t>(nsrc) * kBwdCW * sizeof(float) + (kBwdThreads / 32) * kBwdRing * 32 * 8;
     if (nsrc > 0 && smem <= 216 * 1024) {
@@ -1308,7 +1315,7 @@ void launch_spmm_bwd(const int64_t* t_rowptr, int32_t nt, const int32_t* t_src, 
             std::max<int64_t>(1, std::min<int64_t>(sms / nchunks, ceil_div(nt, kBwdThreads / 32))));
         dim3 grid(static_cast<unsigned>(nchunks), static_cast<unsigned>(splits));
         spmm_bwd_smem_kernel<<<grid, kBwdThreads, smem, st>>>(t_rowptr, nt, t_src, t_coeffs, gy, ldgy, nsrc, dim,
-                                                             mask, ldm, gx, ldgx, splits, accumulate ? 1 : 0);
+                                                             mask, ldm, gx, ldgx, splits, accumulate ? 1 : 0, order);
         ++t_launches;
         GASB_CUDA(cudaGetLastError());
         return;

@@ -337,6 +337,19 @@ void gasb_trainer_s::build(const float* h_features, const int32_t* h_labels, con
     t_src.upload(h_tsrc);
     t_cf.upload(h_tcf);
     t_rowptr.upload(h_trp);
+    {  // per part: intra-batch targets heaviest first (spmm_bwd claims them in this order)
+        std::vector<int32_t> h_ord(static_cast<size_t>(R));
+#pragma omp parallel for schedule(dynamic, 1)
+        for (int32_t p = 0; p < num_parts; ++p) {
+            int32_t* o = h_ord.data() + row_off[p];
+            const int64_t* trp = h_trp.data() + row_off[p] + p;
+            std::iota(o, o + nb[p], 0);
+            std::stable_sort(o, o + nb[p], [&](int32_t a, int32_t b) {
+                return trp[a + 1] - trp[a] > trp[b + 1] - trp[b];
+            });
+        }
+        t_order.upload(h_ord);
+    }
     train_rows.upload(h_trr);
     train_labels.upload(h_trl);
     row_label.upload(h_rlab);
@@ -691,7 +704,7 @@ void gasb_trainer_s::enqueue_batch_res(int32_t p, bool train, bool push, bool fu
             launch_mix_bwd(dmix, ldm, m, D, spec.alpha, br, h0g.p, ldD, dprop.p, ldD, stream);
             if (l >= 2) {  // to act_{l-1}'s batch rows (compose bwd), relu mask for GCNII
                 launch_spmm_bwd(t_rowptr.p + r0 + p, m, t_src.p, t_cf.p, dprop.p, ldD, D, gcnii ? act[l - 1].p : nullptr,
-                                ldD, gout.p, ldD, stream, m);
+                                ldD, gout.p, ldD, stream, m, false, t_order.p + r0);
                 dout = gout.p;
                 ldo = ldD;
             } else {  // layer 1: every V_b row of h0, accumulated onto the residual terms
@@ -821,7 +834,7 @@ void gasb_trainer_s::enqueue_batch(int32_t p, bool train, bool push, bool use_ho
                 // gradient first, then the dgrad GEMM and the relu mask: A^T (g W^T) == (A^T g) W^T,
                 // dout/din of the gather work (reassociation only; within the 1e-5 grad contract)
                 launch_spmm_bwd(t_rowptr.p + r0 + p, m, t_src.p, t_cf.p, g, ldg, dout, nullptr, 0, g_agg.p, ldC,
-                                stream, m);
+                                stream, m, false, t_order.p + r0);
                 launch_gemm(1, m, din, dout, g_agg.p, ldC, W(l), pp(layer_param[l]), go, ldH, 0.f, false, nullptr,
                             stream);
                 launch_mask(go, ldH, act[l - 1].p, ldH, m, din, stream);
@@ -830,7 +843,7 @@ void gasb_trainer_s::enqueue_batch(int32_t p, bool train, bool push, bool use_ho
                             stream);
                 // aggregate backward over intra-batch edges + compose bwd + relu bwd (mask = act)
                 launch_spmm_bwd(t_rowptr.p + r0 + p, m, t_src.p, t_cf.p, g_agg.p, ldH, din, act[l - 1].p, ldH, go,
-                                ldH, stream, m);
+                                ldH, stream, m, false, t_order.p + r0);
             }
             g = go;
             ldg = ldH;

@@ -103,6 +103,7 @@ struct gasb_trainer_s {
     DevBuf<double> coef64;
     DevBuf<float> t_cf;
     DevBuf<int64_t> t_rowptr;
+    DevBuf<int32_t> t_order;  // per part: intra-batch targets by descending entry count
     SegTable seg_batch, seg_all;
     DevBuf<int32_t> counters, row_label, xflags, ce_done;  // xflags: value flags of X (kernels.cuh)
     DevBuf<double> partial_batch, partial_all;
