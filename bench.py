@@ -78,6 +78,37 @@ def spmm_bytes(nb: int, ne: int, nnz: int, d: int) -> tuple[float, float]:
     return 8 * (nb + 1) + 8 * nnz + 4 * d * ne + 4 * d * nb, 4.0 * d * nnz
 
 
+def epoch_roofline(sched, w, ms_per_epoch: float, gpus: int = 1) -> dict:
+    """Epoch-level roofline (SURVEY §8d "roofline fraction"): t_min = algorithmic bytes /
+    HBM peak + tensor-core flops / TF32 peak, against the measured epoch. Bytes: the per-batch
+    SpMM compulsory model for layers 2..L, layer 1 hoisted (stencil + X once + output), the
+    intra-batch SpMM backward (gy + gx rows + pointers; its ~8 B/entry is omitted), pushes and
+    Adam; flops: 3xTF32 = 3 MMAs per fwd / dgrad / wgrad GEMM."""
+    F, H, C, L = w.in_dim, w.hidden, w.num_classes, w.num_layers
+    dims = [F] + [H] * (L - 1) + [C]
+    by, fl, E = 0.0, 0.0, 0
+    for p in range(w.parts):
+        nb, ne, _, _, nnz, _ = (int(v) for v in sched.sizes(p))
+        E += nnz
+        for _ in range(1, L):  # layers 2..L gather d = H
+            by += spmm_bytes(nb, ne, nnz, H)[0]
+        by += (L - 1) * (8 * (nb + 1) + 8 * H * nb)  # backward over batch rows
+        by += (L - 1) * nb * (8 * H + 4)  # pushes
+        fwd = sum(2.0 * nb * dims[l] * dims[l + 1] for l in range(L))
+        dgrad = sum(2.0 * nb * dims[l] * dims[l + 1] for l in range(1, L))
+        fl += 3 * (2 * fwd + dgrad)  # fwd + wgrad (same flops) + dgrad, 3 MMAs each
+    by += 12.0 * E + 8.0 * w.num_nodes * F  # hoisted layer 1: stencil, X once, output
+    try:
+        pk = json.loads(PEAKS.read_text())
+        tc = float(pk["bf16_tflops"]) / 2  # dense TF32 = half the dense bf16 rate
+    except Exception:
+        tc = 1125.0
+    hbm, _ = peak_hbm()
+    t_min = (by / (hbm * 1e9) + fl / (tc * 1e12)) / gpus  # data-parallel: the epoch's work splits over gpus
+    return {"gpus": gpus, "bytes_GB": by / 1e9, "tflop": fl / 1e12, "t_min_ms": 1e3 * t_min, "measured_ms": ms_per_epoch,
+            "frac": 1e3 * t_min / ms_per_epoch, "hbm_GBps": hbm, "tf32_TFLOPs": tc}
+
+
 def peak_hbm() -> tuple[float, str]:
     try:
         return float(json.loads(PEAKS.read_text())["hbm_gbs"]), "measured"
@@ -304,7 +335,7 @@ def run_ours(args):
         "config": workload_config(ds, f"dp{ws} (partition batches split over ranks, peer-memory exchange)"
                                   if ws > 1 else "single-gpu"),
         "e2e": e2e, "gpu_launches": launches, "roofline": roof, "clocks": clk, "final_loss": loss,
-        "history_pull_GBps": pull, **extra,
+        "history_pull_GBps": pull, "epoch_roofline": epoch_roofline(sched, w, ms / args.steps, ws), **extra,
     }
     if rank == 0 and ws == 1 and not args.no_cpu:
         line["cpu_baseline"] = cpu_baseline(ds, args.cpu_sample)
