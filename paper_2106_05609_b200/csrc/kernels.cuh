@@ -148,9 +148,11 @@ void launch_softmax_ce(const float* logits, int64_t ldl, int32_t m, int32_t n, c
                        cudaStream_t st);
 // AdamState::step (nn.cpp:20-41) over the flat parameter vector; bias corrections from
 // bc[2*t], t = ++(*t_counter) on device. clip_max_norm > 0 applies grad_clip first.
+// end_step (optional): the end of the batch fused in — the last block advances *end_step and
+// *t_counter (end_done: a zero-initialised, self-resetting int).
 void launch_adam(float* p, float* m, float* v, float* g, int64_t size, int64_t* t_counter, const double* bc,
                  float lr, float b1, float b2, float eps, float clip_max_norm, double* norm_scratch,
-                 cudaStream_t st);
+                 cudaStream_t st, int64_t* end_step = nullptr, int32_t* end_done = nullptr);
 void launch_zero(float* p, int64_t count, cudaStream_t st);
 // l2_penalty (tensor.cpp:649-678): g += 2 w p (before clip / Adam), *loss = float(*loss) + float(w sum p^2).
 // scratch: kNormBlocks doubles.

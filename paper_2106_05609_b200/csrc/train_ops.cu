@@ -119,9 +119,9 @@ constexpr int kNormBlocks = 128;
 
 __global__ void __launch_bounds__(256) adam_kernel(float* __restrict__ p, float* __restrict__ m, float* __restrict__ v,
                                                    const float* __restrict__ g, int64_t size,
-                                                   const int64_t* __restrict__ t_counter, const double* __restrict__ bc,
+                                                   int64_t* t_counter, const double* __restrict__ bc,
                                                    float lr, float b1, float b2, float eps, float clip,
-                                                   const double* __restrict__ norm) {
+                                                   const double* __restrict__ norm, int64_t* __restrict__ end_step, int32_t* __restrict__ end_done) {
     const int64_t t = *t_counter + 1;
     const double bc1 = bc[2 * t], bc2 = bc[2 * t + 1];
     float s = 1.0f;
@@ -146,10 +146,22 @@ __global__ void __launch_bounds__(256) adam_kernel(float* __restrict__ p, float*
         const double upd = __ddiv_rn(__dmul_rn(LR, mhat), __dadd_rn(__dsqrt_rn(vhat), EPS));
         p[e] = static_cast<float>(__dsub_rn(static_cast<double>(p[e]), upd));
     }
+    if (end_step) {  // end of batch fused in: the last block to finish advances the counters
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            if (atomicAdd(end_done, 1) == static_cast<int32_t>(gridDim.x) - 1) {
+                *end_step += 1;  // HistoryStore::advance_step (trainer.cpp:426)
+                *t_counter += 1;  // AdamState::step count
+                *end_done = 0;
+            }
+        }
+    }
 }
 
 void launch_adam(float* p, float* m, float* v, float* g, int64_t size, int64_t* t_counter, const double* bc, float lr,
-                 float b1, float b2, float eps, float clip_max_norm, double* norm_scratch, cudaStream_t st) {
+                 float b1, float b2, float eps, float clip_max_norm, double* norm_scratch, cudaStream_t st,
+                 int64_t* end_step, int32_t* end_done) {
     if (clip_max_norm > 0.0f) {
         sumsq_kernel<<<kNormBlocks, 256, 0, st>>>(g, size, norm_scratch);
         finish_norm_kernel<<<1, 1, 0, st>>>(norm_scratch, kNormBlocks);
@@ -157,7 +169,8 @@ void launch_adam(float* p, float* m, float* v, float* g, int64_t size, int64_t* 
     }
     const int64_t blocks = std::min<int64_t>(ceil_div(size, 256), 4 * 148);
     adam_kernel<<<static_cast<unsigned>(blocks), 256, 0, st>>>(p, m, v, g, size, t_counter, bc, lr, b1, b2, eps,
-                                                               clip_max_norm, norm_scratch + kNormBlocks);
+                                                               clip_max_norm, norm_scratch + kNormBlocks, end_step,
+                                                               end_done);
     ++t_launches;
     GASB_CUDA(cudaGetLastError());
 }

@@ -424,6 +424,8 @@ void gasb_trainer_s::build(const float* h_features, const int32_t* h_labels, con
     adam_v.zero();
     t_counter.alloc(1);
     t_counter.zero();
+    adam_done.alloc(1);
+    adam_done.zero();
     norm_scratch.alloc(512);  // [0, 256): clip norm, [256, 512): l2 penalty
     ensure_bc(4096);
 
@@ -727,9 +729,12 @@ void gasb_trainer_s::enqueue_batch_res(int32_t p, bool train, bool push, bool fu
         }
         if (spec.l2_weight > 0.0f)  // l2_penalty (tensor.cpp:649-678): loss term + 2 w p on every gradient
             launch_l2_penalty(params.p, grads.p, nparam, spec.l2_weight, loss.p + p, norm_scratch.p + 256, stream);
-        if (!dp)  // data-parallel: Adam runs on the cross-rank gradient sum (dp.cu)
+        if (!dp) {  // data-parallel: Adam runs on the cross-rank gradient sum (dp.cu)
             launch_adam(params.p, adam_m.p, adam_v.p, grads.p, nparam, t_counter.p, bc.p, spec.lr, spec.beta1,
-                        spec.beta2, spec.eps, spec.clip_max_norm, norm_scratch.p, stream);
+                        spec.beta2, spec.eps, spec.clip_max_norm, norm_scratch.p, stream, history_step_ptr(hist),
+                        adam_done.p);  // + the end of the batch
+            return;
+        }
     }
     if (dp) return;
     end_batch_kernel<<<1, 1, 0, stream>>>(history_step_ptr(hist), t_counter.p, stepped ? 1 : 0);
@@ -837,7 +842,7 @@ void gasb_trainer_s::enqueue_batch(int32_t p, bool train, bool push, bool use_ho
                                 stream, m, false, t_order.p + r0);
                 launch_gemm(1, m, din, dout, g_agg.p, ldC, W(l), pp(layer_param[l]), go, ldH, 0.f, false, nullptr,
                             stream);
-                launch_mask(go, ldH, act[l - 1].p, ldH, m, din, stream);
+                launch_mask(go, ldH, act[l - 1].p, ldH, m, din, stream);  // relu backward (mask = act_{l-1})
             } else {
                 launch_gemm(1, m, din, dout, g, ldg, W(l), pp(layer_param[l]), g_agg.p, ldH, 0.f, false, nullptr,
                             stream);
@@ -852,9 +857,12 @@ void gasb_trainer_s::enqueue_batch(int32_t p, bool train, bool push, bool use_ho
         GASB_CUDA(cudaStreamWaitEvent(stream, ev_join, 0));
         if (spec.l2_weight > 0.0f)  // l2_penalty (tensor.cpp:649-678): loss term + 2 w p on every gradient
             launch_l2_penalty(params.p, grads.p, nparam, spec.l2_weight, loss.p + p, norm_scratch.p + 256, stream);
-        if (!dp)  // data-parallel: Adam runs on the cross-rank gradient sum (dp.cu)
+        if (!dp) {  // data-parallel: Adam runs on the cross-rank gradient sum (dp.cu)
             launch_adam(params.p, adam_m.p, adam_v.p, grads.p, nparam, t_counter.p, bc.p, spec.lr, spec.beta1,
-                        spec.beta2, spec.eps, spec.clip_max_norm, norm_scratch.p, stream);
+                        spec.beta2, spec.eps, spec.clip_max_norm, norm_scratch.p, stream, history_step_ptr(hist),
+                        adam_done.p);  // + the end of the batch
+            return;
+        }
     }
     if (dp) return;
     end_batch_kernel<<<1, 1, 0, stream>>>(history_step_ptr(hist), t_counter.p, stepped ? 1 : 0);

@@ -120,6 +120,7 @@ struct gasb_trainer_s {
     std::vector<float> h_params_init;
     DevBuf<float> params, grads, adam_m, adam_v;
     DevBuf<int64_t> t_counter;
+    DevBuf<int32_t> adam_done;  // Adam's fused end-of-batch arrival counter
     DevBuf<double> bc, norm_scratch;
     int64_t bc_cap = 0, t_host = 0;
 
