@@ -89,8 +89,15 @@ typedef struct gasb_schedule_s* gasb_schedule;
  * flags & GASB_PLAN_FULL also materializes plan.local_graph and the `sum` stencil (only
  * needed for parity checks / GIN); the GCN stencil and node lists are always built. */
 #define GASB_PLAN_FULL 1
+/* flags & GASB_PLAN_DEVICE builds every plan on the current CUDA device (GPU batch-plan
+ * builder: part x node bitmaps + popcount scans, bit-exact with the host
+ * builder) and copies the results into the schedule; same errors. */
+#define GASB_PLAN_DEVICE 2
 gasb_status gasb_schedule_build(gasb_graph g, const int32_t* h_assignment, int32_t num_parts, int32_t flags,
                                 gasb_schedule* out);
+/* Build timing: device_ms = GPU time of the device builder (-1 for host builds), total_ms =
+ * wall time of gasb_schedule_build (inputs, kernels and copies into the host plans). */
+gasb_status gasb_schedule_timing(gasb_schedule s, double* device_ms, double* total_ms);
 /* Single plan for an explicit sorted batch (make_batch_plan semantics and errors). */
 gasb_status gasb_schedule_build_batches(gasb_graph g, const int32_t* const* h_batches, const int64_t* sizes,
                                         int32_t num_batches, int32_t flags, gasb_schedule* out);

@@ -74,6 +74,7 @@ _SIGS = {
     "gasb_schedule_build": (i32, [vp, vp, i32, i32, P(vp)]),
     "gasb_schedule_build_batches": (i32, [vp, vp, vp, i32, i32, P(vp)]),
     "gasb_schedule_num_parts": (i32, [vp, P(i32)]),
+    "gasb_schedule_timing": (i32, [vp, P(f64), P(f64)]),
     "gasb_plan_sizes": (i32, [vp, i32, vp]),
     "gasb_plan_copy": (i32, [vp, i32] + [vp] * 13),
     "gasb_schedule_destroy": (i32, [vp]),

@@ -83,11 +83,16 @@ struct Schedule {
     const Graph* graph = nullptr;
     int32_t num_parts = 0;
     std::vector<HostPlan> plans;
+    double device_ms = -1.0;  // GPU builder: device time (event-timed) and wall time incl. copies
+    double total_ms = -1.0;
 };
 
 // Builds one plan with caller scratch (size n each), bit-exact with make_batch_plan +
 // build_plan_aggregation. `full` also materializes local_graph and the sum stencil.
 void build_plan(const Graph& g, const int32_t* batch, int64_t nb, bool full, HostPlan& out,
                 std::vector<uint8_t>& mark, std::vector<int32_t>& g2l);
+
+// The same schedule built on the current CUDA device (plan_dev.cu), bit-exact with build_plan.
+void build_schedule_device(const Graph& g, const int32_t* assignment, int32_t num_parts, bool full, Schedule& out);
 
 }  // namespace gasb

@@ -11,6 +11,7 @@
 #include <omp.h>
 
 #include <cerrno>
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <random>
@@ -376,6 +377,20 @@ gasb_status gasb_schedule_build(gasb_graph g, const int32_t* assignment, int32_t
         require(g && assignment && out, "schedule_build: null argument");
         require(num_parts > 0, "schedule_build: num_parts must be positive");
         const Graph& G = g->g;
+        if (flags & GASB_PLAN_DEVICE) {
+            auto* h = new gasb_schedule_s();
+            try {
+                const auto t0 = std::chrono::steady_clock::now();
+                build_schedule_device(G, assignment, num_parts, (flags & GASB_PLAN_FULL) != 0, h->s);
+                h->s.total_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+            } catch (...) {
+                delete h;
+                throw;
+            }
+            *out = h;
+            return;
+        }
+        const auto t0 = std::chrono::steady_clock::now();
         // partition_from_assignment (partition.cpp:314-328): parts sorted, non-empty.
         std::vector<std::vector<int32_t>> parts(static_cast<size_t>(num_parts));
         for (int32_t v = 0; v < G.num_nodes; ++v) {
@@ -390,6 +405,7 @@ gasb_status gasb_schedule_build(gasb_graph g, const int32_t* assignment, int32_t
             delete h;
             throw;
         }
+        h->s.total_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
         *out = h;
     });
 }
@@ -415,6 +431,14 @@ gasb_status gasb_schedule_num_parts(gasb_schedule s, int32_t* out) {
     return guard([&] {
         require(s && out, "schedule: null argument");
         *out = s->s.num_parts;
+    });
+}
+
+gasb_status gasb_schedule_timing(gasb_schedule s, double* device_ms, double* total_ms) {
+    return guard([&] {
+        require(s, "schedule: null argument");
+        if (device_ms) *device_ms = s->s.device_ms;
+        if (total_ms) *total_ms = s->s.total_ms;
     });
 }
 

@@ -10,7 +10,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
-from ._native import SynthParams, check, i32, i64, lib, ptr, vp
+from ._native import SynthParams, check, f64, i32, i64, lib, ptr, vp
 
 
 class Graph:
@@ -123,13 +123,23 @@ class BatchSchedule:
         return self._h
 
     @staticmethod
-    def build(graph: Graph, assignment: np.ndarray, num_parts: int, full: bool = False) -> "BatchSchedule":
+    def build(graph: Graph, assignment: np.ndarray, num_parts: int, full: bool = False,
+              device: bool = False) -> "BatchSchedule":
+        """device=True runs the GPU batch-plan builder (plan_dev.cu) on the current CUDA
+        device; the plans are bit-identical to the host builder's."""
         a = np.ascontiguousarray(assignment, dtype=np.int32)
         if len(a) != graph.num_nodes:
             raise ValueError("partition: assignment length != num_nodes")
         h = vp()
-        check(lib.gasb_schedule_build(graph.handle, ptr(a), int(num_parts), 1 if full else 0, C.byref(h)))
+        flags = (1 if full else 0) | (2 if device else 0)
+        check(lib.gasb_schedule_build(graph.handle, ptr(a), int(num_parts), flags, C.byref(h)))
         return BatchSchedule(h.value, graph)
+
+    def timing(self) -> tuple[float, float]:
+        """(device_ms, total_ms) of the build; device_ms is -1 for host builds."""
+        d, t = f64(), f64()
+        check(lib.gasb_schedule_timing(self._h, C.byref(d), C.byref(t)))
+        return d.value, t.value
 
     def sizes(self, part: int) -> np.ndarray:
         z = np.zeros(6, np.int64)
