@@ -25,6 +25,9 @@
 #include <omp.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <memory>
@@ -180,6 +183,15 @@ __global__ void __launch_bounds__(256) repitch_flags_kernel(const float* __restr
 using namespace gasb;
 
 void gasb_trainer_s::build(const float* h_features, const int32_t* h_labels, const uint8_t* h_train) {
+    // GASB_TRACE_SETUP=1: wall time of each setup phase on stderr
+    const bool trace_on = std::getenv("GASB_TRACE_SETUP") != nullptr;
+    auto t_last = std::chrono::steady_clock::now();
+    auto trace = [&](const char* what) {
+        if (!trace_on) return;
+        const auto now = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "[setup] %-28s %8.1f ms\n", what, std::chrono::duration<double, std::milli>(now - t_last).count());
+        t_last = now;
+    };
     const Graph& g = *sched->graph;
     n = g.num_nodes;
     num_parts = sched->num_parts;
@@ -236,17 +248,20 @@ void gasb_trainer_s::build(const float* h_features, const int32_t* h_labels, con
         ne_max = std::max(ne_max, ne[p]);
     }
     const int64_t R = row_off[num_parts], E = edge_off[num_parts], T = t_off[num_parts], NE = ext_off[num_parts];
+    trace("sizes");
 
     // ---- host staging of the concatenated stencils ----
-    std::vector<int32_t> h_bn(R), h_cg(E), h_cl(E), h_tsrc(T), h_trr(tr_off[num_parts]), h_trl(tr_off[num_parts]);
-    std::vector<int32_t> h_ext(NE), h_cidx(NE), h_rlab(R);
-    std::vector<double> h_cf(E);
-    std::vector<float> h_tcf(T);
+    std::vector<int32_t> h_bn(R), h_trr(tr_off[num_parts]), h_trl(tr_off[num_parts]);
+    HVec<int32_t> h_cg(E), h_cl(E), h_tsrc(T), h_ext(NE), h_cidx(NE);
+    std::vector<int32_t> h_rlab(R);
+    HVec<double> h_cf(E);
+    HVec<float> h_tcf(T);
     std::vector<int64_t> h_rp(R + 1), h_trp(R + num_parts);
     h_rp[R] = E;
     // residual models: batch_local_rows, and the all-edge CSC for the layer-1 backward
-    std::vector<int32_t> h_brow, h_asrc;
-    std::vector<float> h_acf;
+    std::vector<int32_t> h_brow;
+    HVec<int32_t> h_asrc;
+    HVec<float> h_acf;
     std::vector<int64_t> h_arp;
     if (residual) {
         h_brow.resize(R);
@@ -323,6 +338,7 @@ void gasb_trainer_s::build(const float* h_features, const int32_t* h_labels, con
     }
     for (int32_t i = 0; i < static_cast<int32_t>(h_trl.size()); ++i)
         require(h_trl[i] >= 0 && h_trl[i] < C, "softmax_cross_entropy: label out of range");
+    trace("host staging");
 
     GASB_CUDA(cudaSetDevice(opt.device));
     GASB_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
@@ -330,6 +346,7 @@ void gasb_trainer_s::build(const float* h_features, const int32_t* h_labels, con
     GASB_CUDA(cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking));
     GASB_CUDA(cudaEventCreateWithFlags(&ev_staged, cudaEventDisableTiming));
     GASB_CUDA(cudaEventCreateWithFlags(&ev_stage_free, cudaEventDisableTiming));
+    trace("cuda context + streams");
     batch_nodes.upload(h_bn);
     cols_g.upload(h_cg);
     cols_l.upload(h_cl);
@@ -350,6 +367,7 @@ void gasb_trainer_s::build(const float* h_features, const int32_t* h_labels, con
         }
         t_order.upload(h_ord);
     }
+    trace("stencil uploads + t_order");
     train_rows.upload(h_trr);
     train_labels.upload(h_trl);
     row_label.upload(h_rlab);
@@ -364,6 +382,7 @@ void gasb_trainer_s::build(const float* h_features, const int32_t* h_labels, con
         std::vector<int64_t> one{0, R};
         build_segments(h_rp, one, opt.seg_edges > 0, false, seg_all);
     }
+    trace("segments");
     max_chunks = static_cast<int32_t>(ceil_div(std::max(F, H), 64));
     counters.alloc(R * max_chunks);
     counters.zero();
@@ -384,6 +403,7 @@ void gasb_trainer_s::build(const float* h_features, const int32_t* h_labels, con
     launch_scan_special(X.p, n, ldF, F, xflags.p, nullptr);
     ce_done.alloc(1);
     ce_done.zero();
+    trace("features");
 
     // ---- Model::build (trainer.cpp:55-129); params in Model::params() order ----
     layer_param.assign(static_cast<size_t>(L) + 1, -1);
@@ -431,6 +451,7 @@ void gasb_trainer_s::build(const float* h_features, const int32_t* h_labels, con
 
     // ---- HistoryStore(L-1, n, H) ----
     hist = history_create(std::max(0, L - 1), n, hist_dim);
+    trace("params + history");
 
     // ---- activations ----
     agg.resize(static_cast<size_t>(L) + 1);
@@ -467,6 +488,7 @@ void gasb_trainer_s::build(const float* h_features, const int32_t* h_labels, con
     graphs.assign(num_parts, nullptr);
     graph_launches.assign(num_parts, 0);
     GASB_CUDA(cudaDeviceSynchronize());
+    trace("activations + sync");
 }
 
 // Layer 1 hoisted over a subset of parts (one data-parallel rank's batches of an epoch):
@@ -561,8 +583,8 @@ void gasb_trainer_s::enqueue_hoisted() {
                     counters.p, max_chunks, stream, source_flags(1), source_tmap(1));
 }
 
-void gasb_trainer_s::build_residual(const std::vector<int64_t>& h_arp, const std::vector<int32_t>& h_asrc,
-                                    const std::vector<float>& h_acf, const std::vector<int32_t>& h_brow) {
+void gasb_trainer_s::build_residual(const std::vector<int64_t>& h_arp, const HVec<int32_t>& h_asrc,
+                                    const HVec<float>& h_acf, const std::vector<int32_t>& h_brow) {
     brow.upload(h_brow);
     a_rowptr.upload(h_arp);
     a_src.upload(h_asrc);

@@ -3,6 +3,8 @@
 #pragma once
 
 #include <algorithm>
+#include <memory>
+#include <utility>
 #include <vector>
 
 #include "gasb_internal.hpp"
@@ -18,6 +20,30 @@ int64_t* history_stamps(gasb_history h, int32_t layer);
 int64_t* history_step_ptr(gasb_history h);
 int32_t* history_flags(gasb_history h, int32_t layer);
 
+// Host staging vectors whose elements are default-initialised (not zeroed): the setup loops
+// write every element from OpenMP threads, so the pages are first touched in parallel
+// instead of by a serial zero-fill on the constructing thread.
+template <class T>
+struct UninitAlloc : std::allocator<T> {
+    template <class U>
+    struct rebind {
+        using other = UninitAlloc<U>;
+    };
+    UninitAlloc() = default;
+    template <class U>
+    UninitAlloc(const UninitAlloc<U>&) noexcept {}
+    template <class U>
+    void construct(U* q) noexcept {
+        ::new (static_cast<void*>(q)) U;
+    }
+    template <class U, class... A>
+    void construct(U* q, A&&... a) {
+        ::new (static_cast<void*>(q)) U(std::forward<A>(a)...);
+    }
+};
+template <class T>
+using HVec = std::vector<T, UninitAlloc<T>>;
+
 template <class T>
 struct DevBuf {
     T* p = nullptr;
@@ -27,7 +53,8 @@ struct DevBuf {
         n = count;
         GASB_CUDA(cudaMalloc(&p, sizeof(T) * std::max<int64_t>(count, 1)));
     }
-    void upload(const std::vector<T>& v) {
+    template <class V>
+    void upload(const V& v) {
         alloc(static_cast<int64_t>(v.size()));
         if (!v.empty()) GASB_CUDA(cudaMemcpy(p, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice));
     }
@@ -223,8 +250,8 @@ struct gasb_trainer_s {
             o += prow[i] * pcol[i];
         }
     }
-    void build_residual(const std::vector<int64_t>& h_arp, const std::vector<int32_t>& h_asrc,
-                        const std::vector<float>& h_acf, const std::vector<int32_t>& h_brow);
+    void build_residual(const std::vector<int64_t>& h_arp, const HVec<int32_t>& h_asrc,
+                        const HVec<float>& h_acf, const std::vector<int32_t>& h_brow);
     void enqueue_batch_res(int32_t p, bool train, bool push, bool fused, bool dp = false);
 
     // graphs
