@@ -81,7 +81,8 @@ void launch_spmm_fwd(const SpmmSegs& s, const int32_t* cols, const double* coeff
                      int32_t* counters, int32_t counters_ld, cudaStream_t st, const int32_t* special = nullptr,
                      const CUtensorMap* tmap = nullptr);
 bool make_row_tmap(const float* base, int64_t rows, int32_t dim, int64_t ld, int32_t box_cols, CUtensorMap* out);
-int32_t spmm_box_cols();
+int32_t spmm_box_cols(int32_t dim);
+int32_t spmm_cpl_for(int32_t dim);
 // special[0] |= table_flag_of(v) over the values v of x[rows x dim] (pitch ld).
 void launch_scan_special(const float* x, int64_t rows, int64_t ld, int32_t dim, int32_t* special, cudaStream_t st);
 // Transposed (CSC) gather, fp32 multiply-then-add in entry order (bit-exact with the

@@ -134,7 +134,18 @@ template <int CPL, int MODE>
 __device__ __forceinline__ void edge_fma(const float* rows, const double* cf, int j, double (&acc)[CPL]) {
     constexpr int kCols = 32 * CPL;
     const double c = cf[j];
-    if constexpr (CPL == 4) {
+    if constexpr (CPL == 8) {  // lane owns columns [4 lane, +4) and [128 + 4 lane, +4): conflict-free LDS.128
+        const float4 v = *reinterpret_cast<const float4*>(rows + j * kCols);
+        const float4 w = *reinterpret_cast<const float4*>(rows + j * kCols + 128);
+        acc[0] = __fma_rn(c, widen_scaled<MODE>(v.x), acc[0]);
+        acc[1] = __fma_rn(c, widen_scaled<MODE>(v.y), acc[1]);
+        acc[2] = __fma_rn(c, widen_scaled<MODE>(v.z), acc[2]);
+        acc[3] = __fma_rn(c, widen_scaled<MODE>(v.w), acc[3]);
+        acc[4] = __fma_rn(c, widen_scaled<MODE>(w.x), acc[4]);
+        acc[5] = __fma_rn(c, widen_scaled<MODE>(w.y), acc[5]);
+        acc[6] = __fma_rn(c, widen_scaled<MODE>(w.z), acc[6]);
+        acc[7] = __fma_rn(c, widen_scaled<MODE>(w.w), acc[7]);
+    } else if constexpr (CPL == 4) {
         const float4 v = *reinterpret_cast<const float4*>(rows + j * kCols);
         acc[0] = __fma_rn(c, widen_scaled<MODE>(v.x), acc[0]);
         acc[1] = __fma_rn(c, widen_scaled<MODE>(v.y), acc[1]);
@@ -450,6 +461,13 @@ __device__ __forceinline__ float4 ldg_row_piece(const float* p) {
     return v;
 }
 
+// Column of accumulator k of a lane whose first column is `col` (CPL = 8: two 4-column
+// groups 128 apart, see edge_fma).
+template <int CPL>
+__device__ __forceinline__ int32_t col_of(int32_t col, int k) {
+    return CPL == 8 ? col + (k & 3) + ((k >> 2) << 7) : col + k;
+}
+
 // Ends segment `k` of the warp's window: store the row (single-segment row) or publish an
 // fp64 partial, the last-arriving warp of the row summing the partials in segment order.
 template <int CPL>
@@ -462,9 +480,9 @@ __device__ __forceinline__ void seg_finish(double (&acc)[CPL], int32_t row, int3
                                            const int32_t* __restrict__ row_nseg) {
     bool store = true;
     if (slot >= 0) {
-        double* pp = partial + static_cast<int64_t>(slot) * pld + col;
+        double* pp = partial + static_cast<int64_t>(slot) * pld;
 #pragma unroll
-        for (int k = 0; k < CPL; ++k) pp[k] = acc[k];
+        for (int k = 0; k < CPL; ++k) pp[col_of<CPL>(col, k)] = acc[k];
         __threadfence();
         __syncwarp();
         int last = 0;
@@ -477,9 +495,9 @@ __device__ __forceinline__ void seg_finish(double (&acc)[CPL], int32_t row, int3
 #pragma unroll
             for (int k = 0; k < CPL; ++k) acc[k] = 0.0;
             for (int32_t i = 0; i < nk; ++i) {
-                const double* q2 = partial + static_cast<int64_t>(seg_slot[s0 + i]) * pld + col;
+                const double* q2 = partial + static_cast<int64_t>(seg_slot[s0 + i]) * pld;
 #pragma unroll
-                for (int k = 0; k < CPL; ++k) acc[k] += __ldcg(q2 + k);
+                for (int k = 0; k < CPL; ++k) acc[k] += __ldcg(q2 + col_of<CPL>(col, k));
             }
             if (lane == 0) counters[static_cast<int64_t>(row) * cld + chunk] = 0;  // self-reset
         }
@@ -488,7 +506,7 @@ __device__ __forceinline__ void seg_finish(double (&acc)[CPL], int32_t row, int3
         float* yr = y + (static_cast<int64_t>(row) - row_base) * ldy;
 #pragma unroll
         for (int k = 0; k < CPL; ++k)
-            if (col + k < dim) yr[col + k] = static_cast<float>(acc[k]);
+            if (col_of<CPL>(col, k) < dim) yr[col_of<CPL>(col, k)] = static_cast<float>(acc[k]);
     }
 #pragma unroll
     for (int k = 0; k < CPL; ++k) acc[k] = 0.0;
@@ -688,7 +706,7 @@ __device__ __forceinline__ void flat_items(
         const int32_t r = static_cast<int32_t>(item - static_cast<int64_t>(chunk) * nranges);
         const int32_t s_lo = range_seg[r], s_hi = range_seg[r + 1];
         if (s_lo >= s_hi) continue;
-        const int32_t col = chunk * Cfg::kCols + lane * CPL;
+        const int32_t col = chunk * Cfg::kCols + lane * (CPL == 8 ? 4 : CPL);
         const int64_t e_lo = seg_beg[s_lo], e_hi = seg_beg[s_hi];
         const int32_t nst = static_cast<int32_t>((e_hi - e_lo + KE - 1) / KE);
         // consumer-side window of 32 segment records (end offset, row, slot)
@@ -785,10 +803,15 @@ __device__ __forceinline__ void flat_items(
             mbar_wait(bars + sl, (phases >> sl) & 1u);
             phases ^= 1u << sl;
             const unsigned char* st = wbase + sl * Cfg::kStageBytes;
-            const float* rows = reinterpret_cast<const float*>(st) + lane * CPL;
+            const float* rows = reinterpret_cast<const float*>(st) + lane * (CPL == 8 ? 4 : CPL);
             const double* cf = reinterpret_cast<const double*>(st + kStageDataBytes);
             const int64_t eb = e_lo + static_cast<int64_t>(b) * KE;
             const int cnt = static_cast<int>(e_hi - eb < KE ? e_hi - eb : KE);
+#ifdef GASB_SPMM_NOFMA  // timing probe only (wrong values): the gathers without the FMAs
+            if (cnt == KE && cur_end >= eb + KE) {
+                acc[0] += cf[lane & 15] * rows[0];
+            } else
+#endif
             if (cnt == KE && cur_end >= eb + KE) {  // no segment ends inside: straight FMAs
                 if constexpr (DUAL) {
 #pragma unroll
@@ -946,7 +969,24 @@ bool spmm_use_tma() {
     return v != 0;
 }
 
-int32_t spmm_box_cols() { return 32 * (getenv("GASB_SPMM_CPL") && atoi(getenv("GASB_SPMM_CPL")) == 2 ? 2 : 4); }
+// Columns per lane of the flat SpMM for a table of width dim (tuning knob GASB_SPMM_CPL =
+// 2 | 4 | 8 forces one). Default: 8 (256-column chunks, 1 KB TMA rows) when the 256-column
+// rounding wastes no more than the 128-column one plus 64 columns, else 4. Fewer, wider
+// gathered rows: a probe timing the gathers alone (FMAs removed) fitted
+// t = 35 us per (rows of a 512 B batch) + 29 us per 573 MB at C3, i.e. a per-row TMA cost
+// next to the L2 -> SM byte rate (19.6 TB/s measured by tools/l2bw).
+int32_t spmm_cpl_for(int32_t dim) {
+    static const int forced = [] {
+        const char* e = getenv("GASB_SPMM_CPL");
+        const int v = e ? atoi(e) : 0;
+        return v == 2 || v == 4 || v == 8 ? v : 0;
+    }();
+    if (forced) return forced;
+    const int32_t r = dim % 256;
+    return (dim >= 192 && (r == 0 || r > 192)) ? 8 : 4;
+}
+
+int32_t spmm_box_cols(int32_t dim) { return 32 * spmm_cpl_for(dim); }
 
 int32_t spmm_ranges_per_launch() {
     static int32_t v = 0;
@@ -1069,7 +1109,10 @@ void launch_spmm_fwd(const SpmmSegs& s, const int32_t* cols, const double* coeff
 #define GASB_FLAT_LAUNCH(C, D) \
     launch_flat<C, D>(s, cols, coeffs, dim, y, ldy, row_base, partial, partial_ld, counters, counters_ld, st, special, tmap)
         const bool dual = !s.exact && spmm_dual();
-        if (spmm_cpl() == 2) {
+        const int cpl = spmm_cpl_for(dim);  // must match the tensor map's box (spmm_box_cols(dim))
+        if (cpl == 8) {
+            GASB_FLAT_LAUNCH(8, false);
+        } else if (cpl == 2) {
             if (dual) GASB_FLAT_LAUNCH(2, true);
             else GASB_FLAT_LAUNCH(2, false);
         } else {
@@ -1088,7 +1131,8 @@ void launch_spmm_fwd(const SpmmSegs& s, const int32_t* cols, const double* coeff
         GASB_CUDA(cudaGetLastError());
         return;
     }
-    const bool tma = tmap != nullptr && spmm_use_tma() && spmm_engine() == 0;
+    // (a 256-column tensor map belongs to the flat kernel: the staged kernels use cp.async then)
+    const bool tma = tmap != nullptr && spmm_use_tma() && spmm_engine() == 0 && spmm_cpl_for(dim) != 8;
 #define GASB_PIPE(C, T)                                                                                               \
     launch_pipe<C, T>(s, cols, coeffs, x, ldx, dim, y, ldy, row_base, partial, partial_ld, counters, counters_ld, st, \
                       special, tmap)
@@ -1403,7 +1447,7 @@ extern "C" gasb_status gasb_spmm_fwd(const int32_t* d_rowptr, int32_t m, const i
             GASB_CUDA(cudaMemcpyAsync(d_rs, rs.data(), sizeof(int32_t) * (nranges + 1), cudaMemcpyHostToDevice, st));
             SpmmSegs segs{z.seg_beg, z.seg_row, z.seg_slot, z.row_seg0, z.row_nseg, d_rs, nranges};
             CUtensorMap tm;
-            const bool have_tm = make_row_tmap(d_x, num_src, dim, ldx, spmm_box_cols(), &tm);
+            const bool have_tm = make_row_tmap(d_x, num_src, dim, ldx, spmm_box_cols(dim), &tm);
             launch_spmm_fwd(segs, d_cols, coeffs64, d_x, ldx, dim, d_y, ldy, 0, z.partial,
                             round_up(dim, 128), z.counters, nchunks, st, special, have_tm ? &tm : nullptr);
             GASB_CUDA(cudaStreamSynchronize(st));

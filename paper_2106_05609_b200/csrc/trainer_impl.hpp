@@ -165,17 +165,16 @@ struct gasb_trainer_s {
         return tm_ok[1] ? &tm_hist[l - 2] : nullptr;
     }
     void build_tmaps() {
-        const int32_t bc = spmm_box_cols();
-        tm_ok[0] = make_row_tmap(X.p, n, F, ldF, bc, &tm_x);
+        tm_ok[0] = make_row_tmap(X.p, n, F, ldF, spmm_box_cols(F), &tm_x);
         tm_hist.resize(static_cast<size_t>(std::max(0, L - 1)));
         tm_ok[1] = L >= 2;
         for (int32_t l = 1; l < L; ++l)
-            tm_ok[1] = tm_ok[1] && make_row_tmap(history_table(hist, l), n, hist_dim, history_ld(hist), bc,
+            tm_ok[1] = tm_ok[1] && make_row_tmap(history_table(hist, l), n, hist_dim, history_ld(hist), spmm_box_cols(hist_dim),
                                                  &tm_hist[l - 1]);
-        if (x_ext.p) tm_ok[2] = make_row_tmap(x_ext.p, ne_max, F, ldF, bc, &tm_xext);
+        if (x_ext.p) tm_ok[2] = make_row_tmap(x_ext.p, ne_max, F, ldF, spmm_box_cols(F), &tm_xext);
         const int32_t hdim = residual ? D : H;
-        if (h_ext.p) tm_ok[3] = make_row_tmap(h_ext.p, ne_max, hdim, ld_of(hdim), bc, &tm_hext);
-        if (residual && h0.p) tm_h0_ok = make_row_tmap(h0.p, ne_max, D, ldD, bc, &tm_h0);
+        if (h_ext.p) tm_ok[3] = make_row_tmap(h_ext.p, ne_max, hdim, ld_of(hdim), spmm_box_cols(hdim), &tm_hext);
+        if (residual && h0.p) tm_h0_ok = make_row_tmap(h0.p, ne_max, D, ldD, spmm_box_cols(D), &tm_h0);
     }
     DevBuf<double> loss, row_scratch;
 
