@@ -314,6 +314,17 @@ def run_ours(args):
             "peak": peak, "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
             "avg_launch_ms": tot_t / len(parts), "algorithmic_bytes_per_launch": tot_b / len(parts),
             "effective_gather_GBps": tot_eff / (tot_t / 1000.0) / 1e9, "traffic": None}
+    # second ceiling: the measured L2 -> SM rate of 1 KB row gathers from an L2-resident table
+    # (tools/l2bw/l2_bw.cu on a B200); the SpMM's gathered bytes are mostly L2 hits
+    l2f = ROOT / "profiles" / "r1_l2_gather_ceiling.jsonl"
+    if l2f.exists():
+        try:
+            rows = [json.loads(x) for x in l2f.read_text().splitlines() if x.strip()]
+            l2peak = max(r["gbs"] for r in rows if r["pattern"] == "gather_1kb_rows" and r["buffer_mb"] <= 64)
+            roof["l2_gather_peak_GBps"] = l2peak
+            roof["l2_gather_frac"] = roof["effective_gather_GBps"] / l2peak
+        except Exception:
+            pass
     prof = ROOT / "profiles" / "spmm_traffic.json"
     if prof.exists():
         try:
