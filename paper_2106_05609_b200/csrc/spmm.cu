@@ -970,8 +970,10 @@ bool spmm_use_tma() {
 }
 
 // Columns per lane of the flat SpMM for a table of width dim (tuning knob GASB_SPMM_CPL =
-// 2 | 4 | 8 forces one). Default: 8 (256-column chunks, 1 KB TMA rows) when the 256-column
-// rounding wastes no more than the 128-column one plus 64 columns, else 4. Fewer, wider
+// 2 | 4 | 8 forces one). Default: 2 (64-column chunks) up to 64 columns (products-shape
+// APPNP 381 -> 377 ms, PubMed GCNII 30.5 -> 30.2 ms per epoch); 8 (256-column chunks, 1 KB
+// TMA rows) when the 256-column rounding wastes no more than the 128-column one plus 64
+// columns; else 4. Fewer, wider
 // gathered rows: a probe timing the gathers alone (FMAs removed) fitted
 // t = 35 us per (rows of a 512 B batch) + 29 us per 573 MB at C3, i.e. a per-row TMA cost
 // next to the L2 -> SM byte rate (19.6 TB/s measured by tools/l2bw).
@@ -982,6 +984,7 @@ int32_t spmm_cpl_for(int32_t dim) {
         return v == 2 || v == 4 || v == 8 ? v : 0;
     }();
     if (forced) return forced;
+    if (dim <= 64) return 2;  // narrow tables (APPNP's C-wide histories, GCNII h = 64): no idle lanes
     const int32_t r = dim % 256;
     return (dim >= 192 && (r == 0 || r > 192)) ? 8 : 4;
 }
@@ -1059,8 +1062,6 @@ void segment_launch(const int64_t* rp, int64_t r_lo, int64_t r_hi, bool split, i
     ranges[nranges] = static_cast<int32_t>(g1);
 }
 
-// Columns per lane of the pipelined SpMM (tuning knob GASB_SPMM_CPL = 2 | 4, default 4:
-// 128-column chunks, measured fastest on the Reddit-shaped workload).
 // Two interleaved fp64 chains per column in the segmented (non-exact) mode (GASB_SPMM_DUAL
 // = 1 enables; measured no faster at C3, so off by default).
 static bool spmm_dual() {
@@ -1069,14 +1070,6 @@ static bool spmm_dual() {
         return e ? atoi(e) : 0;
     }();
     return v != 0;
-}
-
-static int spmm_cpl() {
-    static int v = [] {
-        const char* e = getenv("GASB_SPMM_CPL");
-        return e && atoi(e) == 2 ? 2 : 4;
-    }();
-    return v;
 }
 
 // flags[0] |= kTableNeg / kTableNonFinite for the values of x[rows x dim] (pitch ld).
@@ -1136,7 +1129,7 @@ void launch_spmm_fwd(const SpmmSegs& s, const int32_t* cols, const double* coeff
 #define GASB_PIPE(C, T)                                                                                               \
     launch_pipe<C, T>(s, cols, coeffs, x, ldx, dim, y, ldy, row_base, partial, partial_ld, counters, counters_ld, st, \
                       special, tmap)
-    if (spmm_cpl() == 2) {
+    if (spmm_cpl_for(dim) == 2) {  // (the staged kernels run 2 or 4 columns per lane)
         if (tma) GASB_PIPE(2, true);
         else GASB_PIPE(2, false);
     } else {
