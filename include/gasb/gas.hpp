@@ -130,12 +130,15 @@ struct BatchPlan {
 // Trainer uploads them.
 class BatchSchedule {
   public:
+    // device = true: the GPU batch-plan builder on the current CUDA device (plan_dev.cu),
+    // bit-identical plans
     static BatchSchedule build(const Graph& g, std::span<const std::int32_t> assignment, std::int32_t num_parts,
-                               bool full = false) {
+                               bool full = false, bool device = false) {
         if (static_cast<std::int64_t>(assignment.size()) != g.num_nodes())
             throw std::invalid_argument("BatchSchedule::build: assignment size != num_nodes");
         gasb_schedule s = nullptr;
-        check(gasb_schedule_build(g.raw(), assignment.data(), num_parts, full ? GASB_PLAN_FULL : 0, &s));
+        check(gasb_schedule_build(g.raw(), assignment.data(), num_parts,
+                                  (full ? GASB_PLAN_FULL : 0) | (device ? GASB_PLAN_DEVICE : 0), &s));
         return BatchSchedule(s);
     }
     std::int32_t num_parts() const {

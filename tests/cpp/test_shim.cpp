@@ -87,6 +87,12 @@ int main() {
         EXPECT(throws<std::invalid_argument>([&] { h.pull(0, ids); }));
         std::vector<NodeId> oob{3};
         EXPECT(throws<std::invalid_argument>([&] { h.pull(1, oob); }));  // id out of range
+        // GPU batch-plan builder: same plan as the host builder, same errors
+        BatchSchedule d2 = BatchSchedule::build(g, two, 2, false, true);
+        BatchPlan dq = d2.plan(0);
+        EXPECT(dq.extended_nodes == q.extended_nodes && dq.halo_nodes == q.halo_nodes);
+        EXPECT(dq.gcn_cols == q.gcn_cols && dq.gcn_coeffs == q.gcn_coeffs && dq.gcn_row_ptr == q.gcn_row_ptr);
+        EXPECT(throws<std::invalid_argument>([&] { BatchSchedule::build(g, bad_assign, 2, false, true); }));
         // GASH checkpoint round trip (history.cpp:130-178): tables kept, stamps 0, step 0
         const std::string path = "/tmp/gasb_shim_test.gash";
         h.save_checkpoint(path);
