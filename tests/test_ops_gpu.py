@@ -42,13 +42,19 @@ def _dev(torch, a):
     return torch.from_numpy(np.ascontiguousarray(a)).cuda()
 
 
-@pytest.mark.parametrize("d", [16, 47, 64, 256, 602])
+# widths cover every chunk layout of the flat kernel (spmm_cpl_for): 64-column chunks up to
+# 64, 128-column chunks (65, 602), 256-column chunks / 1 KB rows (200, 256, 480, 512)
+@pytest.mark.parametrize("d", [16, 47, 64, 65, 200, 256, 480, 512, 602])
 @pytest.mark.parametrize("seg", [0, 64])
-def test_aggregate_forward(torch, oracle, hub_plan, d, seg):
+@pytest.mark.parametrize("nonneg", [False, True])
+def test_aggregate_forward(torch, oracle, hub_plan, d, seg, nonneg):
+    """nonneg: post-ReLU tables take the one-IMAD widening path, signed ones the two-IMAD path."""
     p = hub_plan
     rng = np.random.default_rng(d)
     ne, nb = len(p.extended_nodes), len(p.batch_nodes)
     x = rng.standard_normal((ne, d)).astype(np.float32)
+    if nonneg:
+        x = np.abs(x)
     ld = (d + 3) // 4 * 4  # source rows 16 B aligned
     xp = np.zeros((ne, ld), np.float32)
     xp[:, :d] = x
