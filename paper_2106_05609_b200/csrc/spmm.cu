@@ -37,7 +37,7 @@ constexpr int kUnroll = 8;  // edges in flight per lane
 // (exact) and the source value x is re-laid-out as the double D = x * 2^-896 (exact for
 // every finite float, zeros and denormals included):
 //   non-negative x : hi = u >> 3,                               lo = u << 29   (2 int ops)
-//   signed x       : hi = ((u & 0x7fffffff) >> 3) | (u & sign), lo = u << 29   (4 int ops)
+//   signed x       : hi = ((u & 0x7fffffff) >> 3) | (u & sign), lo = u << 29   (IMAD.WIDE + LOP3)
 // so fma(c * 2^896, D, acc) == acc + c*x rounded once — the reference's `acc += c * src`.
 // A per-table flag word (kTableNeg / kTableNonFinite) selects the path; tables holding
 // inf/nan take F2F (D = double(x) * 2^-896, also exact).
@@ -61,8 +61,7 @@ constexpr int kStageDataBytes = GASB_SPMM_STAGE_BYTES;
 enum WidenMode { kWidenF2F = 0, kWidenSigned = 1, kWidenNonNeg = 2 };
 
 // The bit pattern {hi = u >> 3, lo = u << 29} is the 64-bit product u * 2^29: one
-// IMAD.WIDE.U32. For a negative x the product carries the sign at bit 28 of hi; adding
-// s * 0x70000000 (s = sign) moves it to bit 31 (carry through bits 28..30): one more IMAD.
+// IMAD.WIDE.U32. Signed tables use the signed product and one LOP3 (widen_scaled).
 __device__ __forceinline__ uint64_t mul_wide_2p29(uint32_t u) {
     uint64_t d;
     asm("mul.wide.u32 %0, %1, 536870912;" : "=l"(d) : "r"(u));
@@ -74,8 +73,12 @@ __device__ __forceinline__ double widen_scaled(float f) {
     const uint32_t u = __float_as_uint(f);
     if (MODE == kWidenNonNeg) return __longlong_as_double(static_cast<long long>(mul_wide_2p29(u)));
     if (MODE == kWidenSigned) {
-        const uint64_t d = mul_wide_2p29(u);
-        const uint32_t hi = static_cast<uint32_t>(d >> 32) + (u >> 31) * 0x70000000u;
+        // signed product u * 2^29 (u read as int32): for a negative x the sign extension sets
+        // hi bits 28..31; clearing bits 28..30 leaves the sign at bit 31 and the exponent
+        // field untouched. IMAD.WIDE + LOP3.
+        long long d;
+        asm("mul.wide.s32 %0, %1, 536870912;" : "=l"(d) : "r"(u));
+        const uint32_t hi = static_cast<uint32_t>(static_cast<unsigned long long>(d) >> 32) & 0x8FFFFFFFu;
         return __hiloint2double(static_cast<int>(hi), static_cast<int>(static_cast<uint32_t>(d)));
     }
     return __dmul_rn(static_cast<double>(f), 0x1.0p-896);
