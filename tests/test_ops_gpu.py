@@ -48,7 +48,7 @@ def _dev(torch, a):
 @pytest.mark.parametrize("seg", [0, 64])
 @pytest.mark.parametrize("nonneg", [False, True])
 def test_aggregate_forward(torch, oracle, hub_plan, d, seg, nonneg):
-    """nonneg: post-ReLU tables take the one-IMAD widening path, signed ones the two-IMAD path."""
+    """nonneg: post-ReLU tables take the one-IMAD widening path, signed ones the IMAD.WIDE + LOP3 path."""
     p = hub_plan
     rng = np.random.default_rng(d)
     ne, nb = len(p.extended_nodes), len(p.batch_nodes)
@@ -92,6 +92,35 @@ def test_aggregate_forward_zeros_and_denormals(torch, oracle, hub_plan, special)
     check(lib.gasb_spmm_fwd(d_rp.data_ptr(), nb, d_cols.data_ptr(), d_cf.data_ptr(), d_x.data_ptr(), ne, d, d,
                             d_y.data_ptr(), d, 0, None))
     assert np.array_equal(d_y.cpu().numpy(), want)
+
+
+@pytest.mark.parametrize("d", [64, 256, 602])
+def test_aggregate_forward_signed_extremes(torch, oracle, hub_plan, d):
+    """Signed tables (no denormals, no inf/nan) take the signed integer widening: -0.0, the
+    smallest normal of either sign, values near FLT_MAX and every sign/exponent mix must
+    widen exactly (the mask 0x8FFFFFFF keeps the sign and the exponent field)."""
+    p = hub_plan
+    rng = np.random.default_rng(900 + d)
+    ne, nb = len(p.extended_nodes), len(p.batch_nodes)
+    mant = rng.uniform(1.0, 2.0, (ne, d))
+    expo = rng.integers(-126, 100, (ne, d))
+    sign = np.where(rng.random((ne, d)) < 0.5, -1.0, 1.0)
+    x = (sign * np.ldexp(mant, expo)).astype(np.float32)
+    tiny = np.finfo(np.float32).tiny
+    x[0, :4] = [-0.0, tiny, -tiny, 0.0]
+    x[1, :2] = [np.float32(1e30), np.float32(-1e30)]
+    assert not np.any((x != 0) & (np.abs(x) < tiny))
+    ld = (d + 3) // 4 * 4
+    xp = np.zeros((ne, ld), np.float32)
+    xp[:, :d] = x
+    want = oracle.aggregate(p.gcn_row_ptr, p.gcn_cols, p.gcn_coeffs, x)
+    d_rp = _dev(torch, p.gcn_row_ptr.astype(np.int32))
+    d_cols, d_cf, d_x = _dev(torch, p.gcn_cols), _dev(torch, p.gcn_coeffs), _dev(torch, xp)
+    d_y = torch.zeros(nb, ld, device="cuda")
+    check(lib.gasb_spmm_fwd(d_rp.data_ptr(), nb, d_cols.data_ptr(), d_cf.data_ptr(), d_x.data_ptr(), ne, ld, d,
+                            d_y.data_ptr(), ld, 0, None))
+    got = d_y.cpu().numpy()[:, :d]
+    assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
 
 
 @pytest.mark.parametrize("d", [16, 64, 256])
