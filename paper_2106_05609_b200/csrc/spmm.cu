@@ -1416,7 +1416,7 @@ extern "C" gasb_status gasb_spmm_fwd(const int32_t* d_rowptr, int32_t m, const i
         GASB_CUDA(cudaMallocAsync(&z.row_seg0, sizeof(int32_t) * m, st));
         GASB_CUDA(cudaMallocAsync(&z.row_nseg, sizeof(int32_t) * m, st));
         GASB_CUDA(cudaMallocAsync(&z.counters, sizeof(int32_t) * m * nchunks, st));
-        GASB_CUDA(cudaMallocAsync(&z.partial, sizeof(double) * std::max<int64_t>(slots, 1) * round_up(dim, 128), st));
+        GASB_CUDA(cudaMallocAsync(&z.partial, sizeof(double) * std::max<int64_t>(slots, 1) * round_up(dim, 256), st));
         GASB_CUDA(cudaMallocAsync(&coeffs64, sizeof(double) * std::max<int64_t>(nnz, 1), st));
         GASB_CUDA(cudaMemcpyAsync(z.seg_beg, sb.data(), sizeof(int64_t) * (nseg + 1), cudaMemcpyHostToDevice, st));
         GASB_CUDA(cudaMemcpyAsync(z.seg_row, sr.data(), sizeof(int32_t) * nseg, cudaMemcpyHostToDevice, st));
@@ -1445,7 +1445,7 @@ extern "C" gasb_status gasb_spmm_fwd(const int32_t* d_rowptr, int32_t m, const i
             CUtensorMap tm;
             const bool have_tm = make_row_tmap(d_x, num_src, dim, ldx, spmm_box_cols(dim), &tm);
             launch_spmm_fwd(segs, d_cols, coeffs64, d_x, ldx, dim, d_y, ldy, 0, z.partial,
-                            round_up(dim, 128), z.counters, nchunks, st, special, have_tm ? &tm : nullptr);
+                            round_up(dim, 256), z.counters, nchunks, st, special, have_tm ? &tm : nullptr);
             GASB_CUDA(cudaStreamSynchronize(st));
             cudaFreeAsync(special, st);
             cudaFreeAsync(d_rs, st);

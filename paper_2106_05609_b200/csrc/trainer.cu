@@ -386,8 +386,8 @@ void gasb_trainer_s::build(const float* h_features, const int32_t* h_labels, con
     max_chunks = static_cast<int32_t>(ceil_div(std::max(F, H), 64));
     counters.alloc(R * max_chunks);
     counters.zero();
-    pld = round_up(std::max(F, H), 128);  // fp64 partial row width, any SpMM chunk width
-    pld_all = round_up(F, 128);
+    pld = round_up(std::max(F, H), 256);  // fp64 partial row width, any SpMM chunk width (64 | 128 | 256)
+    pld_all = round_up(F, 256);
     partial_batch.alloc(std::max<int64_t>(seg_batch.max_group_slots, 1) * pld);
     partial_all.alloc(std::max<int64_t>(seg_all.total_slots, 1) * pld_all);
 
@@ -975,7 +975,7 @@ void gasb_trainer_s::ensure_eval() {
     eval_flags.zero();
     eval_masks.alloc(3LL * n);
     eval_counts.alloc(6);
-    eval_pld = round_up(std::max(F, H), 128);
+    eval_pld = round_up(std::max(F, H), 256);
     eval_partial.alloc(std::max<int64_t>(seg_all.total_slots, 1) * eval_pld);
 }
 
