@@ -464,7 +464,7 @@ static bool launch_tc(int m, int n, int k, const float* a, int64_t lda, const fl
     int S = 1;
     static const int split_div = [] {  // GASB_GEMM_SPLITK_DIV: min k-blocks per split-K slice (0 = off)
         const char* e = getenv("GASB_GEMM_SPLITK_DIV");
-        return e ? atoi(e) : 8;  // measured: fewer, longer slices beat more fixups at C3 sizes
+        return e ? atoi(e) : 6;  // measured at C3 (ms/epoch): 4: 110.0, 6: 106.5, 8: 107.3, 12: 109.2, 16: 111.0
     }();
     if (!TALL && split_div > 0 && t_gemm_ws && tiles < num_sms()) {
         S = static_cast<int>(std::min<int64_t>(num_sms() / tiles, std::max(1, nkb / split_div)));
