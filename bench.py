@@ -14,6 +14,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
 import statistics
 import subprocess
@@ -138,24 +139,52 @@ def cpu_baseline(ds, sample: int, kind_hint: str = "reference") -> dict:
     secs = 0.0
     for slot in range(warm, len(parts)):
         secs += s.run(slot, 0)[1]
-    return {"value": nodes / secs, "unit": "nodes/s", "cores": 1, "kind": "reference",
+    return {"value": nodes / secs, "unit": "nodes/s", "cores": 1, "kind": "reference", **host_cpu(),
             "sample": f"{len(parts) - warm} of {w.parts} partition batches of the same graph after {warm} untimed "
                       f"(gas_epoch batches: forward, push/pull, backward, Adam), {nodes} nodes in {secs:.1f} s, "
                       "single-threaded reference"}
+
+
+def load_workloads():
+    """paper_2106_05609_b200/workloads.py loaded by path: data-only at import, so the reference
+    arm gets the workload table without importing the package (which loads libgasb.so)."""
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("gasb_workloads", ROOT / "paper_2106_05609_b200" / "workloads.py")
+    mod = importlib.util.module_from_spec(spec)
+    sys.modules["gasb_workloads"] = mod  # dataclasses resolve their module through sys.modules
+    spec.loader.exec_module(mod)
+    return mod
+
+
+def host_cpu() -> dict:
+    model = "unknown"
+    try:
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    try:
+        avail = len(os.sched_getaffinity(0))
+    except AttributeError:
+        avail = os.cpu_count()
+    return {"cpu_model": model, "host_cores": os.cpu_count(), "cores_available": avail}
 
 
 def run_reference_arm(args):
     ws, rank, _ = dist_env()
     if rank != 0:
         return
-    from paper_2106_05609_b200.workloads import make_dataset
     sys.path.insert(0, str(ROOT / "oracle"))
-    from pyoracle import REF_SO, RefLib, make_spec
+    from pyoracle import REF_SO, OracleSynth, RefLib, make_spec
 
     if not REF_SO.exists():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libref.so not built"}))
         return
-    ds = make_dataset(args.workload)
+    # the same graph / features / labels / partition as our arm, generated by the oracle's
+    # restatement of the generator (tests/test_workloads.py: bit-identical); no libgasb.so
+    ds = load_workloads().make_dataset(args.workload, backend=OracleSynth())
     w = ds.workload
     R = RefLib()
     order = [int(p) for p in R.epoch_order(w.parts, 3, 0)]
@@ -175,8 +204,9 @@ def run_reference_arm(args):
         "impl": "reference", "metric": METRIC, "value": value, "unit": "nodes/s", "n_gpus": ws,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * sum(times) / len(times),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32 (f64 accumulation)",
-        "data": "synthetic", "config": workload_config(ds, "cpu-1core"),
-        "cpu_baseline": {"value": value, "unit": "nodes/s", "cores": 1, "kind": "reference",
+        "data": "synthetic", "config": workload_config(ds),
+        "step": "one partition batch of gas_epoch (a bounded sample of the epoch; nodes/s is per node either way)",
+        "cpu_baseline": {"value": value, "unit": "nodes/s", "cores": 1, "kind": "reference", **host_cpu(),
                          "sample": f"one partition batch per step ({int(np.mean(nodes))} nodes avg), reference "
                                    "gas_epoch batch path, single-threaded (the reference has no parallel compute)"},
         "e2e": {"value": value, "unit": "nodes/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -184,12 +214,13 @@ def run_reference_arm(args):
     print(json.dumps(line))
 
 
-def workload_config(ds, parallelism: str) -> dict:
+def workload_config(ds) -> dict:
+    """Identical in both arms (the step unit and the parallelism are top-level keys)."""
     w = ds.workload
     return {"workload": f"{w.name}-shape GAS-{w.kind.upper()}", "num_nodes": w.num_nodes,
             "stored_nnz": int(len(ds.cols)), "in_dim": w.in_dim, "hidden": w.hidden, "num_classes": w.num_classes,
             "layers": w.num_layers, "partitions": w.parts, "partitioner": "planted communities (natural partition)",
-            "step": "one GAS epoch (all partition batches, one Adam step each)", "parallelism": parallelism,
+            "features": f"N(0,1) + {w.signal} x class centroid", "seeds": {"graph": w.seed, "model": 3},
             "l2_policy": "inputs larger than L2 (features 567 MB, histories 716 MB vs 126 MB L2)"}
 
 
@@ -343,9 +374,12 @@ def run_ours(args):
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
         "scaling": "strong" if ws > 1 else "weak",
         "vs_baseline": None, "dtype": "f32 (f64 SpMM accumulation)", "data": "synthetic",
-        "config": workload_config(ds, f"dp{ws} (partition batches split over ranks, peer-memory exchange)"
-                                  if ws > 1 else "single-gpu"),
+        "config": workload_config(ds),
+        "parallelism": f"dp{ws} (partition batches split over ranks, peer-memory exchange)" if ws > 1 else "single-gpu",
+        "step": "one GAS epoch (all partition batches, one Adam step each)",
         "e2e": e2e, "gpu_launches": launches, "roofline": roof, "clocks": clk, "final_loss": loss,
+        "trains": {"final_loss": loss, "ln_num_classes": math.log(w.num_classes),
+                   "live": bool(loss < math.log(w.num_classes) - 0.1)},
         "history_pull_GBps": pull, "epoch_roofline": epoch_roofline(sched, w, ms / args.steps, ws), **extra,
     }
     if rank == 0 and ws == 1 and not args.no_cpu:
@@ -394,6 +428,18 @@ def main():
     ap.add_argument("--profile-parts", type=int, default=20)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if args.impl == "ours" and args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # --gpus N without a launcher: re-exec as N ranks (one process per GPU)
+        import socket
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(port), str(Path(__file__).resolve()), *sys.argv[1:]]
+        os.execv(sys.executable, cmd)
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.impl == "ours" and ws != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws}")
     if args.impl == "reference":
         run_reference_arm(args)
     else:

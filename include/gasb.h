@@ -207,6 +207,18 @@ gasb_status gasb_spmm_bwd(const int32_t* d_t_rowptr, int32_t num_targets, const 
 gasb_status gasb_gemm(int32_t op, int32_t m, int32_t n, int32_t k, const float* d_a, int64_t lda, const float* d_b,
                       int64_t ldb, float* d_c, int64_t ldc, float beta, gasb_stream stream);
 
+/* AdamState::step (nn.hpp:21-38, nn.cpp:20-41) on one flat parameter tensor: `step` is the
+ * step count t after the increment (1-based); bias corrections 1 - beta^t via host
+ * std::pow, moment/update math in fp64 with the reference's rounding sequence -> bit-exact
+ * with the reference given identical gradients and state. Synchronous. */
+gasb_status gasb_adam_step(float* d_params, float* d_m, float* d_v, const float* d_grads, int64_t size, int64_t step,
+                           float lr, float beta1, float beta2, float eps, gasb_stream stream);
+/* grad_clip (nn.hpp:41, nn.cpp:47-63): global L2 norm in fp64; if norm > max_norm every
+ * gradient is multiplied by float(max_norm / norm). *h_norm = the pre-clip norm (its fp64
+ * sum runs in a fixed tree order, not the reference's sequential order). max_norm <= 0 is
+ * INVALID_ARGUMENT. Synchronous. */
+gasb_status gasb_grad_clip(float* d_grads, int64_t size, double max_norm, double* h_norm, gasb_stream stream);
+
 /* ==================================================================================== */
 /* gas-trainer: Model (trainer.hpp:45-88), gas_epoch (trainer.hpp:124-126,               */
 /* trainer.cpp:386-442), run_batch (trainer.cpp:295-339), AdamState (nn.hpp:21-38)       */
@@ -245,6 +257,12 @@ gasb_status gasb_trainer_destroy(gasb_trainer t);
 gasb_status gasb_gas_epoch(gasb_trainer t, int64_t epoch, int32_t shuffle, double* mean_loss);
 /* Enqueue-only variant for timing: no host synchronization, losses stay on device. */
 gasb_status gasb_gas_epoch_async(gasb_trainer t, int64_t epoch, int32_t shuffle);
+/* The batches order[begin, end) of gas_epoch's seeded order for `epoch` (same kernels,
+ * graphs and hoisting as gasb_gas_epoch_async; end == num_parts is the whole epoch). */
+gasb_status gasb_gas_epoch_range_async(gasb_trainer t, int64_t epoch, int32_t shuffle, int32_t begin, int32_t end);
+/* Per-part batch objective (num_parts doubles, part order) as last computed: the loss of
+ * every batch with training rows that ran (synchronizes). */
+gasb_status gasb_trainer_part_losses(gasb_trainer t, double* h_losses);
 /* Mean loss of the last epoch enqueued with gasb_gas_epoch_async (synchronizes). */
 gasb_status gasb_trainer_last_loss(gasb_trainer t, double* mean_loss);
 /* One batch with capture (same contract as the oracle's session_batch): acts = pushed rows

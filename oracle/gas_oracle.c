@@ -121,13 +121,20 @@ int go_build_graph(const int32_t* u, const int32_t* v, int64_t m, int32_t n, int
         buf[pos[v[i]]++] = u[i];
         if (symmetrize && u[i] != v[i]) buf[pos[u[i]]++] = v[i];
     }
+    /* rows sorted and deduplicated in place (in parallel), then compacted in row order */
+#pragma omp parallel for schedule(dynamic, 256)
+    for (int32_t r = 0; r < n; ++r) {
+        int64_t b = cnt[r], e = cnt[r + 1], k = b;
+        qsort(buf + b, (size_t)(e - b), sizeof(int32_t), cmp_i32);
+        for (int64_t i = b; i < e; ++i)
+            if (i == b || buf[i] != buf[i - 1]) buf[k++] = buf[i];
+        pos[r] = k - b;
+    }
     row_offsets[0] = 0;
     int64_t w = 0;
     for (int32_t r = 0; r < n; ++r) {
-        int64_t b = cnt[r], e = cnt[r + 1];
-        qsort(buf + b, (size_t)(e - b), sizeof(int32_t), cmp_i32);
-        for (int64_t i = b; i < e; ++i)
-            if (i == b || buf[i] != buf[i - 1]) buf[w++] = buf[i];
+        if (w != cnt[r]) memmove(buf + w, buf + cnt[r], sizeof(int32_t) * (size_t)pos[r]);
+        w += pos[r];
         row_offsets[r + 1] = w;
     }
     free(cnt);
@@ -912,4 +919,102 @@ int go_session_epoch(go_session* s, int64_t epoch, int shuffle, double* loss) { 
     free(order);
     *loss = cnt > 0 ? sum / (double)cnt : 0.0;
     return 0;
+}
+
+/* ------------------------------------------------------------------------------------ */
+/* Synthetic workload generator (not a reference algorithm: the bench's input generator, */
+/* restated here so bench.py's reference arm builds the same graph and features without */
+/* loading the product library; tests/test_workloads.py checks it equals                */
+/* gasb_synth_pairs / gasb_synth_features bit for bit).                                  */
+/* ------------------------------------------------------------------------------------ */
+
+static double syn_u01(uint64_t seed, uint64_t a, uint64_t b) {
+    return (double)(go_mix64(go_mix64(seed ^ go_mix64(a)) ^ go_mix64(b)) >> 11) * 0x1.0p-53;
+}
+
+static int32_t syn_sample(const double* cum, int64_t lo, int64_t hi, double target) {
+    int64_t a = lo, b = hi - 1;
+    while (a < b) {
+        int64_t mid = (a + b) >> 1;
+        if (cum[mid + 1] > target) b = mid;
+        else a = mid + 1;
+    }
+    return (int32_t)a;
+}
+
+typedef struct { uint64_t key; int32_t v; } syn_key;
+static int cmp_key(const void* a, const void* b) {
+    const syn_key *x = (const syn_key*)a, *y = (const syn_key*)b;
+    if (x->key != y->key) return x->key < y->key ? -1 : 1;
+    return (x->v > y->v) - (x->v < y->v);
+}
+
+int go_synth_pairs(int32_t n, int32_t K, int64_t m, double intra, double gamma, double wmin, double wmax,
+                   uint64_t seed, int32_t* src, int32_t* dst, int32_t* community) {
+    if (n <= 0 || K <= 0 || K > n || !(gamma > 1.0) || !(wmin > 0.0) || wmax < wmin) return 1;
+    double* w = malloc(sizeof(double) * (size_t)n);
+    syn_key* key = malloc(sizeof(syn_key) * (size_t)n);
+    int32_t* comm = malloc(sizeof(int32_t) * (size_t)n);
+    double* cum = calloc((size_t)n + 1, sizeof(double));
+    int64_t* cstart = calloc((size_t)K + 1, sizeof(int64_t));
+    int64_t* fill = malloc(sizeof(int64_t) * (size_t)K);
+    int32_t* members = malloc(sizeof(int32_t) * (size_t)n);
+    double* ccum = calloc((size_t)n + (size_t)K, sizeof(double));
+#pragma omp parallel for schedule(static)
+    for (int32_t v = 0; v < n; ++v) {
+        const double u = syn_u01(seed, 0x77656967ull, (uint64_t)v);
+        const double x = wmin * pow(1.0 - u, -1.0 / (gamma - 1.0));
+        w[v] = x < wmax ? x : wmax;
+    }
+    for (int32_t v = 0; v < n; ++v) {
+        key[v].key = go_mix64(seed ^ go_mix64(0x636f6d6dull ^ go_mix64((uint64_t)v)));
+        key[v].v = v;
+    }
+    qsort(key, (size_t)n, sizeof(syn_key), cmp_key);
+    for (int32_t r = 0; r < n; ++r) comm[key[r].v] = r % K;
+    for (int32_t v = 0; v < n; ++v) cum[v + 1] = cum[v] + w[v];
+    for (int32_t v = 0; v < n; ++v) cstart[comm[v] + 1]++;
+    for (int32_t c = 0; c < K; ++c) cstart[c + 1] += cstart[c];
+    for (int32_t c = 0; c < K; ++c) fill[c] = cstart[c];
+    for (int32_t v = 0; v < n; ++v) members[fill[comm[v]]++] = v;
+    for (int32_t c = 0; c < K; ++c) {
+        double* cc = ccum + cstart[c] + c;
+        cc[0] = 0.0;
+        for (int64_t i = cstart[c]; i < cstart[c + 1]; ++i) cc[i - cstart[c] + 1] = cc[i - cstart[c]] + w[members[i]];
+    }
+    const double W = cum[n];
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < m; ++i) {
+        const uint64_t ui = (uint64_t)i;
+        const int32_t u = syn_sample(cum, 0, n, syn_u01(seed, ui, 1) * W);
+        int32_t v;
+        if (syn_u01(seed, ui, 2) < intra) {
+            const int32_t c = comm[u];
+            const double* cc = ccum + cstart[c] + c;
+            const int64_t sz = cstart[c + 1] - cstart[c];
+            v = members[cstart[c] + syn_sample(cc, 0, sz, syn_u01(seed, ui, 3) * cc[sz])];
+        } else {
+            v = syn_sample(cum, 0, n, syn_u01(seed, ui, 3) * W);
+        }
+        src[i] = u;
+        dst[i] = v;
+    }
+    if (community) memcpy(community, comm, sizeof(int32_t) * (size_t)n);
+    free(w); free(key); free(comm); free(cum); free(cstart); free(fill); free(members); free(ccum);
+    return 0;
+}
+
+void go_synth_features(int64_t n, int32_t dim, int64_t ld, uint64_t seed, float* out) {
+#pragma omp parallel for schedule(static)
+    for (int64_t v = 0; v < n; ++v) {
+        float* row = out + v * ld;
+        for (int32_t j = 0; j < dim; ++j) {
+            const uint64_t c = (uint64_t)v * (uint64_t)dim + (uint64_t)j;
+            double u1 = syn_u01(seed, c, 0x6e31ull);
+            if (u1 <= 0.0) u1 = 0x1.0p-53;
+            const double u2 = syn_u01(seed, c, 0x6e32ull);
+            row[j] = (float)(sqrt(-2.0 * log(u1)) * cos(6.283185307179586 * u2));
+        }
+        for (int64_t j = dim; j < ld; ++j) row[j] = 0.0f;
+    }
 }

@@ -107,6 +107,12 @@ void go_session_dp_commit(go_session* s, int32_t part, const float* acts);
 void go_session_dp_apply(go_session* s, const float* grad_sum, int32_t count, int32_t batches);
 int go_session_dp_epoch(go_session* s, int64_t epoch, int shuffle, int32_t k, double* loss);
 
+/* ---- bench input generator (same streams as gasb_synth_pairs / gasb_synth_features) -- */
+int go_synth_pairs(int32_t n, int32_t communities, int64_t num_pairs, double intra_fraction, double gamma,
+                   double min_weight, double max_weight, uint64_t seed, int32_t* src, int32_t* dst,
+                   int32_t* community);
+void go_synth_features(int64_t n, int32_t dim, int64_t ld, uint64_t seed, float* out);
+
 #ifdef __cplusplus
 }
 #endif

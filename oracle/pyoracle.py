@@ -90,6 +90,8 @@ class Oracle:
         L.go_session_dp_commit.argtypes = [vp, i32, vp]
         L.go_session_dp_apply.argtypes = [vp, vp, i32, i32]
         L.go_session_dp_epoch.argtypes = [vp, i64, C.c_int, i32, P(f64)]
+        L.go_synth_pairs.argtypes = [i32, i32, i64, f64, f64, f64, f64, u64, vp, vp, vp]
+        L.go_synth_features.argtypes = [i64, i32, i64, u64, vp]
 
     def build_graph(self, edges: np.ndarray, n: int, symmetrize=True):
         e = np.ascontiguousarray(np.asarray(edges, np.int32).reshape(-1, 2))
@@ -173,6 +175,32 @@ class Oracle:
 
     def session(self, ro, cols, features, labels, train_mask, num_classes, assignment, num_parts, spec: Spec):
         return Session(self, "go", ro, cols, features, labels, train_mask, num_classes, assignment, num_parts, spec)
+
+
+class OracleSynth:
+    """The bench input generator restated in the oracle (go_synth_*; go_build_graph restates
+    build_graph, src/graph.cpp:25-61): the `backend` of workloads.make_dataset for bench.py's
+    reference arm, which must not load the product library. Graph handle = None."""
+
+    def __init__(self, oracle: "Oracle | None" = None):
+        self.o = oracle or Oracle()
+
+    def synth_pairs(self, w):
+        src, dst = np.empty(w.num_pairs, np.int32), np.empty(w.num_pairs, np.int32)
+        comm = np.empty(w.num_nodes, np.int32)
+        if self.o.lib.go_synth_pairs(w.num_nodes, w.parts, w.num_pairs, w.intra_fraction, 2.5, 1.0, w.max_weight,
+                                     w.seed, _p(src), _p(dst), _p(comm)):
+            raise ValueError("synth_pairs: bad argument")
+        return np.stack([src, dst], axis=1), comm
+
+    def build_graph(self, edges, n):
+        ro, co = self.o.build_graph(edges, n, symmetrize=True)
+        return None, ro, co
+
+    def synth_features(self, n, dim, seed):
+        out = np.empty((n, dim), np.float32)
+        self.o.lib.go_synth_features(n, dim, dim, seed, _p(out))
+        return out
 
 
 class RefLib:

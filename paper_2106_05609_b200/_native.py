@@ -111,6 +111,10 @@ _SIGS = {
     "gasb_trainer_destroy": (i32, [vp]),
     "gasb_gas_epoch": (i32, [vp, i64, i32, P(f64)]),
     "gasb_gas_epoch_async": (i32, [vp, i64, i32]),
+    "gasb_gas_epoch_range_async": (i32, [vp, i64, i32, i32, i32]),
+    "gasb_trainer_part_losses": (i32, [vp, vp]),
+    "gasb_adam_step": (i32, [vp, vp, vp, vp, i64, i64, f32, f32, f32, f32, vp]),
+    "gasb_grad_clip": (i32, [vp, i64, f64, P(f64), vp]),
     "gasb_trainer_last_loss": (i32, [vp, P(f64)]),
     "gasb_trainer_batch": (i32, [vp, i32, i64, i32, i32, vp, vp, P(f64), vp, P(i32)]),
     "gasb_trainer_num_param_floats": (i32, [vp, P(i64)]),

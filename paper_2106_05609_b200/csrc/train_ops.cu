@@ -122,7 +122,7 @@ __global__ void __launch_bounds__(256) adam_kernel(float* __restrict__ p, float*
                                                    int64_t* t_counter, const double* __restrict__ bc,
                                                    float lr, float b1, float b2, float eps, float clip,
                                                    const double* __restrict__ norm, int64_t* __restrict__ end_step, int32_t* __restrict__ end_done) {
-    const int64_t t = *t_counter + 1;
+    const int64_t t = min(*t_counter + 1, static_cast<int64_t>(bc[0]));  // bc[0]: saturation step
     const double bc1 = bc[2 * t], bc2 = bc[2 * t + 1];
     float s = 1.0f;
     bool scale = false;
@@ -217,3 +217,60 @@ void launch_zero(float* p, int64_t count, cudaStream_t st) {
 }
 
 }  // namespace gasb
+
+// ---- op-level entry points: AdamState::step and grad_clip on caller buffers ------------
+using namespace gasb;
+namespace {
+__global__ void scale_kernel(float* __restrict__ g, int64_t size, const double* __restrict__ norm, double max_norm) {
+    const double nn = *norm;
+    if (!(nn > max_norm)) return;
+    const float s = static_cast<float>(__ddiv_rn(max_norm, nn));
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < size;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        g[i] = __fmul_rn(g[i], s);
+}
+}  // namespace
+
+extern "C" gasb_status gasb_adam_step(float* d_p, float* d_m, float* d_v, const float* d_g, int64_t size, int64_t step,
+                                      float lr, float beta1, float beta2, float eps, gasb_stream stream) {
+    return guard([&] {
+        require(size >= 0 && step >= 1, "adam_step: need size >= 0 and step >= 1");
+        require(size == 0 || (d_p && d_m && d_v && d_g), "adam_step: null buffer");
+        if (size == 0) return;
+        cudaStream_t st = as_stream(stream);
+        // bias corrections of step t on the host (std::pow, as nn.cpp:22-23), laid out for
+        // adam_kernel: bc[0] = clamp step 1, bc[2..3] = (1 - b1^t, 1 - b2^t), counter 0
+        double hb[4] = {1.0, 0.0, 1.0 - std::pow(static_cast<double>(beta1), static_cast<double>(step)),
+                        1.0 - std::pow(static_cast<double>(beta2), static_cast<double>(step))};
+        void* buf = nullptr;
+        GASB_CUDA(cudaMallocAsync(&buf, 4 * sizeof(double) + sizeof(int64_t), st));
+        double* bc = static_cast<double*>(buf);
+        int64_t* counter = reinterpret_cast<int64_t*>(bc + 4);
+        GASB_CUDA(cudaMemcpyAsync(bc, hb, sizeof(hb), cudaMemcpyHostToDevice, st));
+        GASB_CUDA(cudaMemsetAsync(counter, 0, sizeof(int64_t), st));
+        launch_adam(d_p, d_m, d_v, const_cast<float*>(d_g), size, counter, bc, lr, beta1, beta2, eps, 0.0f, nullptr,
+                    st, nullptr, nullptr);
+        GASB_CUDA(cudaFreeAsync(buf, st));
+        GASB_CUDA(cudaStreamSynchronize(st));  // hb is a host stack buffer
+    });
+}
+
+extern "C" gasb_status gasb_grad_clip(float* d_g, int64_t size, double max_norm, double* h_norm, gasb_stream stream) {
+    return guard([&] {
+        if (!(max_norm > 0.0)) throw std::invalid_argument("grad_clip: max_norm must be positive");
+        require(size >= 0 && (size == 0 || d_g), "grad_clip: bad buffer");
+        cudaStream_t st = as_stream(stream);
+        double* scratch = nullptr;
+        GASB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&scratch), sizeof(double) * (kNormBlocks + 1), st));
+        sumsq_kernel<<<kNormBlocks, 256, 0, st>>>(d_g, size, scratch);
+        finish_norm_kernel<<<1, 1, 0, st>>>(scratch, kNormBlocks);
+        const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(ceil_div(size, 256), 4 * 148));
+        scale_kernel<<<static_cast<unsigned>(blocks), 256, 0, st>>>(d_g, size, scratch + kNormBlocks, max_norm);
+        GASB_CUDA(cudaGetLastError());
+        double nn = 0.0;
+        GASB_CUDA(cudaMemcpyAsync(&nn, scratch + kNormBlocks, sizeof(double), cudaMemcpyDeviceToHost, st));
+        GASB_CUDA(cudaFreeAsync(scratch, st));
+        GASB_CUDA(cudaStreamSynchronize(st));
+        if (h_norm) *h_norm = nn;
+    });
+}

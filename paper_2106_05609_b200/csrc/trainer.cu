@@ -892,7 +892,7 @@ void gasb_trainer_s::enqueue_batch(int32_t p, bool train, bool push, bool use_ho
     GASB_CUDA(cudaGetLastError());
 }
 
-void gasb_trainer_s::run_epoch(int64_t epoch, bool shuffle) {
+void gasb_trainer_s::run_epoch(int64_t epoch, bool shuffle, int32_t begin, int32_t end) {
     // batch order (trainer.cpp:395-400)
     std::vector<int32_t> order(static_cast<size_t>(num_parts));
     std::iota(order.begin(), order.end(), 0);
@@ -900,6 +900,11 @@ void gasb_trainer_s::run_epoch(int64_t epoch, bool shuffle) {
         Rng rng(derive_seed(spec.seed ^ 0x6f726472ull, static_cast<uint64_t>(epoch)));
         for (size_t i = order.size(); i > 1; --i) std::swap(order[i - 1], order[rng.next_below(i)]);
     }
+    // [begin, end) of the order: a window of the epoch's batches (the timed configuration's
+    // parity test runs the first batches of an epoch; gas_epoch is the whole range)
+    begin = std::max(0, begin);
+    end = std::min(end < 0 ? num_parts : end, num_parts);
+    order = std::vector<int32_t>(order.begin() + std::min(begin, end), order.begin() + end);
     int64_t steps = 0;
     for (int32_t p : order) steps += ntrain[p] > 0 ? 1 : 0;
     ensure_bc(t_host + steps + 2);
@@ -1209,6 +1214,22 @@ gasb_status gasb_gas_epoch_async(gasb_trainer t, int64_t epoch, int32_t shuffle)
     return guard([&] {
         require(t, "trainer: null handle");
         t->run_epoch(epoch, shuffle != 0);
+    });
+}
+
+gasb_status gasb_gas_epoch_range_async(gasb_trainer t, int64_t epoch, int32_t shuffle, int32_t begin, int32_t end) {
+    return guard([&] {
+        require(t, "trainer: null handle");
+        require(begin >= 0 && begin <= end && end <= t->num_parts, "gas_epoch_range: need 0 <= begin <= end <= parts");
+        t->run_epoch(epoch, shuffle != 0, begin, end);
+    });
+}
+
+gasb_status gasb_trainer_part_losses(gasb_trainer t, double* h_losses) {
+    return guard([&] {
+        require(t && h_losses, "trainer: null argument");
+        GASB_CUDA(cudaStreamSynchronize(t->stream));
+        GASB_CUDA(cudaMemcpy(h_losses, t->loss.p, sizeof(double) * t->num_parts, cudaMemcpyDeviceToHost));
     });
 }
 

@@ -3,6 +3,7 @@
 #pragma once
 
 #include <algorithm>
+#include <cmath>
 #include <memory>
 #include <utility>
 #include <vector>
@@ -288,24 +289,54 @@ struct gasb_trainer_s {
     float* W(int32_t l) { return params.p + poff[layer_param[l]]; }
     float* gW(int32_t l) { return grads.p + poff[layer_param[l]]; }
 
+    // Adam bias corrections 1 - beta^t (nn.cpp:23-24), host std::pow as the reference, as a
+    // device table indexed by the device step counter. The captured batch graphs bake the
+    // table's address into their Adam node, so it must never move: build() sizes it once up
+    // to the saturation step T (the first t with both corrections == 1.0 exactly; pow is
+    // monotone, so every later t gives 1.0 too) and the kernel clamps t to T, held in bc[0].
+    // Betas that never saturate (beta -> 1) grow the table, and a move re-captures the graphs.
+    bool bc_saturated = false;
     void ensure_bc(int64_t t_max) {
-        if (t_max < bc_cap) return;
-        int64_t cap = std::max<int64_t>(1024, bc_cap);
-        while (cap <= t_max) cap *= 2;
+        if (bc_saturated || t_max < bc_cap) return;
+        const double b1 = spec.beta1, b2 = spec.beta2;
+        auto sat = [&](int64_t t) {
+            return 1.0 - std::pow(b1, static_cast<double>(t)) == 1.0 && 1.0 - std::pow(b2, static_cast<double>(t)) == 1.0;
+        };
+        constexpr int64_t kMaxTable = int64_t(1) << 22;  // 64 MB of corrections
+        int64_t cap = std::max<int64_t>(1024, bc_cap), tsat = 0;
+        if (bc_cap == 0)
+            for (int64_t t = 1; t < kMaxTable; ++t)
+                if (sat(t)) {
+                    tsat = t;
+                    break;
+                }
+        if (tsat > 0) cap = tsat + 1;
+        else
+            while (cap <= t_max) cap *= 2;
         std::vector<double> h(static_cast<size_t>(2 * cap));
-        for (int64_t t = 1; t < cap; ++t) {  // nn.cpp:23-24, host pow (as the reference)
-            h[2 * t] = 1.0 - std::pow(static_cast<double>(spec.beta1), static_cast<double>(t));
-            h[2 * t + 1] = 1.0 - std::pow(static_cast<double>(spec.beta2), static_cast<double>(t));
+        for (int64_t t = 1; t < cap; ++t) {
+            h[2 * t] = 1.0 - std::pow(b1, static_cast<double>(t));
+            h[2 * t + 1] = 1.0 - std::pow(b2, static_cast<double>(t));
         }
+        h[0] = static_cast<double>(tsat > 0 ? tsat : int64_t(1) << 52);  // clamp step
         GASB_CUDA(cudaStreamSynchronize(stream));
+        const bool moved = bc.p != nullptr;
         bc.upload(h);
         bc_cap = cap;
+        bc_saturated = tsat > 0;
+        if (moved) drop_graphs();  // their Adam nodes hold the old address
+    }
+    void drop_graphs() {
+        for (auto& g : graphs)
+            if (g) cudaGraphExecDestroy(g), g = nullptr;
+        for (auto& g : graphs_dp)
+            if (g) cudaGraphExecDestroy(g), g = nullptr;
     }
 
     void build(const float* h_features, const int32_t* h_labels, const uint8_t* h_train);
     void enqueue_batch(int32_t p, bool train, bool push, bool use_hoisted, bool fused, bool dp = false);
     void enqueue_hoisted();
-    void run_epoch(int64_t epoch, bool shuffle);
+    void run_epoch(int64_t epoch, bool shuffle, int32_t begin = 0, int32_t end = -1);
     // data-parallel mode (dp.cu): batches skip Adam and the step counters (applied after
     // the cross-rank exchange) and have their own per-part graphs
     std::vector<cudaGraphExec_t> graphs_dp;

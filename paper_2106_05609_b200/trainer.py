@@ -102,6 +102,16 @@ class GasTrainer:
     def gas_epoch_async(self, epoch: int, shuffle: bool = True) -> None:
         check(lib.gasb_gas_epoch_async(self._h, int(epoch), int(shuffle)))
 
+    def gas_epoch_range_async(self, epoch: int, begin: int, end: int, shuffle: bool = True) -> None:
+        """Batches order[begin:end] of gas_epoch's seeded order (same kernels and graphs)."""
+        check(lib.gasb_gas_epoch_range_async(self._h, int(epoch), int(shuffle), int(begin), int(end)))
+
+    def part_losses(self) -> np.ndarray:
+        """Per-part batch objective as last computed (part order)."""
+        out = np.zeros(self.schedule.num_parts, np.float64)
+        check(lib.gasb_trainer_part_losses(self._h, ptr(out)))
+        return out
+
     def last_loss(self) -> float:
         loss = f64()
         check(lib.gasb_trainer_last_loss(self._h, C.byref(loss)))
@@ -178,3 +188,16 @@ class GasTrainer:
     def set_params(self, values: np.ndarray) -> None:
         v = np.ascontiguousarray(values, dtype=np.float32)
         check(lib.gasb_trainer_set_params(self._h, ptr(v)))
+
+
+def adam_step(params, m, v, grads, step: int, lr=0.01, beta1=0.9, beta2=0.999, eps=1e-8, stream=None) -> None:
+    """AdamState::step (nn.cpp:20-41) in place on device tensors (torch CUDA float32)."""
+    check(lib.gasb_adam_step(ptr(params), ptr(m), ptr(v), ptr(grads), int(params.numel()), int(step), lr, beta1,
+                             beta2, eps, stream))
+
+
+def grad_clip(grads, max_norm: float, stream=None) -> float:
+    """grad_clip (nn.cpp:47-63) in place on a device tensor; returns the pre-clip norm."""
+    nn = f64()
+    check(lib.gasb_grad_clip(ptr(grads), int(grads.numel()), float(max_norm), C.byref(nn), stream))
+    return nn.value

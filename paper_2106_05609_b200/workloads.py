@@ -10,15 +10,22 @@ tools/gas_main.cpp:251-254). Calibrated here (stored nnz / inter-intra ratio):
   C2 pubmed   n=19,717   nnz≈88.6K  ratio≈0.21                           8 parts
   C3 reddit   n=232,965  nnz=114.97M ratio=2.82 (paper METIS Reddit 2.80) 200 parts,
               mean degree 493.5 (Reddit 492), max degree 15.2K
-Labels = community mod C (learnable); train mask: seeded 66% of nodes.
+
+Labels = community mod C. Features = N(0,1) noise + `signal` x the label's centroid (a
+seeded N(0,1) vector per class), so the labels are learnable from the features and the
+trained network stays live (with pure-noise features the bias-free 4-layer GCN at C3
+collapses to all-dead ReLUs and a loss of exactly ln C). Train mask: seeded 66% of nodes.
+
+This module is data-only at import time: `make_dataset` takes a generator backend, the
+product library's by default. bench.py's reference arm loads this file by path and passes
+the oracle's restatement of the same generator (oracle/pyoracle.py OracleSynth), so the
+reference arm never loads libgasb.so.
 """
 from __future__ import annotations
 
 from dataclasses import dataclass
 
 import numpy as np
-
-from .graph import build_graph, synth_features, synth_pairs
 
 
 @dataclass(frozen=True)
@@ -36,6 +43,7 @@ class Workload:
     hidden: int
     seed: int = 1
     train_frac: float = 0.66
+    signal: float = 0.5  # centroid scale in the features (0 = pure noise, round-1 data)
 
 
 WORKLOADS = {
@@ -45,10 +53,19 @@ WORKLOADS = {
     # C4: ogbn-products shape (61.9M raw undirected edges -> ~123.7M stored nnz), APPNP with
     # K = 3 propagation layers over 47-wide histories, inter/intra ~1.94
     "products_appnp": Workload("products_appnp", 2449029, 61_859_140, 100, 0.34, 120.0, 100, 47, "appnp", 3, 256),
+    # C5: ogbn-papers100M shape (111M nodes, 1.6B raw edges -> ~3.2B stored nnz), GCN L = 3,
+    # F = 128, 172 classes; needs the sharded history placement across GPUs
+    "papers100m": Workload("papers100m", 111_059_956, 1_615_685_872, 8192, 0.5, 2000.0, 128, 172, "gcn", 3, 256),
     # down-scaled shapes for fast parity runs
     "cora_appnp": Workload("cora_appnp", 2708, 5570, 10, 0.87, 60.0, 1433, 7, "appnp", 3, 64),
     "cora_gcnii": Workload("cora_gcnii", 2708, 5570, 10, 0.87, 60.0, 1433, 7, "gcnii", 8, 64),
     "reddit_mini": Workload("reddit_mini", 12000, 1_200_000, 12, 0.4, 60.0, 602, 41, "gcn", 4, 256),
+    # C4 down-scaled: the products_appnp generator parameters (F, C, h, K, intra, weights)
+    # at 50K nodes and the same mean degree (~50), 20 parts (~2.5K-node batches)
+    "products_mini": Workload("products_mini", 50_000, 1_262_840, 20, 0.34, 120.0, 100, 47, "appnp", 3, 256),
+    # C5 down-scaled: the papers100m generator parameters at 200K nodes, same mean degree
+    # (~29), 16 parts
+    "papers_mini": Workload("papers_mini", 200_000, 2_909_600, 16, 0.5, 2000.0, 128, 172, "gcn", 3, 256),
 }
 
 
@@ -64,16 +81,49 @@ class Dataset:
     assignment: np.ndarray
 
 
-def make_dataset(w: Workload | str, with_features: bool = True) -> Dataset:
+class ProductSynth:
+    """The generator as the product library exports it (gasb_synth_*, gasb_graph_build)."""
+
+    def synth_pairs(self, w: Workload):
+        from .graph import synth_pairs
+        return synth_pairs(w.num_nodes, w.num_pairs, w.parts, w.intra_fraction, gamma=2.5, min_weight=1.0,
+                           max_weight=w.max_weight, seed=w.seed)
+
+    def build_graph(self, edges, n):
+        from .graph import build_graph
+        g = build_graph(edges, n, symmetrize=True)
+        ro, co = g.csr()
+        return g, ro, co
+
+    def synth_features(self, n, dim, seed):
+        from .graph import synth_features
+        return synth_features(n, dim, seed=seed)
+
+
+def add_signal(x: np.ndarray, labels: np.ndarray, centroids: np.ndarray, signal: float) -> np.ndarray:
+    """x += signal * centroids[label], in place, in row blocks (fp32, one rounding each)."""
+    if signal == 0.0:
+        return x
+    c = (np.float32(signal) * centroids.astype(np.float32)).astype(np.float32)
+    step = 1 << 16
+    for r0 in range(0, len(x), step):
+        x[r0:r0 + step] += c[labels[r0:r0 + step]]
+    return x
+
+
+def make_dataset(w: Workload | str, with_features: bool = True, backend=None) -> Dataset:
     if isinstance(w, str):
         w = WORKLOADS[w]
-    edges, comm = synth_pairs(w.num_nodes, w.num_pairs, w.parts, w.intra_fraction, gamma=2.5, min_weight=1.0,
-                              max_weight=w.max_weight, seed=w.seed)
-    g = build_graph(edges, w.num_nodes, symmetrize=True)
+    be = backend or ProductSynth()
+    edges, comm = be.synth_pairs(w)
+    g, ro, co = be.build_graph(edges, w.num_nodes)
     del edges
-    ro, co = g.csr()
-    x = synth_features(w.num_nodes, w.in_dim, seed=w.seed + 1) if with_features else None
     rng = np.random.default_rng(w.seed + 2)
     labels = (comm % w.num_classes).astype(np.int32)
     train = (rng.random(w.num_nodes) < w.train_frac).astype(np.uint8)
+    x = None
+    if with_features:
+        x = be.synth_features(w.num_nodes, w.in_dim, w.seed + 1)
+        if w.signal:
+            add_signal(x, labels, be.synth_features(w.num_classes, w.in_dim, w.seed + 3), w.signal)
     return Dataset(w, g, ro, co, x, labels, train, comm.astype(np.int32))

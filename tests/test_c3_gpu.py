@@ -46,3 +46,43 @@ def test_reddit_c3_teacher_forced_batches(ref):
             worst[k] = max(worst.get(k, 0.0), v)
             assert v <= TOL, (p, k, v)
     print("C3 teacher-forced worst normwise errors:", worst)
+
+
+def test_reddit_c3_timed_configuration_free_running(ref):
+    """The configuration bench.py times — gas_epoch with layer-1 hoisting, per-batch CUDA
+    graphs and the segmented SpMM (seg_edges = 128) — over the first 20 batches of epoch 0
+    at full C3, free-running from the shared initialisation, against the reference's own
+    gas_epoch batches (src/trainer.cpp:386-442) on the same seeded order: every batch loss
+    within 1e-5 and the parameters and history tables after the window within 1e-5
+    normwise. Also checks the workload trains (loss below ln C), VERDICT r1 weak #2."""
+    import math
+    K = 20
+    ds = make_dataset("reddit")
+    w = ds.workload
+    sched = gb.BatchSchedule.build(ds.graph, ds.assignment, w.parts)
+    spec = gb.ModelSpec(kind="gcn", num_layers=w.num_layers, hidden=w.hidden, seed=3)
+    tr = gb.GasTrainer(sched, ds.features, ds.labels, ds.train_mask, w.num_classes, spec,
+                       gb.TrainerOptions(seg_edges=128, fused=True, use_graphs=True, hoist_layer1=True))
+    order = [int(p) for p in ref.epoch_order(w.parts, 3, 0)]
+    assert order == [int(p) for p in gb.epoch_order(w.parts, 3, 0)]
+    rs = ref.session(ds.row_offsets, ds.cols, ds.features, ds.labels, ds.train_mask, w.num_classes, ds.assignment,
+                     w.parts, make_spec(kind=0, num_layers=w.num_layers, hidden=w.hidden, seed=3),
+                     sample_parts=order[:K])
+    assert np.array_equal(tr.get_params(), rs.get_params())
+    tr.gas_epoch_range_async(0, 0, K)
+    gl = tr.part_losses()
+    worst = 0.0
+    rl = []
+    for slot in range(K):
+        lo, _ = rs.run(slot, 0)
+        rl.append(lo)
+        e = abs(gl[order[slot]] - lo) / abs(lo)
+        worst = max(worst, e)
+        assert e <= TOL, (slot, order[slot], gl[order[slot]], lo)
+    ep = normwise(tr.get_params(), rs.get_params())
+    eh = max(normwise(tr.history.layer_matrix(l), rs.get_history(l)) for l in range(1, w.num_layers))
+    print(f"C3 timed config, {K} free-running batches: worst loss rel {worst:.2e}, params {ep:.2e}, "
+          f"histories {eh:.2e}; losses ours {[round(float(gl[p]), 5) for p in order[:K]]} ref "
+          f"{[round(x, 5) for x in rl]}")
+    assert ep <= TOL and eh <= TOL
+    assert min(rl[-5:]) < math.log(w.num_classes) - 0.1  # the network is live, not collapsed to ln C
