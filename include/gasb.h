@@ -220,6 +220,42 @@ gasb_status gasb_adam_step(float* d_params, float* d_m, float* d_v, const float*
 gasb_status gasb_grad_clip(float* d_grads, int64_t size, double max_norm, double* h_norm, gasb_stream stream);
 
 /* ==================================================================================== */
+/* layer-level ops: Layer::forward and its tape backward (layers.hpp:51-72,               */
+/* layers.cpp:120-168) over one batch plan, for callers with their own Model::forward     */
+/* ==================================================================================== */
+/* One plan's device stencils (gcn stencil over local ids with segment tables, its
+ * transpose over every extended row, batch_local_rows), built once from the schedule;
+ * layers up to max_dim wide. */
+typedef struct gasb_batch_ops_s* gasb_batch_ops;
+gasb_status gasb_batch_ops_create(gasb_schedule s, int32_t part, int32_t max_dim, gasb_batch_ops* out);
+gasb_status gasb_batch_ops_sizes(gasb_batch_ops b, int32_t* num_batch, int32_t* num_extended);
+gasb_status gasb_batch_ops_destroy(gasb_batch_ops b);
+/* LayerConfig (layers.hpp:17-27) without GIN: kind 0 GCN, 2 APPNP, 3 GCNII. */
+typedef struct {
+    int32_t kind;
+    int32_t in_dim, out_dim;
+    float alpha, beta;
+} gasb_layer_config;
+/* Layer::forward (LayerContext{plan, agg, h_in, h0}, layers.hpp:40-45): h_in is |V_b| x
+ * in_dim in the plan's extended-node order (halo rows included), h0 (APPNP / GCNII) |V_b| x
+ * out_dim, W in_dim x out_dim (GCN, GCNII). out = |B_b| x out_dim. d_saved (|B_b| x in_dim)
+ * receives what the backward needs (GCN: the aggregation; GCNII: the mixed rows). The
+ * aggregation is the exact-fp64 SpMM; mixing and W~ = (1-beta) I + beta W follow the
+ * reference's rounding sequence. Stream-ordered, capturable. Same errors as the reference
+ * ("APPNP: missing h0", dimension checks). */
+gasb_status gasb_layer_fwd(gasb_batch_ops b, const gasb_layer_config* cfg, const float* d_h_in, int64_t ld_in,
+                           const float* d_h0, int64_t ld_h0, const float* d_w, int64_t ld_w, float* d_out,
+                           int64_t ld_out, float* d_saved, int64_t ld_saved, gasb_stream stream);
+/* The tape backward of that forward given gy = d loss / d out (|B_b| x out_dim): ACCUMULATES
+ * into gh_in (|V_b| x in_dim, every extended row, tensor.cpp:531-549), gh0 (|V_b| x out_dim,
+ * batch rows, APPNP / GCNII) and gW (in_dim x out_dim, GCN / GCNII); NULL outputs are
+ * skipped. d_scratch: |B_b| x max(in_dim, out_dim). Stream-ordered, capturable. */
+gasb_status gasb_layer_bwd(gasb_batch_ops b, const gasb_layer_config* cfg, const float* d_gy, int64_t ld_gy,
+                           const float* d_saved, int64_t ld_saved, const float* d_w, int64_t ld_w, float* d_gh_in,
+                           int64_t ld_gh_in, float* d_gh0, int64_t ld_gh0, float* d_gw, int64_t ld_gw,
+                           float* d_scratch, int64_t ld_scratch, gasb_stream stream);
+
+/* ==================================================================================== */
 /* gas-trainer: Model (trainer.hpp:45-88), gas_epoch (trainer.hpp:124-126,               */
 /* trainer.cpp:386-442), run_batch (trainer.cpp:295-339), AdamState (nn.hpp:21-38)       */
 /* ==================================================================================== */
@@ -263,6 +299,30 @@ gasb_status gasb_gas_epoch_range_async(gasb_trainer t, int64_t epoch, int32_t sh
 /* Per-part batch objective (num_parts doubles, part order) as last computed: the loss of
  * every batch with training rows that ran (synchronizes). */
 gasb_status gasb_trainer_part_losses(gasb_trainer t, double* h_losses);
+/* EpochReport (trainer.hpp:107-115) of one gas_epoch (EpochOptions{evaluate = false}):
+ *  loss            mean batch objective (as gasb_gas_epoch);
+ *  edges_per_layer sum over batches of plan.local_graph.num_edges() (stored in-edges of the
+ *                  batch rows), exactly as the reference;
+ *  peak_floats / h_batch_peak_floats (num_parts, epoch order): the activation floats each
+ *                  batch's device step writes (forward agg_l / act_l / logits and their
+ *                  gradients over the batch rows). This stands in for the reference's
+ *                  activation_meter (tensor.cpp:12-25), which counts its CPU tensors: the fused
+ *                  path materializes no V_b-row tensors, so the figure is linear in L and in
+ *                  B_b (SPEC A8), not equal to the reference's;
+ *  device_bytes    HBM the trainer holds (free-memory drop since its construction);
+ *  measure_staleness != 0: the frozen snapshot pass (gas_forward_snapshot, no push, no step)
+ *                  then measure_staleness (trainer.cpp:434-438): h_eps_max[L-1], per layer. */
+typedef struct {
+    int64_t epoch;
+    double loss;
+    int64_t peak_floats;
+    int64_t edges_per_layer;
+    int64_t device_bytes;
+    int32_t num_batches;
+    int32_t staleness_layers; /* L - 1 when measured, else 0 */
+} gasb_epoch_report;
+gasb_status gasb_gas_epoch_report(gasb_trainer t, int64_t epoch, int32_t shuffle, int32_t measure_staleness,
+                                  gasb_epoch_report* out, int64_t* h_batch_peak_floats, double* h_eps_max);
 /* Mean loss of the last epoch enqueued with gasb_gas_epoch_async (synchronizes). */
 gasb_status gasb_trainer_last_loss(gasb_trainer t, double* mean_loss);
 /* One batch with capture (same contract as the oracle's session_batch): acts = pushed rows

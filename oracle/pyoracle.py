@@ -188,7 +188,7 @@ class OracleSynth:
     def synth_pairs(self, w):
         src, dst = np.empty(w.num_pairs, np.int32), np.empty(w.num_pairs, np.int32)
         comm = np.empty(w.num_nodes, np.int32)
-        if self.o.lib.go_synth_pairs(w.num_nodes, w.parts, w.num_pairs, w.intra_fraction, 2.5, 1.0, w.max_weight,
+        if self.o.lib.go_synth_pairs(w.num_nodes, w.parts * w.comm_per_part, w.num_pairs, w.intra_fraction, 2.5, 1.0, w.max_weight,
                                      w.seed, _p(src), _p(dst), _p(comm)):
             raise ValueError("synth_pairs: bad argument")
         return np.stack([src, dst], axis=1), comm
@@ -265,6 +265,7 @@ class RefLib:
         L.ref_session_epoch.argtypes = [vp, i64, C.c_int, C.c_int, P(f64), P(f64)]
         L.ref_session_batch.argtypes = [vp, i32, i64, C.c_int, C.c_int, vp, vp, P(f64), vp, P(C.c_int)]
         L.ref_session_run.argtypes = [vp, i32, i64, P(f64), P(f64)]
+        L.ref_session_epoch_report.argtypes = [vp, i64, C.c_int, C.c_int, P(f64), P(i64), P(i64), vp, vp]
         L.ref_session_evaluate.argtypes = [vp, vp, vp, vp, vp]
         L.ref_session_infer.argtypes = [vp, vp, P(C.c_int)]
 
@@ -500,6 +501,18 @@ class Session:
         self.owner.check(self.owner.lib.ref_session_epoch(self.h, epoch, int(shuffle), int(prefetch), C.byref(loss),
                                                           C.byref(secs)))
         return loss.value, secs.value
+
+    def epoch_report(self, epoch, num_parts, measure_staleness=True, shuffle=True):
+        """Reference only: gas_epoch's EpochReport (loss, peak_floats, edges_per_layer,
+        batch_peak_floats, eps_max) with EpochOptions{evaluate=false}."""
+        loss, pk, epl = f64(), i64(), i64()
+        bp = np.zeros(num_parts, np.int64)
+        eps = np.zeros(max(self.spec.num_layers - 1, 1), np.float64)
+        self.owner.check(self.owner.lib.ref_session_epoch_report(self.h, epoch, int(shuffle), int(measure_staleness),
+                                                                 C.byref(loss), C.byref(pk), C.byref(epl), _p(bp),
+                                                                 _p(eps)))
+        return dict(loss=loss.value, peak_floats=pk.value, edges_per_layer=epl.value, batch_peak_floats=bp,
+                    eps_max=eps[:max(self.spec.num_layers - 1, 0)] if measure_staleness else np.zeros(0))
 
     # ---- data-parallel step semantics (SURVEY §8e; C restatement only) ----
     def dp_epoch(self, epoch, k, shuffle=True):

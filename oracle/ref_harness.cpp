@@ -508,6 +508,26 @@ int ref_session_epoch(void* sp, std::int64_t epoch, int shuffle, int use_prefetc
     });
 }
 
+// gas_epoch with the report fields (EpochReport, trainer.hpp:107-115): measure_staleness runs
+// the frozen gas_forward_snapshot pass and measure_staleness after the epoch (trainer.cpp:434-438).
+int ref_session_epoch_report(void* sp, std::int64_t epoch, int shuffle, int measure_staleness, double* loss,
+                             std::int64_t* peak_floats, std::int64_t* edges_per_layer, std::int64_t* batch_peak,
+                             double* eps_max) {
+    return guard([&] {
+        Session* s = static_cast<Session*>(sp);
+        EpochOptions o;
+        o.evaluate = false;
+        o.measure_staleness = measure_staleness != 0;
+        o.shuffle = shuffle != 0;
+        EpochReport r = gas_epoch(*s->model, *s->opt, s->ds, s->sched, s->store, epoch, o);
+        *loss = r.loss;
+        *peak_floats = r.peak_floats;
+        *edges_per_layer = r.edges_per_layer;
+        if (batch_peak) std::copy(r.batch_peak_floats.begin(), r.batch_peak_floats.end(), batch_peak);
+        if (eps_max) std::copy(r.eps_max.begin(), r.eps_max.end(), eps_max);
+    });
+}
+
 // One batch exactly as gas_epoch runs it (run_batch without capture, trainer.cpp:295-339,
 // then advance_step :426), timed with steady_clock: the reference arm's unit of work.
 int ref_session_run(void* sp, std::int32_t slot, std::int64_t epoch, double* loss_out, double* seconds) {

@@ -61,6 +61,11 @@ class TrainerOptionsC(C.Structure):
                 ("hoist_layer1", i32), ("device", i32)]
 
 
+class EpochReportC(C.Structure):  # gasb_epoch_report
+    _fields_ = [("epoch", i64), ("loss", f64), ("peak_floats", i64), ("edges_per_layer", i64),
+                ("device_bytes", i64), ("num_batches", i32), ("staleness_layers", i32)]
+
+
 _SIGS = {
     "gasb_last_error": (C.c_char_p, []),
     "gasb_abi_version": (i32, []),
@@ -113,6 +118,7 @@ _SIGS = {
     "gasb_gas_epoch_async": (i32, [vp, i64, i32]),
     "gasb_gas_epoch_range_async": (i32, [vp, i64, i32, i32, i32]),
     "gasb_trainer_part_losses": (i32, [vp, vp]),
+    "gasb_gas_epoch_report": (i32, [vp, i64, i32, i32, P(EpochReportC), vp, vp]),
     "gasb_adam_step": (i32, [vp, vp, vp, vp, i64, i64, f32, f32, f32, f32, vp]),
     "gasb_grad_clip": (i32, [vp, i64, f64, P(f64), vp]),
     "gasb_trainer_last_loss": (i32, [vp, P(f64)]),

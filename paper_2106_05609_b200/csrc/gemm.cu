@@ -184,16 +184,10 @@ extern "C" gasb_status gasb_gemm(int32_t op, int32_t m, int32_t n, int32_t k, co
     return gasb::guard([&] {
         gasb::require(m >= 0 && n >= 0 && k >= 0, "matmul: negative shape");
         gasb::require(beta == 0.f || beta == 1.f, "matmul: beta must be 0 or 1");
-        // split-K scratch for the standalone entry point (allocated once, never captured)
-        static float* ws = nullptr;
-        if (!ws) {
-            GASB_CUDA(cudaMalloc(&ws, sizeof(float) * (gasb::kGemmWsFloats + gasb::kGemmTileCounters)));
-            GASB_CUDA(cudaMemset(ws, 0, sizeof(float) * (gasb::kGemmWsFloats + gasb::kGemmTileCounters)));
-        }
-        gasb::set_gemm_workspace(ws, gasb::kGemmWsFloats);
-        struct Reset {
-            ~Reset() { gasb::set_gemm_workspace(nullptr, 0); }
-        } reset;
+        // the standalone entry point never splits K: split-K tiles share a workspace and spin
+        // on their peer slices, which is only safe for one grid in flight, and callers may
+        // use several streams
+        gasb::set_gemm_workspace(nullptr, 0);
         gasb::launch_gemm(op, m, n, k, a, lda, b, ldb, c, ldc, beta, false, nullptr, gasb::as_stream(stream));
     });
 }

@@ -365,7 +365,7 @@ __global__ void __launch_bounds__(kThreads, TALL ? 2 : 1) gemm_tc_kernel(const _
                         int v;
                         asm volatile("ld.acquire.gpu.global.b32 %0, [%1];\n" : "=r"(v) : "l"(arrive) : "memory");
                         if (v >= S) break;
-                        if (spins > (1u << 28)) __trap();  // grid <= #SMs: all slices are co-resident
+                        if (spins > (1u << 28)) __trap();  // grid <= #SMs and the only split-K grid in flight (launch_tc callers): every slice gets resident
                         __nanosleep(64);
                     }
                 }

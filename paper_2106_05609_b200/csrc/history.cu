@@ -565,6 +565,9 @@ gasb_status gasb_history_staleness(gasb_history h, const float* const* d_referen
     return guard([&] {
         require(h && d_reference && ld_reference, "measure_staleness: null argument");
         require(h_eps_max && h_eps_mean && h_age_max && h_age_mean, "measure_staleness: null argument");
+        // as every other host accessor: the trainer's streams are non-blocking, so wait for its
+        // in-flight pushes and step updates before reading the tables
+        GASB_CUDA(cudaDeviceSynchronize());
         const int64_t n = h->n;
         double* d_norm = nullptr;
         int64_t* d_age = nullptr;

@@ -57,20 +57,22 @@ __global__ void wtilde_kernel(const float* __restrict__ w, float* __restrict__ w
 // Backward of the mixing: dprop = (1 - alpha) * dmix; h0g[rows[i]] += alpha * dmix[i]
 // (scale bwd then select_rows bwd, tensor.cpp:254-275, :434-457). Rows of one batch are
 // distinct, so the read-modify-write of h0g is race-free.
-__global__ void __launch_bounds__(256) mix_bwd_kernel(const float* __restrict__ dmix, int64_t ldd, int32_t m,
-                                                      int32_t d, float alpha, float one_m_alpha,
+// dmix and dprop may alias (in place: each element is read before it is written); h0g may be
+// null (no h0 gradient wanted).
+__global__ void __launch_bounds__(256) mix_bwd_kernel(const float* dmix, int64_t ldd, int32_t m, int32_t d,
+                                                      float alpha, float one_m_alpha,
                                                       const int32_t* __restrict__ rows, float* __restrict__ h0g,
-                                                      int64_t ldh, float* __restrict__ dprop, int64_t ldp) {
+                                                      int64_t ldh, float* dprop, int64_t ldp) {
     const int lane = threadIdx.x & 31;
     const int64_t w = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     if (w >= m) return;
     const float* g = dmix + w * ldd;
-    float* hg = h0g + static_cast<int64_t>(rows[w]) * ldh;
+    float* hg = h0g ? h0g + static_cast<int64_t>(rows[w]) * ldh : nullptr;
     float* pg = dprop + w * ldp;
     for (int c = lane; c < d; c += 32) {
         const float v = g[c];
         pg[c] = __fmul_rn(one_m_alpha, v);
-        hg[c] = __fadd_rn(hg[c], __fmul_rn(alpha, v));
+        if (hg) hg[c] = __fadd_rn(hg[c], __fmul_rn(alpha, v));
     }
 }
 

@@ -341,6 +341,11 @@ void gasb_trainer_s::build(const float* h_features, const int32_t* h_labels, con
     trace("host staging");
 
     GASB_CUDA(cudaSetDevice(opt.device));
+    {
+        size_t fr = 0, tot = 0;
+        GASB_CUDA(cudaMemGetInfo(&fr, &tot));
+        mem_free_at_build = fr;
+    }
     GASB_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
     GASB_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
     GASB_CUDA(cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking));
@@ -485,6 +490,19 @@ void gasb_trainer_s::build(const float* h_features, const int32_t* h_labels, con
         GASB_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
     }
     row_scratch.alloc(nb_max);
+    // EpochReport bookkeeping (host): stored in-edges of each batch's rows, and the activation
+    // floats of its step: every forward layer input/output over the batch rows (+ the residual
+    // heads over all V_b rows) and their gradients (GCN's layer-1 input has none)
+    part_edges.assign(num_parts, 0);
+    part_act_floats.assign(num_parts, 0);
+    for (int32_t p = 0; p < num_parts; ++p) {
+        const Graph& G = *sched->graph;
+        for (int32_t v : sched->plans[p].batch) part_edges[p] += G.row_offsets[v + 1] - G.row_offsets[v];
+        int64_t fwd = 0;
+        for (int32_t l = 1; l <= L; ++l) fwd += static_cast<int64_t>(nb[p]) * (dims[l - 1] + dims[l]);
+        if (residual) fwd += static_cast<int64_t>(ne[p]) * (F + H + D);
+        part_act_floats[p] = 2 * fwd - (residual ? 0 : static_cast<int64_t>(nb[p]) * F);
+    }
     graphs.assign(num_parts, nullptr);
     graph_launches.assign(num_parts, 0);
     GASB_CUDA(cudaDeviceSynchronize());
@@ -848,9 +866,14 @@ void gasb_trainer_s::enqueue_batch(int32_t p, bool train, bool push, bool use_ho
             // after g is complete) ; dagg = g W^T on the main stream
             GASB_CUDA(cudaEventRecord(ev_fork[l], stream));
             GASB_CUDA(cudaStreamWaitEvent(side, ev_fork[l], 0));
+            // Split-K CTAs spin until every slice of their tile arrived, which is only safe while
+            // one split-K grid is in flight: the side-stream wgrads may split, the main-stream
+            // dgrads overlapping them run unsplit (no workspace) and never wait, so they always
+            // drain and the wgrad's slices become resident (at C3 the dgrads have 8 k-blocks and
+            // would not split anyway)
             set_gemm_workspace(gemm_ws2.p, kGemmWsFloats);
             launch_gemm(2, din, dout, m, a, lda, g, ldg, gW(l), pp(layer_param[l]), 0.f, false, nullptr, side);
-            set_gemm_workspace(gemm_ws.p, kGemmWsFloats);
+            set_gemm_workspace(nullptr, 0);
             GASB_CUDA(cudaEventRecord(ev_wdone[l], side));
             if (l == 1) break;  // x_ext carries no gradient
             // into the buffer the wgrad of layer l + 1 read: wait for it
@@ -875,6 +898,7 @@ void gasb_trainer_s::enqueue_batch(int32_t p, bool train, bool push, bool use_ho
             g = go;
             ldg = ldH;
         }
+        set_gemm_workspace(gemm_ws.p, kGemmWsFloats);
         GASB_CUDA(cudaEventRecord(ev_join, side));  // every weight gradient is complete
         GASB_CUDA(cudaStreamWaitEvent(stream, ev_join, 0));
         if (spec.l2_weight > 0.0f)  // l2_penalty (tensor.cpp:649-678): loss term + 2 w p on every gradient
@@ -915,6 +939,25 @@ void gasb_trainer_s::run_epoch(int64_t epoch, bool shuffle, int32_t begin, int32
     for (int32_t p : order) epoch_launches += launch_batch_graph(p, false);
     t_host += steps;
     last_order = order;
+}
+
+// gas_forward_snapshot (trainer.cpp:466-483): every batch in PART order, forward only against
+// the frozen store (no push, no step: the reference-structured path composes the batch's
+// fresh rows with pulled halos), each history layer's batch rows scattered by global id into
+// the snapshot tables (layer_values) that measure_staleness compares the store with.
+void gasb_trainer_s::enqueue_snapshot() {
+    if (L < 2) return;
+    const int64_t ldh = history_ld(hist), tab = static_cast<int64_t>(n) * ldh;
+    if (!snap.p) {
+        snap.alloc(static_cast<int64_t>(L - 1) * tab);
+        GASB_CUDA(cudaMemsetAsync(snap.p, 0, sizeof(float) * snap.n, stream));
+    }
+    for (int32_t p = 0; p < num_parts; ++p) {
+        enqueue_batch(p, false, false, false, false, /*dp: no Adam, no step*/ true);
+        for (int32_t l = 1; l < L; ++l)
+            launch_rows(0, batch_nodes.p + row_off[p], nb[p], act[l].p, ldA, snap.p + (l - 1) * tab, ldh, hist_dim,
+                        n, nullptr, nullptr, nullptr, stream);
+    }
 }
 
 // Enqueues one training batch (forward, push, loss, backward; + Adam and the step counters
@@ -1230,6 +1273,54 @@ gasb_status gasb_trainer_part_losses(gasb_trainer t, double* h_losses) {
         require(t && h_losses, "trainer: null argument");
         GASB_CUDA(cudaStreamSynchronize(t->stream));
         GASB_CUDA(cudaMemcpy(h_losses, t->loss.p, sizeof(double) * t->num_parts, cudaMemcpyDeviceToHost));
+    });
+}
+
+gasb_status gasb_gas_epoch_report(gasb_trainer t, int64_t epoch, int32_t shuffle, int32_t measure_staleness,
+                                  gasb_epoch_report* out, int64_t* h_batch_peak_floats, double* h_eps_max) {
+    return guard([&] {
+        require(t && out, "trainer: null argument");
+        t->run_epoch(epoch, shuffle != 0);
+        gasb_epoch_report r{};
+        r.epoch = epoch;
+        r.num_batches = static_cast<int32_t>(t->last_order.size());
+        {
+            GASB_CUDA(cudaStreamSynchronize(t->stream));
+            std::vector<double> l(static_cast<size_t>(t->num_parts));
+            GASB_CUDA(cudaMemcpy(l.data(), t->loss.p, sizeof(double) * l.size(), cudaMemcpyDeviceToHost));
+            double sum = 0.0;
+            int64_t cnt = 0;
+            for (int32_t p : t->last_order)
+                if (t->ntrain[p] > 0) {
+                    sum += l[p];
+                    ++cnt;
+                }
+            r.loss = cnt > 0 ? sum / static_cast<double>(cnt) : 0.0;
+        }
+        for (size_t i = 0; i < t->last_order.size(); ++i) {  // epoch order, as batch_peak_floats
+            const int32_t p = t->last_order[i];
+            r.peak_floats = std::max(r.peak_floats, t->part_act_floats[p]);
+            r.edges_per_layer += t->part_edges[p];
+            if (h_batch_peak_floats) h_batch_peak_floats[i] = t->part_act_floats[p];
+        }
+        size_t fr = 0, tot = 0;
+        GASB_CUDA(cudaMemGetInfo(&fr, &tot));
+        r.device_bytes = t->mem_free_at_build > fr ? static_cast<int64_t>(t->mem_free_at_build - fr) : 0;
+        if (measure_staleness && t->L >= 2) {  // trainer.cpp:434-438
+            t->enqueue_snapshot();
+            GASB_CUDA(cudaStreamSynchronize(t->stream));
+            const int64_t ldh = history_ld(t->hist), tab = static_cast<int64_t>(t->n) * ldh;
+            std::vector<const float*> refs(static_cast<size_t>(t->L - 1));
+            std::vector<int64_t> lds(refs.size(), ldh), amax(refs.size());
+            std::vector<double> emax(refs.size()), emean(refs.size()), amean(refs.size());
+            for (int32_t l = 1; l < t->L; ++l) refs[l - 1] = t->snap.p + (l - 1) * tab;
+            const gasb_status st = gasb_history_staleness(t->hist, refs.data(), lds.data(), emax.data(), emean.data(),
+                                                          amax.data(), amean.data());
+            if (st != GASB_OK) throw std::runtime_error(gasb_last_error());
+            r.staleness_layers = t->L - 1;
+            if (h_eps_max) std::copy(emax.begin(), emax.end(), h_eps_max);
+        }
+        *out = r;
     });
 }
 

@@ -333,6 +333,14 @@ struct gasb_trainer_s {
             if (g) cudaGraphExecDestroy(g), g = nullptr;
     }
 
+    // EpochReport (trainer.hpp:107-115): per part, the stored in-edges of its batch rows
+    // (plan.local_graph.num_edges(), summed into edges_per_layer) and the activation floats
+    // its step writes; the frozen snapshot tables of the staleness pass (gas_forward_snapshot,
+    // trainer.cpp:466-483), allocated on first use
+    std::vector<int64_t> part_edges, part_act_floats;
+    DevBuf<float> snap;
+    size_t mem_free_at_build = 0;
+    void enqueue_snapshot();
     void build(const float* h_features, const int32_t* h_labels, const uint8_t* h_train);
     void enqueue_batch(int32_t p, bool train, bool push, bool use_hoisted, bool fused, bool dp = false);
     void enqueue_hoisted();

@@ -7,7 +7,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from ._native import ModelSpecC, TrainerOptionsC, check, f64, i32, i64, lib, ptr, vp  # noqa: F401
+from ._native import EpochReportC, ModelSpecC, TrainerOptionsC, check, f64, i32, i64, lib, ptr, vp  # noqa: F401
 from .graph import BatchSchedule
 from .history import HistoryStore
 
@@ -111,6 +111,18 @@ class GasTrainer:
         out = np.zeros(self.schedule.num_parts, np.float64)
         check(lib.gasb_trainer_part_losses(self._h, ptr(out)))
         return out
+
+    def gas_epoch_report(self, epoch: int, shuffle: bool = True, measure_staleness: bool = False) -> dict:
+        """gas_epoch returning EpochReport's fields (trainer.hpp:107-115; gasb.h explains
+        batch_peak_floats); measure_staleness runs the frozen snapshot pass (trainer.cpp:434-438)."""
+        r = EpochReportC()
+        bp = np.zeros(self.schedule.num_parts, np.int64)
+        eps = np.zeros(max(self.spec.num_layers - 1, 1), np.float64)
+        check(lib.gasb_gas_epoch_report(self._h, int(epoch), int(shuffle), int(measure_staleness), C.byref(r),
+                                        ptr(bp), ptr(eps)))
+        return dict(epoch=r.epoch, loss=r.loss, peak_floats=r.peak_floats, edges_per_layer=r.edges_per_layer,
+                    device_bytes=r.device_bytes, batch_peak_floats=bp[:r.num_batches],
+                    eps_max=eps[:r.staleness_layers])
 
     def last_loss(self) -> float:
         loss = f64()

@@ -43,7 +43,8 @@ class Workload:
     hidden: int
     seed: int = 1
     train_frac: float = 0.66
-    signal: float = 0.5  # centroid scale in the features (0 = pure noise, round-1 data)
+    signal: float = 1.0  # centroid scale in the features (0 = pure noise, round-1 data)
+    comm_per_part: int = 4  # planted communities per partition (labels = community mod C)
 
 
 WORKLOADS = {
@@ -86,7 +87,8 @@ class ProductSynth:
 
     def synth_pairs(self, w: Workload):
         from .graph import synth_pairs
-        return synth_pairs(w.num_nodes, w.num_pairs, w.parts, w.intra_fraction, gamma=2.5, min_weight=1.0,
+        return synth_pairs(w.num_nodes, w.num_pairs, w.parts * w.comm_per_part, w.intra_fraction, gamma=2.5,
+                           min_weight=1.0,
                            max_weight=w.max_weight, seed=w.seed)
 
     def build_graph(self, edges, n):
@@ -120,10 +122,11 @@ def make_dataset(w: Workload | str, with_features: bool = True, backend=None) ->
     del edges
     rng = np.random.default_rng(w.seed + 2)
     labels = (comm % w.num_classes).astype(np.int32)
+    part = (comm // w.comm_per_part).astype(np.int32)  # comm = rank mod K: parts stay balanced
     train = (rng.random(w.num_nodes) < w.train_frac).astype(np.uint8)
     x = None
     if with_features:
         x = be.synth_features(w.num_nodes, w.in_dim, w.seed + 1)
         if w.signal:
             add_signal(x, labels, be.synth_features(w.num_classes, w.in_dim, w.seed + 3), w.signal)
-    return Dataset(w, g, ro, co, x, labels, train, comm.astype(np.int32))
+    return Dataset(w, g, ro, co, x, labels, train, part)

@@ -207,3 +207,45 @@ def test_l2_penalty_teacher_forced(ref, name):
         if sto:
             assert abs(lossg - losso) / abs(losso) <= TOL
             assert normwise(gg, go) <= TOL
+
+
+@pytest.mark.parametrize("name", ["cora", "reddit_mini", "cora_appnp", "cora_gcnii"])
+def test_epoch_report_with_staleness_vs_reference(ref, name):
+    """EpochReport of gas_epoch (trainer.hpp:107-115) with measure_staleness: the frozen
+    gas_forward_snapshot pass + measure_staleness (trainer.cpp:434-438) after the epoch,
+    against the compiled reference from the same initialisation. edges_per_layer exact;
+    loss within 1e-5; eps_max (per history layer) within the free-running drift."""
+    ds = make_dataset(name)
+    w = ds.workload
+    sched = gb.BatchSchedule.build(ds.graph, ds.assignment, w.parts)
+    spec = ModelSpec(kind=w.kind, num_layers=w.num_layers, hidden=w.hidden, seed=3)
+    tr = GasTrainer(sched, ds.features, ds.labels, ds.train_mask, w.num_classes, spec, TrainerOptions())
+    rs = ref.session(ds.row_offsets, ds.cols, ds.features, ds.labels, ds.train_mask, w.num_classes, ds.assignment,
+                     w.parts, make_spec(kind=gb.trainer.KINDS[w.kind], num_layers=w.num_layers, hidden=w.hidden,
+                                        seed=3))
+    for ep in range(2):
+        g = tr.gas_epoch_report(ep, measure_staleness=True)
+        r = rs.epoch_report(ep, w.parts, measure_staleness=True)
+        assert g["edges_per_layer"] == r["edges_per_layer"]
+        assert abs(g["loss"] - r["loss"]) / abs(r["loss"]) <= TOL
+        assert len(g["eps_max"]) == w.num_layers - 1
+        assert np.allclose(g["eps_max"], r["eps_max"], rtol=2e-3, atol=1e-5), (g["eps_max"], r["eps_max"])
+        assert len(g["batch_peak_floats"]) == w.parts and g["peak_floats"] == g["batch_peak_floats"].max()
+        assert g["device_bytes"] > 0
+    # the snapshot pass neither pushes nor steps: the next epoch still matches
+    assert normwise(tr.history.layer_matrix(1), rs.get_history(1)) <= 1e-4
+
+
+def test_epoch_report_activation_floats_linear_in_layers():
+    """SPEC A8: per-batch activation memory grows linearly with L (no V_b-row tensors kept
+    per layer)."""
+    ds = make_dataset("cora")
+    w = ds.workload
+    sched = gb.BatchSchedule.build(ds.graph, ds.assignment, w.parts)
+    peaks = []
+    for L in (2, 3, 4, 5):
+        tr = GasTrainer(sched, ds.features, ds.labels, ds.train_mask, w.num_classes,
+                        ModelSpec(kind="gcn", num_layers=L, hidden=64, seed=3), TrainerOptions())
+        peaks.append(tr.gas_epoch_report(0, shuffle=False)["peak_floats"])
+    d = np.diff(peaks)
+    assert (d > 0).all() and np.all(d[1:] == d[0]), peaks
