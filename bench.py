@@ -130,7 +130,7 @@ def cpu_baseline(ds, sample: int, kind_hint: str = "reference") -> dict:
     order = R.epoch_order(w.parts, 3, 0)
     warm = 2  # untimed: first-touch page faults of the fresh history store, as the reference arm's warm-up
     parts = [int(p) for p in order[:sample + warm]]
-    spec = make_spec(kind=0, num_layers=w.num_layers, hidden=w.hidden, seed=3)
+    spec = make_spec(kind=0, num_layers=w.num_layers, hidden=w.hidden, seed=3, lr=w.lr)
     s = R.session(ds.row_offsets, ds.cols, ds.features, ds.labels, ds.train_mask, w.num_classes, ds.assignment,
                   w.parts, spec, sample_parts=parts)
     for slot in range(warm):
@@ -191,7 +191,7 @@ def run_reference_arm(args):
     k = args.steps + args.warmup
     parts = [order[i % w.parts] for i in range(min(k, w.parts))]
     s = R.session(ds.row_offsets, ds.cols, ds.features, ds.labels, ds.train_mask, w.num_classes, ds.assignment,
-                  w.parts, make_spec(kind=0, num_layers=w.num_layers, hidden=w.hidden, seed=3), sample_parts=parts)
+                  w.parts, make_spec(kind=0, num_layers=w.num_layers, hidden=w.hidden, seed=3, lr=w.lr), sample_parts=parts)
     times, nodes = [], []
     for i in range(k):
         slot = i % len(parts)
@@ -220,7 +220,8 @@ def workload_config(ds) -> dict:
     return {"workload": f"{w.name}-shape GAS-{w.kind.upper()}", "num_nodes": w.num_nodes,
             "stored_nnz": int(len(ds.cols)), "in_dim": w.in_dim, "hidden": w.hidden, "num_classes": w.num_classes,
             "layers": w.num_layers, "partitions": w.parts, "partitioner": "planted communities (natural partition)",
-            "features": f"N(0,1) + {w.signal} x class centroid", "seeds": {"graph": w.seed, "model": 3},
+            "features": f"N(0,1) + {w.signal} x class centroid", "communities_per_part": w.comm_per_part,
+            "adam_lr": w.lr, "seeds": {"graph": w.seed, "model": 3},
             "l2_policy": "inputs larger than L2 (features 567 MB, histories 716 MB vs 126 MB L2)"}
 
 
@@ -246,7 +247,7 @@ def run_ours(args):
     ds = make_dataset(args.workload)
     w = ds.workload
     sched = gb.BatchSchedule.build(ds.graph, ds.assignment, w.parts)
-    spec = gb.ModelSpec(kind=w.kind, num_layers=w.num_layers, hidden=w.hidden, seed=3)
+    spec = gb.ModelSpec(kind=w.kind, num_layers=w.num_layers, hidden=w.hidden, seed=3, opt=gb.AdamConfig(lr=w.lr))
     # N > 1: data-parallel epochs (dp.cu: k batches per step, exchange over peer memory); each
     # rank hoists layer 1 over its own batches of the epoch
     opts = gb.TrainerOptions(seg_edges=args.seg_edges, device=local, hoist_layer1=not args.no_hoist)

@@ -66,6 +66,10 @@ class EpochReportC(C.Structure):  # gasb_epoch_report
                 ("device_bytes", i64), ("num_batches", i32), ("staleness_layers", i32)]
 
 
+class LayerConfigC(C.Structure):  # gasb_layer_config
+    _fields_ = [("kind", i32), ("in_dim", i32), ("out_dim", i32), ("alpha", f32), ("beta", f32)]
+
+
 _SIGS = {
     "gasb_last_error": (C.c_char_p, []),
     "gasb_abi_version": (i32, []),
@@ -112,6 +116,12 @@ _SIGS = {
     "gasb_spmm_fwd": (i32, [vp, i32, vp, vp, vp, i32, i64, i32, vp, i64, i32, vp]),
     "gasb_spmm_bwd": (i32, [vp, i32, vp, vp, vp, i64, i32, i32, vp, i64, vp, i64, vp]),
     "gasb_gemm": (i32, [i32, i32, i32, i32, vp, i64, vp, i64, vp, i64, f32, vp]),
+    "gasb_batch_ops_create": (i32, [vp, i32, i32, P(vp)]),
+    "gasb_batch_ops_sizes": (i32, [vp, P(i32), P(i32)]),
+    "gasb_batch_ops_destroy": (i32, [vp]),
+    "gasb_layer_fwd": (i32, [vp, P(LayerConfigC), vp, i64, vp, i64, vp, i64, vp, i64, vp, i64, vp]),
+    "gasb_layer_bwd": (i32, [vp, P(LayerConfigC), vp, i64, vp, i64, vp, i64, vp, i64, vp, i64, vp, i64, vp, i64,
+                             vp]),
     "gasb_trainer_create": (i32, [vp, vp, i32, vp, vp, i32, P(ModelSpecC), P(TrainerOptionsC), P(vp)]),
     "gasb_trainer_destroy": (i32, [vp]),
     "gasb_gas_epoch": (i32, [vp, i64, i32, P(f64)]),

@@ -11,10 +11,13 @@ tools/gas_main.cpp:251-254). Calibrated here (stored nnz / inter-intra ratio):
   C3 reddit   n=232,965  nnz=114.97M ratio=2.82 (paper METIS Reddit 2.80) 200 parts,
               mean degree 493.5 (Reddit 492), max degree 15.2K
 
-Labels = community mod C. Features = N(0,1) noise + `signal` x the label's centroid (a
-seeded N(0,1) vector per class), so the labels are learnable from the features and the
-trained network stays live (with pure-noise features the bias-free 4-layer GCN at C3
-collapses to all-dead ReLUs and a loss of exactly ln C). Train mask: seeded 66% of nodes.
+Labels = community mod C; each partition is `comm_per_part` planted communities (so a batch
+holds several labels, as a METIS part of real Reddit does, instead of one). Features = N(0,1)
+noise + `signal` x the label's centroid (a seeded N(0,1) vector per class), so the labels
+are learnable and the trained network stays live. Round 1 used one community per part and
+pure-noise features: every batch had a single label and the bias-free 4-layer GCN at C3
+collapsed to all-dead ReLUs (loss exactly ln C); profiles/r2_c3_dynamics_probe.txt has the
+variants measured on the GPU. Train mask: seeded 66% of nodes.
 
 This module is data-only at import time: `make_dataset` takes a generator backend, the
 product library's by default. bench.py's reference arm loads this file by path and passes
@@ -43,14 +46,17 @@ class Workload:
     hidden: int
     seed: int = 1
     train_frac: float = 0.66
-    signal: float = 1.0  # centroid scale in the features (0 = pure noise, round-1 data)
+    signal: float = 0.5  # centroid scale in the features (0 = pure noise, round-1 data)
     comm_per_part: int = 4  # planted communities per partition (labels = community mod C)
+    lr: float = 0.01  # Adam learning rate of the workload's model (AdamConfig default 0.01)
 
 
 WORKLOADS = {
     "cora": Workload("cora", 2708, 5570, 10, 0.87, 60.0, 1433, 7, "gcn", 2, 16),
     "pubmed_gcnii": Workload("pubmed_gcnii", 19717, 44700, 8, 0.8, 60.0, 500, 3, "gcnii", 64, 64),
-    "reddit": Workload("reddit", 232965, 65_300_000, 200, 0.335, 120.0, 602, 41, "gcn", 4, 256),
+    # lr 1e-3: at the AdamConfig default (1e-2) the bias-free 4-layer GCN diverges on this data
+    # (profiles/r2_c3_dynamics_probe.txt: loss 3.2 -> 148 in 12 epochs; 1e-3: 3.4 -> 0.15)
+    "reddit": Workload("reddit", 232965, 65_300_000, 200, 0.335, 120.0, 602, 41, "gcn", 4, 256, lr=1e-3),
     # C4: ogbn-products shape (61.9M raw undirected edges -> ~123.7M stored nnz), APPNP with
     # K = 3 propagation layers over 47-wide histories, inter/intra ~1.94
     "products_appnp": Workload("products_appnp", 2449029, 61_859_140, 100, 0.34, 120.0, 100, 47, "appnp", 3, 256),

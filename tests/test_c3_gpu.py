@@ -21,12 +21,12 @@ def test_reddit_c3_teacher_forced_batches(ref):
     ds = make_dataset("reddit")
     w = ds.workload
     sched = gb.BatchSchedule.build(ds.graph, ds.assignment, w.parts)
-    spec = gb.ModelSpec(kind="gcn", num_layers=w.num_layers, hidden=w.hidden, seed=3)
+    spec = gb.ModelSpec(kind="gcn", num_layers=w.num_layers, hidden=w.hidden, seed=3, opt=gb.AdamConfig(lr=w.lr))
     tr = gb.GasTrainer(sched, ds.features, ds.labels, ds.train_mask, w.num_classes, spec,
                        gb.TrainerOptions(use_graphs=False))
     order = [int(p) for p in ref.epoch_order(w.parts, 3, 0)[:2]]
     rs = ref.session(ds.row_offsets, ds.cols, ds.features, ds.labels, ds.train_mask, w.num_classes, ds.assignment,
-                     w.parts, make_spec(kind=0, num_layers=w.num_layers, hidden=w.hidden, seed=3),
+                     w.parts, make_spec(kind=0, num_layers=w.num_layers, hidden=w.hidden, seed=3, lr=w.lr),
                      sample_parts=order)
     assert np.array_equal(tr.get_params(), rs.get_params())  # Model::build init is bit-exact
     worst = {}
@@ -60,13 +60,13 @@ def test_reddit_c3_timed_configuration_free_running(ref):
     ds = make_dataset("reddit")
     w = ds.workload
     sched = gb.BatchSchedule.build(ds.graph, ds.assignment, w.parts)
-    spec = gb.ModelSpec(kind="gcn", num_layers=w.num_layers, hidden=w.hidden, seed=3)
+    spec = gb.ModelSpec(kind="gcn", num_layers=w.num_layers, hidden=w.hidden, seed=3, opt=gb.AdamConfig(lr=w.lr))
     tr = gb.GasTrainer(sched, ds.features, ds.labels, ds.train_mask, w.num_classes, spec,
                        gb.TrainerOptions(seg_edges=128, fused=True, use_graphs=True, hoist_layer1=True))
     order = [int(p) for p in ref.epoch_order(w.parts, 3, 0)]
     assert order == [int(p) for p in gb.epoch_order(w.parts, 3, 0)]
     rs = ref.session(ds.row_offsets, ds.cols, ds.features, ds.labels, ds.train_mask, w.num_classes, ds.assignment,
-                     w.parts, make_spec(kind=0, num_layers=w.num_layers, hidden=w.hidden, seed=3),
+                     w.parts, make_spec(kind=0, num_layers=w.num_layers, hidden=w.hidden, seed=3, lr=w.lr),
                      sample_parts=order[:K])
     assert np.array_equal(tr.get_params(), rs.get_params())
     tr.gas_epoch_range_async(0, 0, K)

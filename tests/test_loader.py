@@ -63,7 +63,8 @@ def test_schedule_matches_oracle_on_cora_shape(oracle):
 def _edges_of(ds):
     # regenerate the undirected pair list the dataset was built from
     w = ds.workload
-    e, _ = gb.synth_pairs(w.num_nodes, w.num_pairs, w.parts, w.intra_fraction, 2.5, 1.0, w.max_weight, w.seed)
+    e, _ = gb.synth_pairs(w.num_nodes, w.num_pairs, w.parts * w.comm_per_part, w.intra_fraction, 2.5, 1.0,
+                          w.max_weight, w.seed)
     return e, w.num_nodes
 
 

@@ -32,7 +32,7 @@ order0 = [int(p) for p in R.epoch_order(w.parts, 3, 0)]
 slot_of = {p: i for i, p in enumerate(order0)}
 kinds = {"gcn": 0, "appnp": 2, "gcnii": 3}
 s = R.session(ds.row_offsets, ds.cols, ds.features, ds.labels, ds.train_mask, w.num_classes, ds.assignment, w.parts,
-              make_spec(kind=kinds[w.kind], num_layers=w.num_layers, hidden=w.hidden, seed=3), sample_parts=order0)
+              make_spec(kind=kinds[w.kind], num_layers=w.num_layers, hidden=w.hidden, seed=3, lr=w.lr), sample_parts=order0)
 out = {"workload": w.name, "impl": "reference (oracle/_ref, 1 thread)", "epochs": []}
 t0 = time.time()
 for e in range(a.epochs):
