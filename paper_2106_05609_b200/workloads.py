@@ -6,10 +6,11 @@ build_graph semantics on both sides, so the stored graph is identical. The plant
 communities are the partition (the reference's own bench uses the natural partition,
 tools/gas_main.cpp:251-254). Calibrated here (stored nnz / inter-intra ratio):
 
-  C1 cora     n=2,708    nnz≈10.5K  ratio≈0.15 (paper METIS Cora 0.14)   10 parts
-  C2 pubmed   n=19,717   nnz≈88.6K  ratio≈0.21                           8 parts
-  C3 reddit   n=232,965  nnz=114.97M ratio=2.82 (paper METIS Reddit 2.80) 200 parts,
-              mean degree 493.5 (Reddit 492), max degree 15.2K
+  C1 cora     n=2,708    nnz=10,554  ratio 0.150 (paper METIS Cora 0.14)   10 parts
+  C2 pubmed   n=19,717   nnz=88,722  ratio 0.215                          8 parts
+  C3 reddit   n=232,965  nnz=114.23M ratio 2.800 (paper METIS Reddit 2.80) 200 parts,
+              mean degree 490.4 (Reddit 492), max degree 14.3K
+  C4 products n=2.45M    nnz=122.5M  ratio 1.938 (paper METIS products 1.94) 100 parts
 
 Labels = community mod C; each partition is `comm_per_part` planted communities (so a batch
 holds several labels, as a METIS part of real Reddit does, instead of one). Features = N(0,1)
@@ -52,11 +53,11 @@ class Workload:
 
 
 WORKLOADS = {
-    "cora": Workload("cora", 2708, 5570, 10, 0.87, 60.0, 1433, 7, "gcn", 2, 16),
-    "pubmed_gcnii": Workload("pubmed_gcnii", 19717, 44700, 8, 0.8, 60.0, 500, 3, "gcnii", 64, 64),
+    "cora": Workload("cora", 2708, 6150, 10, 0.88, 60.0, 1433, 7, "gcn", 2, 16),
+    "pubmed_gcnii": Workload("pubmed_gcnii", 19717, 45700, 8, 0.8, 60.0, 500, 3, "gcnii", 64, 64),
     # lr 1e-3: at the AdamConfig default (1e-2) the bias-free 4-layer GCN diverges on this data
     # (profiles/r2_c3_dynamics_probe.txt: loss 3.2 -> 148 in 12 epochs; 1e-3: 3.4 -> 0.15)
-    "reddit": Workload("reddit", 232965, 65_300_000, 200, 0.335, 120.0, 602, 41, "gcn", 4, 256, lr=1e-3),
+    "reddit": Workload("reddit", 232965, 82_000_000, 200, 0.475, 120.0, 602, 41, "gcn", 4, 256, lr=1e-3),
     # C4: ogbn-products shape (61.9M raw undirected edges -> ~123.7M stored nnz), APPNP with
     # K = 3 propagation layers over 47-wide histories, inter/intra ~1.94
     "products_appnp": Workload("products_appnp", 2449029, 61_859_140, 100, 0.34, 120.0, 100, 47, "appnp", 3, 256),
@@ -64,8 +65,8 @@ WORKLOADS = {
     # F = 128, 172 classes; needs the sharded history placement across GPUs
     "papers100m": Workload("papers100m", 111_059_956, 1_615_685_872, 8192, 0.5, 2000.0, 128, 172, "gcn", 3, 256),
     # down-scaled shapes for fast parity runs
-    "cora_appnp": Workload("cora_appnp", 2708, 5570, 10, 0.87, 60.0, 1433, 7, "appnp", 3, 64),
-    "cora_gcnii": Workload("cora_gcnii", 2708, 5570, 10, 0.87, 60.0, 1433, 7, "gcnii", 8, 64),
+    "cora_appnp": Workload("cora_appnp", 2708, 6150, 10, 0.88, 60.0, 1433, 7, "appnp", 3, 64),
+    "cora_gcnii": Workload("cora_gcnii", 2708, 6150, 10, 0.88, 60.0, 1433, 7, "gcnii", 8, 64),
     "reddit_mini": Workload("reddit_mini", 12000, 1_200_000, 12, 0.4, 60.0, 602, 41, "gcn", 4, 256),
     # C4 down-scaled: the products_appnp generator parameters (F, C, h, K, intra, weights)
     # at 50K nodes and the same mean degree (~50), 20 parts (~2.5K-node batches)

@@ -23,7 +23,15 @@ def cora():
 
 
 def _t(a):
-    return torch.from_numpy(np.ascontiguousarray(a, np.float32)).cuda()
+    """Device copy with a 16 B row pitch (the SpMM / TMA contract), as a strided view."""
+    a = np.asarray(a, np.float32)
+    t = torch.zeros(a.shape[0], (a.shape[1] + 3) // 4 * 4, device="cuda")
+    t[:, :a.shape[1]] = torch.from_numpy(np.ascontiguousarray(a))
+    return t[:, :a.shape[1]]
+
+
+def _z(r, c):
+    return _t(np.zeros((r, c), np.float32))
 
 
 @pytest.mark.parametrize("kind,din,dout", [("gcn", 96, 40), ("gcn", 256, 256), ("appnp", 47, 47), ("gcnii", 64, 64)])
@@ -63,13 +71,13 @@ def test_layer_forward_backward(oracle, cora, kind, din, dout):
         _, gx_ref = oracle.aggregate(rp, cols, cf, h, b * dmix)
     # ---- device ----
     H, H0, W, GY = _t(h), _t(h0), _t(w), _t(gy)
-    out = torch.zeros(nb, dout, device="cuda")
-    saved = torch.zeros(nb, din, device="cuda")
+    out = _z(nb, dout)
+    saved = _z(nb, din)
     gb.layer_forward(ops, cfg, H, out, saved, h0=H0 if kind != "gcn" else None, w=W if kind != "appnp" else None)
-    ghin = torch.zeros(ne, din, device="cuda")
-    gh0 = torch.zeros(ne, dout, device="cuda")
-    gw = torch.zeros(din, dout, device="cuda")
-    scratch = torch.zeros(nb, max(din, dout), device="cuda")
+    ghin = _z(ne, din)
+    gh0 = _z(ne, dout)
+    gw = _z(din, dout)
+    scratch = _z(nb, max(din, dout))
     gb.layer_backward(ops, cfg, GY, saved, scratch, w=W if kind != "appnp" else None, gh_in=ghin,
                       gh0=gh0 if kind != "gcn" else None, gw=gw if kind != "appnp" else None)
     torch.cuda.synchronize()
