@@ -381,6 +381,18 @@ typedef struct gasb_dp_s* gasb_dp;
 /* Turns a trainer into rank `rank` of `world` (1..8): allocates the exchange region and
  * makes the trainer's gradient and pushed-row buffers views into it. */
 gasb_status gasb_dp_create(gasb_trainer t, int32_t rank, int32_t world, gasb_dp* out);
+/* History placement of a data-parallel group.
+ * REPLICATED: every rank keeps the whole HistoryStore; a step's pushed rows are committed
+ *   into every replica (graphs whose tables fit one GPU: C3 716 MB).
+ * SHARDED: partition p's rows belong to rank p mod world; each rank keeps only its rows
+ *   (L-1 layers x its nodes, in its exported region; the trainer's full tables are freed).
+ *   Batches pull their halo rows from the owners' shards (NVLink P2P loads) into the
+ *   reference-structured compose -> SpMM path and push nothing; after the step barrier every
+ *   rank commits the step's rows it owns from all ranks' act slots. Same step semantics,
+ *   so the result is bit-identical to REPLICATED (C5: 2 x 111M x 256 tables need it). */
+#define GASB_DP_REPLICATED 0
+#define GASB_DP_SHARDED 1
+gasb_status gasb_dp_create_ex(gasb_trainer t, int32_t rank, int32_t world, int32_t placement, gasb_dp* out);
 /* This rank's region handle (GASB_DP_HANDLE_BYTES), to be all-gathered by the caller. */
 gasb_status gasb_dp_export(gasb_dp d, uint8_t* h_handle);
 /* Maps every peer's region from the gathered handles (world x GASB_DP_HANDLE_BYTES). */
@@ -393,6 +405,17 @@ gasb_status gasb_dp_check(gasb_dp d);
  * the arrays over ranks gives every part's loss exactly. Synchronizes. */
 gasb_status gasb_dp_last_losses(gasb_dp d, double* h_losses);
 gasb_status gasb_dp_launch_count(gasb_dp d, int64_t* out);
+/* SHARDED: gathers history layer `layer` (n x hist_dim, host) from every rank's shard
+ * (synchronizes; the trainer's own HistoryStore raises logic_error once its tables are
+ * sharded). */
+gasb_status gasb_dp_read_history(gasb_dp d, int32_t layer, float* h_out);
+/* Bytes of the last epoch: NVLink = peer gradient slots read by the reduce + peer act rows
+ * read by the commits + (sharded) halo rows read from peer shards; local_pull = halo rows
+ * this rank read from its own shard; shard_rows = history rows this rank holds per layer. */
+gasb_status gasb_dp_traffic(gasb_dp d, int64_t* nvlink_bytes, int64_t* local_pull_bytes, int64_t* shard_rows);
+/* The SHARDED row ownership (host): owner_local[v] = owner << 29 | row in the owner's
+ * shard (n entries), rows_per_rank[world]. */
+gasb_status gasb_dp_shard_map(gasb_schedule s, int32_t world, uint32_t* h_owner_local, int64_t* h_rows_per_rank);
 gasb_status gasb_dp_destroy(gasb_dp d);
 /* gas_epoch's batch order (trainer.cpp:395-400) for `epoch` (host only). */
 gasb_status gasb_epoch_order(int32_t num_parts, uint64_t seed, int64_t epoch, int32_t shuffle, int32_t* h_order);

@@ -12,11 +12,11 @@ from .graph import (BatchPlan, BatchSchedule, Graph, build_graph, graph_from_csr
 from .history import HistoryStore, Prefetcher, PrefetchHandle  # noqa: F401
 from .trainer import AdamConfig, GasTrainer, ModelSpec, TrainerOptions, adam_step, grad_clip  # noqa: F401
 from .layers import BatchOps, LayerConfig, layer_backward, layer_forward  # noqa: F401
-from .dp import DataParallelTrainer, epoch_order, step_plan  # noqa: F401
+from .dp import DataParallelTrainer, epoch_order, shard_map, step_plan  # noqa: F401
 
 __all__ = [
     "Graph", "build_graph", "graph_from_csr", "make_batch_plan", "BatchPlan", "BatchSchedule", "partition_parts",
     "synth_pairs", "synth_features", "save_partition", "load_partition", "random_partition", "HistoryStore", "Prefetcher", "PrefetchHandle", "ModelSpec", "AdamConfig",
     "TrainerOptions", "GasTrainer", "adam_step", "grad_clip", "BatchOps", "LayerConfig", "layer_forward",
-    "layer_backward", "DataParallelTrainer", "epoch_order", "step_plan",
+    "layer_backward", "DataParallelTrainer", "epoch_order", "step_plan", "shard_map",
 ]

@@ -149,6 +149,10 @@ _SIGS = {
     "gasb_trainer_full_logits": (i32, [vp, vp]),
     "gasb_trainer_infer_from_history": (i32, [vp, vp, P(i32)]),
     "gasb_dp_create": (i32, [vp, i32, i32, P(vp)]),
+    "gasb_dp_create_ex": (i32, [vp, i32, i32, i32, P(vp)]),
+    "gasb_dp_read_history": (i32, [vp, i32, vp]),
+    "gasb_dp_traffic": (i32, [vp, P(i64), P(i64), P(i64)]),
+    "gasb_dp_shard_map": (i32, [vp, i32, vp, vp]),
     "gasb_dp_export": (i32, [vp, vp]),
     "gasb_dp_connect": (i32, [vp, vp]),
     "gasb_dp_epoch_async": (i32, [vp, i64, i32]),

@@ -159,6 +159,64 @@ __global__ void __launch_bounds__(256) dp_commit_kernel(CommitJobs jobs, int32_t
     }
 }
 
+// ---- partition-sharded placement ---------------------------------------------------
+// dst[i] = H_layer[ids[i]] from the owner's shard: one warp per row, float4 columns; rows
+// owned by a peer are NVLink P2P loads through its IPC-mapped region.
+__global__ void __launch_bounds__(256) shard_pull_kernel(ShardView s, int32_t layer, const int32_t* __restrict__ ids,
+                                                         int64_t count, float* __restrict__ dst, int64_t ldd,
+                                                         int32_t dim) {
+    const int lane = threadIdx.x & 31;
+    const int64_t w = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    if (w >= count) return;
+    const uint32_t ol = s.owner_local[ids ? ids[w] : w];
+    const int32_t o = static_cast<int32_t>(ol >> kShardLocalBits);
+    const int64_t li = ol & ((1u << kShardLocalBits) - 1);
+    const float* src = s.tables[o] + (layer - 1) * s.layer_stride[o] + li * s.ld;
+    float* d = dst + w * ldd;
+    if ((dim & 3) == 0 && (ldd & 3) == 0) {
+        for (int c = lane; c < dim / 4; c += 32)
+            reinterpret_cast<float4*>(d)[c] = __ldcv(reinterpret_cast<const float4*>(src) + c);
+    } else {
+        for (int c = lane; c < dim; c += 32) d[c] = __ldcv(src + c);
+    }
+}
+
+// Sharded commit: of every job's (rank's) batch rows, the ones this rank owns go into its
+// shard (stamps = the start-of-step store step, the layer's value flags), from the job's
+// act slot (a peer's over NVLink, or this rank's own).
+__global__ void __launch_bounds__(256) dp_commit_sharded_kernel(CommitJobs jobs, int32_t total_rows, int32_t layers,
+                                                                int64_t layer_stride, int64_t lda, int32_t dim,
+                                                                const uint32_t* __restrict__ owner_local, int32_t me,
+                                                                float* shard, int64_t shard_stride, int64_t ldt,
+                                                                int64_t* stamps, int64_t n_owned, const int64_t* step,
+                                                                int32_t* flags) {
+    const int lane = threadIdx.x & 31;
+    const int64_t w = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    if (w >= static_cast<int64_t>(total_rows) * layers) return;
+    const int32_t l = static_cast<int32_t>(w / total_rows);
+    const int32_t r = static_cast<int32_t>(w % total_rows);
+    int jb = 0;
+    while (jb + 1 < jobs.njobs && r >= jobs.j[jb + 1].row0) ++jb;
+    const CommitJob& J = jobs.j[jb];
+    const int32_t i = r - J.row0;
+    const uint32_t ol = owner_local[J.ids[i]];
+    if (static_cast<int32_t>(ol >> kShardLocalBits) != me) return;
+    const int64_t li = ol & ((1u << kShardLocalBits) - 1);
+    const float* src = J.acts + l * layer_stride + static_cast<int64_t>(i) * lda;
+    float* dst = shard + l * shard_stride + li * ldt;
+    int32_t f = 0;
+    for (int c = lane; c < dim; c += 32) {
+        const float x = __ldcv(src + c);
+        dst[c] = x;
+        f |= table_flag_of(x);
+    }
+    f = __reduce_or_sync(0xffffffffu, f);
+    if (lane == 0) {
+        stamps[l * n_owned + li] = *step;
+        if (f) atomicOr(flags + l, f);
+    }
+}
+
 __global__ void dp_end_step_kernel(int64_t* step, int64_t* t_counter, int32_t batches, int32_t stepped) {
     *step += batches;
     if (stepped) *t_counter += 1;
@@ -175,6 +233,29 @@ uint64_t derive_seed(uint64_t s, uint64_t a, uint64_t b = 0, uint64_t c = 0) {
 }
 
 }  // namespace
+
+void launch_shard_pull(const ShardView& s, int32_t layer, const int32_t* ids, int64_t count, float* dst, int64_t ldd,
+                       int32_t dim, cudaStream_t st) {
+    if (count <= 0) return;
+    shard_pull_kernel<<<static_cast<unsigned>(ceil_div(count * 32, 256)), 256, 0, st>>>(s, layer, ids, count, dst,
+                                                                                        ldd, dim);
+    ++t_launches;
+    GASB_CUDA(cudaGetLastError());
+}
+
+// Row ownership of the sharded placement: partition p belongs to rank p mod world; a rank's
+// rows are its parts' batch nodes in part order (then id order), packed owner << 29 | row.
+void shard_map(const Schedule& S, int32_t world, std::vector<uint32_t>& owner_local, std::vector<int64_t>& n_owned) {
+    owner_local.assign(static_cast<size_t>(S.graph->num_nodes), 0xffffffffu);
+    n_owned.assign(static_cast<size_t>(world), 0);
+    for (int32_t p = 0; p < S.num_parts; ++p) {
+        const int32_t o = p % world;
+        for (int32_t v : S.plans[p].batch) {
+            require(n_owned[o] < (int64_t(1) << kShardLocalBits), "dp: shard exceeds 2^29 rows");
+            owner_local[v] = (static_cast<uint32_t>(o) << kShardLocalBits) | static_cast<uint32_t>(n_owned[o]++);
+        }
+    }
+}
 
 // gas_epoch's batch order (trainer.cpp:395-400): Fisher-Yates with Rng(derive_seed(seed ^
 // "ordr", epoch)).next_below (include/gas/rng.hpp), identity when !shuffle.
@@ -202,6 +283,22 @@ using namespace gasb;
 struct gasb_dp_s {
     gasb_trainer t = nullptr;
     int32_t rank = 0, world = 1;
+    // sharded placement (GASB_DP_SHARDED): this rank's shard of every history layer sits in
+    // its region at off_shard (n_owned[rank] rows per layer, pitch shard_ld); stamps / value
+    // flags of the shard are local
+    bool sharded = false;
+    size_t off_shard = 0;
+    int64_t shard_ld = 0;
+    std::vector<int64_t> n_owned;
+    std::vector<uint32_t> h_owner_local;
+    DevBuf<uint32_t> owner_local;
+    DevBuf<int64_t> shard_stamps;
+    DevBuf<int32_t> shard_flags;
+    // NVLink bytes of the last epoch (host-counted from the plans): halo rows read from peer
+    // shards + peer act rows read by the commits (sharded), or peer act rows committed into
+    // the replica (replicated); plus the gradient slots read by the reduce
+    int64_t nvlink_bytes = 0, local_pull_bytes = 0;
+    std::vector<int64_t> part_remote_halo, part_local_halo;
     char* region = nullptr;
     size_t off_flags = 0, off_grads = 0, off_acts = 0, bytes = 0;
     int64_t act_layer_stride = 0;  // floats between act_l slots
@@ -223,6 +320,18 @@ struct gasb_dp_s {
     uint64_t* flags_of(int32_t j) const { return reinterpret_cast<uint64_t*>(peer[j] + off_flags); }
     const float* grads_of(int32_t j) const { return reinterpret_cast<const float*>(peer[j] + off_grads); }
     const float* acts_of(int32_t j) const { return reinterpret_cast<const float*>(peer[j] + off_acts); }
+    float* shard_of(int32_t j) const { return reinterpret_cast<float*>(peer[j] + off_shard); }
+    void bind_shard_view() {
+        ShardView v{};
+        v.owner_local = owner_local.p;
+        v.ld = shard_ld;
+        v.world = world;
+        for (int32_t j = 0; j < world; ++j) {
+            v.tables[j] = shard_of(j);
+            v.layer_stride[j] = n_owned[j] * shard_ld;
+        }
+        t->shard = v;
+    }
 
     void barrier() {
         PeerPtrs pp{};
@@ -256,7 +365,50 @@ struct gasb_dp_s {
             ++t_launches;
             GASB_CUDA(cudaGetLastError());
         }
-        if (hist_layers > 0) {
+        // NVLink traffic of the step (bookkeeping): gradient slots of the peers, halo rows from
+        // peer shards (sharded), peer act rows read by the commit
+        {
+            const int64_t rowb = static_cast<int64_t>(T.hist_dim) * 4 * hist_layers;
+            if (count > 0) nvlink_bytes += static_cast<int64_t>(T.nparam) * 4 * (count - ((mask >> rank) & 1u));
+            for (int32_t j = 0; j < kk; ++j) {
+                if (j == rank) {
+                    if (sharded) {
+                        nvlink_bytes += part_remote_halo[parts[j]] * rowb;
+                        local_pull_bytes += part_local_halo[parts[j]] * rowb;
+                    }
+                    continue;
+                }
+                int64_t rows_in = T.nb[parts[j]];
+                if (sharded) {
+                    rows_in = 0;
+                    for (int32_t v : T.sched->plans[parts[j]].batch)
+                        rows_in += static_cast<int32_t>(h_owner_local[v] >> kShardLocalBits) == rank;
+                }
+                nvlink_bytes += rows_in * rowb;
+            }
+        }
+        if (hist_layers > 0 && sharded) {
+            CommitJobs jobs{};
+            int32_t rows = 0;
+            for (int32_t j = 0; j < kk; ++j) {  // every rank's batch, this rank's own included
+                const int32_t p = parts[j];
+                CommitJob& J = jobs.j[jobs.njobs++];
+                J.acts = acts_of(j);
+                J.ids = T.batch_nodes.p + T.row_off[p];
+                J.nb = T.nb[p];
+                J.row0 = rows;
+                rows += T.nb[p];
+            }
+            if (rows > 0) {
+                const int64_t warps = static_cast<int64_t>(rows) * hist_layers;
+                dp_commit_sharded_kernel<<<static_cast<unsigned>(ceil_div(warps * 32, 256)), 256, 0, T.stream>>>(
+                    jobs, rows, hist_layers, act_layer_stride, T.ldA, T.hist_dim, owner_local.p, rank,
+                    shard_of(rank), n_owned[rank] * shard_ld, shard_ld, shard_stamps.p, n_owned[rank],
+                    history_step_ptr(T.hist), shard_flags.p);
+                ++t_launches;
+                GASB_CUDA(cudaGetLastError());
+            }
+        } else if (hist_layers > 0) {
             CommitJobs jobs{};
             int32_t rows = 0;
             for (int32_t j = 0; j < kk; ++j) {
@@ -300,7 +452,12 @@ struct gasb_dp_s {
 extern "C" {
 
 gasb_status gasb_dp_create(gasb_trainer t, int32_t rank, int32_t world, gasb_dp* out) {
+    return gasb_dp_create_ex(t, rank, world, GASB_DP_REPLICATED, out);
+}
+
+gasb_status gasb_dp_create_ex(gasb_trainer t, int32_t rank, int32_t world, int32_t placement, gasb_dp* out) {
     return guard([&] {
+        require(placement == GASB_DP_REPLICATED || placement == GASB_DP_SHARDED, "dp: unknown history placement");
         require(t && out, "dp: null argument");
         require(world >= 1 && world <= kMaxWorld, "dp: world size must be in [1, 8]");
         require(rank >= 0 && rank < world, "dp: rank out of range");
@@ -318,6 +475,27 @@ gasb_status gasb_dp_create(gasb_trainer t, int32_t rank, int32_t world, gasb_dp*
         d->off_acts = align_up(d->off_grads + sizeof(float) * static_cast<size_t>(t->nparam));
         d->bytes = align_up(d->off_acts + sizeof(float) * static_cast<size_t>(d->act_layer_stride) *
                                               static_cast<size_t>(std::max(d->hist_layers, 1)));
+        d->sharded = placement == GASB_DP_SHARDED && d->hist_layers > 0;
+        if (d->sharded) {
+            if (t->opt.prefetch) throw std::invalid_argument("dp: the sharded placement has no prefetch mode");
+            shard_map(*t->sched, world, d->h_owner_local, d->n_owned);
+            d->shard_ld = round_up(t->hist_dim, 4);
+            d->off_shard = d->bytes;
+            d->bytes = align_up(d->off_shard + sizeof(float) * static_cast<size_t>(d->hist_layers) *
+                                                   static_cast<size_t>(d->n_owned[rank] * d->shard_ld));
+            d->owner_local.upload(d->h_owner_local);
+            d->shard_stamps.alloc(static_cast<int64_t>(d->hist_layers) * std::max<int64_t>(d->n_owned[rank], 1));
+            GASB_CUDA(cudaMemset(d->shard_stamps.p, 0xff, sizeof(int64_t) * d->shard_stamps.n));  // -1: never pushed
+            d->shard_flags.alloc(d->hist_layers);
+            d->shard_flags.zero();
+            // halo rows per part by owner (this rank's view): remote = NVLink, local = HBM
+            d->part_remote_halo.assign(t->num_parts, 0);
+            d->part_local_halo.assign(t->num_parts, 0);
+            for (int32_t p = 0; p < t->num_parts; ++p)
+                for (int32_t v : t->sched->plans[p].halo)
+                    (static_cast<int32_t>(d->h_owner_local[v] >> kShardLocalBits) == rank ? d->part_local_halo
+                                                                                           : d->part_remote_halo)[p]++;
+        }
         require(!t->dp_region.p, "dp: the trainer already belongs to a data-parallel group");
         t->dp_region.alloc(static_cast<int64_t>(d->bytes));  // owned by the trainer (its grads/act_l live there)
         d->region = t->dp_region.p;
@@ -346,11 +524,22 @@ gasb_status gasb_dp_create(gasb_trainer t, int32_t rank, int32_t world, gasb_dp*
         d->err.zero();
         // every part can land on any rank (the epoch order is reshuffled): capture all the
         // data-parallel batch graphs now, not inside timed epochs
-        if (t->opt.use_graphs)
+        if (t->opt.use_graphs && !d->sharded)  // (sharded: once the peers' shards are mapped)
             for (int32_t p = 0; p < t->num_parts; ++p) t->capture_batch_graph(p, true);
         d->peer.assign(static_cast<size_t>(world), nullptr);
         d->peer[rank] = d->region;
-        if (world == 1) d->connected = true;
+        if (d->sharded) {
+            // the store's full tables are replaced by the group's shards (start: zeros, as the
+            // fresh store), the batches pull halos from them and push nothing (see step())
+            history_release_tables(t->hist);
+            t->sharded_dp = true;
+        }
+        if (world == 1) {
+            d->connected = true;
+            if (d->sharded) d->bind_shard_view();
+        }
+        if (d->sharded && t->opt.use_graphs && world == 1)
+            for (int32_t p = 0; p < t->num_parts; ++p) t->capture_batch_graph(p, true);
         *out = d.release();
     });
 }
@@ -379,6 +568,11 @@ gasb_status gasb_dp_connect(gasb_dp d, const uint8_t* h_handles) {
             d->peer[j] = static_cast<char*>(p);
         }
         d->connected = true;
+        if (d->sharded) {  // the batch graphs bake the peers' shard pointers: capture them now
+            d->bind_shard_view();
+            if (d->t->opt.use_graphs)
+                for (int32_t p = 0; p < d->t->num_parts; ++p) d->t->capture_batch_graph(p, true);
+        }
     });
 }
 
@@ -394,6 +588,8 @@ gasb_status gasb_dp_epoch_async(gasb_dp d, int64_t epoch, int32_t shuffle) {
         for (int32_t s0 = 0; s0 < T.num_parts; s0 += d->world) ++steps;
         T.ensure_bc(T.t_host + steps + 2);
         d->epoch_launches = 0;
+        d->nvlink_bytes = 0;
+        d->local_pull_bytes = 0;
         d->last_parts.clear();
         for (int32_t s0 = 0; s0 < T.num_parts; s0 += d->world)
             if (d->rank < std::min(d->world, T.num_parts - s0)) d->last_parts.push_back(order[s0 + d->rank]);
@@ -442,6 +638,43 @@ gasb_status gasb_dp_launch_count(gasb_dp d, int64_t* out) {
     return guard([&] {
         require(d && out, "dp: null argument");
         *out = d->epoch_launches;
+    });
+}
+
+gasb_status gasb_dp_read_history(gasb_dp d, int32_t layer, float* h_out) {
+    return guard([&] {
+        require(d && h_out, "dp: null argument");
+        gasb_trainer_s& T = *d->t;
+        if (!d->sharded) throw std::logic_error("dp: the replicated placement keeps the trainer's HistoryStore");
+        if (!d->connected) throw std::logic_error("dp: connect() before reading the shards");
+        require(layer >= 1 && layer <= d->hist_layers, "HistoryStore: layer out of range");
+        GASB_CUDA(cudaStreamSynchronize(T.stream));
+        DevBuf<float> full;
+        full.alloc(static_cast<int64_t>(T.n) * d->shard_ld);
+        launch_shard_pull(T.shard, layer, nullptr, T.n, full.p, d->shard_ld, T.hist_dim, T.stream);
+        GASB_CUDA(cudaMemcpy2DAsync(h_out, sizeof(float) * T.hist_dim, full.p, sizeof(float) * d->shard_ld,
+                                    sizeof(float) * T.hist_dim, T.n, cudaMemcpyDeviceToHost, T.stream));
+        GASB_CUDA(cudaStreamSynchronize(T.stream));
+    });
+}
+
+gasb_status gasb_dp_traffic(gasb_dp d, int64_t* nvlink_bytes, int64_t* local_pull_bytes, int64_t* shard_rows) {
+    return guard([&] {
+        require(d, "dp: null handle");
+        if (nvlink_bytes) *nvlink_bytes = d->nvlink_bytes;
+        if (local_pull_bytes) *local_pull_bytes = d->local_pull_bytes;
+        if (shard_rows) *shard_rows = d->sharded ? d->n_owned[d->rank] : d->t->n;
+    });
+}
+
+gasb_status gasb_dp_shard_map(gasb_schedule s, int32_t world, uint32_t* h_owner_local, int64_t* h_rows_per_rank) {
+    return guard([&] {
+        require(s && world >= 1 && world <= kMaxWorld, "dp: bad argument");
+        std::vector<uint32_t> ol;
+        std::vector<int64_t> no;
+        shard_map(schedule_of(s), world, ol, no);
+        if (h_owner_local) std::copy(ol.begin(), ol.end(), h_owner_local);
+        if (h_rows_per_rank) std::copy(no.begin(), no.end(), h_rows_per_rank);
     });
 }
 

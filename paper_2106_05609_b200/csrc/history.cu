@@ -232,10 +232,14 @@ struct gasb_history_s {
     int32_t* err = nullptr;
     int32_t* flags = nullptr;  // per layer: OR of table_flag_of over every value ever stored
 
+    bool released = false;  // tables handed over to a sharded data-parallel group (dp.cu)
     float* table(int32_t layer) const { return tables + static_cast<int64_t>(layer - 1) * n * ld; }
     int64_t* stamp(int32_t layer) const { return stamps + static_cast<int64_t>(layer - 1) * n; }
     int32_t* flag(int32_t layer) const { return flags + (layer - 1); }
     void check_layer(int32_t layer) const {
+        if (released)
+            throw std::logic_error("HistoryStore: the tables are sharded across a data-parallel group "
+                                   "(read them through gasb_dp_read_history)");
         if (layer < 1 || layer > layers)
             throw std::invalid_argument("HistoryStore: layer " + std::to_string(layer) + " out of range [1," +
                                         std::to_string(layers) + "]");
@@ -301,6 +305,14 @@ int64_t* history_stamps(gasb_history h, int32_t layer) { return h->stamp(layer);
 int64_t* history_step_ptr(gasb_history h) { return h->step; }
 int32_t* history_flags(gasb_history h, int32_t layer) { return h->flag(layer); }
 void history_destroy(gasb_history h) { delete h; }
+// Frees the tables (stamps, flags and the step counter stay): a sharded data-parallel group
+// keeps each rank's rows in its exchange region instead.
+void history_release_tables(gasb_history h) {
+    cudaDeviceSynchronize();
+    cudaFree(h->tables);
+    h->tables = nullptr;
+    h->released = true;
+}
 }  // namespace gasb
 
 extern "C" {

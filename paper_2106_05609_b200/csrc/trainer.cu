@@ -679,8 +679,7 @@ void gasb_trainer_s::enqueue_batch_res(int32_t p, bool train, bool push, bool fu
                 halo = halo_pf.p + static_cast<int64_t>(l - 2) * halo_pf_rows * halo_pf_ld;
                 ldh = halo_pf_ld;
             } else {
-                launch_rows(1, halo_ids.p + (ext_off[p] - row_off[p]), nh[p], history_table(hist, l - 1),
-                            history_ld(hist), halo_buf.p, ldD, D, n, nullptr, nullptr, nullptr, stream);
+                pull_halo(p, l - 1, halo_buf.p, ldD, D);
             }
             const int64_t blocks = ceil_div(static_cast<int64_t>(me) * 32, 256);
             compose_kernel<<<static_cast<unsigned>(blocks), 256, 0, stream>>>(compose_idx.p + ext_off[p],
@@ -822,8 +821,7 @@ void gasb_trainer_s::enqueue_batch(int32_t p, bool train, bool push, bool use_ho
                     halo = halo_pf.p + static_cast<int64_t>(l - 2) * halo_pf_rows * halo_pf_ld;
                     ldh = halo_pf_ld;
                 } else {
-                    launch_rows(1, halo_ids.p + (ext_off[p] - row_off[p]), nh[p], history_table(hist, l - 1),
-                                history_ld(hist), halo_buf.p, ldx, din, n, nullptr, nullptr, nullptr, stream);
+                    pull_halo(p, l - 1, halo_buf.p, ldx, din);
                 }
                 const int64_t blocks = ceil_div(static_cast<int64_t>(ne[p]) * 32, 256);
                 compose_kernel<<<static_cast<unsigned>(blocks), 256, 0, stream>>>(
@@ -965,9 +963,10 @@ void gasb_trainer_s::enqueue_snapshot() {
 // number of kernels it launches.
 int64_t gasb_trainer_s::launch_batch_graph(int32_t p, bool dp) {
     const bool hoisted = opt.hoist_layer1 && opt.fused && !residual;
+    const bool push = !sharded_dp, fused = opt.fused != 0 && !sharded_dp;
     if (!opt.use_graphs) {
         const int64_t c0 = t_launches;
-        enqueue_batch(p, true, true, hoisted, opt.fused != 0, dp);
+        enqueue_batch(p, true, push, hoisted, fused, dp);
         return t_launches - c0;
     }
     std::vector<cudaGraphExec_t>& gs = dp ? graphs_dp : graphs;
@@ -994,7 +993,7 @@ void gasb_trainer_s::capture_batch_graph(int32_t p, bool dp) {
         cudaGraph_t graph;
         const int64_t c0 = t_launches;
         GASB_CUDA(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
-        enqueue_batch(p, true, true, hoisted, opt.fused != 0, dp);
+        enqueue_batch(p, true, !sharded_dp, hoisted, opt.fused != 0 && !sharded_dp, dp);
         GASB_CUDA(cudaStreamEndCapture(stream, &graph));
         gl[p] = t_launches - c0;
         t_launches = c0;

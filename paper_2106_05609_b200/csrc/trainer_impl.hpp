@@ -20,6 +20,22 @@ int64_t history_ld(gasb_history h);
 int64_t* history_stamps(gasb_history h, int32_t layer);
 int64_t* history_step_ptr(gasb_history h);
 int32_t* history_flags(gasb_history h, int32_t layer);
+void history_release_tables(gasb_history h);
+
+// Partition-sharded history tables of a data-parallel group (dp.cu): node v's rows live in
+// rank owner(v)'s shard (in its peer-mapped exchange region) at row local(v).
+constexpr int kShardMaxWorld = 8;
+constexpr int kShardLocalBits = 29;
+struct ShardView {
+    const uint32_t* owner_local = nullptr;  // per global node: owner << 29 | row in the owner's shard
+    const float* tables[kShardMaxWorld] = {};  // rank j's shard of H_1 (layer l at + (l-1) * layer_stride[j])
+    int64_t layer_stride[kShardMaxWorld] = {};
+    int64_t ld = 0;
+    int32_t world = 0;  // 0: the trainer's histories are local tables
+};
+// dst[i] = H_layer[ids[i]] read from the owners' shards (NVLink P2P loads for remote rows).
+void launch_shard_pull(const ShardView& s, int32_t layer, const int32_t* ids, int64_t count, float* dst,
+                       int64_t ldd, int32_t dim, cudaStream_t st);
 
 // Host staging vectors whose elements are default-initialised (not zeroed): the setup loops
 // write every element from OpenMP threads, so the pages are first touched in parallel
@@ -195,6 +211,17 @@ struct gasb_trainer_s {
     cudaEvent_t ev_pf_start = nullptr;
     std::vector<cudaEvent_t> ev_pf;
     void enqueue_prefetch(int32_t p);
+    // sharded data-parallel mode: halo rows come from the owners' shards, batches push
+    // nothing (the group commits the step's rows to their owners after the step barrier)
+    ShardView shard{};
+    bool sharded_dp = false;
+    void pull_halo(int32_t p, int32_t layer, float* dst, int64_t ldd, int32_t dim) {
+        const int32_t* ids = halo_ids.p + (ext_off[p] - row_off[p]);
+        if (shard.world > 0) launch_shard_pull(shard, layer, ids, nh[p], dst, ldd, dim, stream);
+        else
+            launch_rows(1, ids, nh[p], history_table(hist, layer), history_ld(hist), dst, ldd, dim, n, nullptr,
+                        nullptr, nullptr, stream);
+    }
     DevBuf<double> colsum_ws;  // row-block partials of the bias-gradient column sums
     struct WsGuard {        // scopes the thread's GEMM / column-sum workspaces to one enqueue
         explicit WsGuard(DevBuf<float>& w, DevBuf<double>* c = nullptr) {

@@ -40,11 +40,17 @@ class DataParallelTrainer:
     group (any backend) used to all-gather the IPC handles and to sum the per-part losses;
     None for world == 1."""
 
-    def __init__(self, trainer: GasTrainer, rank: int, world: int, group=None):
+    PLACEMENTS = {"replicated": 0, "sharded": 1}
+
+    def __init__(self, trainer: GasTrainer, rank: int, world: int, group=None, placement: str = "replicated"):
+        """placement: "replicated" (every rank holds every history row) or "sharded" (rank j
+        holds the rows of partitions p with p mod world == j; halo rows are read from the
+        owners over NVLink, the step's rows are committed to their owners; gasb.h)."""
         self.trainer = trainer
         self.rank, self.world, self.group = rank, world, group
+        self.placement = placement
         h = vp()
-        check(lib.gasb_dp_create(trainer._h, int(rank), int(world), C.byref(h)))
+        check(lib.gasb_dp_create_ex(trainer._h, int(rank), int(world), self.PLACEMENTS[placement], C.byref(h)))
         self._h = h
         if world > 1:
             import torch.distributed as dist
@@ -95,3 +101,30 @@ class DataParallelTrainer:
         n = i64()
         check(lib.gasb_dp_launch_count(self._h, C.byref(n)))
         return n.value
+
+    def history_layer(self, layer: int) -> np.ndarray:
+        """History layer `layer` (n x hist_dim): the trainer's table when replicated, gathered
+        from every rank's shard when sharded."""
+        if self.placement == "replicated":
+            return self.trainer.history.layer_matrix(layer)
+        n = len(self.trainer.train_mask)
+        hd = self.trainer.num_classes if self.trainer.spec.kind == "appnp" else self.trainer.spec.hidden
+        out = np.empty((n, hd), np.float32)
+        check(lib.gasb_dp_read_history(self._h, int(layer), ptr(out)))
+        return out
+
+    def traffic(self) -> dict:
+        """Bytes of the last epoch (gasb_dp_traffic): NVLink (peer gradients, peer act rows,
+        halo rows from peer shards), halo rows from this rank's own shard, rows held per layer."""
+        a, b, c = i64(), i64(), i64()
+        check(lib.gasb_dp_traffic(self._h, C.byref(a), C.byref(b), C.byref(c)))
+        return {"nvlink_bytes": a.value, "local_pull_bytes": b.value, "shard_rows": c.value}
+
+
+def shard_map(schedule, world: int) -> tuple[np.ndarray, np.ndarray]:
+    """The sharded placement's row ownership: (owner[n], row-in-owner's-shard[n]), rows per rank."""
+    n = schedule.graph.num_nodes
+    ol = np.empty(n, np.uint32)
+    rows = np.empty(world, np.int64)
+    check(lib.gasb_dp_shard_map(schedule.handle, int(world), ptr(ol), ptr(rows)))
+    return (ol >> 29).astype(np.int32), (ol & ((1 << 29) - 1)).astype(np.int64), rows

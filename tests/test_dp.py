@@ -76,3 +76,38 @@ def test_dp_protocol_two_gloo_ranks(oracle, tmp_path):
         assert np.array_equal(got["params"], s.get_params()), r
         assert np.array_equal(got["hist1"], s.get_history(1)), r
         assert np.allclose(got["losses"], losses, rtol=0, atol=0), (got["losses"], losses)
+
+
+@pytest.mark.parametrize("name,k", [("cora", 2), ("cora", 3), ("cora_appnp", 2)])
+def test_dp_sharded_protocol_gloo_ranks(oracle, tmp_path, name, k):
+    """The SHARDED placement's protocol (libgasb's shard map: each rank holds only its parts'
+    history rows; halo reads of start-of-step shards; owners commit the step's rows) run as
+    k gloo processes over the C oracle equals go_session_dp_epoch(k) bit for bit."""
+    env = dict(os.environ, MASTER_ADDR="127.0.0.1", MASTER_PORT=str(28500 + (os.getpid() + 7 * k) % 1000),
+               WORLD_SIZE=str(k))
+    procs = [subprocess.Popen([sys.executable, str(HERE / "helpers" / "dp_oracle_sharded_rank.py"), str(tmp_path), name],
+                              env=dict(env, RANK=str(r)), stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)
+             for r in range(k)]
+    outs = [p.communicate(timeout=300)[0] for p in procs]
+    assert all(p.returncode == 0 for p in procs), outs
+    ds = make_dataset(name)
+    w = ds.workload
+    s = oracle.session(ds.row_offsets, ds.cols, ds.features, ds.labels, ds.train_mask, w.num_classes, ds.assignment,
+                       w.parts, make_spec(kind=gb.trainer.KINDS[w.kind], num_layers=w.num_layers, hidden=w.hidden,
+                                          seed=3))
+    losses = [s.dp_epoch(e, k) for e in range(2)]
+    for r in range(k):
+        got = np.load(tmp_path / f"rank{r}.npz")
+        assert np.array_equal(got["params"], s.get_params()), r
+        for l in range(1, w.num_layers):
+            assert np.array_equal(got[f"hist{l}"], s.get_history(l)), (r, l)
+        assert np.allclose(got["losses"], losses, rtol=0, atol=0)
+
+
+def test_shard_map_partitions_rows():
+    ds = make_dataset("cora", with_features=False)
+    sched = gb.BatchSchedule.build(ds.graph, ds.assignment, ds.workload.parts)
+    owner, local, rows = gb.shard_map(sched, 3)
+    assert np.array_equal(owner, ds.assignment % 3)
+    for j in range(3):
+        assert np.array_equal(np.sort(local[owner == j]), np.arange(rows[j]))

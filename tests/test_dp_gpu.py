@@ -61,15 +61,12 @@ def test_dp_world1_hoisted_layer1_is_gas_epoch():
     assert np.array_equal(a.get_params(), b.get_params())
 
 
-@pytest.mark.parametrize("name,world,hoist", [("cora", 2, ""), ("cora", 3, ""), ("cora_appnp", 2, ""),
-                                              ("reddit_mini", 2, "hoist")])
-def test_dp_ranks_share_one_gpu(oracle, tmp_path, name, world, hoist):
-    epochs = 2
-    env = dict(os.environ, MASTER_ADDR="127.0.0.1", MASTER_PORT=str(29600 + (os.getpid() + world) % 1000),
-               WORLD_SIZE=str(world))
+def _run_ranks(tmp_path, name, world, epochs, hoist, placement):
+    env = dict(os.environ, MASTER_ADDR="127.0.0.1",
+               MASTER_PORT=str(29600 + (os.getpid() + world + 17 * len(placement)) % 1000), WORLD_SIZE=str(world))
     procs = [subprocess.Popen([sys.executable, str(HERE / "helpers" / "dp_gpu_rank.py"), str(tmp_path), name,
-                               str(world), str(epochs), hoist], env=dict(env, RANK=str(r)), stdout=subprocess.PIPE,
-                              stderr=subprocess.STDOUT, text=True) for r in range(world)]
+                               str(world), str(epochs), hoist or "-", placement], env=dict(env, RANK=str(r)),
+                              stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True) for r in range(world)]
     try:
         outs = [p.communicate(timeout=600)[0] for p in procs]
     finally:
@@ -77,7 +74,16 @@ def test_dp_ranks_share_one_gpu(oracle, tmp_path, name, world, hoist):
             if p.poll() is None:
                 p.kill()
     assert all(p.returncode == 0 for p in procs), outs
-    got = [np.load(tmp_path / f"rank{r}.npz") for r in range(world)]
+    return [np.load(tmp_path / f"rank{r}.npz") for r in range(world)]
+
+
+@pytest.mark.parametrize("name,world,hoist,placement", [
+    ("cora", 2, "", "replicated"), ("cora", 3, "", "replicated"), ("cora_appnp", 2, "", "replicated"),
+    ("reddit_mini", 2, "hoist", "replicated"), ("cora", 2, "", "sharded"), ("cora", 3, "", "sharded"),
+    ("cora_gcnii", 2, "", "sharded"), ("reddit_mini", 3, "hoist", "sharded")])
+def test_dp_ranks_share_one_gpu(oracle, tmp_path, name, world, hoist, placement):
+    epochs = 2
+    got = _run_ranks(tmp_path, name, world, epochs, hoist, placement)
     w = make_dataset(name).workload
     for r in range(1, world):  # replicas bit-identical (deterministic exchange, same Adam)
         assert np.array_equal(got[r]["params"], got[0]["params"])
@@ -97,3 +103,35 @@ def test_dp_ranks_share_one_gpu(oracle, tmp_path, name, world, hoist):
         assert normwise(got[0][f"hist{l}"], s.get_history(l)) <= bound
     assert np.allclose(got[0]["losses"], losses, rtol=TOL, atol=0)
     assert int(got[0]["step"][0]) == epochs * w.parts  # advance_step once per batch
+
+
+@pytest.mark.parametrize("name", ["cora", "cora_appnp", "reddit_mini"])
+def test_dp_sharded_world1_is_gas_epoch(name):
+    """One rank owning every shard: halo pulls from the shard + post-step commit == gas_epoch."""
+    ds = make_dataset(name)
+    a = _trainer(ds)
+    b = _trainer(ds)
+    dp = gb.DataParallelTrainer(b, 0, 1, placement="sharded")
+    for e in range(2):
+        assert a.gas_epoch(e) == dp.gas_epoch(e)
+    assert np.array_equal(a.get_params(), b.get_params())
+    for l in range(1, ds.workload.num_layers):
+        assert np.array_equal(a.history.layer_matrix(l), dp.history_layer(l))
+    with pytest.raises(RuntimeError, match="sharded"):
+        b.history.layer_matrix(1)  # the trainer's own tables were handed to the group
+
+
+def test_dp_sharded_equals_replicated(tmp_path):
+    """Same step semantics, so the two placements end bit-identical; the sharded ranks hold
+    1/world of the rows and read the rest over peer memory."""
+    (tmp_path / "s").mkdir()
+    (tmp_path / "r").mkdir()
+    sh = _run_ranks(tmp_path / "s", "reddit_mini", 2, 2, "hoist", "sharded")
+    rp = _run_ranks(tmp_path / "r", "reddit_mini", 2, 2, "hoist", "replicated")
+    assert np.array_equal(sh[0]["params"], rp[0]["params"])
+    for l in range(1, 4):
+        assert np.array_equal(sh[0][f"hist{l}"], rp[0][f"hist{l}"])
+    n = make_dataset("reddit_mini").workload.num_nodes
+    assert sum(int(g["traffic"][2]) for g in sh) == n  # every row held exactly once
+    assert int(rp[0]["traffic"][2]) == n
+    print("sharded NVLink bytes/epoch (rank 0):", int(sh[0]["traffic"][0]), "replicated:", int(rp[0]["traffic"][0]))
