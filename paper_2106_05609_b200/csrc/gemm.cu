@@ -184,10 +184,23 @@ extern "C" gasb_status gasb_gemm(int32_t op, int32_t m, int32_t n, int32_t k, co
     return gasb::guard([&] {
         gasb::require(m >= 0 && n >= 0 && k >= 0, "matmul: negative shape");
         gasb::require(beta == 0.f || beta == 1.f, "matmul: beta must be 0 or 1");
-        // the standalone entry point never splits K: split-K tiles share a workspace and spin
-        // on their peer slices, which is only safe for one grid in flight, and callers may
-        // use several streams
-        gasb::set_gemm_workspace(nullptr, 0);
-        gasb::launch_gemm(op, m, n, k, a, lda, b, ldb, c, ldc, beta, false, nullptr, gasb::as_stream(stream));
+        // the standalone entry point may be called on several streams at once: a split-K
+        // workspace of its own per call (stream-ordered allocation) and the serial fixup, in
+        // which no CTA waits for its peer slices
+        cudaStream_t st = gasb::as_stream(stream);
+        constexpr int64_t total = gasb::kGemmWsFloats + gasb::kGemmTileCounters;
+        float* ws = nullptr;
+        GASB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&ws), sizeof(float) * total, st));
+        GASB_CUDA(cudaMemsetAsync(ws + gasb::kGemmWsFloats, 0, sizeof(float) * gasb::kGemmTileCounters, st));
+        gasb::set_gemm_workspace(ws, gasb::kGemmWsFloats, /*serial_fixup=*/true);
+        struct Reset {
+            float* ws;
+            cudaStream_t st;
+            ~Reset() {
+                gasb::set_gemm_workspace(nullptr, 0);
+                cudaFreeAsync(ws, st);
+            }
+        } reset{ws, st};
+        gasb::launch_gemm(op, m, n, k, a, lda, b, ldb, c, ldc, beta, false, nullptr, st);
     });
 }

@@ -25,9 +25,11 @@ namespace gasb {
 // per-tile arrival counters (zero-initialised by the owner, self-resetting).
 thread_local float* t_gemm_ws = nullptr;
 thread_local int64_t t_gemm_ws_floats = 0;
-void set_gemm_workspace(float* ws, int64_t floats) {
+thread_local bool t_gemm_serial = false;
+void set_gemm_workspace(float* ws, int64_t floats, bool serial_fixup) {
     t_gemm_ws = ws;
     t_gemm_ws_floats = ws ? floats : 0;
+    t_gemm_serial = serial_fixup;
 }
 
 static int num_sms() {
@@ -144,7 +146,7 @@ __global__ void __launch_bounds__(kThreads, TALL ? 2 : 1) gemm_tc_kernel(const _
                                                              const __grid_constant__ CUtensorMap tma_b, int M,
                                                              int N, int K, float* __restrict__ C, int64_t ldc,
                                                              GemmEpilogue ep, int kbs, float* __restrict__ ws,
-                                                             int64_t ws_floats) {
+                                                             int64_t ws_floats, int serial_fixup) {
     const PushEpilogue& push = ep.push;
     using Lay = Layout<BN, A_MN, B_MN, TALL>;
     constexpr int kStagesTC = Lay::kStages;
@@ -359,7 +361,18 @@ __global__ void __launch_bounds__(kThreads, TALL ? 2 : 1) gemm_tc_kernel(const _
                 }
                 const int S = static_cast<int>(gridDim.z);
                 int* arrive = reinterpret_cast<int*>(ws + ws_floats) + 2 * (blockIdx.y * gridDim.x + blockIdx.x);
-                if (threadIdx.x == 0) {
+                __shared__ int last_flag;
+                if (serial_fixup) {
+                    // serial fixup: no CTA ever waits; the last slice to arrive reduces the whole
+                    // tile (in slice order), so any number of split-K grids may be in flight
+                    if (threadIdx.x == 0) {
+                        const int prev = atomicAdd(arrive, 1);
+                        last_flag = prev == S - 1;
+                        if (last_flag) __threadfence();
+                    }
+                    asm volatile("bar.sync 1, 128;\n" ::: "memory");
+                    if (!last_flag) goto fixup_done;
+                } else if (threadIdx.x == 0) {
                     atomicAdd(arrive, 1);
                     for (uint32_t spins = 0;; ++spins) {
                         int v;
@@ -369,11 +382,12 @@ __global__ void __launch_bounds__(kThreads, TALL ? 2 : 1) gemm_tc_kernel(const _
                         __nanosleep(64);
                     }
                 }
-                asm volatile("bar.sync 1, 128;\n" ::: "memory");
+                if (!serial_fixup) asm volatile("bar.sync 1, 128;\n" ::: "memory");
+                {
                 const int Np = (N + 3) & ~3;
                 const int64_t slice = static_cast<int64_t>(M) * Np;
-                const int rows_per = (BM + S - 1) / S;
-                const int rlo = blockIdx.z * rows_per, rhi = min(BM, rlo + rows_per);
+                const int rows_per = serial_fixup ? BM : (BM + S - 1) / S;
+                const int rlo = serial_fixup ? 0 : blockIdx.z * rows_per, rhi = min(BM, rlo + rows_per);
                 constexpr int kQ = BN / 4;  // float4 quads per tile row
                 for (int idx = threadIdx.x; idx < (rhi - rlo) * kQ; idx += 128) {
                     const int r = m0 + rlo + idx / kQ, c = n0 + 4 * (idx % kQ);
@@ -399,10 +413,14 @@ __global__ void __launch_bounds__(kThreads, TALL ? 2 : 1) gemm_tc_kernel(const _
                     }
                     if (pr && c == 0 && push.stamps) push.stamps[push.ids[r]] = *push.step;
                 }
-                if (threadIdx.x == 0 && atomicAdd(arrive + 1, 1) == S - 1) {  // last to leave resets
+                if (serial_fixup) {
+                    if (threadIdx.x == 0) arrive[0] = 0;  // the only CTA left on this tile
+                } else if (threadIdx.x == 0 && atomicAdd(arrive + 1, 1) == S - 1) {  // last to leave resets
                     arrive[0] = 0;
                     arrive[1] = 0;
                 }
+                }
+            fixup_done:;
             }
             if (push.special) {
                 flags = __reduce_or_sync(0xffffffffu, flags);
@@ -476,7 +494,7 @@ static bool launch_tc(int m, int n, int k, const float* a, int64_t lda, const fl
     dim3 grid(static_cast<unsigned>(ceil_div(m, BM)), static_cast<unsigned>(ceil_div(n, BN)), static_cast<unsigned>(S));
     gemm_tc_kernel<BN, A_MN, B_MN, TALL><<<grid, kThreads, Lay::kSmem, st>>>(ta, tb, m, n, k, c, ldc, ep, kbs,
                                                                         S > 1 ? t_gemm_ws : nullptr,
-                                                                        t_gemm_ws_floats);
+                                                                        t_gemm_ws_floats, t_gemm_serial ? 1 : 0);
     return true;
 }
 

@@ -129,7 +129,10 @@ void launch_gemm(int op, int m, int n, int k, const float* a, int64_t lda, const
 // `floats` floats followed by kGemmTileCounters ints that must be zero initially.
 constexpr int64_t kGemmTileCounters = 1024;
 constexpr int64_t kGemmWsFloats = 148LL * 128 * 64 + 4096;
-void set_gemm_workspace(float* ws, int64_t floats);
+// serial_fixup: the last slice of a tile to arrive reduces it (no CTA waits, so any number of
+// split-K grids may run concurrently); otherwise every slice CTA waits for its peers and
+// reduces 1/S of the tile — faster, but only one such grid may be in flight at a time.
+void set_gemm_workspace(float* ws, int64_t floats, bool serial_fixup = false);
 void launch_gemm(int op, int m, int n, int k, const float* a, int64_t lda, const float* b, int64_t ldb, float* c,
                  int64_t ldc, float beta, bool relu, const PushEpilogue* push, cudaStream_t st);
 __device__ __forceinline__ float gemm_epilogue_value(const GemmEpilogue& ep, float x, const float* crow, int col) {
