@@ -276,7 +276,15 @@ typedef struct {
     int32_t use_graphs;    /* capture each batch into a CUDA graph */
     int32_t hoist_layer1;  /* compute layer-1 aggregation of all batches up front per epoch */
     int32_t device;        /* CUDA device ordinal */
+    int32_t dropout_rng;   /* ModelSpec.dropout > 0 (tensor.cpp:374-401): the keep-mask stream.
+                              GASB_DROPOUT_EXACT: the reference's own, Rng(derive_seed(seed ^
+                              "drop", epoch, part, slot)).next_double() >= p element by element
+                              (host mt19937_64, copied per batch) -> bit-exact, host-bound;
+                              GASB_DROPOUT_PHILOX: Philox4x32-10 on the device keyed by the same
+                              derive_seed value -> same keep rate, different masks, no host work */
 } gasb_trainer_options;
+#define GASB_DROPOUT_EXACT 0
+#define GASB_DROPOUT_PHILOX 1
 
 typedef struct gasb_trainer_s* gasb_trainer;
 
@@ -323,6 +331,10 @@ typedef struct {
 } gasb_epoch_report;
 gasb_status gasb_gas_epoch_report(gasb_trainer t, int64_t epoch, int32_t shuffle, int32_t measure_staleness,
                                   gasb_epoch_report* out, int64_t* h_batch_peak_floats, double* h_eps_max);
+/* The keep mask of dropout slot `layer` (the layer-`layer` input, V_b x d_{layer-1} elements,
+ * row-major; bit i % 32 of word i / 32) that batch `part` uses in `epoch`, under the
+ * trainer's dropout_rng. LOGIC_ERROR when dropout == 0. Synchronous. */
+gasb_status gasb_trainer_dropout_mask(gasb_trainer t, int32_t part, int64_t epoch, int32_t layer, uint32_t* h_words);
 /* Mean loss of the last epoch enqueued with gasb_gas_epoch_async (synchronizes). */
 gasb_status gasb_trainer_last_loss(gasb_trainer t, double* mean_loss);
 /* One batch with capture (same contract as the oracle's session_batch): acts = pushed rows

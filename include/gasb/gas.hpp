@@ -355,7 +355,7 @@ struct ModelSpec : gasb_model_spec {
     ModelSpec() : gasb_model_spec{0, 2, 16, 0.f, 0.1f, 0.5f, 0.f, 0.f, 0.01f, 0.9f, 0.999f, 1e-8f, 0} {}
 };
 struct TrainerOptions : gasb_trainer_options {
-    TrainerOptions() : gasb_trainer_options{128, 1, 0, 1, 1, 0} {}
+    TrainerOptions() : gasb_trainer_options{128, 1, 0, 1, 1, 0, GASB_DROPOUT_EXACT} {}
 };
 
 class Trainer {

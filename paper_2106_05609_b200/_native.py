@@ -58,7 +58,7 @@ class ModelSpecC(C.Structure):
 
 class TrainerOptionsC(C.Structure):
     _fields_ = [("seg_edges", i32), ("fused", i32), ("prefetch", i32), ("use_graphs", i32),
-                ("hoist_layer1", i32), ("device", i32)]
+                ("hoist_layer1", i32), ("device", i32), ("dropout_rng", i32)]
 
 
 class EpochReportC(C.Structure):  # gasb_epoch_report
@@ -128,6 +128,7 @@ _SIGS = {
     "gasb_gas_epoch_async": (i32, [vp, i64, i32]),
     "gasb_gas_epoch_range_async": (i32, [vp, i64, i32, i32, i32]),
     "gasb_trainer_part_losses": (i32, [vp, vp]),
+    "gasb_trainer_dropout_mask": (i32, [vp, i32, i64, i32, vp]),
     "gasb_gas_epoch_report": (i32, [vp, i64, i32, i32, P(EpochReportC), vp, vp]),
     "gasb_adam_step": (i32, [vp, vp, vp, vp, i64, i64, f32, f32, f32, f32, vp]),
     "gasb_grad_clip": (i32, [vp, i64, f64, P(f64), vp]),

@@ -158,6 +158,12 @@ void launch_adam(float* p, float* m, float* v, float* g, int64_t size, int64_t* 
                  float lr, float b1, float b2, float eps, float clip_max_norm, double* norm_scratch,
                  cudaStream_t st, int64_t* end_step = nullptr, int32_t* end_done = nullptr);
 void launch_zero(float* p, int64_t count, cudaStream_t st);
+// dropout (tensor.cpp:374-401) with bit-word keep masks over the row-major rows x dim input
+void launch_dropout_apply(float* x, int64_t ldx, int64_t rows, int32_t dim, const uint32_t* mask, float inv_keep,
+                          cudaStream_t st);
+void launch_dropout_rows_bwd(float* g, int64_t ldg, int32_t m, int32_t dim, const int32_t* rows, const uint32_t* mask,
+                             float inv_keep, cudaStream_t st);
+void launch_philox_mask(uint32_t* mask, int64_t count, uint64_t key, float p, cudaStream_t st);
 // l2_penalty (tensor.cpp:649-678): g += 2 w p (before clip / Adam), *loss = float(*loss) + float(w sum p^2).
 // scratch: kNormBlocks doubles.
 void launch_l2_penalty(const float* p, float* g, int64_t size, float w, double* loss, double* scratch,

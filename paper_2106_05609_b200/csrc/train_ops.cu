@@ -209,6 +209,109 @@ __global__ void zero_kernel(float* p, int64_t n) {
         p[i] = 0.0f;
 }
 
+// ---- dropout (tensor.cpp:374-401): keep masks as bit words, element i = r * dim + c of the
+// row-major rows x dim input (the reference's draw order), bit i%32 of word i/32 ----------
+// y = keep ? x * inv_keep : 0  (one fp32 rounding, as `x.data()[i] * inv_keep`), in place.
+__global__ void __launch_bounds__(256) dropout_apply_kernel(float* __restrict__ x, int64_t ldx, int64_t rows,
+                                                            int32_t dim, const uint32_t* __restrict__ mask,
+                                                            float inv_keep) {
+    const int64_t total = rows * dim;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t r = i / dim;
+        const int32_t c = static_cast<int32_t>(i - r * dim);
+        const bool keep = (mask[i >> 5] >> (i & 31)) & 1u;
+        float* p = x + r * ldx + c;
+        *p = keep ? __fmul_rn(*p, inv_keep) : 0.0f;
+    }
+}
+
+// The backward on a subset of the rows (the batch rows of the composed input, compose_rows'
+// backward keeps only those): g[i, c] = keep(rows[i], c) ? g[i, c] * inv_keep : 0.
+__global__ void __launch_bounds__(256) dropout_rows_bwd_kernel(float* __restrict__ g, int64_t ldg, int32_t m,
+                                                               int32_t dim, const int32_t* __restrict__ rows,
+                                                               const uint32_t* __restrict__ mask, float inv_keep) {
+    const int64_t total = static_cast<int64_t>(m) * dim;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int32_t r = static_cast<int32_t>(i / dim);
+        const int32_t c = static_cast<int32_t>(i - static_cast<int64_t>(r) * dim);
+        const int64_t e = static_cast<int64_t>(rows[r]) * dim + c;
+        const bool keep = (mask[e >> 5] >> (e & 31)) & 1u;
+        float* p = g + static_cast<int64_t>(r) * ldg + c;
+        *p = keep ? __fmul_rn(*p, inv_keep) : 0.0f;
+    }
+}
+
+// Philox4x32-10 keep masks: element i draws lane i%4 of philox(counter = i/4, key); keep =
+// u >= p with u = (x >> 8) * 2^-24 (24-bit uniform, compared in double like next_double()).
+__device__ __forceinline__ void philox_round(uint32_t& c0, uint32_t& c1, uint32_t& c2, uint32_t& c3, uint32_t k0,
+                                             uint32_t k1) {
+    const uint32_t hi0 = __umulhi(0xD2511F53u, c0), lo0 = 0xD2511F53u * c0;
+    const uint32_t hi1 = __umulhi(0xCD9E8D57u, c2), lo1 = 0xCD9E8D57u * c2;
+    const uint32_t n0 = hi1 ^ c1 ^ k0, n2 = hi0 ^ c3 ^ k1;
+    c0 = n0;
+    c1 = lo1;
+    c2 = n2;
+    c3 = lo0;
+}
+__global__ void __launch_bounds__(256) philox_mask_kernel(uint32_t* __restrict__ mask, int64_t count, uint64_t key,
+                                                          double p) {
+    const int64_t words = (count + 31) >> 5;
+    for (int64_t w = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; w < words;
+         w += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        uint32_t bits = 0;
+        for (int q = 0; q < 8; ++q) {  // 8 philox calls x 4 lanes = 32 elements
+            const uint64_t ctr = static_cast<uint64_t>(w) * 8 + q;
+            uint32_t c0 = static_cast<uint32_t>(ctr), c1 = static_cast<uint32_t>(ctr >> 32), c2 = 0, c3 = 0;
+            uint32_t k0 = static_cast<uint32_t>(key), k1 = static_cast<uint32_t>(key >> 32);
+#pragma unroll
+            for (int r = 0; r < 10; ++r) {
+                philox_round(c0, c1, c2, c3, k0, k1);
+                k0 += 0x9E3779B9u;
+                k1 += 0xBB67AE85u;
+            }
+            const uint32_t x[4] = {c0, c1, c2, c3};
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const double u = static_cast<double>(x[j] >> 8) * 0x1.0p-24;
+                if (u >= p) bits |= 1u << (q * 4 + j);
+            }
+        }
+        if (w == words - 1 && (count & 31)) bits &= (1u << (count & 31)) - 1u;
+        mask[w] = bits;
+    }
+}
+
+void launch_dropout_apply(float* x, int64_t ldx, int64_t rows, int32_t dim, const uint32_t* mask, float inv_keep,
+                          cudaStream_t st) {
+    const int64_t total = rows * dim;
+    if (total <= 0) return;
+    dropout_apply_kernel<<<static_cast<unsigned>(std::min<int64_t>(ceil_div(total, 256), 8 * 148)), 256, 0, st>>>(
+        x, ldx, rows, dim, mask, inv_keep);
+    ++t_launches;
+    GASB_CUDA(cudaGetLastError());
+}
+
+void launch_dropout_rows_bwd(float* g, int64_t ldg, int32_t m, int32_t dim, const int32_t* rows, const uint32_t* mask,
+                             float inv_keep, cudaStream_t st) {
+    const int64_t total = static_cast<int64_t>(m) * dim;
+    if (total <= 0) return;
+    dropout_rows_bwd_kernel<<<static_cast<unsigned>(std::min<int64_t>(ceil_div(total, 256), 8 * 148)), 256, 0, st>>>(
+        g, ldg, m, dim, rows, mask, inv_keep);
+    ++t_launches;
+    GASB_CUDA(cudaGetLastError());
+}
+
+void launch_philox_mask(uint32_t* mask, int64_t count, uint64_t key, float p, cudaStream_t st) {
+    const int64_t words = (count + 31) >> 5;
+    if (words <= 0) return;
+    philox_mask_kernel<<<static_cast<unsigned>(std::min<int64_t>(ceil_div(words, 256), 8 * 148)), 256, 0, st>>>(
+        mask, count, key, static_cast<double>(p));
+    ++t_launches;
+    GASB_CUDA(cudaGetLastError());
+}
+
 void launch_zero(float* p, int64_t count, cudaStream_t st) {
     if (count <= 0) return;
     zero_kernel<<<static_cast<unsigned>(std::min<int64_t>(ceil_div(count, 256), 1184)), 256, 0, st>>>(p, count);

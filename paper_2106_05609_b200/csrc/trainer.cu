@@ -200,7 +200,11 @@ void gasb_trainer_s::build(const float* h_features, const int32_t* h_labels, con
     require(spec.kind == 0 || spec.kind == 2 || spec.kind == 3,
             "trainer: the device path implements GCN, APPNP and GCNII (GIN is out of scope)");
     require(L >= 1 && H > 0 && F > 0 && C > 0, "trainer: bad model dims");
-    require(spec.dropout == 0.0f, "trainer: dropout > 0 is not supported by the device path yet");
+    drop = spec.dropout > 0.0f;
+    require(!drop || spec.kind == 0, "trainer: dropout > 0 is implemented for GCN (APPNP/GCNII: dropout = 0)");
+    require(opt.dropout_rng == GASB_DROPOUT_EXACT || opt.dropout_rng == GASB_DROPOUT_PHILOX,
+            "trainer: unknown dropout_rng");
+    inv_keep = 1.0f / (1.0f - spec.dropout);  // tensor.cpp:380
     require(spec.l2_weight >= 0.0f, "l2_penalty: negative weight");
     residual = spec.kind != 0;
     D = spec.kind == 2 ? C : H;  // Model::history_dim (trainer.cpp:130-140)
@@ -263,8 +267,8 @@ void gasb_trainer_s::build(const float* h_features, const int32_t* h_labels, con
     HVec<int32_t> h_asrc;
     HVec<float> h_acf;
     std::vector<int64_t> h_arp;
+    if (residual || drop) h_brow.resize(R);
     if (residual) {
-        h_brow.resize(R);
         h_asrc.resize(E);
         h_acf.resize(E);
         h_arp.resize(NE + num_parts);
@@ -319,8 +323,9 @@ void gasb_trainer_s::build(const float* h_features, const int32_t* h_labels, con
             h_ext[ext_off[p] + i] = P.extended[i];
             h_cidx[ext_off[p] + i] = P.is_halo[i] ? -(hk++) - 1 : local2batch[i];
         }
-        if (residual) {
+        if (residual || drop)
             for (int32_t i = 0; i < nb[p]; ++i) h_brow[r0 + i] = P.batch_local_rows[i];
+        if (residual) {
             // transposed stencil over every V_b target (tensor.cpp:531-549 writes all rows of
             // h_in; layer 1 of APPNP/GCNII keeps the halo rows)
             std::vector<int64_t> ac(static_cast<size_t>(ne[p]) + 1, 0);
@@ -490,6 +495,19 @@ void gasb_trainer_s::build(const float* h_features, const int32_t* h_labels, con
         GASB_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
     }
     row_scratch.alloc(nb_max);
+    if (drop) {
+        brow.upload(h_brow);
+        dmask_off.assign(static_cast<size_t>(L) + 2, 0);
+        for (int32_t l = 1; l <= L; ++l)
+            dmask_off[l + 1] = dmask_off[l] + round_up(ceil_div(static_cast<int64_t>(ne_max) * dims[l - 1], 32), 32);
+        dmask.alloc(dmask_off[L + 1]);
+        if (opt.dropout_rng == GASB_DROPOUT_EXACT)
+            for (int i = 0; i < 2; ++i) {
+                GASB_CUDA(cudaHostAlloc(&dmask_host[i], sizeof(uint32_t) * dmask_off[L + 1], cudaHostAllocDefault));
+                GASB_CUDA(cudaEventCreateWithFlags(&dmask_done[i], cudaEventDisableTiming));
+                GASB_CUDA(cudaEventRecord(dmask_done[i], stream));
+            }
+    }
     // EpochReport bookkeeping (host): stored in-edges of each batch's rows, and the activation
     // floats of its step: every forward layer input/output over the batch rows (+ the residual
     // heads over all V_b rows) and their gradients (GCN's layer-1 input has none)
@@ -791,6 +809,8 @@ void gasb_trainer_s::enqueue_batch(int32_t p, bool train, bool push, bool use_ho
     const int64_t r0 = row_off[p];
     const SpmmSegs segs = seg_batch.segs(p);
     const int32_t* bn = batch_nodes.p + r0;
+    const bool dr = drop && train;  // dropout only while training (ForwardOptions.training)
+    require(!dr || !fused, "trainer: dropout batches run the materialized path");
     if (!fused && halo_pf.p) enqueue_prefetch(p);
     // ---------------- forward (Model::forward, trainer.cpp:174-251) ----------------
     for (int32_t l = 1; l <= L; ++l) {
@@ -812,6 +832,7 @@ void gasb_trainer_s::enqueue_batch(int32_t p, bool train, bool push, bool use_ho
                 launch_rows(1, extended.p + ext_off[p], ne[p], X.p, ldF, x_ext.p, ldx, din, n, nullptr, nullptr,
                             nullptr, stream);  // gather_features (trainer.cpp:20-27)
                 hsrc = x_ext.p;
+                if (dr) launch_dropout_apply(x_ext.p, ldx, ne[p], din, dmask.p + dmask_off[l], inv_keep, stream);
             } else {
                 // HistoryStore::pull of the halo rows, then compose_rows (tensor.cpp:459-512)
                 const float* halo = halo_buf.p;
@@ -829,11 +850,14 @@ void gasb_trainer_s::enqueue_batch(int32_t p, bool train, bool push, bool use_ho
                 ++t_launches;
                 GASB_CUDA(cudaGetLastError());
                 hsrc = h_ext.p;
+                // dropout of the layer input, every V_b row (trainer.cpp:203-204)
+                if (dr) launch_dropout_apply(h_ext.p, ldx, ne[p], din, dmask.p + dmask_off[l], inv_keep, stream);
             }
             // the composed rows come from X / H_{l-1} (+ act_{l-1}, pushed to H_{l-1} when push);
-            // without push the act rows are unflagged, so take the exact F2F widening
+            // without push the act rows are unflagged, so take the exact F2F widening (as after
+            // dropout's scaling, which may overflow a finite value)
             launch_spmm_fwd(segs, cols_l.p, coef64.p, hsrc, ldx, din, a, lda, r0, partial_batch.p, pld, counters.p,
-                            max_chunks, stream, (push || l == 1) ? source_flags(l) : nullptr,
+                            max_chunks, stream, ((push || l == 1) && !dr) ? source_flags(l) : nullptr,
                             l == 1 ? (tm_ok[2] ? &tm_xext : nullptr) : (tm_ok[3] ? &tm_hext : nullptr));
         }
         float* Wl = W(l);
@@ -893,6 +917,8 @@ void gasb_trainer_s::enqueue_batch(int32_t p, bool train, bool push, bool use_ho
                 launch_spmm_bwd(t_rowptr.p + r0 + p, m, t_src.p, t_cf.p, g_agg.p, ldH, din, act[l - 1].p, ldH, go,
                                 ldH, stream, m, false, t_order.p + r0);
             }
+            // dropout backward on the batch rows of the layer input (tensor.cpp:390-397)
+            if (dr) launch_dropout_rows_bwd(go, ldH, m, din, brow.p + r0, dmask.p + dmask_off[l], inv_keep, stream);
             g = go;
             ldg = ldH;
         }
@@ -914,6 +940,42 @@ void gasb_trainer_s::enqueue_batch(int32_t p, bool train, bool push, bool use_ho
     GASB_CUDA(cudaGetLastError());
 }
 
+// Keep masks of every dropout of batch p in epoch `epoch`: the layer-l input (V_b x d_{l-1},
+// row-major) with seed derive_seed(seed ^ "drop", epoch, p, l) (trainer.cpp:181-184, 203-204;
+// batch_index = the partition id).
+void gasb_trainer_s::enqueue_masks(int32_t p, int64_t epoch) {
+    const uint64_t base = spec.seed ^ 0x64726f70ull;  // kDropTag
+    if (opt.dropout_rng == GASB_DROPOUT_PHILOX) {
+        for (int32_t l = 1; l <= L; ++l)
+            launch_philox_mask(dmask.p + dmask_off[l], static_cast<int64_t>(ne[p]) * dims[l - 1],
+                               derive_seed(base, static_cast<uint64_t>(epoch), static_cast<uint64_t>(p),
+                                           static_cast<uint64_t>(l)),
+                               spec.dropout, stream);
+        return;
+    }
+    // the reference's stream (Rng(seed).next_double() >= p per element, in order), one host
+    // thread per layer, into the page-locked slot not read by the copy still in flight
+    const int s = dmask_slot;
+    dmask_slot ^= 1;
+    GASB_CUDA(cudaEventSynchronize(dmask_done[s]));
+    uint32_t* h = dmask_host[s];
+    const double pd = spec.dropout;
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int32_t l = 1; l <= L; ++l) {
+        Rng rng(derive_seed(base, static_cast<uint64_t>(epoch), static_cast<uint64_t>(p), static_cast<uint64_t>(l)));
+        const int64_t cnt = static_cast<int64_t>(ne[p]) * dims[l - 1];
+        uint32_t* w = h + dmask_off[l];
+        for (int64_t i0 = 0; i0 < cnt; i0 += 32) {
+            uint32_t bits = 0;
+            const int e = static_cast<int>(std::min<int64_t>(32, cnt - i0));
+            for (int b = 0; b < e; ++b) bits |= static_cast<uint32_t>(rng.next_double() >= pd) << b;
+            w[i0 >> 5] = bits;
+        }
+    }
+    GASB_CUDA(cudaMemcpyAsync(dmask.p, h, sizeof(uint32_t) * dmask_off[L + 1], cudaMemcpyHostToDevice, stream));
+    GASB_CUDA(cudaEventRecord(dmask_done[s], stream));
+}
+
 void gasb_trainer_s::run_epoch(int64_t epoch, bool shuffle, int32_t begin, int32_t end) {
     // batch order (trainer.cpp:395-400)
     std::vector<int32_t> order(static_cast<size_t>(num_parts));
@@ -930,11 +992,18 @@ void gasb_trainer_s::run_epoch(int64_t epoch, bool shuffle, int32_t begin, int32
     int64_t steps = 0;
     for (int32_t p : order) steps += ntrain[p] > 0 ? 1 : 0;
     ensure_bc(t_host + steps + 2);
-    const bool hoisted = opt.hoist_layer1 && opt.fused && !residual;
+    const bool hoisted = opt.hoist_layer1 && opt.fused && !residual && !drop;
     const int64_t l0 = t_launches;
     if (hoisted) enqueue_hoisted();
     epoch_launches = t_launches - l0;
-    for (int32_t p : order) epoch_launches += launch_batch_graph(p, false);
+    for (int32_t p : order) {
+        if (drop) {
+            const int64_t c0 = t_launches;
+            enqueue_masks(p, epoch);
+            epoch_launches += t_launches - c0;
+        }
+        epoch_launches += launch_batch_graph(p, false);
+    }
     t_host += steps;
     last_order = order;
 }
@@ -962,8 +1031,8 @@ void gasb_trainer_s::enqueue_snapshot() {
 // unless dp) on `stream`, through its captured per-part graph when use_graphs. Returns the
 // number of kernels it launches.
 int64_t gasb_trainer_s::launch_batch_graph(int32_t p, bool dp) {
-    const bool hoisted = opt.hoist_layer1 && opt.fused && !residual;
-    const bool push = !sharded_dp, fused = opt.fused != 0 && !sharded_dp;
+    const bool hoisted = opt.hoist_layer1 && opt.fused && !residual && !drop;
+    const bool push = !sharded_dp, fused = opt.fused != 0 && !sharded_dp && !drop;
     if (!opt.use_graphs) {
         const int64_t c0 = t_launches;
         enqueue_batch(p, true, push, hoisted, fused, dp);
@@ -982,7 +1051,7 @@ int64_t gasb_trainer_s::launch_batch_graph(int32_t p, bool dp) {
 
 // Captures (without launching) the per-part batch graph of part p.
 void gasb_trainer_s::capture_batch_graph(int32_t p, bool dp) {
-    const bool hoisted = opt.hoist_layer1 && opt.fused && !residual;
+    const bool hoisted = opt.hoist_layer1 && opt.fused && !residual && !drop;
     std::vector<cudaGraphExec_t>& gs = dp ? graphs_dp : graphs;
     std::vector<int64_t>& gl = dp ? graph_launches_dp : graph_launches;
     if (gs.empty()) {
@@ -993,7 +1062,7 @@ void gasb_trainer_s::capture_batch_graph(int32_t p, bool dp) {
         cudaGraph_t graph;
         const int64_t c0 = t_launches;
         GASB_CUDA(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
-        enqueue_batch(p, true, !sharded_dp, hoisted, opt.fused != 0 && !sharded_dp, dp);
+        enqueue_batch(p, true, !sharded_dp, hoisted, opt.fused != 0 && !sharded_dp && !drop, dp);
         GASB_CUDA(cudaStreamEndCapture(stream, &graph));
         gl[p] = t_launches - c0;
         t_launches = c0;
@@ -1214,7 +1283,7 @@ gasb_status gasb_trainer_create(gasb_schedule s, const float* h_features, int32_
         auto t = std::make_unique<gasb_trainer_s>();
         t->spec = *spec;
         if (opt) t->opt = *opt;
-        else t->opt = gasb_trainer_options{128, 1, 0, 1, 1, 0};
+        else t->opt = gasb_trainer_options{128, 1, 0, 1, 1, 0, GASB_DROPOUT_EXACT};
         t->sched = &schedule_of(s);
         t->F = in_dim;
         t->C = num_classes;
@@ -1264,6 +1333,19 @@ gasb_status gasb_gas_epoch_range_async(gasb_trainer t, int64_t epoch, int32_t sh
         require(t, "trainer: null handle");
         require(begin >= 0 && begin <= end && end <= t->num_parts, "gas_epoch_range: need 0 <= begin <= end <= parts");
         t->run_epoch(epoch, shuffle != 0, begin, end);
+    });
+}
+
+gasb_status gasb_trainer_dropout_mask(gasb_trainer t, int32_t part, int64_t epoch, int32_t layer, uint32_t* h_words) {
+    return guard([&] {
+        require(t && h_words, "trainer: null argument");
+        if (!t->drop) throw std::logic_error("dropout_mask: the model has dropout == 0");
+        require(part >= 0 && part < t->num_parts && layer >= 1 && layer <= t->L, "dropout_mask: part/layer out of range");
+        t->enqueue_masks(part, epoch);
+        GASB_CUDA(cudaStreamSynchronize(t->stream));
+        const int64_t words = ceil_div(static_cast<int64_t>(t->ne[part]) * t->dims[layer - 1], 32);
+        GASB_CUDA(cudaMemcpy(h_words, t->dmask.p + t->dmask_off[layer], sizeof(uint32_t) * words,
+                             cudaMemcpyDeviceToHost));
     });
 }
 
@@ -1352,12 +1434,13 @@ gasb_status gasb_gas_epoch(gasb_trainer t, int64_t epoch, int32_t shuffle, doubl
 gasb_status gasb_trainer_batch(gasb_trainer t, int32_t part, int64_t epoch, int32_t train, int32_t push,
                                float* h_acts, float* h_logits, double* loss, float* h_grads, int32_t* stepped) {
     return guard([&] {
-        (void)epoch;
         require(t, "trainer: null handle");
         require(part >= 0 && part < t->num_parts, "trainer: part out of range");
         const bool tr = train != 0;
         t->ensure_bc(t->t_host + 2);
-        t->enqueue_batch(part, tr, push != 0, false, push != 0 && t->opt.fused != 0);
+        const bool dr = t->drop && tr;
+        if (dr) t->enqueue_masks(part, epoch);
+        t->enqueue_batch(part, tr, push != 0, false, push != 0 && t->opt.fused != 0 && !dr);
         const bool st = tr && t->ntrain[part] > 0;
         if (st) t->t_host++;
         GASB_CUDA(cudaStreamSynchronize(t->stream));

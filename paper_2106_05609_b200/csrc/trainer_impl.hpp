@@ -306,6 +306,10 @@ struct gasb_trainer_s {
         if (ev_staged) cudaEventDestroy(ev_staged);
         if (ev_stage_free) cudaEventDestroy(ev_stage_free);
         if (copy_stream) cudaStreamDestroy(copy_stream);
+        for (int i = 0; i < 2; ++i) {
+            if (dmask_done[i]) cudaEventDestroy(dmask_done[i]);
+            if (dmask_host[i]) cudaFreeHost(dmask_host[i]);
+        }
         if (side) cudaStreamDestroy(side);
         if (stream) cudaStreamDestroy(stream);
     }
@@ -360,6 +364,18 @@ struct gasb_trainer_s {
             if (g) cudaGraphExecDestroy(g), g = nullptr;
     }
 
+    // dropout (ModelSpec.dropout > 0, GCN): per-layer keep masks of the running batch (bit
+    // words over the layer input's V_b x d_{l-1} elements) at dmask + dmask_off[l], refilled
+    // before every training batch (philox kernels, or the reference's mt19937_64 stream from
+    // the host through a 2-slot page-locked ring); the batch runs the materialized path
+    bool drop = false;
+    float inv_keep = 1.0f;
+    DevBuf<uint32_t> dmask;
+    std::vector<int64_t> dmask_off;
+    uint32_t* dmask_host[2] = {nullptr, nullptr};
+    cudaEvent_t dmask_done[2] = {nullptr, nullptr};
+    int dmask_slot = 0;
+    void enqueue_masks(int32_t p, int64_t epoch);
     // EpochReport (trainer.hpp:107-115): per part, the stored in-edges of its batch rows
     // (plan.local_graph.num_edges(), summed into edges_per_layer) and the activation floats
     // its step writes; the frozen snapshot tables of the staleness pass (gas_forward_snapshot,

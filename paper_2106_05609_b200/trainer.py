@@ -49,10 +49,11 @@ class TrainerOptions:
     use_graphs: bool = True
     hoist_layer1: bool = True
     device: int = 0
+    dropout_rng: str = "exact"  # "exact" (the reference's mt19937_64 masks) or "philox" (gasb.h)
 
     def to_c(self) -> TrainerOptionsC:
         return TrainerOptionsC(self.seg_edges, int(self.fused), int(self.prefetch), int(self.use_graphs),
-                               int(self.hoist_layer1), self.device)
+                               int(self.hoist_layer1), self.device, {"exact": 0, "philox": 1}[self.dropout_rng])
 
 
 class GasTrainer:
@@ -78,6 +79,7 @@ class GasTrainer:
         check(lib.gasb_trainer_history(self._h, C.byref(hh)))
         self.history = HistoryStore(0, 0, 0, _handle=hh.value, _owned=False) if spec.num_layers >= 1 else None
         self.num_classes = num_classes
+        self._in_dim = x.shape[1]
         self.train_mask = tm.astype(bool)
         self._part_train = None
 
@@ -105,6 +107,15 @@ class GasTrainer:
     def gas_epoch_range_async(self, epoch: int, begin: int, end: int, shuffle: bool = True) -> None:
         """Batches order[begin:end] of gas_epoch's seeded order (same kernels and graphs)."""
         check(lib.gasb_gas_epoch_range_async(self._h, int(epoch), int(shuffle), int(begin), int(end)))
+
+    def dropout_mask(self, part: int, epoch: int, layer: int) -> np.ndarray:
+        """Keep mask (bool, V_b x d_{layer-1}) of the layer-`layer` input dropout of batch `part`."""
+        ne = int(self.schedule.sizes(part)[1])
+        d = self._in_dim if layer == 1 else (self.num_classes if self.spec.kind == "appnp" else self.spec.hidden)
+        words = np.zeros((ne * d + 31) // 32, np.uint32)
+        check(lib.gasb_trainer_dropout_mask(self._h, int(part), int(epoch), int(layer), ptr(words)))
+        bits = np.unpackbits(words.view(np.uint8), bitorder="little")[:ne * d]
+        return bits.reshape(ne, d).astype(bool)
 
     def part_losses(self) -> np.ndarray:
         """Per-part batch objective as last computed (part order)."""
