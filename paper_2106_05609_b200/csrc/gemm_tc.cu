@@ -505,7 +505,7 @@ static bool launch_tc(int m, int n, int k, const float* a, int64_t lda, const fl
 bool launch_gemm_tc(int op, int m, int n, int k, const float* a, int64_t lda, const float* b, int64_t ldb, float* c,
                     int64_t ldc, const GemmEpilogue& ep, cudaStream_t st) {
     if (m <= 0 || n <= 0) return true;
-    bool ok;
+    bool ok, n32 = false;
     // many tiles with a short K (the residual heads over every V_b row): two CTAs per SM
     const bool tall = ceil_div(m, tc::BM) * ceil_div(n, 64) >= 2LL * num_sms() && k <= 16 * tc::BK;
     if (tall && n > 32) {
@@ -521,17 +521,22 @@ bool launch_gemm_tc(int op, int m, int n, int k, const float* a, int64_t lda, co
         return true;
     }
     // narrow N tiles keep enough CTAs in flight for the ~1K-row batch GEMMs
+    static const int bn_thresh = [] {  // GASB_GEMM_BN32_BELOW: N-tile 32 while the 64-wide grid < this many CTAs
+        const char* e = getenv("GASB_GEMM_BN32_BELOW");
+        return e ? atoi(e) : 0;
+    }();
+    if (ceil_div(m, tc::BM) * ceil_div(n, 64) < bn_thresh) n32 = true;
     switch (op) {
         case 0:
-            ok = n <= 32 ? tc::launch_tc<32, false, true>(m, n, k, a, lda, b, ldb, c, ldc, ep, st)
+            ok = (n <= 32 || n32) ? tc::launch_tc<32, false, true>(m, n, k, a, lda, b, ldb, c, ldc, ep, st)
                          : tc::launch_tc<64, false, true>(m, n, k, a, lda, b, ldb, c, ldc, ep, st);
             break;
         case 1:
-            ok = n <= 32 ? tc::launch_tc<32, false, false>(m, n, k, a, lda, b, ldb, c, ldc, ep, st)
+            ok = (n <= 32 || n32) ? tc::launch_tc<32, false, false>(m, n, k, a, lda, b, ldb, c, ldc, ep, st)
                          : tc::launch_tc<64, false, false>(m, n, k, a, lda, b, ldb, c, ldc, ep, st);
             break;
         case 2:
-            ok = n <= 32 ? tc::launch_tc<32, true, true>(m, n, k, a, lda, b, ldb, c, ldc, ep, st)
+            ok = (n <= 32 || n32) ? tc::launch_tc<32, true, true>(m, n, k, a, lda, b, ldb, c, ldc, ep, st)
                          : tc::launch_tc<64, true, true>(m, n, k, a, lda, b, ldb, c, ldc, ep, st);
             break;
         default: throw std::invalid_argument("gemm: op must be 0, 1 or 2");

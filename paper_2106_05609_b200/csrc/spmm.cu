@@ -486,14 +486,14 @@ __device__ __forceinline__ void seg_finish(double (&acc)[CPL], int32_t row, int3
         double* pp = partial + static_cast<int64_t>(slot) * pld;
 #pragma unroll
         for (int k = 0; k < CPL; ++k) pp[col_of<CPL>(col, k)] = acc[k];
-        __threadfence();
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");  // publish the partial before arriving
         __syncwarp();
         int last = 0;
         const int32_t nk = row_nseg[row];
         if (lane == 0) last = atomicAdd(counters + static_cast<int64_t>(row) * cld + chunk, 1) == nk - 1;
         store = __shfl_sync(0xffffffffu, last, 0) != 0;
         if (store) {
-            __threadfence();
+            asm volatile("fence.acq_rel.gpu;" ::: "memory");  // see every peer's published partial
             const int32_t s0 = row_seg0[row];
 #pragma unroll
             for (int k = 0; k < CPL; ++k) acc[k] = 0.0;
@@ -1002,6 +1002,7 @@ int32_t spmm_ranges_per_launch() {
             cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0)
             sms = 148;
         v = kPipeCtas * kPipeWarps * sms;
+        if (const char* e = getenv("GASB_SPMM_RANGES_PER_SM")) v = std::max(1, atoi(e)) * sms;  // (the reg engine)
     }
     return v;
 }
