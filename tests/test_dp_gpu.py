@@ -127,17 +127,21 @@ def test_dp_sharded_world1_is_gas_epoch(name):
         b.history.layer_matrix(1)  # the trainer's own tables were handed to the group
 
 
-def test_dp_sharded_equals_replicated(tmp_path):
+@pytest.mark.parametrize("name,world", [("reddit_mini", 2), ("papers_mini", 3)])
+def test_dp_sharded_equals_replicated(tmp_path, name, world):
     """Same step semantics, so the two placements end bit-identical; the sharded ranks hold
-    1/world of the rows and read the rest over peer memory."""
+    1/world of the rows and read the rest over peer memory (papers_mini: the C5 shape, whose
+    full-size histories need the sharded placement)."""
     (tmp_path / "s").mkdir()
     (tmp_path / "r").mkdir()
-    sh = _run_ranks(tmp_path / "s", "reddit_mini", 2, 2, "hoist", "sharded")
-    rp = _run_ranks(tmp_path / "r", "reddit_mini", 2, 2, "hoist", "replicated")
+    sh = _run_ranks(tmp_path / "s", name, world, 2, "hoist", "sharded")
+    rp = _run_ranks(tmp_path / "r", name, world, 2, "hoist", "replicated")
+    w = make_dataset(name, with_features=False).workload
     assert np.array_equal(sh[0]["params"], rp[0]["params"])
-    for l in range(1, 4):
+    for l in range(1, w.num_layers):
         assert np.array_equal(sh[0][f"hist{l}"], rp[0][f"hist{l}"])
-    n = make_dataset("reddit_mini").workload.num_nodes
+    n = w.num_nodes
     assert sum(int(g["traffic"][2]) for g in sh) == n  # every row held exactly once
     assert int(rp[0]["traffic"][2]) == n
-    print("sharded NVLink bytes/epoch (rank 0):", int(sh[0]["traffic"][0]), "replicated:", int(rp[0]["traffic"][0]))
+    print(name, "NVLink bytes/epoch (rank 0): sharded", int(sh[0]["traffic"][0]), "replicated",
+          int(rp[0]["traffic"][0]), "; rows held per rank (sharded):", [int(g["traffic"][2]) for g in sh])
