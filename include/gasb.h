@@ -117,6 +117,11 @@ gasb_status gasb_partition_save(const char* path, const int32_t* h_assignment, i
 gasb_status gasb_partition_load(const char* path, int32_t num_nodes, int32_t* h_assignment, int32_t* num_parts);
 /* random_partition (partition.hpp:23, partition.cpp:330-342), bit-exact (seeded shuffle). */
 gasb_status gasb_random_partition(int32_t num_nodes, int32_t num_parts, uint64_t seed, int32_t* h_assignment);
+/* cluster_partition (partition.hpp, partition.cpp:344-388): the reference's multilevel
+ * partitioner (heavy-edge matching, greedy growth, boundary refinement, balance repair),
+ * restated with sparse per-node connectivity and a one-pass balance repair: the SAME
+ * assignment as the reference for the same graph, part count and seed, far faster. Host. */
+gasb_status gasb_cluster_partition(gasb_graph g, int32_t num_parts, uint64_t seed, int32_t* h_assignment);
 
 /* ==================================================================================== */
 /* history-store: HistoryStore (include/gas/history.hpp:29-66, src/history.cpp:10-178)   */

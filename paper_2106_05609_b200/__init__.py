@@ -6,7 +6,8 @@ The native library is libgasb.so (C ABI: include/gasb.h); importing this package
 loudly when it has not been built.
 """
 from ._native import LIB_PATH, lib  # noqa: F401  (raises ImportError when unbuilt)
-from .graph import (BatchPlan, BatchSchedule, Graph, build_graph, graph_from_csr, make_batch_plan,  # noqa: F401
+from .graph import (BatchPlan, BatchSchedule, Graph, build_graph, cluster_partition, graph_from_csr,  # noqa: F401
+                    make_batch_plan,
                     load_partition, partition_parts, random_partition, save_partition, synth_features,
                     synth_pairs)
 from .history import HistoryStore, Prefetcher, PrefetchHandle  # noqa: F401
@@ -16,7 +17,7 @@ from .dp import DataParallelTrainer, epoch_order, shard_map, step_plan  # noqa: 
 
 __all__ = [
     "Graph", "build_graph", "graph_from_csr", "make_batch_plan", "BatchPlan", "BatchSchedule", "partition_parts",
-    "synth_pairs", "synth_features", "save_partition", "load_partition", "random_partition", "HistoryStore", "Prefetcher", "PrefetchHandle", "ModelSpec", "AdamConfig",
+    "synth_pairs", "synth_features", "cluster_partition", "save_partition", "load_partition", "random_partition", "HistoryStore", "Prefetcher", "PrefetchHandle", "ModelSpec", "AdamConfig",
     "TrainerOptions", "GasTrainer", "adam_step", "grad_clip", "BatchOps", "LayerConfig", "layer_forward",
     "layer_backward", "DataParallelTrainer", "epoch_order", "step_plan", "shard_map",
 ]

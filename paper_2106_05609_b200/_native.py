@@ -90,6 +90,7 @@ _SIGS = {
     "gasb_partition_save": (i32, [C.c_char_p, vp, i32]),
     "gasb_partition_load": (i32, [C.c_char_p, i32, vp, P(i32)]),
     "gasb_random_partition": (i32, [i32, i32, u64, vp]),
+    "gasb_cluster_partition": (i32, [vp, i32, u64, vp]),
     "gasb_history_create": (i32, [i32, i32, i32, P(vp)]),
     "gasb_history_destroy": (i32, [vp]),
     "gasb_history_info": (i32, [vp, P(i32), P(i32), P(i32), P(i64)]),

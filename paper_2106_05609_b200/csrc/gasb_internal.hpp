@@ -92,6 +92,9 @@ struct Schedule {
 void build_plan(const Graph& g, const int32_t* batch, int64_t nb, bool full, HostPlan& out,
                 std::vector<uint8_t>& mark, std::vector<int32_t>& g2l);
 
+// cluster_partition (partition.cpp:344-388), same assignment as the reference (partition_host.cpp).
+void cluster_partition(const Graph& g, int32_t num_parts, uint64_t seed, int32_t* assignment);
+
 // The same schedule built on the current CUDA device (plan_dev.cu), bit-exact with build_plan.
 void build_schedule_device(const Graph& g, const int32_t* assignment, int32_t num_parts, bool full, Schedule& out);
 

@@ -571,6 +571,13 @@ gasb_status gasb_random_partition(int32_t num_nodes, int32_t num_parts, uint64_t
     });
 }
 
+gasb_status gasb_cluster_partition(gasb_graph g, int32_t num_parts, uint64_t seed, int32_t* assignment) {
+    return guard([&] {
+        require(g && assignment, "cluster_partition: null argument");
+        cluster_partition(g->g, num_parts, seed, assignment);
+    });
+}
+
 }  // extern "C"
 
 namespace gasb {

@@ -214,3 +214,11 @@ def random_partition(num_nodes: int, num_parts: int, seed: int = 0) -> np.ndarra
     a = np.empty(num_nodes, np.int32)
     check(lib.gasb_random_partition(int(num_nodes), int(num_parts), int(seed), ptr(a)))
     return a
+
+
+def cluster_partition(graph: Graph, num_parts: int, seed: int = 0) -> np.ndarray:
+    """cluster_partition (partition.cpp:344-388): the reference's multilevel partitioner,
+    same assignment for the same graph / parts / seed."""
+    a = np.empty(graph.num_nodes, np.int32)
+    check(lib.gasb_cluster_partition(graph.handle, int(num_parts), int(seed), ptr(a)))
+    return a

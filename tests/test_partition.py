@@ -69,3 +69,24 @@ def test_partition_file_comments_and_overrides(tmp_path):
         gb.load_partition(p, 2)
     with pytest.raises(RuntimeError):
         gb.load_partition(tmp_path / "missing.part", 2)
+
+
+@pytest.mark.parametrize("name,parts,seed", [("cora", 10, 0), ("cora", 7, 3), ("pubmed_gcnii", 8, 0),
+                                             ("reddit_mini", 12, 1)])
+def test_cluster_partition_equals_reference(ref, name, parts, seed):
+    """cluster_partition (partition.cpp:344-388): the same assignment as the compiled
+    reference (multilevel coarsening, growth, refinement, balance repair)."""
+    from paper_2106_05609_b200.workloads import make_dataset
+    ds = make_dataset(name, with_features=False)
+    a = gb.cluster_partition(ds.graph, parts, seed)
+    b = ref.graph(csr=(ds.row_offsets, ds.cols)).cluster_partition(parts, seed)
+    assert np.array_equal(a, b)
+    assert np.bincount(a, minlength=parts).min() > 0
+
+
+def test_cluster_partition_errors():
+    g = gb.build_graph(np.array([[0, 1], [1, 2]]), 3)
+    with pytest.raises(ValueError):
+        gb.cluster_partition(g, 0)
+    with pytest.raises(ValueError):
+        gb.cluster_partition(g, 4)
