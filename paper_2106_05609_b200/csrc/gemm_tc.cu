@@ -44,7 +44,13 @@ static int num_sms() {
 
 namespace tc {
 
-constexpr int BM = 128, BK = 32, kStagesTC = 3;
+#ifndef GASB_GEMM_STAGES
+#define GASB_GEMM_STAGES 3
+#endif
+#ifndef GASB_GEMM_MAXACC
+#define GASB_GEMM_MAXACC 8
+#endif
+constexpr int BM = 128, BK = 32, kStagesTC = GASB_GEMM_STAGES;
 constexpr int kSplitHelpers = 4;                      // extra warps that only split tiles
 constexpr int kSplitThreads = 128 + 32 * kSplitHelpers;  // warps 0-3 + helpers
 constexpr int kThreads = 192 + 32 * kSplitHelpers;
@@ -56,7 +62,7 @@ constexpr int kThreads = 192 + 32 * kSplitHelpers;
 // one CTA's epilogue with the other's mainloop.
 template <int BN, bool TALL = false>
 struct Acc {
-    static constexpr int kMax = TALL ? 4 : 8;
+    static constexpr int kMax = TALL ? 4 : GASB_GEMM_MAXACC;
     static constexpr int kAcc = 512 / BN < kMax ? 512 / BN : kMax;
     static constexpr int kCols = kAcc * BN;  // TMEM allocation (power of two)
 };
