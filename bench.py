@@ -254,7 +254,7 @@ def run_ours(args):
     tr = gb.GasTrainer(sched, ds.features, ds.labels, ds.train_mask, w.num_classes, spec, opts)
     runner = tr
     if ws > 1:
-        runner = gb.DataParallelTrainer(tr, rank, ws, group=torch.distributed.group.WORLD)
+        runner = gb.DataParallelTrainer(tr, rank, ws, group=torch.distributed.group.WORLD, placement=args.placement)
     log(f"[rank {rank}] setup {time.time() - t0:.1f}s  n={w.num_nodes} nnz={len(ds.cols)}")
     stream = torch.cuda.ExternalStream(tr.stream())
 
@@ -364,6 +364,14 @@ def run_ours(args):
         except Exception:
             pass
     extra = {}
+    if ws > 1:  # exchange bytes of the last timed epoch (dp.cu bookkeeping), max over ranks
+        tf = runner.traffic()
+        t = torch.tensor([float(tf["nvlink_bytes"])], device="cpu" if shared else "cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        extra["exchange"] = {"placement": args.placement, "nvlink_bytes_per_epoch_max_rank": int(t.item()),
+                             "nvlink_GBps_avg_over_epoch": float(t.item()) / (ms / args.steps / 1000) / 1e9,
+                             "history_rows_held_rank0": tf["shard_rows"],
+                             "link_peak_GBps_per_direction": 900.0}
     if not args.no_hoist and ws == 1:
         ms_h = tr.profile_spmm(-1, 1, 2)
         extra["hoisted_layer1_ms"] = ms_h
@@ -427,6 +435,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=3)
     ap.add_argument("--profile-parts", type=int, default=20)
+    ap.add_argument("--placement", default="replicated", choices=["replicated", "sharded"],
+                    help="history placement of a data-parallel run (gasb.h GASB_DP_*)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "ours" and args.gpus > 1 and "WORLD_SIZE" not in os.environ:

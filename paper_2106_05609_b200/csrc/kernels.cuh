@@ -90,11 +90,12 @@ void launch_scan_special(const float* x, int64_t rows, int64_t ld, int32_t dim, 
 // accumulate: gx[t] continues from its current value (the reference's `g += c * gy` into
 // a grad buffer that already holds other contributions) instead of starting at 0.
 // order (optional): the targets heaviest first (claimed in that order, so a hub's serial
-// chain starts early instead of setting the tail).
+// chain starts early instead of setting the tail). exact = false: four interleaved chains
+// per target (deterministic reassociation; the trainer's segmented mode, seg_edges > 0).
 void launch_spmm_bwd(const int64_t* t_rowptr, int32_t ntargets, const int32_t* t_src, const float* t_coeffs,
                      const float* gy, int64_t ldgy, int32_t dim, const float* mask, int64_t ldm, float* gx,
                      int64_t ldgx, cudaStream_t st, int32_t nsrc = 0, bool accumulate = false,
-                     const int32_t* order = nullptr);
+                     const int32_t* order = nullptr, bool exact = true);
 
 // ---- GEMM (gemm.cu) -------------------------------------------------------------------
 // op 0: C = A B ; 1: C = A B^T ; 2: C = A^T B.  Row-major fp32, fp32 accumulation.
@@ -164,6 +165,8 @@ void launch_dropout_apply(float* x, int64_t ldx, int64_t rows, int32_t dim, cons
 void launch_dropout_rows_bwd(float* g, int64_t ldg, int32_t m, int32_t dim, const int32_t* rows, const uint32_t* mask,
                              float inv_keep, cudaStream_t st);
 void launch_philox_mask(uint32_t* mask, int64_t count, uint64_t key, float p, cudaStream_t st);
+void launch_dropout_bwd_acc(float* g, int64_t ldg, int64_t rows, int32_t dim, const float* gin, int64_t ldi,
+                            const uint32_t* mask, float inv_keep, cudaStream_t st);
 // l2_penalty (tensor.cpp:649-678): g += 2 w p (before clip / Adam), *loss = float(*loss) + float(w sum p^2).
 // scratch: kNormBlocks doubles.
 void launch_l2_penalty(const float* p, float* g, int64_t size, float w, double* loss, double* scratch,

@@ -283,6 +283,33 @@ __global__ void __launch_bounds__(256) philox_mask_kernel(uint32_t* __restrict__
     }
 }
 
+// Dropout backward into an input that other ops also feed: g[i] += gin[i] * inv_keep where
+// kept (tensor.cpp:393-396: `if (mask[i]) g[i] += gy[i] * inv_keep`, untouched otherwise).
+__global__ void __launch_bounds__(256) dropout_bwd_acc_kernel(float* __restrict__ g, int64_t ldg, int64_t rows,
+                                                              int32_t dim, const float* __restrict__ gin, int64_t ldi,
+                                                              const uint32_t* __restrict__ mask, float inv_keep) {
+    const int64_t total = rows * dim;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t r = i / dim;
+        const int32_t c = static_cast<int32_t>(i - r * dim);
+        if ((mask[i >> 5] >> (i & 31)) & 1u) {
+            float* p = g + r * ldg + c;
+            *p = __fadd_rn(*p, __fmul_rn(gin[r * ldi + c], inv_keep));
+        }
+    }
+}
+
+void launch_dropout_bwd_acc(float* g, int64_t ldg, int64_t rows, int32_t dim, const float* gin, int64_t ldi,
+                            const uint32_t* mask, float inv_keep, cudaStream_t st) {
+    const int64_t total = rows * dim;
+    if (total <= 0) return;
+    dropout_bwd_acc_kernel<<<static_cast<unsigned>(std::min<int64_t>(ceil_div(total, 256), 8 * 148)), 256, 0, st>>>(
+        g, ldg, rows, dim, gin, ldi, mask, inv_keep);
+    ++t_launches;
+    GASB_CUDA(cudaGetLastError());
+}
+
 void launch_dropout_apply(float* x, int64_t ldx, int64_t rows, int32_t dim, const uint32_t* mask, float inv_keep,
                           cudaStream_t st) {
     const int64_t total = rows * dim;

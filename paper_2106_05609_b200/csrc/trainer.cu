@@ -201,7 +201,6 @@ void gasb_trainer_s::build(const float* h_features, const int32_t* h_labels, con
             "trainer: the device path implements GCN, APPNP and GCNII (GIN is out of scope)");
     require(L >= 1 && H > 0 && F > 0 && C > 0, "trainer: bad model dims");
     drop = spec.dropout > 0.0f;
-    require(!drop || spec.kind == 0, "trainer: dropout > 0 is implemented for GCN (APPNP/GCNII: dropout = 0)");
     require(opt.dropout_rng == GASB_DROPOUT_EXACT || opt.dropout_rng == GASB_DROPOUT_PHILOX,
             "trainer: unknown dropout_rng");
     inv_keep = 1.0f / (1.0f - spec.dropout);  // tensor.cpp:380
@@ -496,14 +495,29 @@ void gasb_trainer_s::build(const float* h_features, const int32_t* h_labels, con
     }
     row_scratch.alloc(nb_max);
     if (drop) {
-        brow.upload(h_brow);
-        dmask_off.assign(static_cast<size_t>(L) + 2, 0);
-        for (int32_t l = 1; l <= L; ++l)
-            dmask_off[l + 1] = dmask_off[l] + round_up(ceil_div(static_cast<int64_t>(ne_max) * dims[l - 1], 32), 32);
-        dmask.alloc(dmask_off[L + 1]);
+        if (!residual) brow.upload(h_brow);
+        // dropout sites in the reference's forward order
+        auto site = [&](uint64_t slot, int32_t w, bool batch_rows) {
+            dslot.push_back(slot);
+            dslot_w.push_back(w);
+            dslot_batch.push_back(batch_rows ? 1 : 0);
+        };
+        if (residual) {
+            site(100, F, false);  // head input x_ext (trainer.cpp:149/158)
+            if (spec.kind == 2) site(101, H, false);  // APPNP head hidden (:151)
+        }
+        for (int32_t l = 1; l <= L; ++l) site(static_cast<uint64_t>(l), dims[l - 1], false);  // layer inputs (:203-204)
+        if (spec.kind == 3) site(9000, H, true);  // GCNII output head input (:222-223)
+        dmask_off.assign(dslot.size() + 1, 0);
+        for (size_t i = 0; i < dslot.size(); ++i)
+            dmask_off[i + 1] = dmask_off[i] + round_up(ceil_div(static_cast<int64_t>(dslot_batch[i] ? nb_max : ne_max) *
+                                                                    dslot_w[i], 32), 32);
+        const int64_t words = dmask_off.back();
+        dmask.alloc(words);
+        if (residual) dtmp.alloc(static_cast<int64_t>(ne_max) * ldD);
         if (opt.dropout_rng == GASB_DROPOUT_EXACT)
             for (int i = 0; i < 2; ++i) {
-                GASB_CUDA(cudaHostAlloc(&dmask_host[i], sizeof(uint32_t) * dmask_off[L + 1], cudaHostAllocDefault));
+                GASB_CUDA(cudaHostAlloc(&dmask_host[i], sizeof(uint32_t) * words, cudaHostAllocDefault));
                 GASB_CUDA(cudaEventCreateWithFlags(&dmask_done[i], cudaEventDisableTiming));
                 GASB_CUDA(cudaEventRecord(dmask_done[i], stream));
             }
@@ -666,14 +680,20 @@ void gasb_trainer_s::enqueue_batch_res(int32_t p, bool train, bool push, bool fu
     const int32_t* bn = batch_nodes.p + r0;
     const int32_t* br = brow.p + r0;
     const bool gcnii = spec.kind == 3;
+    const bool dr = drop && train;  // dropout only while training (ForwardOptions.training)
+    require(!dr || !fused, "trainer: dropout batches run the materialized path");
     if (!fused && halo_pf.p) enqueue_prefetch(p);
     // ---- head_forward over the extended rows: x_ext = X[V_b] (gather_features, trainer.cpp:20-27)
     launch_rows(1, extended.p + ext_off[p], me, X.p, ldF, x_ext.p, ldF, F, n, nullptr, nullptr, nullptr, stream);
+    if (dr) launch_dropout_apply(x_ext.p, ldF, me, F, mask_of(100), inv_keep, stream);  // trainer.cpp:149/158
     {
         GemmEpilogue e1;
         e1.bias = P(p_hb1);
         e1.relu = 1;
         launch_gemm(0, me, H, F, x_ext.p, ldF, P(p_hw1), pp(p_hw1), gcnii ? h0.p : z.p, gcnii ? ldD : ldH, e1, stream);
+        // APPNP head hidden (trainer.cpp:151): dropped in place — dropped z > 0 exactly where the
+        // relu mask and the keep mask both hold, so the backward's relu mask reads it as well
+        if (!gcnii && dr) launch_dropout_apply(z.p, ldH, me, H, mask_of(101), inv_keep, stream);
         if (!gcnii) {
             GemmEpilogue e2;
             e2.bias = P(p_hb2);
@@ -683,7 +703,13 @@ void gasb_trainer_s::enqueue_batch_res(int32_t p, bool train, bool push, bool fu
     if (gcnii) launch_wtilde(P(layer_param[1]), wt.p, L, H, pp(layer_param[1]), spec.beta, stream);
     // ---- propagation layers ----
     for (int32_t l = 1; l <= L; ++l) {
-        if (l == 1) {  // input = h0 over V_b (local ids)
+        if (l == 1 && dr) {  // input = dropout(h0) over V_b (trainer.cpp:203-204; h0 itself feeds the mixing)
+            GASB_CUDA(cudaMemcpy2DAsync(h_ext.p, sizeof(float) * ldD, h0.p, sizeof(float) * ldD, sizeof(float) * D, me,
+                                        cudaMemcpyDeviceToDevice, stream));
+            launch_dropout_apply(h_ext.p, ldD, me, D, mask_of(1), inv_keep, stream);
+            launch_spmm_fwd(segs, cols_l.p, coef64.p, h_ext.p, ldD, D, prop.p, ldD, r0, partial_batch.p, pld,
+                            counters.p, max_chunks, stream, nullptr, tm_ok[3] ? &tm_hext : nullptr);
+        } else if (l == 1) {  // input = h0 over V_b (local ids)
             launch_spmm_fwd(segs, cols_l.p, coef64.p, h0.p, ldD, D, prop.p, ldD, r0, partial_batch.p, pld, counters.p,
                             max_chunks, stream, nullptr, tm_h0_ok ? &tm_h0 : nullptr);
         } else if (fused) {  // pull-free: H_{l-1} by global id
@@ -705,8 +731,9 @@ void gasb_trainer_s::enqueue_batch_res(int32_t p, bool train, bool push, bool fu
                                                                                D, h_ext.p, ldD);
             ++t_launches;
             GASB_CUDA(cudaGetLastError());
+            if (dr) launch_dropout_apply(h_ext.p, ldD, me, D, mask_of(l), inv_keep, stream);
             launch_spmm_fwd(segs, cols_l.p, coef64.p, h_ext.p, ldD, D, prop.p, ldD, r0, partial_batch.p, pld,
-                            counters.p, max_chunks, stream, push ? source_flags(l) : nullptr,
+                            counters.p, max_chunks, stream, (push && !dr) ? source_flags(l) : nullptr,
                             tm_ok[3] ? &tm_hext : nullptr);
         }
         PushEpilogue pe{history_table(hist, l), history_ld(hist), bn, history_stamps(hist, l),
@@ -720,7 +747,8 @@ void gasb_trainer_s::enqueue_batch_res(int32_t p, bool train, bool push, bool fu
             launch_gemm(0, m, H, H, mixed[l].p, ldD, wt.p + static_cast<int64_t>(l - 1) * H * pp(layer_param[1]),
                         pp(layer_param[1]), act[l].p, ldD, e,
                         stream);
-            if (l == L) {  // relu -> out_w, out_b (trainer.cpp:221-227)
+            if (l == L) {  // relu -> [dropout] -> out_w, out_b (trainer.cpp:221-227)
+                if (dr) launch_dropout_apply(act[L].p, ldD, m, H, mask_of(9000), inv_keep, stream);
                 GemmEpilogue eo;
                 eo.bias = P(p_ob);
                 launch_gemm(0, m, C, H, act[L].p, ldD, P(p_ow), pp(p_ow), logits.p, ldC, eo, stream);
@@ -743,6 +771,7 @@ void gasb_trainer_s::enqueue_batch_res(int32_t p, bool train, bool push, bool fu
             launch_gemm(2, H, C, m, act[L].p, ldD, glogits.p, ldC, G(p_ow), pp(p_ow), plain, stream);
             launch_colsum(glogits.p, ldC, m, C, G(p_ob), stream);
             launch_gemm(1, m, H, C, glogits.p, ldC, P(p_ow), pp(p_ow), gout.p, ldD, plain, stream);
+            if (dr) launch_dropout_apply(gout.p, ldD, m, H, mask_of(9000), inv_keep, stream);  // dropout bwd
             launch_mask(gout.p, ldD, act[L].p, ldD, m, H, stream);
             dout = gout.p;
             ldo = ldD;
@@ -763,12 +792,17 @@ void gasb_trainer_s::enqueue_batch_res(int32_t p, bool train, bool push, bool fu
             launch_mix_bwd(dmix, ldm, m, D, spec.alpha, br, h0g.p, ldD, dprop.p, ldD, stream);
             if (l >= 2) {  // to act_{l-1}'s batch rows (compose bwd), relu mask for GCNII
                 launch_spmm_bwd(t_rowptr.p + r0 + p, m, t_src.p, t_cf.p, dprop.p, ldD, D, gcnii ? act[l - 1].p : nullptr,
-                                ldD, gout.p, ldD, stream, m, false, t_order.p + r0);
+                                ldD, gout.p, ldD, stream, m, false, t_order.p + r0, opt.seg_edges == 0);
+                if (dr) launch_dropout_rows_bwd(gout.p, ldD, m, D, br, mask_of(l), inv_keep, stream);
                 dout = gout.p;
                 ldo = ldD;
+            } else if (dr) {  // layer 1 input = dropout(h0): its gradient, then the dropout bwd into h0g
+                launch_spmm_bwd(a_rowptr.p + a_off[p], me, a_src.p, a_cf.p, dprop.p, ldD, D, nullptr, 0, dtmp.p, ldD,
+                                stream, m, false, nullptr, opt.seg_edges == 0);
+                launch_dropout_bwd_acc(h0g.p, ldD, me, D, dtmp.p, ldD, mask_of(1), inv_keep, stream);
             } else {  // layer 1: every V_b row of h0, accumulated onto the residual terms
                 launch_spmm_bwd(a_rowptr.p + a_off[p], me, a_src.p, a_cf.p, dprop.p, ldD, D, nullptr, 0, h0g.p, ldD,
-                                stream, m, true);
+                                stream, m, true, nullptr, opt.seg_edges == 0);
             }
         }
         // head backward (x_ext carries no gradient)
@@ -780,6 +814,7 @@ void gasb_trainer_s::enqueue_batch_res(int32_t p, bool train, bool push, bool fu
             launch_colsum(h0g.p, ldD, me, C, G(p_hb2), stream);
             launch_gemm(2, H, C, me, z.p, ldH, h0g.p, ldD, G(p_hw2), pp(p_hw2), plain, stream);
             launch_gemm(1, me, H, C, h0g.p, ldD, P(p_hw2), pp(p_hw2), zg.p, ldH, plain, stream);
+            if (dr) launch_dropout_apply(zg.p, ldH, me, H, mask_of(101), inv_keep, stream);  // dropout bwd
             launch_mask(zg.p, ldH, z.p, ldH, me, H, stream);
             launch_colsum(zg.p, ldH, me, H, G(p_hb1), stream);
             launch_gemm(2, F, H, me, x_ext.p, ldF, zg.p, ldH, G(p_hw1), pp(p_hw1), plain, stream);
@@ -832,7 +867,7 @@ void gasb_trainer_s::enqueue_batch(int32_t p, bool train, bool push, bool use_ho
                 launch_rows(1, extended.p + ext_off[p], ne[p], X.p, ldF, x_ext.p, ldx, din, n, nullptr, nullptr,
                             nullptr, stream);  // gather_features (trainer.cpp:20-27)
                 hsrc = x_ext.p;
-                if (dr) launch_dropout_apply(x_ext.p, ldx, ne[p], din, dmask.p + dmask_off[l], inv_keep, stream);
+                if (dr) launch_dropout_apply(x_ext.p, ldx, ne[p], din, mask_of(l), inv_keep, stream);
             } else {
                 // HistoryStore::pull of the halo rows, then compose_rows (tensor.cpp:459-512)
                 const float* halo = halo_buf.p;
@@ -851,7 +886,7 @@ void gasb_trainer_s::enqueue_batch(int32_t p, bool train, bool push, bool use_ho
                 GASB_CUDA(cudaGetLastError());
                 hsrc = h_ext.p;
                 // dropout of the layer input, every V_b row (trainer.cpp:203-204)
-                if (dr) launch_dropout_apply(h_ext.p, ldx, ne[p], din, dmask.p + dmask_off[l], inv_keep, stream);
+                if (dr) launch_dropout_apply(h_ext.p, ldx, ne[p], din, mask_of(l), inv_keep, stream);
             }
             // the composed rows come from X / H_{l-1} (+ act_{l-1}, pushed to H_{l-1} when push);
             // without push the act rows are unflagged, so take the exact F2F widening (as after
@@ -906,7 +941,7 @@ void gasb_trainer_s::enqueue_batch(int32_t p, bool train, bool push, bool use_ho
                 // gradient first, then the dgrad GEMM and the relu mask: A^T (g W^T) == (A^T g) W^T,
                 // dout/din of the gather work (reassociation only; within the 1e-5 grad contract)
                 launch_spmm_bwd(t_rowptr.p + r0 + p, m, t_src.p, t_cf.p, g, ldg, dout, nullptr, 0, g_agg.p, ldC,
-                                stream, m, false, t_order.p + r0);
+                                stream, m, false, t_order.p + r0, opt.seg_edges == 0);
                 launch_gemm(1, m, din, dout, g_agg.p, ldC, W(l), pp(layer_param[l]), go, ldH, 0.f, false, nullptr,
                             stream);
                 launch_mask(go, ldH, act[l - 1].p, ldH, m, din, stream);  // relu backward (mask = act_{l-1})
@@ -915,10 +950,10 @@ void gasb_trainer_s::enqueue_batch(int32_t p, bool train, bool push, bool use_ho
                             stream);
                 // aggregate backward over intra-batch edges + compose bwd + relu bwd (mask = act)
                 launch_spmm_bwd(t_rowptr.p + r0 + p, m, t_src.p, t_cf.p, g_agg.p, ldH, din, act[l - 1].p, ldH, go,
-                                ldH, stream, m, false, t_order.p + r0);
+                                ldH, stream, m, false, t_order.p + r0, opt.seg_edges == 0);
             }
             // dropout backward on the batch rows of the layer input (tensor.cpp:390-397)
-            if (dr) launch_dropout_rows_bwd(go, ldH, m, din, brow.p + r0, dmask.p + dmask_off[l], inv_keep, stream);
+            if (dr) launch_dropout_rows_bwd(go, ldH, m, din, brow.p + r0, mask_of(l), inv_keep, stream);
             g = go;
             ldg = ldH;
         }
@@ -940,31 +975,32 @@ void gasb_trainer_s::enqueue_batch(int32_t p, bool train, bool push, bool use_ho
     GASB_CUDA(cudaGetLastError());
 }
 
-// Keep masks of every dropout of batch p in epoch `epoch`: the layer-l input (V_b x d_{l-1},
-// row-major) with seed derive_seed(seed ^ "drop", epoch, p, l) (trainer.cpp:181-184, 203-204;
+// Keep masks of every dropout site of batch p in epoch `epoch` (row-major over the site's
+// input; seed derive_seed(seed ^ "drop", epoch, p, slot): trainer.cpp:144-147, 181-184 —
 // batch_index = the partition id).
 void gasb_trainer_s::enqueue_masks(int32_t p, int64_t epoch) {
     const uint64_t base = spec.seed ^ 0x64726f70ull;  // kDropTag
+    const size_t ns = dslot.size();
+    auto count = [&](size_t i) { return static_cast<int64_t>(dslot_batch[i] ? nb[p] : ne[p]) * dslot_w[i]; };
     if (opt.dropout_rng == GASB_DROPOUT_PHILOX) {
-        for (int32_t l = 1; l <= L; ++l)
-            launch_philox_mask(dmask.p + dmask_off[l], static_cast<int64_t>(ne[p]) * dims[l - 1],
-                               derive_seed(base, static_cast<uint64_t>(epoch), static_cast<uint64_t>(p),
-                                           static_cast<uint64_t>(l)),
+        for (size_t i = 0; i < ns; ++i)
+            launch_philox_mask(dmask.p + dmask_off[i], count(i),
+                               derive_seed(base, static_cast<uint64_t>(epoch), static_cast<uint64_t>(p), dslot[i]),
                                spec.dropout, stream);
         return;
     }
     // the reference's stream (Rng(seed).next_double() >= p per element, in order), one host
-    // thread per layer, into the page-locked slot not read by the copy still in flight
+    // thread per site, into the page-locked slot not read by the copy still in flight
     const int s = dmask_slot;
     dmask_slot ^= 1;
     GASB_CUDA(cudaEventSynchronize(dmask_done[s]));
     uint32_t* h = dmask_host[s];
     const double pd = spec.dropout;
 #pragma omp parallel for schedule(dynamic, 1)
-    for (int32_t l = 1; l <= L; ++l) {
-        Rng rng(derive_seed(base, static_cast<uint64_t>(epoch), static_cast<uint64_t>(p), static_cast<uint64_t>(l)));
-        const int64_t cnt = static_cast<int64_t>(ne[p]) * dims[l - 1];
-        uint32_t* w = h + dmask_off[l];
+    for (size_t i = 0; i < ns; ++i) {
+        Rng rng(derive_seed(base, static_cast<uint64_t>(epoch), static_cast<uint64_t>(p), dslot[i]));
+        const int64_t cnt = count(i);
+        uint32_t* w = h + dmask_off[i];
         for (int64_t i0 = 0; i0 < cnt; i0 += 32) {
             uint32_t bits = 0;
             const int e = static_cast<int>(std::min<int64_t>(32, cnt - i0));
@@ -972,7 +1008,7 @@ void gasb_trainer_s::enqueue_masks(int32_t p, int64_t epoch) {
             w[i0 >> 5] = bits;
         }
     }
-    GASB_CUDA(cudaMemcpyAsync(dmask.p, h, sizeof(uint32_t) * dmask_off[L + 1], cudaMemcpyHostToDevice, stream));
+    GASB_CUDA(cudaMemcpyAsync(dmask.p, h, sizeof(uint32_t) * dmask_off[ns], cudaMemcpyHostToDevice, stream));
     GASB_CUDA(cudaEventRecord(dmask_done[s], stream));
 }
 
@@ -1344,7 +1380,7 @@ gasb_status gasb_trainer_dropout_mask(gasb_trainer t, int32_t part, int64_t epoc
         t->enqueue_masks(part, epoch);
         GASB_CUDA(cudaStreamSynchronize(t->stream));
         const int64_t words = ceil_div(static_cast<int64_t>(t->ne[part]) * t->dims[layer - 1], 32);
-        GASB_CUDA(cudaMemcpy(h_words, t->dmask.p + t->dmask_off[layer], sizeof(uint32_t) * words,
+        GASB_CUDA(cudaMemcpy(h_words, t->mask_of(static_cast<uint64_t>(layer)), sizeof(uint32_t) * words,
                              cudaMemcpyDeviceToHost));
     });
 }

@@ -371,7 +371,18 @@ struct gasb_trainer_s {
     bool drop = false;
     float inv_keep = 1.0f;
     DevBuf<uint32_t> dmask;
-    std::vector<int64_t> dmask_off;
+    // the model's dropout sites (trainer.cpp:142-163, 181-227): seed slot (derive_seed's last
+    // argument), width, and whether the input is the B_b batch rows (else all V_b rows)
+    std::vector<uint64_t> dslot;
+    std::vector<int32_t> dslot_w;
+    std::vector<uint8_t> dslot_batch;
+    std::vector<int64_t> dmask_off;  // word offset of each site's mask (+ total)
+    DevBuf<float> dtmp;              // residual models: layer-1 input gradient before dropout bwd
+    const uint32_t* mask_of(uint64_t slot) const {
+        for (size_t i = 0; i < dslot.size(); ++i)
+            if (dslot[i] == slot) return dmask.p + dmask_off[i];
+        throw std::logic_error("dropout: no such site");
+    }
     uint32_t* dmask_host[2] = {nullptr, nullptr};
     cudaEvent_t dmask_done[2] = {nullptr, nullptr};
     int dmask_slot = 0;

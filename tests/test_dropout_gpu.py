@@ -109,3 +109,52 @@ def test_exact_mask_keep_rate():
     ds, sched, tr, _ = _setup(None, 0.25)
     m = tr.dropout_mask(0, 0, 1)
     assert abs(m.mean() - 0.75) < 5 * np.sqrt(0.1875 / m.size)
+
+
+@pytest.mark.parametrize("name", ["cora_appnp", "cora_gcnii"])
+def test_exact_dropout_residual_teacher_forced_vs_reference(ref, name):
+    """APPNP / GCNII sites too: the head input (slot 100), APPNP's head hidden (101), every
+    layer input (slot l; layer 1 = dropout(h0) while h0 itself feeds the mixing) and the GCNII
+    output head (9000), forward and backward (trainer.cpp:142-163, 203-204, 221-227)."""
+    ds = make_dataset(name)
+    w = ds.workload
+    sched = gb.BatchSchedule.build(ds.graph, ds.assignment, w.parts)
+    spec = gb.ModelSpec(kind=w.kind, num_layers=w.num_layers, hidden=w.hidden, seed=3, dropout=0.3)
+    tr = gb.GasTrainer(sched, ds.features, ds.labels, ds.train_mask, w.num_classes, spec, gb.TrainerOptions())
+    rs = ref.session(ds.row_offsets, ds.cols, ds.features, ds.labels, ds.train_mask, w.num_classes, ds.assignment,
+                     w.parts, make_spec(kind=gb.trainer.KINDS[w.kind], num_layers=w.num_layers, hidden=w.hidden,
+                                        seed=3, dropout=0.3))
+    worst = {}
+    for epoch in (0, 1):
+        for part in [int(x) for x in ref.epoch_order(w.parts, 3, epoch)[:4]]:
+            rs.set_params(tr.get_params())
+            for l in range(1, w.num_layers):
+                rs.set_history(l, tr.history.layer_matrix(l))
+            nb = int(sched.sizes(part)[0])
+            ag, lg, lossg, gg, stg = tr.batch(part, epoch=epoch)
+            ao, lo, losso, go, sto = rs.batch(part, epoch, nb=nb)
+            assert stg == sto
+            errs = {"acts": normwise(ag, ao), "logits": normwise(lg, lo)}
+            if sto:
+                errs["loss"] = abs(lossg - losso) / abs(losso)
+                errs["grads"] = normwise(gg, go)
+            for k, v in errs.items():
+                worst[k] = max(worst.get(k, 0.0), v)
+                assert v <= TOL, (name, epoch, part, k, v)
+    print(name, "dropout 0.3", worst)
+
+
+@pytest.mark.parametrize("name", ["cora_appnp", "cora_gcnii"])
+def test_residual_dropout_graphs_equal_eager(name):
+    out = []
+    for graphs in (True, False):
+        ds = make_dataset(name)
+        w = ds.workload
+        sched = gb.BatchSchedule.build(ds.graph, ds.assignment, w.parts)
+        tr = gb.GasTrainer(sched, ds.features, ds.labels, ds.train_mask, w.num_classes,
+                           gb.ModelSpec(kind=w.kind, num_layers=w.num_layers, hidden=w.hidden, seed=3, dropout=0.2),
+                           gb.TrainerOptions(use_graphs=graphs, dropout_rng="philox"))
+        for e in range(2):
+            tr.gas_epoch(e)
+        out.append(tr.get_params())
+    assert np.array_equal(out[0], out[1])

@@ -1,0 +1,7 @@
+python paper_2106_05609_b200/build.py > /dev/null 2>&1
+run() { env "$@" timeout 300 python tools/spmm_probe.py 2>/dev/null | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['env'], 'batch_us %.1f hoisted_ms %.2f epoch_ms %.2f' % (d['batch_spmm_us'], d['hoisted_ms'], d['epoch_ms']))"; }
+run GASB_X=base
+run GASB_SPMM_CPL=4
+run GASB_SPMM_CPL=4 GASB_SPMM_RANGES_PER_SM=6
+run GASB_SPMM_RANGES_PER_SM=6
+run GASB_SPMM_RANGES_PER_SM=24
