@@ -125,6 +125,19 @@ struct BatchPlan {
     std::vector<float> gcn_coeffs;
 };
 
+// cluster_partition (include/gas/partition.hpp, src/partition.cpp:344-388): the reference's
+// multilevel partitioner, same assignment (host); random_partition (:330-342).
+inline std::vector<std::int32_t> cluster_partition(const Graph& g, std::int32_t num_parts, std::uint64_t seed = 0) {
+    std::vector<std::int32_t> a(static_cast<std::size_t>(g.num_nodes()));
+    check(gasb_cluster_partition(g.raw(), num_parts, seed, a.data()));
+    return a;
+}
+inline std::vector<std::int32_t> random_partition(NodeId num_nodes, std::int32_t num_parts, std::uint64_t seed = 0) {
+    std::vector<std::int32_t> a(static_cast<std::size_t>(num_nodes));
+    check(gasb_random_partition(num_nodes, num_parts, seed, a.data()));
+    return a;
+}
+
 // BatchSchedule::build (include/gas/trainer.hpp:91-96, src/trainer.cpp:253-262): one plan +
 // stencil per part of the partitioning, in part order. Plans stay host-side until a
 // Trainer uploads them.
@@ -348,6 +361,66 @@ inline void matmul(MatmulOp op, std::int32_t m, std::int32_t n, std::int32_t k, 
                     stream));
 }
 
+// AdamState::step / grad_clip (include/gas/nn.hpp:21-41) on device buffers.
+inline void adam_step(float* d_params, float* d_m, float* d_v, const float* d_grads, std::int64_t size,
+                      std::int64_t step, float lr = 0.01f, float beta1 = 0.9f, float beta2 = 0.999f,
+                      float eps = 1e-8f, gasb_stream stream = nullptr) {
+    check(gasb_adam_step(d_params, d_m, d_v, d_grads, size, step, lr, beta1, beta2, eps, stream));
+}
+inline double grad_clip(float* d_grads, std::int64_t size, double max_norm, gasb_stream stream = nullptr) {
+    double n = 0.0;
+    check(gasb_grad_clip(d_grads, size, max_norm, &n, stream));
+    return n;
+}
+
+// Layer (include/gas/layers.hpp:51-72) over one batch plan: LayerContext{plan, agg} is a
+// BatchOps (the plan's device stencils); forward / backward take device buffers
+// (h_in |V_b| x in_dim, h0 for APPNP / GCNII, W, out |B_b| x out_dim; the backward
+// ACCUMULATES into the gradient buffers, as the reference's tape does).
+struct LayerConfig : gasb_layer_config {
+    LayerConfig(std::int32_t kind, std::int32_t in_dim, std::int32_t out_dim, float alpha = 0.1f, float beta = 0.5f)
+        : gasb_layer_config{kind, in_dim, out_dim, alpha, beta} {}
+};
+class BatchOps {
+  public:
+    BatchOps(gasb_schedule schedule, std::int32_t part, std::int32_t max_dim) {
+        gasb_batch_ops b = nullptr;
+        check(gasb_batch_ops_create(schedule, part, max_dim, &b));
+        h_ = Handle<gasb_batch_ops, gasb_batch_ops_destroy>(b);
+        check(gasb_batch_ops_sizes(b, &nb_, &ne_));
+    }
+    std::int32_t num_batch() const { return nb_; }
+    std::int32_t num_extended() const { return ne_; }
+    void forward(const LayerConfig& c, const float* h_in, std::int64_t ld_in, const float* h0, std::int64_t ld_h0,
+                 const float* w, std::int64_t ld_w, float* out, std::int64_t ld_out, float* saved,
+                 std::int64_t ld_saved, gasb_stream stream = nullptr) const {
+        check(gasb_layer_fwd(h_.get(), &c, h_in, ld_in, h0, ld_h0, w, ld_w, out, ld_out, saved, ld_saved, stream));
+    }
+    void backward(const LayerConfig& c, const float* gy, std::int64_t ld_gy, const float* saved, std::int64_t ld_saved,
+                  const float* w, std::int64_t ld_w, float* gh_in, std::int64_t ld_gh_in, float* gh0,
+                  std::int64_t ld_gh0, float* gw, std::int64_t ld_gw, float* scratch, std::int64_t ld_scratch,
+                  gasb_stream stream = nullptr) const {
+        check(gasb_layer_bwd(h_.get(), &c, gy, ld_gy, saved, ld_saved, w, ld_w, gh_in, ld_gh_in, gh0, ld_gh0, gw, ld_gw,
+                             scratch, ld_scratch, stream));
+    }
+
+  private:
+    Handle<gasb_batch_ops, gasb_batch_ops_destroy> h_;
+    std::int32_t nb_ = 0, ne_ = 0;
+};
+
+// EpochReport (include/gas/trainer.hpp:107-115); batch_peak_floats is the device step's
+// activation floats (gasb.h), not the reference's CPU activation_meter.
+struct EpochReport {
+    std::int64_t epoch = 0;
+    double loss = 0.0;
+    std::int64_t peak_floats = 0;
+    std::vector<std::int64_t> batch_peak_floats;
+    std::vector<double> eps_max;
+    std::int64_t edges_per_layer = 0;
+    std::int64_t device_bytes = 0;
+};
+
 // Model + AdamState + HistoryStore + gas_epoch (include/gas/trainer.hpp:45-126) as one
 // device-resident training context. gas_epoch has EpochOptions{evaluate=false,
 // measure_staleness=false} semantics and returns EpochReport.loss.
@@ -374,6 +447,24 @@ class Trainer {
         double loss = 0.0;
         check(gasb_gas_epoch(h_.get(), epoch, shuffle ? 1 : 0, &loss));
         return loss;
+    }
+    // gas_epoch with the EpochReport fields; measure_staleness runs the frozen snapshot pass
+    EpochReport gas_epoch_report(std::int64_t epoch, std::int32_t num_parts, std::int32_t history_layers,
+                                 bool shuffle = true, bool measure_staleness = false) {
+        gasb_epoch_report r{};
+        EpochReport out;
+        out.batch_peak_floats.resize(static_cast<std::size_t>(num_parts));
+        out.eps_max.resize(static_cast<std::size_t>(history_layers > 0 ? history_layers : 0));
+        check(gasb_gas_epoch_report(h_.get(), epoch, shuffle ? 1 : 0, measure_staleness ? 1 : 0, &r,
+                                    out.batch_peak_floats.data(), out.eps_max.empty() ? nullptr : out.eps_max.data()));
+        out.epoch = r.epoch;
+        out.loss = r.loss;
+        out.peak_floats = r.peak_floats;
+        out.edges_per_layer = r.edges_per_layer;
+        out.device_bytes = r.device_bytes;
+        out.batch_peak_floats.resize(static_cast<std::size_t>(r.num_batches));
+        out.eps_max.resize(static_cast<std::size_t>(r.staleness_layers));
+        return out;
     }
     std::vector<float> params() const {
         std::int64_t n = 0;
@@ -417,10 +508,17 @@ class Trainer {
 // and passes the concatenation to connect(). Replicas stay bit-identical.
 class DataParallel {
   public:
-    DataParallel(Trainer& t, std::int32_t rank, std::int32_t world) {
+    // placement: GASB_DP_REPLICATED or GASB_DP_SHARDED (partition-sharded histories, gasb.h)
+    DataParallel(Trainer& t, std::int32_t rank, std::int32_t world, std::int32_t placement = GASB_DP_REPLICATED) {
         gasb_dp d = nullptr;
-        check(gasb_dp_create(t.raw(), rank, world, &d));
+        check(gasb_dp_create_ex(t.raw(), rank, world, placement, &d));
         h_ = Handle<gasb_dp, gasb_dp_destroy>(d);
+    }
+    // sharded placement: one history layer gathered from every rank's shard
+    DenseMatrix history_layer(std::int32_t layer, NodeId num_nodes, std::int32_t dim) const {
+        DenseMatrix m(num_nodes, dim);
+        check(gasb_dp_read_history(h_.get(), layer, m.values.data()));
+        return m;
     }
     std::vector<std::uint8_t> export_handle() const {
         std::vector<std::uint8_t> h(GASB_DP_HANDLE_BYTES);

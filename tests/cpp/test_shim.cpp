@@ -55,6 +55,26 @@ int main() {
     const double y0 = static_cast<double>(p.gcn_coeffs[0]) + p.gcn_coeffs[1];  // h = 1, W = I
     EXPECT(std::fabs(y0 - (0.5 + 1.0 / std::sqrt(6.0))) < 1e-7);
 
+    // partitioners (host): every node assigned, every part non-empty, deterministic
+    {
+        std::vector<NodeId> rs, rd;
+        for (NodeId v = 0; v < 60; ++v) {
+            rs.push_back(v);
+            rd.push_back((v * 7 + 3) % 60);
+            rs.push_back(v);
+            rd.push_back((v + 1) % 60);
+        }
+        Graph rg = Graph::build(rs, rd, 60);
+        auto a = cluster_partition(rg, 4, 1);
+        auto b = cluster_partition(rg, 4, 1);
+        EXPECT(a == b && a.size() == 60);
+        std::vector<int> cnt(4, 0);
+        for (auto x : a) ++cnt[static_cast<std::size_t>(x)];
+        EXPECT(cnt[0] > 0 && cnt[1] > 0 && cnt[2] > 0 && cnt[3] > 0);
+        EXPECT(throws<std::invalid_argument>([&] { cluster_partition(rg, 0); }));
+        EXPECT(random_partition(60, 4, 2).size() == 60);
+    }
+
     // two parts {0,1} | {2}: part 0 sees node 2 as its halo
     std::vector<std::int32_t> two{0, 0, 1};
     BatchSchedule s2 = BatchSchedule::build(g, two, 2);
