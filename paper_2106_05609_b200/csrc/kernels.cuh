@@ -90,12 +90,11 @@ void launch_scan_special(const float* x, int64_t rows, int64_t ld, int32_t dim, 
 // accumulate: gx[t] continues from its current value (the reference's `g += c * gy` into
 // a grad buffer that already holds other contributions) instead of starting at 0.
 // order (optional): the targets heaviest first (claimed in that order, so a hub's serial
-// chain starts early instead of setting the tail). exact = false: four interleaved chains
-// per target (deterministic reassociation; the trainer's segmented mode, seg_edges > 0).
+// chain starts early instead of setting the tail).
 void launch_spmm_bwd(const int64_t* t_rowptr, int32_t ntargets, const int32_t* t_src, const float* t_coeffs,
                      const float* gy, int64_t ldgy, int32_t dim, const float* mask, int64_t ldm, float* gx,
                      int64_t ldgx, cudaStream_t st, int32_t nsrc = 0, bool accumulate = false,
-                     const int32_t* order = nullptr, bool exact = true);
+                     const int32_t* order = nullptr);
 
 // ---- GEMM (gemm.cu) -------------------------------------------------------------------
 // op 0: C = A B ; 1: C = A B^T ; 2: C = A^T B.  Row-major fp32, fp32 accumulation.

@@ -1213,11 +1213,6 @@ constexpr int kBwdCW = 32;
 constexpr int kBwdRing = 8;  // metadata windows in flight per warp (spmm_bwd_smem_kernel)
 constexpr int kBwdThreads = 1024;
 
-// NCH = 1: one fp32 chain per (target, column) in entry order -> bit-exact with the
-// reference's scatter. NCH = 4: entries j % 4 accumulate into four chains combined
-// ((c0 + c1) + (c2 + c3)) + gx at the end — deterministic, a reassociation of the sum (a
-// hub target's ~1,100-entry dependent FADD chain is the kernel's critical path).
-template <int NCH>
 __global__ void __launch_bounds__(kBwdThreads) spmm_bwd_smem_kernel(
     const int64_t* __restrict__ rp, int32_t nt, const int32_t* __restrict__ src, const float* __restrict__ cf,
     const float* __restrict__ gy, int64_t ldgy, int32_t nsrc, int32_t dim, const float* __restrict__ mask,
@@ -1301,9 +1296,6 @@ __global__ void __launch_bounds__(kBwdThreads) spmm_bwd_smem_kernel(
         for (int k = 0; k < kBwdRing; ++k)
             if (issued < nw) prefetch();
         const float* sgl = sg + lane;
-        float ch[NCH];
-#pragma unroll
-        for (int k = 0; k < NCH; ++k) ch[k] = 0.0f;
         for (int32_t q = 0; q < nw; ++q) {
             const int pending = issued - q - 1;  // windows after q that may still be in flight
             if (pending >= 7) cp_async_wait<7>();
@@ -1319,54 +1311,38 @@ __global__ void __launch_bounds__(kBwdThreads) spmm_bwd_smem_kernel(
             const int2* w = ring + slot * 32;
             const int64_t eb = e0 + 32LL * q;
             const int cnt = static_cast<int>(e1 - eb < 32 ? e1 - eb : 32);
-            if constexpr (NCH == 1) {
-                if (cnt == 32) {
+            if (cnt == 32) {
 #pragma unroll
-                    for (int j = 0; j < 32; ++j) {
-                        const int2 rc = w[j];
-                        a = __fadd_rn(a, __fmul_rn(__int_as_float(rc.y), sgl[rc.x * kBwdCW]));
-                    }
-                } else {
-                    for (int j = 0; j < cnt; ++j) {
-                        const int2 rc = w[j];
-                        a = __fadd_rn(a, __fmul_rn(__int_as_float(rc.y), sgl[rc.x * kBwdCW]));
-                    }
+                for (int j = 0; j < 32; ++j) {
+                    const int2 rc = w[j];
+                    a = __fadd_rn(a, __fmul_rn(__int_as_float(rc.y), sgl[rc.x * kBwdCW]));
                 }
             } else {
-                if (cnt == 32) {
-#pragma unroll
-                    for (int j = 0; j < 32; ++j) {
-                        const int2 rc = w[j];
-                        ch[j % NCH] = __fadd_rn(ch[j % NCH], __fmul_rn(__int_as_float(rc.y), sgl[rc.x * kBwdCW]));
-                    }
-                } else {
-                    for (int j = 0; j < cnt; ++j) {
-                        const int2 rc = w[j];
-                        ch[j % NCH] = __fadd_rn(ch[j % NCH], __fmul_rn(__int_as_float(rc.y), sgl[rc.x * kBwdCW]));
-                    }
+                for (int j = 0; j < cnt; ++j) {
+                    const int2 rc = w[j];
+                    a = __fadd_rn(a, __fmul_rn(__int_as_float(rc.y), sgl[rc.x * kBwdCW]));
                 }
             }
             __syncwarp();  // the slot is free again
             if (issued < nw) prefetch();
         }
-        if constexpr (NCH == 4) a = __fadd_rn(a, __fadd_rn(__fadd_rn(ch[0], ch[1]), __fadd_rn(ch[2], ch[3])));
         if (lane < ncol) gx[static_cast<int64_t>(t) * ldgx + col0 + lane] = keep ? a : 0.0f;
         t = tn;
     }
 }
 
-static int g_bwd_smem_set[2] = {0, 0};
+static int g_bwd_smem_set = 0;
 
 void launch_spmm_bwd(const int64_t* t_rowptr, int32_t nt, const int32_t* t_src, const float* t_coeffs,
                      const float* gy, int64_t ldgy, int32_t dim, const float* mask, int64_t ldm, float* gx,
-                     int64_t ldgx, cudaStream_t st, int32_t nsrc, bool accumulate, const int32_t* order, bool exact) {
+                     int64_t ldgx, cudaStream_t st, int32_t nsrc, bool accumulate, const int32_t* order) {
     if (nt <= 0 || dim <= 0) return;
     const int64_t smem = static_cast<int64_t>(nsrc) * kBwdCW * sizeof(float) + (kBwdThreads / 32) * kBwdRing * 32 * 8;
     if (nsrc > 0 && smem <= 216 * 1024) {
-        auto kern = exact ? spmm_bwd_smem_kernel<1> : spmm_bwd_smem_kernel<4>;
-        if (!g_bwd_smem_set[exact]) {
+        auto kern = spmm_bwd_smem_kernel;
+        if (!g_bwd_smem_set) {
             GASB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 216 * 1024));
-            g_bwd_smem_set[exact] = 1;
+            g_bwd_smem_set = 1;
         }
         const int32_t nchunks = static_cast<int32_t>(ceil_div(dim, kBwdCW));
         // one CTA per SM (the staged slice fills shared memory): a single wave of <= #SMs CTAs

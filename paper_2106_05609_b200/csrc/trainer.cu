@@ -792,17 +792,17 @@ void gasb_trainer_s::enqueue_batch_res(int32_t p, bool train, bool push, bool fu
             launch_mix_bwd(dmix, ldm, m, D, spec.alpha, br, h0g.p, ldD, dprop.p, ldD, stream);
             if (l >= 2) {  // to act_{l-1}'s batch rows (compose bwd), relu mask for GCNII
                 launch_spmm_bwd(t_rowptr.p + r0 + p, m, t_src.p, t_cf.p, dprop.p, ldD, D, gcnii ? act[l - 1].p : nullptr,
-                                ldD, gout.p, ldD, stream, m, false, t_order.p + r0, opt.seg_edges == 0);
+                                ldD, gout.p, ldD, stream, m, false, t_order.p + r0);
                 if (dr) launch_dropout_rows_bwd(gout.p, ldD, m, D, br, mask_of(l), inv_keep, stream);
                 dout = gout.p;
                 ldo = ldD;
             } else if (dr) {  // layer 1 input = dropout(h0): its gradient, then the dropout bwd into h0g
                 launch_spmm_bwd(a_rowptr.p + a_off[p], me, a_src.p, a_cf.p, dprop.p, ldD, D, nullptr, 0, dtmp.p, ldD,
-                                stream, m, false, nullptr, opt.seg_edges == 0);
+                                stream, m, false);
                 launch_dropout_bwd_acc(h0g.p, ldD, me, D, dtmp.p, ldD, mask_of(1), inv_keep, stream);
             } else {  // layer 1: every V_b row of h0, accumulated onto the residual terms
                 launch_spmm_bwd(a_rowptr.p + a_off[p], me, a_src.p, a_cf.p, dprop.p, ldD, D, nullptr, 0, h0g.p, ldD,
-                                stream, m, true, nullptr, opt.seg_edges == 0);
+                                stream, m, true);
             }
         }
         // head backward (x_ext carries no gradient)
@@ -941,7 +941,7 @@ void gasb_trainer_s::enqueue_batch(int32_t p, bool train, bool push, bool use_ho
                 // gradient first, then the dgrad GEMM and the relu mask: A^T (g W^T) == (A^T g) W^T,
                 // dout/din of the gather work (reassociation only; within the 1e-5 grad contract)
                 launch_spmm_bwd(t_rowptr.p + r0 + p, m, t_src.p, t_cf.p, g, ldg, dout, nullptr, 0, g_agg.p, ldC,
-                                stream, m, false, t_order.p + r0, opt.seg_edges == 0);
+                                stream, m, false, t_order.p + r0);
                 launch_gemm(1, m, din, dout, g_agg.p, ldC, W(l), pp(layer_param[l]), go, ldH, 0.f, false, nullptr,
                             stream);
                 launch_mask(go, ldH, act[l - 1].p, ldH, m, din, stream);  // relu backward (mask = act_{l-1})
@@ -950,7 +950,7 @@ void gasb_trainer_s::enqueue_batch(int32_t p, bool train, bool push, bool use_ho
                             stream);
                 // aggregate backward over intra-batch edges + compose bwd + relu bwd (mask = act)
                 launch_spmm_bwd(t_rowptr.p + r0 + p, m, t_src.p, t_cf.p, g_agg.p, ldH, din, act[l - 1].p, ldH, go,
-                                ldH, stream, m, false, t_order.p + r0, opt.seg_edges == 0);
+                                ldH, stream, m, false, t_order.p + r0);
             }
             // dropout backward on the batch rows of the layer input (tensor.cpp:390-397)
             if (dr) launch_dropout_rows_bwd(go, ldH, m, din, brow.p + r0, mask_of(l), inv_keep, stream);
