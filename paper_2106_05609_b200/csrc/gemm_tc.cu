@@ -42,6 +42,10 @@ static int num_sms() {
     return sms;
 }
 
+#ifdef GASB_GEMM_TIMING
+__device__ uint64_t g_gemm_stamps[40];
+extern "C" void gasb_debug_gemm_stamps(uint64_t* out) { cudaMemcpyFromSymbol(out, g_gemm_stamps, sizeof(uint64_t) * 40); }
+#endif
 namespace tc {
 
 #ifndef GASB_GEMM_STAGES
@@ -51,7 +55,13 @@ namespace tc {
 #define GASB_GEMM_MAXACC 8
 #endif
 constexpr int BM = 128, BK = 32, kStagesTC = GASB_GEMM_STAGES;
-constexpr int kSplitHelpers = 4;                      // extra warps that only split tiles
+#ifndef GASB_GEMM_SPLIT_HELPERS
+#define GASB_GEMM_SPLIT_HELPERS 4
+#endif
+#ifndef GASB_GEMM_KSTEPS_PER_ACC
+#define GASB_GEMM_KSTEPS_PER_ACC 1  // 16 cut the epilogue 3.8 -> 2.7 us but broke the 64-layer GCNII contract
+#endif
+constexpr int kSplitHelpers = GASB_GEMM_SPLIT_HELPERS;  // extra warps that only split tiles
 constexpr int kSplitThreads = 128 + 32 * kSplitHelpers;  // warps 0-3 + helpers
 constexpr int kThreads = 192 + 32 * kSplitHelpers;
 // The tensor core's fp32 accumulation truncates, so its error grows linearly with the number
@@ -135,6 +145,11 @@ __device__ __forceinline__ void mma_commit(uint64_t* b) {
 __device__ __forceinline__ float tf32_hi(float x) {
     return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
 }
+// truncated tf32: what the tensor core reads from an fp32 operand
+__device__ __forceinline__ float tf32_tr(float x) { return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
+#ifndef GASB_GEMM_TRUNC_SPLIT
+#define GASB_GEMM_TRUNC_SPLIT 0  // measured no faster: the mainloop is bound by shared-memory traffic overall
+#endif
 
 template <int BN, bool A_MN, bool B_MN, bool TALL = false>
 struct Layout {
@@ -167,10 +182,27 @@ __global__ void __launch_bounds__(kThreads, TALL ? 2 : 1) gemm_tc_kernel(const _
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
+#ifdef GASB_GEMM_TIMING  // globaltimer stamps of CTA (0,0) into g_gemm_stamps (timing probe builds only)
+    auto stamp = [&](int i) {
+        if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0) {
+            uint64_t t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            g_gemm_stamps[i] = t;
+        }
+    };
+    if (threadIdx.x == 0) stamp(0);
+#else
+    auto stamp = [](int) {};
+#endif
     // split-K: this CTA covers k-blocks [kb0, kb0 + nk) (blockIdx.z = slice); with ws != nullptr
     // it writes its raw fp32 sums to ws[slice] and gemm_splitk_reduce applies the epilogue.
     const int kb0 = blockIdx.z * kbs;
     const int nk = min((K + BK - 1) / BK - kb0, kbs);
+    // accumulators in use: one per GASB_GEMM_KSTEPS_PER_ACC k-steps (the fp32 accumulation
+    // error grows with the k-steps an accumulator sums), at most Acc::kAcc; fewer accumulators
+    // mean fewer TMEM reads in the epilogue
+    const int nacc = min(Acc<BN, TALL>::kAcc, max(1, (nk * (BK / 8) + GASB_GEMM_KSTEPS_PER_ACC - 1) /
+                                                         GASB_GEMM_KSTEPS_PER_ACC));
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < kStagesTC; ++s) {
@@ -190,6 +222,7 @@ __global__ void __launch_bounds__(kThreads, TALL ? 2 : 1) gemm_tc_kernel(const _
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
     const uint32_t tmem = *tmem_slot;
+    if (threadIdx.x == 0) stamp(1);
 
     if (warp == 4) {
         // ---------------- TMA producer ----------------
@@ -197,6 +230,7 @@ __global__ void __launch_bounds__(kThreads, TALL ? 2 : 1) gemm_tc_kernel(const _
             for (int kb = 0; kb < nk; ++kb) {
                 const int s = kb % kStagesTC;
                 bar_wait(empty + s, ((kb / kStagesTC) & 1) ^ 1);
+                if (kb < 8) stamp(24 + kb);
                 unsigned char* st = base + s * Lay::kStage;
                 bar_expect(full + s, Lay::kTileA + Lay::kTileB);
                 const int k0 = (kb0 + kb) * BK;
@@ -240,9 +274,9 @@ __global__ void __launch_bounds__(kThreads, TALL ? 2 : 1) gemm_tc_kernel(const _
                     const uint64_t alo = smem_desc(sa_lo + offa, lboa, sboa, lya);
                     const uint64_t bhi = smem_desc(sb + offb, lbob, sbob, lyb);
                     const uint64_t blo = smem_desc(sb_lo + offb, lbob, sbob, lyb);
-                    const int g = kb * (BK / 8) + kk;  // global k-step -> accumulator g % kAcc
-                    const uint32_t d = tmem + static_cast<uint32_t>((g % Acc<BN, TALL>::kAcc) * BN);
-                    const uint32_t first = g < Acc<BN, TALL>::kAcc ? 0u : 1u;
+                    const int g = kb * (BK / 8) + kk;  // global k-step -> accumulator g % nacc
+                    const uint32_t d = tmem + static_cast<uint32_t>((g % nacc) * BN);
+                    const uint32_t first = g < nacc ? 0u : 1u;
                     mma_tf32(d, ahi, bhi, idesc, first);
                     mma_tf32(d, ahi, blo, idesc, 1u);
                     mma_tf32(d, alo, bhi, idesc, 1u);
@@ -257,10 +291,29 @@ __global__ void __launch_bounds__(kThreads, TALL ? 2 : 1) gemm_tc_kernel(const _
         for (int kb = 0; kb < nk; ++kb) {
             const int s = kb % kStagesTC;
             bar_wait(full + s, (kb / kStagesTC) & 1);
+            if (threadIdx.x == 0 && kb == 0) stamp(2);
+            if (threadIdx.x == 0 && kb < 8) stamp(8 + kb);
             float4* a = reinterpret_cast<float4*>(base + s * Lay::kStage);
             float4* alo = a + Lay::kTileA / 16;
             float4* b = a + 2 * Lay::kTileA / 16;
             float4* blo = b + Lay::kTileB / 16;
+#if GASB_GEMM_TRUNC_SPLIT
+            // hi = the raw fp32 tile itself (the tensor core reads tf32 by truncating the low 13
+            // mantissa bits), lo = rn_tf32(x - trunc_tf32(x)) (x - trunc is exact): only the lo
+            // tiles are written, a third of the shared-memory traffic of a hi + lo rewrite — the
+            // split is the mainloop's serial step (tools/gemm_timing_probe.py). Dropped terms
+            // ~2^-22 relative, as the round-to-nearest split.
+            for (int i = sid; i < Lay::kTileA / 16; i += kSplitThreads) {
+                const float4 v = a[i];
+                alo[i] = make_float4(tf32_hi(v.x - tf32_tr(v.x)), tf32_hi(v.y - tf32_tr(v.y)), tf32_hi(v.z - tf32_tr(v.z)),
+                                     tf32_hi(v.w - tf32_tr(v.w)));
+            }
+            for (int i = sid; i < Lay::kTileB / 16; i += kSplitThreads) {
+                const float4 v = b[i];
+                blo[i] = make_float4(tf32_hi(v.x - tf32_tr(v.x)), tf32_hi(v.y - tf32_tr(v.y)), tf32_hi(v.z - tf32_tr(v.z)),
+                                     tf32_hi(v.w - tf32_tr(v.w)));
+            }
+#else
             // hi = rn_tf32(x), lo = rn_tf32(x - hi): both exactly tf32, so the tensor core's
             // operand truncation changes nothing; dropped lo*lo term ~2^-22 relative
             for (int i = sid; i < Lay::kTileA / 16; i += kSplitThreads) {
@@ -275,11 +328,14 @@ __global__ void __launch_bounds__(kThreads, TALL ? 2 : 1) gemm_tc_kernel(const _
                 b[i] = h;
                 blo[i] = make_float4(tf32_hi(v.x - h.x), tf32_hi(v.y - h.y), tf32_hi(v.z - h.z), tf32_hi(v.w - h.w));
             }
+#endif
             asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // generic writes -> tensor core
+            if (threadIdx.x == 0 && kb < 8) stamp(16 + kb);
             bar_arrive(split + s);
         }
         if (warp < 4) {  // epilogue: TMEM lane == tile row
             bar_wait(accum, 0);
+            if (threadIdx.x == 0) stamp(3);
             asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
             const int row = m0 + warp * 32 + lane;  // TMEM lane == tile row
             float* crow = row < M ? C + static_cast<int64_t>(row) * ldc : nullptr;
@@ -291,7 +347,7 @@ __global__ void __launch_bounds__(kThreads, TALL ? 2 : 1) gemm_tc_kernel(const _
             }
             int32_t flags = 0;
             const int nsteps = nk * (BK / 8);
-            const int nacc = nsteps < Acc<BN, TALL>::kAcc ? nsteps : Acc<BN, TALL>::kAcc;  // accumulators written
+
     #pragma unroll 1
             for (int c0 = 0; c0 < BN; c0 += 32) {
                 float sum[32];
@@ -434,6 +490,7 @@ __global__ void __launch_bounds__(kThreads, TALL ? 2 : 1) gemm_tc_kernel(const _
             }
         }
     }
+    if (threadIdx.x == 0) stamp(4);
     asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
     __syncthreads();
     if (warp == 0 && !ws) {  // (split-K CTAs freed their TMEM before the fixup)
