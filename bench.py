@@ -400,8 +400,13 @@ def run_ours(args):
 
 
 def pull_bandwidth(tr, sched, w, torch) -> dict:
-    """HistoryStore::pull of a batch's halo rows (ids + d floats read, d floats written)."""
-    hist = tr.history
+    """HistoryStore::pull of a batch's halo rows (ids + d floats read, d floats written), on a
+    store of the trainer's shape (its own store may be sharded across a data-parallel group)."""
+    import paper_2106_05609_b200 as gb
+    th = tr.history
+    if th is None:
+        return None
+    hist = gb.HistoryStore(1, w.num_nodes, w.num_classes if w.kind == "appnp" else w.hidden)
     p = 0
     plan = sched.plan(p)
     halo = torch.from_numpy(plan.halo_nodes).cuda()
