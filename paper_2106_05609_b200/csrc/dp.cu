@@ -342,11 +342,18 @@ struct gasb_dp_s {
     }
 
     // One step over parts[0..kk): batch (if this rank has one), exchange, Adam.
-    int64_t step(const int32_t* parts, int32_t kk) {
+    int64_t step(const int32_t* parts, int32_t kk, int64_t epoch) {
         gasb_trainer_s& T = *t;
         const int64_t c0 = t_launches;
         int64_t n = 0;
-        if (rank < kk) n += T.launch_batch_graph(parts[rank], true);
+        if (rank < kk) {
+            if (T.drop) {  // this batch's dropout masks (epoch, partition id), before its graph
+                const int64_t c1 = t_launches;
+                T.enqueue_masks(parts[rank], epoch);
+                n += t_launches - c1;
+            }
+            n += T.launch_batch_graph(parts[rank], true);
+        }
         barrier();
         uint32_t mask = 0;
         int32_t count = 0;
@@ -593,14 +600,14 @@ gasb_status gasb_dp_epoch_async(gasb_dp d, int64_t epoch, int32_t shuffle) {
         d->last_parts.clear();
         for (int32_t s0 = 0; s0 < T.num_parts; s0 += d->world)
             if (d->rank < std::min(d->world, T.num_parts - s0)) d->last_parts.push_back(order[s0 + d->rank]);
-        if (T.opt.hoist_layer1 && T.opt.fused && !T.residual && T.agg_all.p) {
+        if (T.opt.hoist_layer1 && T.opt.fused && !T.residual && !T.drop && T.agg_all.p) {
             const int64_t c0 = t_launches;  // layer 1 of this rank's batches, one launch
             T.enqueue_hoisted_parts(d->last_parts);
             d->epoch_launches += t_launches - c0;
         }
         for (int32_t s0 = 0; s0 < T.num_parts; s0 += d->world) {
             const int32_t kk = std::min(d->world, T.num_parts - s0);
-            d->epoch_launches += d->step(order.data() + s0, kk);
+            d->epoch_launches += d->step(order.data() + s0, kk, epoch);
         }
         d->last_order = order;
         T.last_order = order;

@@ -158,3 +158,19 @@ def test_residual_dropout_graphs_equal_eager(name):
             tr.gas_epoch(e)
         out.append(tr.get_params())
     assert np.array_equal(out[0], out[1])
+
+
+@pytest.mark.parametrize("name,placement", [("cora", "replicated"), ("cora", "sharded"), ("cora_appnp", "replicated")])
+def test_dropout_data_parallel_world1_is_gas_epoch(name, placement):
+    """A data-parallel step draws its batch's masks like gas_epoch (epoch, partition id)."""
+    ds = make_dataset(name)
+    w = ds.workload
+    sched = gb.BatchSchedule.build(ds.graph, ds.assignment, w.parts)
+    mk = lambda: gb.GasTrainer(sched, ds.features, ds.labels, ds.train_mask, w.num_classes,  # noqa: E731
+                               gb.ModelSpec(kind=w.kind, num_layers=w.num_layers, hidden=w.hidden, seed=3,
+                                            dropout=0.3), gb.TrainerOptions())
+    a, b = mk(), mk()
+    dp = gb.DataParallelTrainer(b, 0, 1, placement=placement)
+    for e in range(2):
+        assert a.gas_epoch(e) == dp.gas_epoch(e)
+    assert np.array_equal(a.get_params(), b.get_params())
