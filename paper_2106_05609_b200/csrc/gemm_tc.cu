@@ -51,6 +51,9 @@ namespace tc {
 #ifndef GASB_GEMM_STAGES
 #define GASB_GEMM_STAGES 3
 #endif
+#ifndef GASB_GEMM_LDGROUP
+#define GASB_GEMM_LDGROUP 2
+#endif
 #ifndef GASB_GEMM_MAXACC
 #define GASB_GEMM_MAXACC 8
 #endif
@@ -351,23 +354,36 @@ __global__ void __launch_bounds__(kThreads, TALL ? 2 : 1) gemm_tc_kernel(const _
     #pragma unroll 1
             for (int c0 = 0; c0 < BN; c0 += 32) {
                 float sum[32];
+                // the accumulators' TMEM loads in groups of kLdGroup, one tcgen05.wait::ld per group
+                // (each wait costs a full TMEM round trip); summed in accumulator order as before
+                constexpr int kLdGroup = TALL ? 1 : GASB_GEMM_LDGROUP;
     #pragma unroll 1
-                for (int q = 0; q < nacc; ++q) {
-                    uint32_t v[32];
-                    const uint32_t taddr =
-                        tmem + (static_cast<uint32_t>(warp * 32) << 16) + static_cast<uint32_t>(q * BN + c0);
-                    asm volatile(
-                        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-                        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
-                        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
-                          "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
-                          "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]),
-                          "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]),
-                          "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
-                        : "r"(taddr));
+                for (int q0 = 0; q0 < nacc; q0 += kLdGroup) {
+                    uint32_t v[kLdGroup][32];
+    #pragma unroll
+                    for (int g = 0; g < kLdGroup; ++g) {
+                        if (q0 + g >= nacc) break;
+                        const uint32_t taddr = tmem + (static_cast<uint32_t>(warp * 32) << 16) +
+                                               static_cast<uint32_t>((q0 + g) * BN + c0);
+                        asm volatile(
+                            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+                            "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+                            : "=r"(v[g][0]), "=r"(v[g][1]), "=r"(v[g][2]), "=r"(v[g][3]), "=r"(v[g][4]), "=r"(v[g][5]),
+                              "=r"(v[g][6]), "=r"(v[g][7]), "=r"(v[g][8]), "=r"(v[g][9]), "=r"(v[g][10]), "=r"(v[g][11]),
+                              "=r"(v[g][12]), "=r"(v[g][13]), "=r"(v[g][14]), "=r"(v[g][15]), "=r"(v[g][16]),
+                              "=r"(v[g][17]), "=r"(v[g][18]), "=r"(v[g][19]), "=r"(v[g][20]), "=r"(v[g][21]),
+                              "=r"(v[g][22]), "=r"(v[g][23]), "=r"(v[g][24]), "=r"(v[g][25]), "=r"(v[g][26]),
+                              "=r"(v[g][27]), "=r"(v[g][28]), "=r"(v[g][29]), "=r"(v[g][30]), "=r"(v[g][31])
+                            : "r"(taddr));
+                    }
                     asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
     #pragma unroll
-                    for (int j = 0; j < 32; ++j) sum[j] = q == 0 ? __uint_as_float(v[j]) : __fadd_rn(sum[j], __uint_as_float(v[j]));
+                    for (int g = 0; g < kLdGroup; ++g) {
+                        if (q0 + g >= nacc) break;
+    #pragma unroll
+                        for (int j = 0; j < 32; ++j)
+                            sum[j] = q0 + g == 0 ? __uint_as_float(v[g][j]) : __fadd_rn(sum[j], __uint_as_float(v[g][j]));
+                    }
                 }
                 if (crow && ws) {  // slice partial, row pitch Np = N rounded up to 4 (float4 stores)
                     const int Np = (N + 3) & ~3;
