@@ -62,6 +62,10 @@ struct SpmmSegs {
     // be split anyway, so each row also runs two interleaved chains (even / odd edges of the
     // stage) added at the row end — twice the independent DFMAs, same fp64 accuracy class
     int32_t exact = 1;
+    // optional: per row, the partial slots of its segments in combine order, indexed from
+    // row_seg0[row] (tables whose rows' segments are not consecutive: the source-blocked
+    // hoisted layer 1); nullptr: the row's segments are consecutive, seg_slot[row_seg0 + i]
+    const int32_t* row_slots = nullptr;
 };
 // Host: splits segments [g0, g1) into nranges contiguous ranges of ~equal edges.
 void split_ranges(const int64_t* seg_beg, int64_t g0, int64_t g1, int32_t nranges, int32_t* out);

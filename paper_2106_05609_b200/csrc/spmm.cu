@@ -695,7 +695,8 @@ __device__ __forceinline__ void flat_items(
     const int32_t* __restrict__ row_seg0, const int32_t* __restrict__ row_nseg, const int32_t* __restrict__ range_seg,
     int32_t nranges, const int32_t* __restrict__ cols, const double* __restrict__ coeffs, int32_t dim,
     int32_t nchunks, float* __restrict__ y, int64_t ldy, int64_t row_base, double* __restrict__ partial, int64_t pld,
-    int32_t* __restrict__ counters, int32_t cld, const CUtensorMap* tmap, unsigned char* wbase, uint64_t* bars,
+    int32_t* __restrict__ counters, int32_t cld, const int32_t* __restrict__ slot_list, const CUtensorMap* tmap,
+    unsigned char* wbase, uint64_t* bars,
     int32_t* ring_c, double* ring_f) {
     using Cfg = PipeCfg<CPL>;
     constexpr int KE = Cfg::kEdges;
@@ -787,7 +788,7 @@ __device__ __forceinline__ void flat_items(
                 }
             }
             seg_finish<CPL>(acc, row, slot, lane, col, chunk, dim, y, ldy, row_base, partial, pld, counters, cld,
-                            seg_slot, row_seg0, row_nseg);
+                            slot_list, row_seg0, row_nseg);
             ++cur;
             if (cur < s_hi) {
                 if (cur - wseg >= 32) load_window(cur);
@@ -852,7 +853,7 @@ __global__ void __launch_bounds__(kPipeWarps * 32, kPipeCtas) spmm_fwd_flat_kern
     int32_t nranges, const int32_t* __restrict__ cols, const double* __restrict__ coeffs, int32_t dim,
     int32_t nchunks, float* __restrict__ y, int64_t ldy, int64_t row_base, double* __restrict__ partial, int64_t pld,
     int32_t* __restrict__ counters, int32_t cld, const int32_t* __restrict__ table_flags,
-    const __grid_constant__ CUtensorMap tmap) {
+    const int32_t* __restrict__ slot_list, const __grid_constant__ CUtensorMap tmap) {
     using Cfg = PipeCfg<CPL>;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -871,7 +872,7 @@ __global__ void __launch_bounds__(kPipeWarps * 32, kPipeCtas) spmm_fwd_flat_kern
     const int mode = widen_mode(table_flags);
 #define GASB_FLAT(M)                                                                                              \
     flat_items<CPL, M, DUAL>(seg_beg, seg_row, seg_slot, row_seg0, row_nseg, range_seg, nranges, cols, coeffs, dim, nchunks, \
-                  y, ldy, row_base, partial, pld, counters, cld, &tmap, wbase, bars, ring_c, ring_f)
+                  y, ldy, row_base, partial, pld, counters, cld, slot_list, &tmap, wbase, bars, ring_c, ring_f)
     if (mode == kWidenNonNeg) GASB_FLAT(kWidenNonNeg);
     else if (mode == kWidenSigned) GASB_FLAT(kWidenSigned);
     else GASB_FLAT(kWidenF2F);
@@ -903,7 +904,8 @@ static void launch_flat(const SpmmSegs& s, const int32_t* cols, const double* co
     const int64_t blocks = std::min<int64_t>(ceil_div(items, kPipeWarps), static_cast<int64_t>(kPipeCtas) * sms);
     spmm_fwd_flat_kernel<CPL, DUAL><<<static_cast<unsigned>(blocks), kPipeWarps * 32, kSmem, st>>>(
         s.seg_beg, s.seg_row, s.seg_slot, s.row_seg0, s.row_nseg, s.range_seg, s.nranges, cols, coeffs, dim, nchunks,
-        y, ldy, row_base, partial, partial_ld, counters, counters_ld, special, *tmap);
+        y, ldy, row_base, partial, partial_ld, counters, counters_ld, special, s.row_slots ? s.row_slots : s.seg_slot,
+        *tmap);
 }
 
 static int g_pipe_smem_set[2][2] = {};
@@ -1121,6 +1123,7 @@ void launch_spmm_fwd(const SpmmSegs& s, const int32_t* cols, const double* coeff
         GASB_CUDA(cudaGetLastError());
         return;
     }
+    require(!s.row_slots, "spmm_fwd: a slot-list segment table needs the flat TMA engine");
     if (spmm_engine() == 2) {
         launch_direct(s, cols, coeffs, x, ldx, dim, y, ldy, row_base, partial, partial_ld, counters, counters_ld, st,
                       special);

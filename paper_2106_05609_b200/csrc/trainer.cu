@@ -399,6 +399,15 @@ void gasb_trainer_s::build(const float* h_features, const int32_t* h_labels, con
     pld_all = round_up(F, 256);
     partial_batch.alloc(std::max<int64_t>(seg_batch.max_group_slots, 1) * pld);
     partial_all.alloc(std::max<int64_t>(seg_all.total_slots, 1) * pld_all);
+    {
+        // GASB_HOIST_BLOCKS: source blocks of the hoisted layer 1 (1 = off)
+        const char* hbe = getenv("GASB_HOIST_BLOCKS");
+        const int32_t hb = hbe ? std::max(1, std::min(64, atoi(hbe))) : 1;
+        if (hb > 1 && opt.hoist_layer1 && opt.fused && !residual && opt.seg_edges > 0) {
+            build_hoist_blocked(h_rp, h_cg, h_cf, hb);
+            trace("blocked hoist table");
+        }
+    }
 
     // ---- features ----
     X.alloc(static_cast<int64_t>(n) * ldF);
@@ -629,8 +638,109 @@ void gasb_trainer_s::enqueue_hoisted_parts(const std::vector<int32_t>& parts) {
 }
 
 void gasb_trainer_s::enqueue_hoisted() {
+    if (hoist_cols.p) {
+        launch_spmm_fwd(seg_hoist.segs(0), hoist_cols.p, hoist_coef.p, X.p, ldF, F, agg_all.p, ldF, 0,
+                        partial_hoist.p, pld_all, counters.p, max_chunks, stream, source_flags(1), source_tmap(1));
+        return;
+    }
     launch_spmm_fwd(seg_all.segs(0), cols_g.p, coef64.p, X.p, ldF, F, agg_all.p, ldF, 0, partial_all.p, pld_all,
                     counters.p, max_chunks, stream, source_flags(1), source_tmap(1));
+}
+
+void gasb_trainer_s::build_hoist_blocked(const std::vector<int64_t>& rp, const HVec<int32_t>& cg,
+                                         const HVec<double>& cf, int32_t B) {
+    const int64_t R = static_cast<int64_t>(rp.size()) - 1, E = rp[R];
+    auto blk = [&](int32_t c) { return static_cast<int32_t>(static_cast<int64_t>(c) * B / n); };
+    // pieces (block, row) laid out block-major; piece offsets by an exclusive scan in that order
+    std::vector<int64_t> off(static_cast<size_t>(B) * R + 1, 0);
+#pragma omp parallel for schedule(dynamic, 4096)
+    for (int64_t r = 0; r < R; ++r)
+        for (int64_t e = rp[r]; e < rp[r + 1]; ++e) ++off[static_cast<size_t>(blk(cg[e])) * R + r + 1];
+    for (size_t i = 1; i < off.size(); ++i) off[i] += off[i - 1];
+    HVec<int32_t> hc(static_cast<size_t>(E));
+    HVec<double> hf(static_cast<size_t>(E));
+#pragma omp parallel for schedule(dynamic, 4096)
+    for (int64_t r = 0; r < R; ++r) {
+        int64_t pos[64];
+        for (int32_t b = 0; b < B; ++b) pos[b] = off[static_cast<size_t>(b) * R + r];
+        for (int64_t e = rp[r]; e < rp[r + 1]; ++e) {  // CSR order within each piece
+            const int32_t b = blk(cg[e]);
+            hc[pos[b]] = cg[e];
+            hf[pos[b]] = cf[e];
+            ++pos[b];
+        }
+    }
+    // ranges: each block's edges cut into one range per resident warp, so that the persistent
+    // grid (warp w takes ranges w, w + W, ...) walks the blocks roughly in lockstep and the
+    // concurrently gathered source rows stay within one block. Segments: the pieces in
+    // sequence, cut where a range boundary falls inside
+    const int32_t W = spmm_ranges_per_launch(), nr = W * B;
+    std::vector<int64_t> bnd(static_cast<size_t>(nr) + 1);
+    for (int32_t b = 0; b < B; ++b) {
+        const int64_t e0 = off[static_cast<size_t>(b) * R], e1 = off[static_cast<size_t>(b + 1) * R];
+        for (int32_t q = 0; q < W; ++q) bnd[static_cast<size_t>(b) * W + q] = e0 + (e1 - e0) * q / W;
+    }
+    bnd[nr] = E;
+    auto bound = [&](int64_t k) { return bnd[static_cast<size_t>(k)]; };
+    std::vector<int64_t> sb;
+    std::vector<int32_t> sr;
+    sb.reserve(static_cast<size_t>(B) * R + nr + 1);
+    sr.reserve(static_cast<size_t>(B) * R + nr + 1);
+    int64_t k = 1;
+    for (int64_t i = 0; i < static_cast<int64_t>(B) * R; ++i) {
+        const int64_t b0 = off[i], b1 = off[i + 1];
+        if (b0 == b1) continue;
+        const int32_t row = static_cast<int32_t>(i % R);
+        while (k < nr && bound(k) <= b0) ++k;
+        sb.push_back(b0);
+        sr.push_back(row);
+        for (; k < nr && bound(k) < b1; ++k)
+            if (sb.back() != bound(k)) {
+                sb.push_back(bound(k));
+                sr.push_back(row);
+            }
+    }
+    const int64_t nseg = static_cast<int64_t>(sr.size());
+    sb.push_back(E);
+    // slots: rows with more than one segment get one per segment; the row's slot list in
+    // sequence (block) order
+    std::vector<int32_t> rn(static_cast<size_t>(R), 0), r0(static_cast<size_t>(R), 0), ss(static_cast<size_t>(nseg));
+    for (int64_t s = 0; s < nseg; ++s) ++rn[sr[s]];
+    int64_t slots = 0, acc = 0;
+    for (int64_t r = 0; r < R; ++r) {
+        r0[r] = static_cast<int32_t>(acc);
+        acc += rn[r];
+    }
+    std::vector<int32_t> fill(r0), rs(static_cast<size_t>(acc));
+    for (int64_t s = 0; s < nseg; ++s) {
+        const int32_t r = sr[s];
+        ss[s] = rn[r] == 1 ? -1 : static_cast<int32_t>(slots++);
+        rs[fill[r]++] = ss[s];
+    }
+    std::vector<int32_t> ranges(static_cast<size_t>(nr) + 1);
+    {
+        int64_t s = 0;
+        ranges[0] = 0;
+        for (int32_t q = 1; q < nr; ++q) {
+            const int64_t t = bound(q);
+            while (s < nseg && sb[s] < t) ++s;
+            ranges[q] = static_cast<int32_t>(s);
+        }
+        ranges[nr] = static_cast<int32_t>(nseg);
+    }
+    seg_hoist.nranges = nr;
+    seg_hoist.split = true;
+    seg_hoist.total_slots = slots;
+    seg_hoist.seg_beg.upload(sb);
+    seg_hoist.seg_row.upload(sr);
+    seg_hoist.seg_slot.upload(ss);
+    seg_hoist.row_seg0.upload(r0);
+    seg_hoist.row_nseg.upload(rn);
+    seg_hoist.row_slots.upload(rs);
+    seg_hoist.ranges.upload(ranges);
+    hoist_cols.upload(hc);
+    hoist_coef.upload(hf);
+    partial_hoist.alloc(std::max<int64_t>(slots, 1) * pld_all);
 }
 
 void gasb_trainer_s::build_residual(const std::vector<int64_t>& h_arp, const HVec<int32_t>& h_asrc,

@@ -111,10 +111,12 @@ struct SegTable {
     bool split = false;  // rows cut at range boundaries (not the bit-exact sequential mode)
     std::vector<int64_t> group_seg0, group_nseg;  // per group (batch) range of segments
     int64_t max_group_slots = 0, total_slots = 0;
+    DevBuf<int32_t> row_slots;  // source-blocked tables: each row's partial slots in combine order
     SpmmSegs segs(int64_t g) const {
-        return SpmmSegs{seg_beg.p, seg_row.p, seg_slot.p, row_seg0.p, row_nseg.p, ranges.p + g * (nranges + 1),
-                        nranges,
-                        split ? 0 : 1};
+        SpmmSegs s{seg_beg.p, seg_row.p, seg_slot.p, row_seg0.p, row_nseg.p, ranges.p + g * (nranges + 1), nranges,
+                   split ? 0 : 1};
+        s.row_slots = row_slots.p;
+        return s;
     }
 };
 
@@ -398,6 +400,15 @@ struct gasb_trainer_s {
     void build(const float* h_features, const int32_t* h_labels, const uint8_t* h_train);
     void enqueue_batch(int32_t p, bool train, bool push, bool use_hoisted, bool fused, bool dp = false);
     void enqueue_hoisted();
+    // source-blocked hoisted layer 1 (GASB_HOIST_BLOCKS = B > 1, segmented mode): the epoch's
+    // edges reordered block-major by source id range, so a chunk pass walks one 1/B slice of X at
+    // a time (an L2-sized working set); every row's per-block pieces are fp64 partials combined in
+    // block order
+    SegTable seg_hoist;
+    DevBuf<int32_t> hoist_cols;
+    DevBuf<double> hoist_coef, partial_hoist;
+    void build_hoist_blocked(const std::vector<int64_t>& rp, const HVec<int32_t>& cg, const HVec<double>& cf,
+                             int32_t blocks);
     void run_epoch(int64_t epoch, bool shuffle, int32_t begin = 0, int32_t end = -1);
     // data-parallel mode (dp.cu): batches skip Adam and the step counters (applied after
     // the cross-rank exchange) and have their own per-part graphs

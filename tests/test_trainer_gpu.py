@@ -249,3 +249,20 @@ def test_epoch_report_activation_floats_linear_in_layers():
         peaks.append(tr.gas_epoch_report(0, shuffle=False)["peak_floats"])
     d = np.diff(peaks)
     assert (d > 0).all() and np.all(d[1:] == d[0]), peaks
+
+
+def test_source_blocked_hoist_matches(oracle, monkeypatch):
+    """GASB_HOIST_BLOCKS > 1 reorders each row's layer-1 edges into source blocks (split-row
+    segments, fp64 partials combined in segment order): same epochs as the unblocked hoist
+    and the oracle (DESIGN.md §3.3 records why it is off by default)."""
+    res = []
+    for hb in ("1", "4"):
+        monkeypatch.setenv("GASB_HOIST_BLOCKS", hb)
+        ds, sched, tr, so = _setup(oracle, "reddit_mini", fused=True, hoist_layer1=True, use_graphs=True)
+        losses = [tr.gas_epoch(ep) for ep in range(2)]
+        res.append((losses, tr.get_params()))
+    for ep in range(2):
+        lo, _ = so.epoch(ep)
+        assert abs(res[1][0][ep] - lo) / abs(lo) <= TOL
+    assert normwise(res[1][1], res[0][1]) <= 1e-6
+    assert normwise(res[1][1], so.get_params()) <= TOL
