@@ -7,13 +7,15 @@
 //   op 1: C[m,n] = A[m,k] B[n,k]^T  (A K-major, B K-major)    dgrad    dY·W^T
 //   op 2: C[m,n] = A[k,m]^T B[k,n]  (A MN-major, B MN-major)  wgrad    X^T·dY
 //
-// CTA = one 128 x BN output tile, 6 warps:
+// CTA = one 128 x BN output tile:
 //   warp 4 (1 thread)   TMA producer: fp32 A/B tiles of BK=32 into a 3-stage ring
-//   warps 0-3           split each landed tile in place into hi = tf32(x) and lo = x - hi
-//                       (exact), then the fused epilogue (TMEM -> registers -> global)
+//   warps 0-3, 6-7      split each landed tile in place into hi = tf32(x) and lo = x - hi (exact)
 //   warp 5 (1 thread)   MMA issuer: per k-step of 8, D += Ahi.Bhi + Ahi.Blo + Alo.Bhi
+//   warps 8-11          drain: sum each accumulator group out of TMEM as soon as it is final,
+//                       then the epilogue (staged through shared memory, coalesced stores)
+//   (TALL kernels, 2 CTAs/SM: no drain warps; warps 0-3 drain and store after the mainloop)
 // mbarriers: full (TMA -> split), split (split -> MMA), empty (tcgen05.commit -> TMA),
-// accum (last commit -> epilogue). Waits are bounded (trap instead of hang).
+// accready[g] (group g's last commit -> drain). Waits are bounded (trap instead of hang).
 #include <cstdlib>
 
 #include "gasb_internal.hpp"
@@ -43,30 +45,40 @@ static int num_sms() {
 }
 
 #ifdef GASB_GEMM_TIMING
-__device__ uint64_t g_gemm_stamps[40];
-extern "C" void gasb_debug_gemm_stamps(uint64_t* out) { cudaMemcpyFromSymbol(out, g_gemm_stamps, sizeof(uint64_t) * 40); }
+__device__ uint64_t g_gemm_stamps[40 + 2 * 256];  // + per-CTA (x + gridDim.x * y) start / end
+extern "C" void gasb_debug_gemm_stamps(uint64_t* out) {
+    cudaMemcpyFromSymbol(out, g_gemm_stamps, sizeof(uint64_t) * (40 + 2 * 256));
+}
 #endif
 namespace tc {
 
 #ifndef GASB_GEMM_STAGES
 #define GASB_GEMM_STAGES 3
 #endif
-#ifndef GASB_GEMM_LDGROUP
-#define GASB_GEMM_LDGROUP 2
-#endif
 #ifndef GASB_GEMM_MAXACC
 #define GASB_GEMM_MAXACC 8
 #endif
 constexpr int BM = 128, BK = 32, kStagesTC = GASB_GEMM_STAGES;
 #ifndef GASB_GEMM_SPLIT_HELPERS
-#define GASB_GEMM_SPLIT_HELPERS 4
+#define GASB_GEMM_SPLIT_HELPERS 2  // 4 measured slower with the drain warps (14 warps cap registers at 128)
 #endif
 #ifndef GASB_GEMM_KSTEPS_PER_ACC
 #define GASB_GEMM_KSTEPS_PER_ACC 1  // 16 cut the epilogue 3.8 -> 2.7 us but broke the 64-layer GCNII contract
 #endif
 constexpr int kSplitHelpers = GASB_GEMM_SPLIT_HELPERS;  // extra warps that only split tiles
 constexpr int kSplitThreads = 128 + 32 * kSplitHelpers;  // warps 0-3 + helpers
-constexpr int kThreads = 192 + 32 * kSplitHelpers;
+// non-TALL kernels add 4 drain warps (6 + kSplitHelpers ..): they sum each accumulator out of
+// TMEM as soon as the tensor core finishes it, concurrently with the split warps' shared-memory
+// work, then run the epilogue. TALL kernels (2 CTAs/SM, ~100 registers) have warps 0-3 drain
+// everything after the mainloop instead.
+template <bool TALL>
+__host__ __device__ constexpr int threads_of() {
+    return 192 + 32 * kSplitHelpers + (TALL ? 0 : 128);
+}
+template <bool TALL>
+__host__ __device__ constexpr int alloc_warp() {  // the warp that allocates (and frees) TMEM: an epilogue warp
+    return TALL ? 0 : 6 + kSplitHelpers;
+}
 // The tensor core's fp32 accumulation truncates, so its error grows linearly with the number
 // of k-steps; k-steps are interleaved over kAcc TMEM accumulators (kAcc * BN <= 512 columns)
 // summed round-to-nearest in the epilogue, cutting that growth kAcc-fold.
@@ -161,16 +173,17 @@ struct Layout {
     static constexpr int kTileB = BN * BK * 4;
     // stage: A, A_lo, B, B_lo (each 1024 B aligned: SW128 atoms)
     static constexpr int kStage = 2 * kTileA + 2 * kTileB;
-    static constexpr int kBars = 8 * (3 * kStages + 1);
+    static constexpr int kBars = 8 * (3 * kStages + GASB_GEMM_MAXACC);
     static constexpr int kSmem = 1024 + kStages * kStage + kBars + 16;
 };
 
 template <int BN, bool A_MN, bool B_MN, bool TALL>
-__global__ void __launch_bounds__(kThreads, TALL ? 2 : 1) gemm_tc_kernel(const __grid_constant__ CUtensorMap tma_a,
+__global__ void __launch_bounds__(threads_of<TALL>(), TALL ? 2 : 1) gemm_tc_kernel(const __grid_constant__ CUtensorMap tma_a,
                                                              const __grid_constant__ CUtensorMap tma_b, int M,
                                                              int N, int K, float* __restrict__ C, int64_t ldc,
                                                              GemmEpilogue ep, int kbs, float* __restrict__ ws,
-                                                             int64_t ws_floats, int serial_fixup) {
+                                                             int64_t ws_floats, int serial_fixup,
+                                                             int acc_groups) {
     const PushEpilogue& push = ep.push;
     using Lay = Layout<BN, A_MN, B_MN, TALL>;
     constexpr int kStagesTC = Lay::kStages;
@@ -180,8 +193,8 @@ __global__ void __launch_bounds__(kThreads, TALL ? 2 : 1) gemm_tc_kernel(const _
     uint64_t* full = bars;
     uint64_t* split = bars + kStagesTC;
     uint64_t* empty = bars + 2 * kStagesTC;
-    uint64_t* accum = bars + 3 * kStagesTC;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * kStagesTC + 1);
+    uint64_t* accready = bars + 3 * kStagesTC;  // one per accumulator group: its last MMA completed
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * kStagesTC + Acc<BN, TALL>::kAcc);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
@@ -194,6 +207,14 @@ __global__ void __launch_bounds__(kThreads, TALL ? 2 : 1) gemm_tc_kernel(const _
         }
     };
     if (threadIdx.x == 0) stamp(0);
+#ifdef GASB_GEMM_TIMING
+    const int cta_id = blockIdx.x + gridDim.x * blockIdx.y;
+    if (threadIdx.x == 0 && blockIdx.z == 0 && cta_id < 256) {
+        uint64_t t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        g_gemm_stamps[40 + 2 * cta_id] = t;
+    }
+#endif
 #else
     auto stamp = [](int) {};
 #endif
@@ -206,6 +227,16 @@ __global__ void __launch_bounds__(kThreads, TALL ? 2 : 1) gemm_tc_kernel(const _
     // mean fewer TMEM reads in the epilogue
     const int nacc = min(Acc<BN, TALL>::kAcc, max(1, (nk * (BK / 8) + GASB_GEMM_KSTEPS_PER_ACC - 1) /
                                                          GASB_GEMM_KSTEPS_PER_ACC));
+    // Accumulator groups: the k-steps are cut into `ng` contiguous blocks, and the k-steps of
+    // block j are interleaved over the accumulators of group j (nacc / ng of them: consecutive
+    // MMAs then write different accumulators, which keeps the tensor core's pipeline full).
+    // A group is final once its last k-step's MMAs complete, so the drain warps sum it out of
+    // TMEM (in accumulator order) while later groups are still in the tensor core, instead of
+    // reading every accumulator after the last MMA (TMEM reads run at ~64 B/clk).
+    const int nsteps_all = nk * (BK / 8);
+    const int ng = (acc_groups > 0 && nacc % acc_groups == 0) ? acc_groups : 1;
+    const int per_g = nacc / ng;
+    auto group_first = [&](int j) { return (j * nsteps_all + ng - 1) / ng; };  // first k-step of block j
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < kStagesTC; ++s) {
@@ -213,10 +244,10 @@ __global__ void __launch_bounds__(kThreads, TALL ? 2 : 1) gemm_tc_kernel(const _
             bar_init(split + s, kSplitThreads);
             bar_init(empty + s, 1);
         }
-        bar_init(accum, 1);
+        for (int q = 0; q < Acc<BN, TALL>::kAcc; ++q) bar_init(accready + q, 1);
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
-    if (warp == 0) {  // TMEM: BN fp32 columns x 128 lanes
+    if (warp == alloc_warp<TALL>()) {  // TMEM: kAcc accumulators of BN fp32 columns x 128 lanes
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(su32(tmem_slot)),
                      "r"(Acc<BN, TALL>::kCols));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
@@ -227,6 +258,8 @@ __global__ void __launch_bounds__(kThreads, TALL ? 2 : 1) gemm_tc_kernel(const _
     const uint32_t tmem = *tmem_slot;
     if (threadIdx.x == 0) stamp(1);
 
+    const bool drainer = !TALL && warp >= 6 + kSplitHelpers;
+    const int etid = (warp & 3) * 32 + lane;  // epilogue thread: TMEM lane == tile row
     if (warp == 4) {
         // ---------------- TMA producer ----------------
         if (lane == 0) {
@@ -254,6 +287,9 @@ __global__ void __launch_bounds__(kThreads, TALL ? 2 : 1) gemm_tc_kernel(const _
         // ---------------- MMA issuer ----------------
         if (lane == 0) {
             constexpr uint32_t idesc = instr_desc(BN, A_MN, B_MN);
+            // (group, position in group) tracked incrementally: the single issuing thread is on
+            // the critical path, so no divisions per k-step
+            int j = 0, r = 0, rq = 0, gnext = group_first(1);
             for (int kb = 0; kb < nk; ++kb) {
                 const int s = kb % kStagesTC;
                 bar_wait(split + s, (kb / kStagesTC) & 1);
@@ -277,21 +313,62 @@ __global__ void __launch_bounds__(kThreads, TALL ? 2 : 1) gemm_tc_kernel(const _
                     const uint64_t alo = smem_desc(sa_lo + offa, lboa, sboa, lya);
                     const uint64_t bhi = smem_desc(sb + offb, lbob, sbob, lyb);
                     const uint64_t blo = smem_desc(sb_lo + offb, lbob, sbob, lyb);
-                    const int g = kb * (BK / 8) + kk;  // global k-step -> accumulator g % nacc
-                    const uint32_t d = tmem + static_cast<uint32_t>((g % nacc) * BN);
-                    const uint32_t first = g < nacc ? 0u : 1u;
+                    const int g = kb * (BK / 8) + kk;  // global k-step: accumulator j * per_g + r % per_g
+                    const uint32_t d = tmem + static_cast<uint32_t>((j * per_g + rq) * BN);
+                    const uint32_t first = r < per_g ? 0u : 1u;
                     mma_tf32(d, ahi, bhi, idesc, first);
+#ifndef GASB_GEMM_DBG_ONEMMA  // (timing experiments only: plain TF32)
                     mma_tf32(d, ahi, blo, idesc, 1u);
                     mma_tf32(d, alo, bhi, idesc, 1u);
+#endif
+                    ++r;
+                    rq = rq + 1 == per_g ? 0 : rq + 1;
+                    if (g + 1 == gnext) {  // the group's last k-step: final once these MMAs complete
+                        mma_commit(accready + j);
+                        ++j;
+                        r = rq = 0;
+                        gnext = group_first(j + 1);
+                    }
                 }
                 mma_commit(empty + s);  // frees the stage once these MMAs have read it
             }
-            mma_commit(accum);
         }
     } else {
-        // ---------------- split (warps 0-3 and the helper warps 6+), then epilogue (0-3) ----------------
-        const int sid = warp < 4 ? threadIdx.x : threadIdx.x - 64;  // 0 .. kSplitThreads-1
-        for (int kb = 0; kb < nk; ++kb) {
+        // ------- split (warps 0-3 and the helper warps 6+); drain + epilogue (drain warps / TALL: 0-3) -------
+        const int sid = warp < 4 ? threadIdx.x : threadIdx.x - 64;  // split thread 0 .. kSplitThreads-1
+        // warps 0-3: the tile row's sums over the drained accumulators (TMEM lane == tile row).
+        // TALL (2 CTAs/SM, ~100 registers): 32 columns at a time, all accumulators at the end
+        constexpr int kSum = TALL ? 32 : BN;
+        float sum[kSum];
+        const uint32_t tlane = tmem + (static_cast<uint32_t>((warp & 3) * 32) << 16);
+        auto drain = [&](int q, int cb) {  // sum[0 .. kSum) += accumulator q, columns cb ..
+            asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+            constexpr int kG = 32;  // columns per tcgen05.wait::ld (64 spills at 448 threads)
+#pragma unroll
+            for (int c0 = 0; c0 < kSum; c0 += kG) {
+                uint32_t v[kG];
+#pragma unroll
+                for (int c1 = 0; c1 < kG; c1 += 32) {
+                    const uint32_t taddr = tlane + static_cast<uint32_t>(q * BN + cb + c0 + c1);
+                    asm volatile(
+                        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+                        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+                        : "=r"(v[c1 + 0]), "=r"(v[c1 + 1]), "=r"(v[c1 + 2]), "=r"(v[c1 + 3]), "=r"(v[c1 + 4]),
+                          "=r"(v[c1 + 5]), "=r"(v[c1 + 6]), "=r"(v[c1 + 7]), "=r"(v[c1 + 8]), "=r"(v[c1 + 9]),
+                          "=r"(v[c1 + 10]), "=r"(v[c1 + 11]), "=r"(v[c1 + 12]), "=r"(v[c1 + 13]), "=r"(v[c1 + 14]),
+                          "=r"(v[c1 + 15]), "=r"(v[c1 + 16]), "=r"(v[c1 + 17]), "=r"(v[c1 + 18]), "=r"(v[c1 + 19]),
+                          "=r"(v[c1 + 20]), "=r"(v[c1 + 21]), "=r"(v[c1 + 22]), "=r"(v[c1 + 23]), "=r"(v[c1 + 24]),
+                          "=r"(v[c1 + 25]), "=r"(v[c1 + 26]), "=r"(v[c1 + 27]), "=r"(v[c1 + 28]), "=r"(v[c1 + 29]),
+                          "=r"(v[c1 + 30]), "=r"(v[c1 + 31])
+                        : "r"(taddr));
+                }
+                asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+                for (int j = 0; j < kG; ++j)
+                    sum[c0 + j] = q == 0 ? __uint_as_float(v[j]) : __fadd_rn(sum[c0 + j], __uint_as_float(v[j]));
+            }
+        };
+        for (int kb = 0; kb < (drainer ? 0 : nk); ++kb) {
             const int s = kb % kStagesTC;
             bar_wait(full + s, (kb / kStagesTC) & 1);
             if (threadIdx.x == 0 && kb == 0) stamp(2);
@@ -316,6 +393,8 @@ __global__ void __launch_bounds__(kThreads, TALL ? 2 : 1) gemm_tc_kernel(const _
                 blo[i] = make_float4(tf32_hi(v.x - tf32_tr(v.x)), tf32_hi(v.y - tf32_tr(v.y)), tf32_hi(v.z - tf32_tr(v.z)),
                                      tf32_hi(v.w - tf32_tr(v.w)));
             }
+#elif defined(GASB_GEMM_DBG_NOSPLIT)  // (timing experiments only: no split)
+            (void)alo, (void)blo, (void)sid;
 #else
             // hi = rn_tf32(x), lo = rn_tf32(x - hi): both exactly tf32, so the tensor core's
             // operand truncation changes nothing; dropped lo*lo term ~2^-22 relative
@@ -336,91 +415,75 @@ __global__ void __launch_bounds__(kThreads, TALL ? 2 : 1) gemm_tc_kernel(const _
             if (threadIdx.x == 0 && kb < 8) stamp(16 + kb);
             bar_arrive(split + s);
         }
-        if (warp < 4) {  // epilogue: TMEM lane == tile row
-            bar_wait(accum, 0);
-            if (threadIdx.x == 0) stamp(3);
-            asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-            const int row = m0 + warp * 32 + lane;  // TMEM lane == tile row
-            float* crow = row < M ? C + static_cast<int64_t>(row) * ldc : nullptr;
-            float* prow = nullptr;
-            if (crow && push.table && !ws) {
-                const int32_t id = push.ids[row];
-                prow = push.table + static_cast<int64_t>(id) * push.ld;
-                if (blockIdx.y == 0 && push.stamps) push.stamps[id] = *push.step;
+        if (drainer || (TALL && warp < 4)) {
+            for (int j = 0; j < ng; ++j) {  // in accumulator order, each group as soon as it is final
+                bar_wait(accready + j, 0);  // (a backed-off poll measured the same)
+                if (!TALL)
+                    for (int q = j * per_g; q < (j + 1) * per_g; ++q) drain(q, 0);
             }
-            int32_t flags = 0;
-            const int nsteps = nk * (BK / 8);
-
-    #pragma unroll 1
+            if (etid == 0) stamp(3);
+            // phase 1: each thread (= tile row) parks its raw sums in shared memory (the stage
+            // buffers are free: every MMA has completed), 16 B chunk c of row r at chunk position
+            // c ^ (r mod kChunks) so that 8 consecutive rows hit distinct banks
+            constexpr int kChunks = BN / 4;
+            float4* stg = reinterpret_cast<float4*>(base);
+    #pragma unroll
             for (int c0 = 0; c0 < BN; c0 += 32) {
-                float sum[32];
-                // the accumulators' TMEM loads in groups of kLdGroup, one tcgen05.wait::ld per group
-                // (each wait costs a full TMEM round trip); summed in accumulator order as before
-                constexpr int kLdGroup = TALL ? 1 : GASB_GEMM_LDGROUP;
-    #pragma unroll 1
-                for (int q0 = 0; q0 < nacc; q0 += kLdGroup) {
-                    uint32_t v[kLdGroup][32];
+                if (TALL)
+                    for (int q = 0; q < nacc; ++q) drain(q, c0);
+                const int cs = TALL ? 0 : c0;  // this chunk's offset in sum[]
     #pragma unroll
-                    for (int g = 0; g < kLdGroup; ++g) {
-                        if (q0 + g >= nacc) break;
-                        const uint32_t taddr = tmem + (static_cast<uint32_t>(warp * 32) << 16) +
-                                               static_cast<uint32_t>((q0 + g) * BN + c0);
-                        asm volatile(
-                            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-                            "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
-                            : "=r"(v[g][0]), "=r"(v[g][1]), "=r"(v[g][2]), "=r"(v[g][3]), "=r"(v[g][4]), "=r"(v[g][5]),
-                              "=r"(v[g][6]), "=r"(v[g][7]), "=r"(v[g][8]), "=r"(v[g][9]), "=r"(v[g][10]), "=r"(v[g][11]),
-                              "=r"(v[g][12]), "=r"(v[g][13]), "=r"(v[g][14]), "=r"(v[g][15]), "=r"(v[g][16]),
-                              "=r"(v[g][17]), "=r"(v[g][18]), "=r"(v[g][19]), "=r"(v[g][20]), "=r"(v[g][21]),
-                              "=r"(v[g][22]), "=r"(v[g][23]), "=r"(v[g][24]), "=r"(v[g][25]), "=r"(v[g][26]),
-                              "=r"(v[g][27]), "=r"(v[g][28]), "=r"(v[g][29]), "=r"(v[g][30]), "=r"(v[g][31])
-                            : "r"(taddr));
+                for (int j = 0; j < 32; j += 4)
+                    stg[etid * kChunks + (((c0 + j) >> 2) ^ (etid & (kChunks - 1)))] =
+                        make_float4(sum[cs + j], sum[cs + j + 1], sum[cs + j + 2], sum[cs + j + 3]);
+            }
+            {
+                const int row = m0 + etid;
+                if (row < M && push.table && push.stamps && !ws && blockIdx.y == 0) push.stamps[push.ids[row]] = *push.step;
+            }
+            __syncwarp();
+            // phase 2: the warp stores its 32 rows coalesced (kChunks lanes per row, 16 B each),
+            // applying the epilogue (scale, beta, bias, relu) and the history push on the way
+            int32_t flags = 0;
+            {
+                const bool v4 = ((ldc & 3) == 0) && ((reinterpret_cast<uintptr_t>(C) & 15) == 0) &&
+                                (!push.table || ((push.ld & 3) == 0 && (reinterpret_cast<uintptr_t>(push.table) & 15) == 0));
+                const int Np = (N + 3) & ~3;  // split-K partial row pitch
+                const int ch = lane % kChunks, c = n0 + 4 * ch;
+    #pragma unroll 2
+                for (int i = lane / kChunks; i < 32; i += 32 / kChunks) {
+                    const int lr = (warp & 3) * 32 + i, r = m0 + lr;
+                    const float4 s4 = stg[lr * kChunks + (ch ^ (lr & (kChunks - 1)))];
+                    if (r >= M) continue;
+                    if (ws) {  // slice partial: raw sums
+                        if (c < Np)
+                            *reinterpret_cast<float4*>(ws + (static_cast<int64_t>(blockIdx.z) * M + r) * Np + c) = s4;
+                        continue;
                     }
-                    asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-    #pragma unroll
-                    for (int g = 0; g < kLdGroup; ++g) {
-                        if (q0 + g >= nacc) break;
-    #pragma unroll
-                        for (int j = 0; j < 32; ++j)
-                            sum[j] = q0 + g == 0 ? __uint_as_float(v[g][j]) : __fadd_rn(sum[j], __uint_as_float(v[g][j]));
-                    }
-                }
-                if (crow && ws) {  // slice partial, row pitch Np = N rounded up to 4 (float4 stores)
-                    const int Np = (N + 3) & ~3;
-                    float4* wrow = reinterpret_cast<float4*>(ws + (static_cast<int64_t>(blockIdx.z) * M + row) * Np);
-    #pragma unroll
-                    for (int j = 0; j < 32; j += 4)
-                        if (n0 + c0 + j < Np) wrow[(n0 + c0 + j) >> 2] = make_float4(sum[j], sum[j + 1], sum[j + 2], sum[j + 3]);
-                } else if (crow) {
-                    // 16 B stores where the row pitch allows (a thread owns one output row: scalar
-                    // stores would cost one instruction per 4 B)
-                    const bool v4 = ((ldc & 3) == 0) && ((reinterpret_cast<uintptr_t>(C) & 15) == 0) &&
-                                    (!prow || ((push.ld & 3) == 0 && (reinterpret_cast<uintptr_t>(push.table) & 15) == 0));
-    #pragma unroll
-                    for (int j = 0; j < 32; j += 4) {
-                        const int col = n0 + c0 + j;
-                        if (v4 && col + 3 < N) {
-                            float4 x;
-                            x.x = gemm_epilogue_value(ep, sum[j], crow, col);
-                            x.y = gemm_epilogue_value(ep, sum[j + 1], crow, col + 1);
-                            x.z = gemm_epilogue_value(ep, sum[j + 2], crow, col + 2);
-                            x.w = gemm_epilogue_value(ep, sum[j + 3], crow, col + 3);
-                            *reinterpret_cast<float4*>(crow + col) = x;
-                            if (prow) {
-                                *reinterpret_cast<float4*>(prow + col) = x;
-                                flags |= table_flag_of(x.x) | table_flag_of(x.y) | table_flag_of(x.z) | table_flag_of(x.w);
-                            }
-                            continue;
+                    float* cr = C + static_cast<int64_t>(r) * ldc;
+                    float* pr = push.table ? push.table + static_cast<int64_t>(push.ids[r]) * push.ld : nullptr;
+                    if (v4 && c + 3 < N) {
+                        float4 x;
+                        x.x = gemm_epilogue_value(ep, s4.x, cr, c);
+                        x.y = gemm_epilogue_value(ep, s4.y, cr, c + 1);
+                        x.z = gemm_epilogue_value(ep, s4.z, cr, c + 2);
+                        x.w = gemm_epilogue_value(ep, s4.w, cr, c + 3);
+                        *reinterpret_cast<float4*>(cr + c) = x;
+                        if (pr) {
+                            *reinterpret_cast<float4*>(pr + c) = x;
+                            flags |= table_flag_of(x.x) | table_flag_of(x.y) | table_flag_of(x.z) | table_flag_of(x.w);
                         }
+                        continue;
+                    }
+                    const float xs[4] = {s4.x, s4.y, s4.z, s4.w};
     #pragma unroll
-                        for (int q = 0; q < 4; ++q) {
-                            if (col + q < N) {
-                                const float x = gemm_epilogue_value(ep, sum[j + q], crow, col + q);
-                                crow[col + q] = x;
-                                if (prow) {
-                                    prow[col + q] = x;
-                                    flags |= table_flag_of(x);
-                                }
+                    for (int q = 0; q < 4; ++q) {
+                        if (c + q < N) {
+                            const float x = gemm_epilogue_value(ep, xs[q], cr, c + q);
+                            cr[c + q] = x;
+                            if (pr) {
+                                pr[c + q] = x;
+                                flags |= table_flag_of(x);
                             }
                         }
                     }
@@ -433,7 +496,7 @@ __global__ void __launch_bounds__(kThreads, TALL ? 2 : 1) gemm_tc_kernel(const _
                 // in slice order (deterministic, independent of arrival order)
                 __threadfence();
                 asm volatile("bar.sync 1, 128;\n" ::: "memory");
-                if (warp == 0) {
+                if (warp == alloc_warp<TALL>()) {
                     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem),
                                  "r"(Acc<BN, TALL>::kCols));
                 }
@@ -443,14 +506,14 @@ __global__ void __launch_bounds__(kThreads, TALL ? 2 : 1) gemm_tc_kernel(const _
                 if (serial_fixup) {
                     // serial fixup: no CTA ever waits; the last slice to arrive reduces the whole
                     // tile (in slice order), so any number of split-K grids may be in flight
-                    if (threadIdx.x == 0) {
+                    if (etid == 0) {
                         const int prev = atomicAdd(arrive, 1);
                         last_flag = prev == S - 1;
                         if (last_flag) __threadfence();
                     }
                     asm volatile("bar.sync 1, 128;\n" ::: "memory");
                     if (!last_flag) goto fixup_done;
-                } else if (threadIdx.x == 0) {
+                } else if (etid == 0) {
                     atomicAdd(arrive, 1);
                     for (uint32_t spins = 0;; ++spins) {
                         int v;
@@ -467,7 +530,7 @@ __global__ void __launch_bounds__(kThreads, TALL ? 2 : 1) gemm_tc_kernel(const _
                 const int rows_per = serial_fixup ? BM : (BM + S - 1) / S;
                 const int rlo = serial_fixup ? 0 : blockIdx.z * rows_per, rhi = min(BM, rlo + rows_per);
                 constexpr int kQ = BN / 4;  // float4 quads per tile row
-                for (int idx = threadIdx.x; idx < (rhi - rlo) * kQ; idx += 128) {
+                for (int idx = etid; idx < (rhi - rlo) * kQ; idx += 128) {
                     const int r = m0 + rlo + idx / kQ, c = n0 + 4 * (idx % kQ);
                     if (r >= M || c >= N) continue;
                     const float4* wp = reinterpret_cast<const float4*>(ws + static_cast<int64_t>(r) * Np + c);
@@ -492,8 +555,8 @@ __global__ void __launch_bounds__(kThreads, TALL ? 2 : 1) gemm_tc_kernel(const _
                     if (pr && c == 0 && push.stamps) push.stamps[push.ids[r]] = *push.step;
                 }
                 if (serial_fixup) {
-                    if (threadIdx.x == 0) arrive[0] = 0;  // the only CTA left on this tile
-                } else if (threadIdx.x == 0 && atomicAdd(arrive + 1, 1) == S - 1) {  // last to leave resets
+                    if (etid == 0) arrive[0] = 0;  // the only CTA left on this tile
+                } else if (etid == 0 && atomicAdd(arrive + 1, 1) == S - 1) {  // last to leave resets
                     arrive[0] = 0;
                     arrive[1] = 0;
                 }
@@ -506,13 +569,20 @@ __global__ void __launch_bounds__(kThreads, TALL ? 2 : 1) gemm_tc_kernel(const _
             }
         }
     }
-    if (threadIdx.x == 0) stamp(4);
+    if ((drainer || (TALL && warp < 4)) && etid == 0) stamp(4);
     asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
     __syncthreads();
-    if (warp == 0 && !ws) {  // (split-K CTAs freed their TMEM before the fixup)
+    if (warp == alloc_warp<TALL>() && !ws) {  // (split-K CTAs freed their TMEM before the fixup)
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(Acc<BN, TALL>::kCols));
     }
+#ifdef GASB_GEMM_TIMING
+    if (threadIdx.x == 0 && blockIdx.z == 0 && cta_id < 256) {
+        uint64_t t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        g_gemm_stamps[41 + 2 * cta_id] = t;
+    }
+#endif
 }
 
 // 2-D fp32 tensor map for TMA with 128 B swizzle: contiguous dim `inner` (elements), `outer`
@@ -568,12 +638,17 @@ static bool launch_tc(int m, int n, int k, const float* a, int64_t lda, const fl
         while (S > 1 && static_cast<int64_t>(S) * m * round_up(n, 4) > t_gemm_ws_floats) --S;
         if (2 * tiles > kGemmTileCounters) S = 1;
     }
+    static const int acc_groups = [] {  // GASB_GEMM_ACC_GROUPS: accumulator groups (1 = drain after the mainloop)
+        const char* e = getenv("GASB_GEMM_ACC_GROUPS");
+        return e ? std::max(1, atoi(e)) : 2;
+    }();
     const int kbs = static_cast<int>(ceil_div(nkb, S));
     S = static_cast<int>(ceil_div(nkb, kbs));  // no empty slices
     dim3 grid(static_cast<unsigned>(ceil_div(m, BM)), static_cast<unsigned>(ceil_div(n, BN)), static_cast<unsigned>(S));
-    gemm_tc_kernel<BN, A_MN, B_MN, TALL><<<grid, kThreads, Lay::kSmem, st>>>(ta, tb, m, n, k, c, ldc, ep, kbs,
+    gemm_tc_kernel<BN, A_MN, B_MN, TALL><<<grid, threads_of<TALL>(), Lay::kSmem, st>>>(ta, tb, m, n, k, c, ldc, ep, kbs,
                                                                         S > 1 ? t_gemm_ws : nullptr,
-                                                                        t_gemm_ws_floats, t_gemm_serial ? 1 : 0);
+                                                                        t_gemm_ws_floats, t_gemm_serial ? 1 : 0,
+                                                                        acc_groups);
     return true;
 }
 
