@@ -256,6 +256,8 @@ __global__ void __launch_bounds__(threads_of<TALL>(), TALL ? 2 : 1) gemm_tc_kern
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
     const uint32_t tmem = *tmem_slot;
+    pdl_trigger();
+    pdl_wait();  // (PDL) the setup above touched no global memory; A and C belong to earlier kernels
     if (threadIdx.x == 0) stamp(1);
 
     const bool drainer = !TALL && warp >= 6 + kSplitHelpers;
@@ -645,10 +647,8 @@ static bool launch_tc(int m, int n, int k, const float* a, int64_t lda, const fl
     const int kbs = static_cast<int>(ceil_div(nkb, S));
     S = static_cast<int>(ceil_div(nkb, kbs));  // no empty slices
     dim3 grid(static_cast<unsigned>(ceil_div(m, BM)), static_cast<unsigned>(ceil_div(n, BN)), static_cast<unsigned>(S));
-    gemm_tc_kernel<BN, A_MN, B_MN, TALL><<<grid, threads_of<TALL>(), Lay::kSmem, st>>>(ta, tb, m, n, k, c, ldc, ep, kbs,
-                                                                        S > 1 ? t_gemm_ws : nullptr,
-                                                                        t_gemm_ws_floats, t_gemm_serial ? 1 : 0,
-                                                                        acc_groups);
+    launch_pdl(gemm_tc_kernel<BN, A_MN, B_MN, TALL>, grid, dim3(threads_of<TALL>()), Lay::kSmem, st, ta, tb, m, n, k, c,
+               ldc, ep, kbs, S > 1 ? t_gemm_ws : nullptr, t_gemm_ws_floats, t_gemm_serial ? 1 : 0, acc_groups);
     return true;
 }
 

@@ -18,6 +18,17 @@ namespace gasb {
 
 thread_local int64_t t_launches = 0;
 
+bool pdl_enabled() {
+    static const bool on = [] {
+        const char* e = getenv("GASB_PDL");  // off by default: C3 epoch 103.5 (off) vs 104.3 ms (on)
+        return e && atoi(e) != 0;
+    }();
+    return on;
+}
+void check_launch(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
 // One warp moves R rows per round; each lane moves float4 (VEC=4) or float (VEC=1) columns.
 // All loads of a round are issued before its stores to keep R*dim/128 requests in flight.
 template <int VEC, int R>

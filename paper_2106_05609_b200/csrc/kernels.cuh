@@ -19,6 +19,33 @@ inline int64_t round_up(int64_t a, int64_t b) { return ceil_div(a, b) * b; }
 // Counts kernel launches issued through these helpers (gpu_launches evidence).
 extern thread_local int64_t t_launches;
 
+// Programmatic dependent launch (PDL). The kernels of the per-batch chain are launched with
+// programmatic stream serialization: the next kernel's grid is set up, and its CTAs become
+// resident as SMs free up (running any prologue that touches no global memory), while this
+// one drains. Every kernel launched this way calls pdl_wait() in every CTA before its first
+// global-memory access. pdl_wait() returns once the preceding grid has completed and its
+// writes are visible, so the chain stays transitively ordered. pdl_trigger() lets the
+// dependent grid launch. Both are no-ops for a normal launch. Opt-in (GASB_PDL=1): measured
+// no faster at C3 (the per-batch graph's launch gaps are already small), GPU suite green with it.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
+bool pdl_enabled();
+void check_launch(cudaError_t e, const char* what);
+template <typename... KArgs, typename... Args>
+inline void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    check_launch(cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...), "launch_pdl");
+}
+
 // Per-table value flags (device int32, OR-accumulated by every producer of a table that the
 // SpMM reads): they pick the fp32 -> fp64 widening path of the forward SpMM (spmm.cu).
 constexpr int32_t kTableNeg = 1;        // some value has its sign bit set

@@ -99,6 +99,8 @@ __global__ void __launch_bounds__(256) colsum_kernel(const float* __restrict__ g
 __global__ void mask_kernel(float* __restrict__ g, int64_t ldg, const float* __restrict__ mask, int64_t ldm,
                             int32_t m, int32_t n) {
     // one warp per row (grid-stride), lanes across the columns: no per-element division
+    pdl_trigger();
+    pdl_wait();
     const int lane = threadIdx.x & 31;
     for (int64_t r = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; r < m;
          r += (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5)
@@ -202,7 +204,7 @@ void launch_colsum(const float* g, int64_t ldg, int32_t m, int32_t n, float* out
 void launch_mask(float* g, int64_t ldg, const float* mask, int64_t ldm, int32_t m, int32_t n, cudaStream_t st) {
     const int64_t total = static_cast<int64_t>(m) * n;
     if (total <= 0) return;
-    mask_kernel<<<grid_for(total, 256), 256, 0, st>>>(g, ldg, mask, ldm, m, n);
+    launch_pdl(mask_kernel, dim3(grid_for(total, 256)), dim3(256), 0, st, g, ldg, mask, ldm, m, n);
     ++t_launches;
     GASB_CUDA(cudaGetLastError());
 }

@@ -856,6 +856,7 @@ __global__ void __launch_bounds__(kPipeWarps * 32, kPipeCtas) spmm_fwd_flat_kern
     const int32_t* __restrict__ slot_list, const __grid_constant__ CUtensorMap tmap) {
     using Cfg = PipeCfg<CPL>;
     extern __shared__ __align__(128) unsigned char smem_raw[];
+    pdl_trigger();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     unsigned char* wbase = smem_raw + static_cast<size_t>(warp) * kStages * Cfg::kStageBytes;
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + kPipeWarps * kStages * Cfg::kStageBytes) + warp * kStages;
@@ -869,6 +870,7 @@ __global__ void __launch_bounds__(kPipeWarps * 32, kPipeCtas) spmm_fwd_flat_kern
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     __syncwarp();
+    pdl_wait();  // (PDL) everything below reads the previous kernels' outputs
     const int mode = widen_mode(table_flags);
 #define GASB_FLAT(M)                                                                                              \
     flat_items<CPL, M, DUAL>(seg_beg, seg_row, seg_slot, row_seg0, row_nseg, range_seg, nranges, cols, coeffs, dim, nchunks, \
@@ -902,10 +904,10 @@ static void launch_flat(const SpmmSegs& s, const int32_t* cols, const double* co
     }
     const int64_t items = static_cast<int64_t>(nchunks) * s.nranges;
     const int64_t blocks = std::min<int64_t>(ceil_div(items, kPipeWarps), static_cast<int64_t>(kPipeCtas) * sms);
-    spmm_fwd_flat_kernel<CPL, DUAL><<<static_cast<unsigned>(blocks), kPipeWarps * 32, kSmem, st>>>(
-        s.seg_beg, s.seg_row, s.seg_slot, s.row_seg0, s.row_nseg, s.range_seg, s.nranges, cols, coeffs, dim, nchunks,
-        y, ldy, row_base, partial, partial_ld, counters, counters_ld, special, s.row_slots ? s.row_slots : s.seg_slot,
-        *tmap);
+    launch_pdl(spmm_fwd_flat_kernel<CPL, DUAL>, dim3(static_cast<unsigned>(blocks)), dim3(kPipeWarps * 32), kSmem, st,
+               s.seg_beg, s.seg_row, s.seg_slot, s.row_seg0, s.row_nseg, s.range_seg, s.nranges, cols, coeffs, dim,
+               nchunks, y, ldy, row_base, partial, partial_ld, counters, counters_ld, special,
+               s.row_slots ? s.row_slots : s.seg_slot, *tmap);
 }
 
 static int g_pipe_smem_set[2][2] = {};
@@ -1222,6 +1224,8 @@ __global__ void __launch_bounds__(kBwdThreads) spmm_bwd_smem_kernel(
     int64_t ldm, float* __restrict__ gx, int64_t ldgx, int32_t targets_per_cta, int accumulate, const int32_t* __restrict__ order) {
     extern __shared__ float sg[];  // nsrc x kBwdCW, then 32 (offset, coeff) pairs per warp
     __shared__ int32_t s_next;
+    pdl_trigger();
+    pdl_wait();
     if (threadIdx.x == 0) s_next = 0;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
     const int32_t col0 = blockIdx.x * kBwdCW;
@@ -1358,8 +1362,8 @@ void launch_spmm_bwd(const int64_t* t_rowptr, int32_t nt, const int32_t* t_src, 
         const int32_t splits = static_cast<int32_t>(
             std::max<int64_t>(1, std::min<int64_t>(sms / nchunks, ceil_div(nt, kBwdThreads / 32))));
         dim3 grid(static_cast<unsigned>(nchunks), static_cast<unsigned>(splits));
-        kern<<<grid, kBwdThreads, smem, st>>>(t_rowptr, nt, t_src, t_coeffs, gy, ldgy, nsrc, dim, mask, ldm, gx, ldgx,
-                                              splits, accumulate ? 1 : 0, order);
+        launch_pdl(kern, grid, dim3(kBwdThreads), smem, st, t_rowptr, nt, t_src, t_coeffs, gy, ldgy, nsrc, dim, mask,
+                   ldm, gx, ldgx, splits, accumulate ? 1 : 0, order);
         ++t_launches;
         GASB_CUDA(cudaGetLastError());
         return;

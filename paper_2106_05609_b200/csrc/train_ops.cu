@@ -26,6 +26,8 @@ __global__ void __launch_bounds__(kCeThreads) softmax_ce_kernel(const float* __r
                                                                 int32_t* __restrict__ done) {
     __shared__ double red[kCeThreads];
     __shared__ int last;
+    pdl_trigger();
+    pdl_wait();
     const int lane = threadIdx.x & 31;
     const int32_t i = blockIdx.x * (kCeThreads / 32) + (threadIdx.x >> 5);
     const float inv_m = __frcp_rn(static_cast<float>(r));  // 1.0f / float(rows.size())
@@ -84,8 +86,8 @@ void launch_softmax_ce(const float* logits, int64_t ldl, int32_t m, int32_t n, c
                        float* glogits, int64_t ldg, double* loss_out, double* row_scratch, int32_t* done,
                        cudaStream_t st) {
     const unsigned blocks = static_cast<unsigned>(ceil_div(m, kCeThreads / 32));
-    softmax_ce_kernel<<<blocks, kCeThreads, 0, st>>>(logits, ldl, m, n, row_label, r, glogits, ldg, loss_out,
-                                                     row_scratch, done);
+    launch_pdl(softmax_ce_kernel, dim3(blocks), dim3(kCeThreads), 0, st, logits, ldl, m, n, row_label, r, glogits, ldg,
+               loss_out, row_scratch, done);
     ++t_launches;
     GASB_CUDA(cudaGetLastError());
 }
@@ -122,6 +124,8 @@ __global__ void __launch_bounds__(256) adam_kernel(float* __restrict__ p, float*
                                                    int64_t* t_counter, const double* __restrict__ bc,
                                                    float lr, float b1, float b2, float eps, float clip,
                                                    const double* __restrict__ norm, int64_t* __restrict__ end_step, int32_t* __restrict__ end_done) {
+    pdl_trigger();
+    pdl_wait();
     const int64_t t = min(*t_counter + 1, static_cast<int64_t>(bc[0]));  // bc[0]: saturation step
     const double bc1 = bc[2 * t], bc2 = bc[2 * t + 1];
     float s = 1.0f;
@@ -168,9 +172,8 @@ void launch_adam(float* p, float* m, float* v, float* g, int64_t size, int64_t* 
         t_launches += 2;
     }
     const int64_t blocks = std::min<int64_t>(ceil_div(size, 256), 4 * 148);
-    adam_kernel<<<static_cast<unsigned>(blocks), 256, 0, st>>>(p, m, v, g, size, t_counter, bc, lr, b1, b2, eps,
-                                                               clip_max_norm, norm_scratch + kNormBlocks, end_step,
-                                                               end_done);
+    launch_pdl(adam_kernel, dim3(static_cast<unsigned>(blocks)), dim3(256), 0, st, p, m, v, g, size, t_counter, bc, lr,
+               b1, b2, eps, clip_max_norm, static_cast<const double*>(norm_scratch + kNormBlocks), end_step, end_done);
     ++t_launches;
     GASB_CUDA(cudaGetLastError());
 }
