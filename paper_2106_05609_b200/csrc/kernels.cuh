@@ -127,6 +127,17 @@ void launch_spmm_bwd(const int64_t* t_rowptr, int32_t ntargets, const int32_t* t
                      int64_t ldgx, cudaStream_t st, int32_t nsrc = 0, bool accumulate = false,
                      const int32_t* order = nullptr);
 
+// Two-columns-per-lane variant (spmm.cu, spmm_bwd2_kernel): same results, bit for bit, over
+// a per-(CTA split, source phase) plan of one part (build_bwd2_plan; false if a blob would
+// not fit shared memory). launch_spmm_bwd2 returns false (nothing launched) when dim < 64 or
+// gy cannot be described to TMA; callers then use launch_spmm_bwd.
+int32_t spmm_bwd2_splits(int32_t dim);
+bool build_bwd2_plan(const int64_t* trp, const int32_t* tsrc, const float* tcf, int32_t nt, int32_t nsrc,
+                     int32_t splits, std::vector<int64_t>& off, std::vector<unsigned char>& blobs);
+bool launch_spmm_bwd2(const int64_t* blob_off, const unsigned char* blobs, int32_t splits, const float* gy,
+                      int64_t ldgy, int32_t dim, const float* mask, int64_t ldm, float* gx, int64_t ldgx,
+                      cudaStream_t st, int32_t nsrc, bool accumulate = false);
+
 // ---- GEMM (gemm.cu) -------------------------------------------------------------------
 // op 0: C = A B ; 1: C = A B^T ; 2: C = A^T B.  Row-major fp32, fp32 accumulation.
 // History push fused into the epilogue (op 0 only): rows also scattered to

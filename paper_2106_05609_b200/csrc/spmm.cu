@@ -14,6 +14,7 @@
 // Backward (tensor.cpp:531-549): the scatter gx[col_e] += c_e * gy[r] becomes a gather
 // over the transposed stencil, entries of each target in ascending r with fp32
 // multiply-then-add -> bit-exact; relu backward (tensor.cpp:363-369) fused as a mask.
+#include <algorithm>
 #include <cstring>
 
 #include "gasb_internal.hpp"
@@ -1217,6 +1218,25 @@ __global__ void __launch_bounds__(256) spmm_bwd_kernel(const int64_t* __restrict
 constexpr int kBwdCW = 32;
 constexpr int kBwdRing = 8;  // metadata windows in flight per warp (spmm_bwd_smem_kernel)
 constexpr int kBwdThreads = 1024;
+#ifdef GASB_BWD_TIMING  // per-CTA globaltimer stamps of the last launch (timing probe builds only)
+__device__ unsigned long long g_bwd_stamps[512 * 4];  // [0, 256): spmm_bwd_smem, [256, 512): spmm_bwd2
+extern "C" void gasb_debug_bwd_stamps(unsigned long long* out) {
+    cudaMemcpyFromSymbol(out, g_bwd_stamps, sizeof(unsigned long long) * 512 * 4);
+}
+__device__ unsigned long long g_bwd_end[512];
+__device__ unsigned long long g_bwd_warp[64 * 3];  // spmm_bwd2, CTA (0, 0), phase 0: per warp entries, targets, end
+extern "C" void gasb_debug_bwd_warp(unsigned long long* out) {
+    cudaMemcpyFromSymbol(out, g_bwd_warp, sizeof(unsigned long long) * 64 * 3);
+}
+extern "C" void gasb_debug_bwd_end(unsigned long long* out) {
+    cudaMemcpyFromSymbol(out, g_bwd_end, sizeof(unsigned long long) * 512);
+}
+__device__ __forceinline__ unsigned long long bwd_now() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#endif
 
 __global__ void __launch_bounds__(kBwdThreads) spmm_bwd_smem_kernel(
     const int64_t* __restrict__ rp, int32_t nt, const int32_t* __restrict__ src, const float* __restrict__ cf,
@@ -1228,6 +1248,15 @@ __global__ void __launch_bounds__(kBwdThreads) spmm_bwd_smem_kernel(
     pdl_wait();
     if (threadIdx.x == 0) s_next = 0;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+#ifdef GASB_BWD_TIMING
+    const int cta = blockIdx.x + gridDim.x * blockIdx.y;
+    if (threadIdx.x == 0 && cta < 256) {
+        g_bwd_stamps[cta * 4] = bwd_now();
+        g_bwd_stamps[cta * 4 + 2] = 0;
+        g_bwd_stamps[cta * 4 + 3] = 0;
+    }
+    unsigned long long my_entries = 0;
+#endif
     const int32_t col0 = blockIdx.x * kBwdCW;
     const int32_t ncol = min(kBwdCW, dim - col0);
     // stage gy[:, col0 : col0+ncol] (zero-padded to 32 columns)
@@ -1259,6 +1288,9 @@ __global__ void __launch_bounds__(kBwdThreads) spmm_bwd_smem_kernel(
         }
     }
     __syncthreads();
+#ifdef GASB_BWD_TIMING
+    if (threadIdx.x == 0 && cta < 256) g_bwd_stamps[cta * 4 + 1] = bwd_now();
+#endif
     // targets t = blockIdx.y + splits * k; warps claim k dynamically (power-law in-degrees)
     const int32_t splits = targets_per_cta;
     // per-warp ring of kBwdRing 32-entry windows of (source row, coeff), filled by cp.async
@@ -1334,8 +1366,17 @@ __global__ void __launch_bounds__(kBwdThreads) spmm_bwd_smem_kernel(
             if (issued < nw) prefetch();
         }
         if (lane < ncol) gx[static_cast<int64_t>(t) * ldgx + col0 + lane] = keep ? a : 0.0f;
+#ifdef GASB_BWD_TIMING
+        my_entries += static_cast<unsigned long long>(e1 - e0);
+#endif
         t = tn;
     }
+#ifdef GASB_BWD_TIMING
+    if (lane == 0 && cta < 256) {
+        atomicMax(&g_bwd_stamps[cta * 4 + 2], bwd_now());
+        atomicMax(&g_bwd_stamps[cta * 4 + 3], my_entries);
+    }
+#endif
 }
 
 static int g_bwd_smem_set = 0;
@@ -1375,6 +1416,325 @@ void launch_spmm_bwd(const int64_t* t_rowptr, int32_t nt, const int32_t* t_src, 
                                                                    nchunks, mask, ldm, gx, ldgx, accumulate ? 1 : 0);
     ++t_launches;
     GASB_CUDA(cudaGetLastError());
+}
+
+// ---- aggregate backward, two columns per lane (spmm_bwd2) ---------------------------------
+// Same per-target sums as spmm_bwd_smem_kernel (entries in ascending source row, fp32 multiply
+// then add -> bit-exact) at half the instructions per column: each lane owns two adjacent
+// columns of a 64-column chunk and does both with one packed multiply and one packed add
+// (FFMA2 / FADD2). The multiply is fma.rn.f32x2(c, x, z) with z = -0.0 held in a kernel
+// parameter: exactly c * x rounded once for every input, and opaque, so ptxas cannot contract
+// the following add into an FMA (it does contract mul.rn.f32x2 + add.rn.f32x2, even with
+// --fmad=false).
+// A 64-column slice of every source row does not fit shared memory next to the metadata, so
+// the sources are staged in phases of kBwd2Rows rows. The plan (build_bwd2_plan) is laid out
+// per (CTA split, phase) as one contiguous blob: a target table {t, first entry, count} in
+// claim order (heaviest first), then each target's entries of that phase (ascending source,
+// padded to a multiple of 8 with (zero row, -0.0), which add exactly nothing: a + (-0.0 *
+// 0.0) == a for every a). At each phase one thread issues the TMA loads of the source slice
+// and one bulk copy of the blob, so no warp waits on a dependent global load afterwards.
+// Between phases the running fp32 sums live in gx: the accumulation sequence is unchanged.
+constexpr int kBwd2CW = 64;
+constexpr int kBwd2Rows = 608;                   // source rows per phase (a multiple of the TMA box)
+#ifndef GASB_BWD2_BOX
+#define GASB_BWD2_BOX 32
+#endif
+constexpr int kBwd2Box = GASB_BWD2_BOX;          // rows per TMA box
+constexpr int kBwd2Threads = 1024;
+constexpr int kBwd2SliceBytes = (kBwd2Rows + 1) * kBwd2CW * 4;  // + the zero row
+constexpr int kBwd2BlobBytes = 52 * 1024;        // per (split, phase) plan blob
+constexpr int kBwd2Slots = 48;                   // targets per split: running sums kept in shared memory
+constexpr int kBwd2MaxPhases = 8;
+// + 64 B for the mbarrier and the claim counter, + 128 B to align the TMA destination
+constexpr int kBwd2Smem = kBwd2SliceBytes + kBwd2BlobBytes + kBwd2Slots * kBwd2CW * 4 + 64 + 128;
+
+__device__ __forceinline__ uint64_t f2_mulz(float c, uint64_t x, uint64_t negz) {
+    uint64_t d;
+    const uint64_t cc = (static_cast<uint64_t>(__float_as_uint(c)) << 32) | __float_as_uint(c);
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(cc), "l"(x), "l"(negz));
+    return d;
+}
+__device__ __forceinline__ uint64_t f2_add(uint64_t a, uint64_t b) {
+    uint64_t d;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+
+// blob_off: (splits * phases + 1) byte offsets into blobs, (split, phase) major.
+__global__ void __launch_bounds__(kBwd2Threads) spmm_bwd2_kernel(
+    const int64_t* __restrict__ blob_off, const unsigned char* __restrict__ blobs, int32_t phases, int32_t nsrc,
+    int32_t dim, const float* __restrict__ mask, int64_t ldm, float* __restrict__ gx, int64_t ldgx, int accumulate,
+    uint64_t negz, const __grid_constant__ CUtensorMap gy_map) {
+    extern __shared__ __align__(128) unsigned char smem_raw2[];
+    __shared__ int64_t s_off[kBwd2MaxPhases + 1];
+    // (pointer arithmetic on the __shared__ array, so the compiler keeps LDS/STS for it)
+    unsigned char* base =
+        smem_raw2 + ((128u - (static_cast<uint32_t>(__cvta_generic_to_shared(smem_raw2)) & 127u)) & 127u);
+    float* sg = reinterpret_cast<float*>(base);  // (kBwd2Rows + 1) x 64: the phase's rows, then a zero row
+    unsigned char* blob = base + kBwd2SliceBytes;
+    float2* run = reinterpret_cast<float2*>(blob + kBwd2BlobBytes);  // [slot][32 lanes]: sums between phases
+    uint64_t* bar = reinterpret_cast<uint64_t*>(blob + kBwd2BlobBytes + kBwd2Slots * kBwd2CW * 4);
+    int32_t* s_next = reinterpret_cast<int32_t*>(bar + 1);
+    const int lane = threadIdx.x & 31;
+    const int32_t col0 = blockIdx.x * kBwd2CW;
+    const int32_t ncol = min(kBwd2CW, dim - col0);
+    const int32_t c = col0 + 2 * lane;  // this lane's columns c, c + 1
+    const bool has0 = 2 * lane < ncol, has1 = 2 * lane + 1 < ncol;
+    const bool vec_gx = (ldgx % 2 == 0) && ((reinterpret_cast<uintptr_t>(gx) & 7) == 0);
+    const bool vec_m = !mask || ((ldm % 2 == 0) && ((reinterpret_cast<uintptr_t>(mask) & 7) == 0));
+    const uint32_t bar_s = static_cast<uint32_t>(__cvta_generic_to_shared(bar));
+    // the plan is static data (not produced by the preceding kernels): its offsets and the first
+    // blob are fetched before pdl_wait; the source slice only after it
+    auto issue_slice = [&](int32_t q) {
+        const int32_t r0 = q * kBwd2Rows, rows = min(kBwd2Rows, nsrc - r0);
+        for (int32_t b = 0; b < (rows + kBwd2Box - 1) / kBwd2Box; ++b)
+            asm volatile(
+                "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n"
+                ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(sg + b * kBwd2Box * kBwd2CW))),
+                "l"(reinterpret_cast<uint64_t>(&gy_map)), "r"(col0), "r"(r0 + b * kBwd2Box), "r"(bar_s)
+                : "memory");
+    };
+    auto expect_and_issue_blob = [&](int32_t q) {  // thread 0: this phase's transaction bytes, then the blob
+        const int32_t rows = min(kBwd2Rows, nsrc - q * kBwd2Rows);
+        const uint32_t blob_bytes = static_cast<uint32_t>(s_off[q + 1] - s_off[q]);
+        mbar_expect_tx(bar, static_cast<uint32_t>((rows + kBwd2Box - 1) / kBwd2Box) * kBwd2Box * kBwd2CW * 4u + blob_bytes);
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+                     ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(blob))), "l"(blobs + s_off[q]),
+                     "r"(blob_bytes), "r"(bar_s)
+                     : "memory");
+    };
+    if (threadIdx.x == 0) {
+        asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&gy_map)) : "memory");
+        mbar_init(bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+        for (int32_t q = 0; q <= phases; ++q) s_off[q] = blob_off[static_cast<int64_t>(blockIdx.y) * phases + q];
+        *s_next = 0;
+        expect_and_issue_blob(0);
+    }
+    if (threadIdx.x < kBwd2CW) sg[kBwd2Rows * kBwd2CW + threadIdx.x] = 0.0f;  // the padding entries' row
+    pdl_trigger();
+    pdl_wait();
+    if (threadIdx.x == 0) issue_slice(0);
+    __syncthreads();  // the zero row
+    const unsigned char* sgl = reinterpret_cast<const unsigned char*>(sg) + 8 * lane;  // this lane's 2 columns
+    const int4* hdr = reinterpret_cast<const int4*>(blob);
+#ifdef GASB_BWD_TIMING
+    const int cta = 256 + blockIdx.x + gridDim.x * blockIdx.y;
+    if (threadIdx.x == 0 && cta < 512) {
+        g_bwd_stamps[cta * 4] = bwd_now();
+        g_bwd_stamps[cta * 4 + 2] = 0;
+    }
+#endif
+    for (int32_t q = 0; q < phases; ++q) {
+        if (q > 0) {
+            __syncthreads();  // every warp is done with the previous phase's slice and blob
+            if (threadIdx.x == 0) {
+                *s_next = 0;  // (published by the mbarrier arrive below)
+                expect_and_issue_blob(q);
+                issue_slice(q);
+            }
+        }
+        mbar_wait(bar, static_cast<uint32_t>(q & 1));
+#ifdef GASB_BWD_TIMING
+        if (threadIdx.x == 0 && cta < 512 && q < 2) g_bwd_stamps[cta * 4 + 1 + 2 * q] = bwd_now();
+#endif
+        const bool last_phase = q + 1 == phases;
+        const int32_t ntq = hdr[0].x;
+#ifdef GASB_BWD_TIMING
+        unsigned long long w_ent = 0, w_tg = 0;
+        const unsigned long long w_t0 = bwd_now();
+#endif
+        for (;;) {
+            int32_t k = 0;
+            if (lane == 0) k = atomicAdd(s_next, 1);
+            k = __shfl_sync(0xffffffffu, k, 0);
+            if (k >= ntq) break;
+            const int4 d = hdr[1 + k];  // {target, entry offset (bytes, in the blob), entries, slot}
+            const int32_t t = d.x;
+            float* gp = gx + static_cast<int64_t>(t) * ldgx + c;
+            float2 mv = make_float2(1.0f, 1.0f);
+            if (last_phase && mask) {  // issued now, used after the entries
+                const float* mp = mask + static_cast<int64_t>(t) * ldm + c;
+                if (vec_m && has1) mv = *reinterpret_cast<const float2*>(mp);
+                else {
+                    if (has0) mv.x = mp[0];
+                    if (has1) mv.y = mp[1];
+                }
+            }
+            float2 a = make_float2(0.0f, 0.0f);
+            if (q > 0) a = run[d.w * 32 + lane];
+            else if (accumulate) {
+                if (vec_gx && has1) a = *reinterpret_cast<const float2*>(gp);
+                else {
+                    if (has0) a.x = gp[0];
+                    if (has1) a.y = gp[1];
+                }
+            }
+            uint64_t acc = (static_cast<uint64_t>(__float_as_uint(a.y)) << 32) | __float_as_uint(a.x);
+            const int4* ent = reinterpret_cast<const int4*>(blob + d.y);  // 2 entries per int4
+#ifdef GASB_BWD_TIMING
+            w_ent += d.z;
+            ++w_tg;
+#endif
+            // 8 entries per step, software-pipelined: the next step's metadata is loaded while this
+            // step's source values are loaded and multiplied (the products are independent; only
+            // the adds form the ordered chain)
+            int4 m[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) m[u] = ent[u];
+            for (int32_t j = 0; j < d.z; j += 8) {
+                uint64_t x[8];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    x[2 * u] = *reinterpret_cast<const uint64_t*>(sgl + m[u].x);
+                    x[2 * u + 1] = *reinterpret_cast<const uint64_t*>(sgl + m[u].z);
+                }
+                float cf[8];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    cf[2 * u] = __int_as_float(m[u].y);
+                    cf[2 * u + 1] = __int_as_float(m[u].w);
+                }
+                if (j + 8 < d.z) {
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) m[u] = ent[((j + 8) >> 1) + u];
+                }
+                uint64_t pr[8];
+#pragma unroll
+                for (int v = 0; v < 8; ++v) pr[v] = f2_mulz(cf[v], x[v], negz);
+#pragma unroll
+                for (int v = 0; v < 8; ++v) acc = f2_add(acc, pr[v]);
+            }
+            float2 r;
+            r.x = __uint_as_float(static_cast<uint32_t>(acc));
+            r.y = __uint_as_float(static_cast<uint32_t>(acc >> 32));
+            if (!last_phase) {
+                run[d.w * 32 + lane] = r;
+                continue;
+            }
+            if (!(mv.x > 0.0f)) r.x = 0.0f;
+            if (!(mv.y > 0.0f)) r.y = 0.0f;
+            if (vec_gx && has1) *reinterpret_cast<float2*>(gp) = r;
+            else {
+                if (has0) gp[0] = r.x;
+                if (has1) gp[1] = r.y;
+            }
+        }
+#ifdef GASB_BWD_TIMING
+        if (lane == 0 && cta < 512 && q == 0) atomicMax(&g_bwd_stamps[cta * 4 + 2], bwd_now());
+        if (lane == 0 && q == 0 && blockIdx.x == 0 && blockIdx.y == 0) {
+            const int w = threadIdx.x >> 5;
+            g_bwd_warp[w * 3] = w_ent;
+            g_bwd_warp[w * 3 + 1] = w_tg;
+            g_bwd_warp[w * 3 + 2] = bwd_now() - w_t0;
+        }
+#endif
+    }
+#ifdef GASB_BWD_TIMING
+    __syncthreads();
+    if (threadIdx.x == 0 && cta < 512) g_bwd_end[cta] = bwd_now();
+#endif
+}
+
+int32_t spmm_bwd2_splits(int32_t dim) {
+    int dev = 0, sms = 148;
+    if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+        sms = 148;
+    return std::max<int32_t>(1, sms / static_cast<int32_t>(ceil_div(dim, kBwd2CW)));
+}
+
+// Blobs of one part: targets t = 0 .. nt-1 dealt round-robin to `splits` CTAs (t mod splits);
+// per (split, phase): int4 {targets, 0, 0, 0}, then per target (heaviest first) int4
+// {t, entry offset in bytes from the blob start, entries, 0}, then the entries as int2
+// {byte offset of the source row in the staged slice, coefficient bits}, per target padded to a
+// multiple of 8. Appends to blobs (16 B aligned) and to off (splits * phases offsets, plus the
+// end offset when `last`). Returns false if some blob exceeds the shared-memory budget.
+bool build_bwd2_plan(const int64_t* trp, const int32_t* tsrc, const float* tcf, int32_t nt, int32_t nsrc,
+                     int32_t splits, std::vector<int64_t>& off, std::vector<unsigned char>& blobs) {
+    const int32_t phases = std::max<int32_t>(1, static_cast<int32_t>(ceil_div(nsrc, kBwd2Rows)));
+    const int2 pad{kBwd2Rows * kBwd2CW * 4, static_cast<int>(0x80000000u)};
+    bool ok = phases <= kBwd2MaxPhases && ceil_div(nt, splits) <= kBwd2Slots;
+    std::vector<int64_t> split_at(static_cast<size_t>(nt) * (phases + 1));  // per target: phase boundaries
+    for (int32_t t = 0; t < nt; ++t) {
+        int64_t e = trp[t];
+        for (int32_t q = 0; q <= phases; ++q) {
+            const int32_t lo = q * kBwd2Rows;
+            while (e < trp[t + 1] && tsrc[e] < lo) ++e;
+            split_at[static_cast<size_t>(t) * (phases + 1) + q] = q == phases ? trp[t + 1] : e;
+        }
+    }
+    for (int32_t s = 0; s < splits; ++s)
+        for (int32_t q = 0; q < phases; ++q) {
+            std::vector<int32_t> ts;
+            for (int32_t t = s; t < nt; t += splits) ts.push_back(t);
+            auto cnt_of = [&](int32_t t) {
+                return split_at[static_cast<size_t>(t) * (phases + 1) + q + 1] - split_at[static_cast<size_t>(t) * (phases + 1) + q];
+            };
+            std::stable_sort(ts.begin(), ts.end(), [&](int32_t a, int32_t b) { return cnt_of(a) > cnt_of(b); });
+            const size_t b0 = blobs.size();
+            off.push_back(static_cast<int64_t>(b0));
+            const size_t hdr_bytes = 16 * (ts.size() + 1);
+            blobs.resize(b0 + hdr_bytes, 0);
+            int32_t h0[4] = {static_cast<int32_t>(ts.size()), 0, 0, 0};
+            std::memcpy(blobs.data() + b0, h0, 16);
+            for (size_t k = 0; k < ts.size(); ++k) {
+                const int32_t t = ts[k];
+                const int64_t e0 = split_at[static_cast<size_t>(t) * (phases + 1) + q], e1 = e0 + cnt_of(t);
+                const int64_t n8 = (e1 - e0 + 7) / 8 * 8;
+                int32_t h[4] = {t, static_cast<int32_t>(blobs.size() - b0), static_cast<int32_t>(n8), t / splits};
+                std::memcpy(blobs.data() + b0 + 16 * (k + 1), h, 16);
+                for (int64_t i = 0; i < n8; ++i) {
+                    int2 m = pad;
+                    if (e0 + i < e1) {
+                        m.x = (tsrc[e0 + i] - q * kBwd2Rows) * kBwd2CW * 4;
+                        std::memcpy(&m.y, &tcf[e0 + i], 4);
+                    }
+                    const size_t at = blobs.size();
+                    blobs.resize(at + 8);
+                    std::memcpy(blobs.data() + at, &m, 8);
+                }
+            }
+            if (blobs.size() - b0 > static_cast<size_t>(kBwd2BlobBytes)) ok = false;
+        }
+    return ok;
+}
+
+static int g_bwd2_smem_set = 0;
+
+bool launch_spmm_bwd2(const int64_t* blob_off, const unsigned char* blobs, int32_t splits, const float* gy,
+                      int64_t ldgy, int32_t dim, const float* mask, int64_t ldm, float* gx, int64_t ldgx,
+                      cudaStream_t st, int32_t nsrc, bool accumulate) {
+    if (dim < kBwd2CW || (ldgy * 4) % 16 != 0 || (reinterpret_cast<uintptr_t>(gy) & 15) != 0) return false;
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    if (!encode) {
+        cudaDriverEntryPointQueryResult qr;
+        void* fn = nullptr;
+        GASB_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &qr));
+        require(qr == cudaDriverEntryPointSuccess && fn, "spmm_bwd2: cuTensorMapEncodeTiled unavailable");
+        encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }
+    CUtensorMap map{};
+    const cuuint64_t gdim[2] = {static_cast<cuuint64_t>(dim), static_cast<cuuint64_t>(nsrc)};
+    const cuuint64_t gstride[1] = {static_cast<cuuint64_t>(ldgy) * 4};
+    const cuuint32_t box[2] = {kBwd2CW, kBwd2Box};
+    const cuuint32_t es[2] = {1, 1};
+    if (encode(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(gy), gdim, gstride, box, es,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return false;
+    if (!g_bwd2_smem_set) {
+        GASB_CUDA(cudaFuncSetAttribute(spmm_bwd2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kBwd2Smem));
+        g_bwd2_smem_set = 1;
+    }
+    const int32_t phases = std::max<int32_t>(1, static_cast<int32_t>(ceil_div(nsrc, kBwd2Rows)));
+    const int32_t nchunks = static_cast<int32_t>(ceil_div(dim, kBwd2CW));
+    const uint64_t negz = 0x8000000080000000ull;
+    launch_pdl(spmm_bwd2_kernel, dim3(static_cast<unsigned>(nchunks), static_cast<unsigned>(splits)),
+               dim3(kBwd2Threads), kBwd2Smem, st, blob_off, blobs, phases, nsrc, dim, mask, ldm, gx, ldgx,
+               accumulate ? 1 : 0, negz, map);
+    ++t_launches;
+    GASB_CUDA(cudaGetLastError());
+    return true;
 }
 
 }  // namespace gasb

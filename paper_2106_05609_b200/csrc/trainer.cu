@@ -376,6 +376,25 @@ void gasb_trainer_s::build(const float* h_features, const int32_t* h_labels, con
         }
         t_order.upload(h_ord);
     }
+    {  // spmm_bwd2 plans (GASB_BWD2=0: the one-column-per-lane kernel everywhere)
+        const char* e = getenv("GASB_BWD2");
+        use_bwd2 = (!e || atoi(e) != 0) && H >= 64;
+        if (use_bwd2) {
+            std::vector<int64_t> boff;
+            std::vector<unsigned char> blobs;
+            bwd2_splits = spmm_bwd2_splits(H);
+            bwd2_off.resize(num_parts);
+            bwd2_ok.resize(num_parts);
+            for (int32_t p = 0; p < num_parts; ++p) {
+                bwd2_off[p] = static_cast<int64_t>(boff.size());
+                bwd2_ok[p] = build_bwd2_plan(h_trp.data() + row_off[p] + p, h_tsrc.data(), h_tcf.data(), nb[p], nb[p],
+                                             bwd2_splits, boff, blobs);
+                boff.push_back(static_cast<int64_t>(blobs.size()));  // the part's end offset
+            }
+            bwd2_boff.upload(boff);
+            bwd2_blobs.upload(blobs);
+        }
+    }
     trace("stencil uploads + t_order");
     train_rows.upload(h_trr);
     train_labels.upload(h_trl);
@@ -645,6 +664,18 @@ void gasb_trainer_s::enqueue_hoisted() {
     }
     launch_spmm_fwd(seg_all.segs(0), cols_g.p, coef64.p, X.p, ldF, F, agg_all.p, ldF, 0, partial_all.p, pld_all,
                     counters.p, max_chunks, stream, source_flags(1), source_tmap(1));
+}
+
+void gasb_trainer_s::spmm_bwd_batch(int32_t p, const float* gy, int64_t ldgy, int32_t dim, const float* mask,
+                                    int64_t ldm, float* gx, int64_t ldgx, cudaStream_t st) {
+    const int64_t r0 = row_off[p];
+    const int32_t m = nb[p];
+    if (use_bwd2 && bwd2_ok[p] && dim == H &&
+        launch_spmm_bwd2(bwd2_boff.p + bwd2_off[p], bwd2_blobs.p, bwd2_splits, gy, ldgy, dim, mask, ldm, gx, ldgx, st,
+                         m, false))
+        return;
+    launch_spmm_bwd(t_rowptr.p + r0 + p, m, t_src.p, t_cf.p, gy, ldgy, dim, mask, ldm, gx, ldgx, st, m, false,
+                    t_order.p + r0);
 }
 
 void gasb_trainer_s::build_hoist_blocked(const std::vector<int64_t>& rp, const HVec<int32_t>& cg,
@@ -1059,8 +1090,7 @@ void gasb_trainer_s::enqueue_batch(int32_t p, bool train, bool push, bool use_ho
                 launch_gemm(1, m, din, dout, g, ldg, W(l), pp(layer_param[l]), g_agg.p, ldH, 0.f, false, nullptr,
                             stream);
                 // aggregate backward over intra-batch edges + compose bwd + relu bwd (mask = act)
-                launch_spmm_bwd(t_rowptr.p + r0 + p, m, t_src.p, t_cf.p, g_agg.p, ldH, din, act[l - 1].p, ldH, go,
-                                ldH, stream, m, false, t_order.p + r0);
+                spmm_bwd_batch(p, g_agg.p, ldH, din, act[l - 1].p, ldH, go, ldH, stream);
             }
             // dropout backward on the batch rows of the layer input (tensor.cpp:390-397)
             if (dr) launch_dropout_rows_bwd(go, ldH, m, din, brow.p + r0, mask_of(l), inv_keep, stream);

@@ -150,6 +150,16 @@ struct gasb_trainer_s {
     DevBuf<float> t_cf;
     DevBuf<int64_t> t_rowptr;
     DevBuf<int32_t> t_order;  // per part: intra-batch targets by descending entry count
+    // spmm_bwd2 plan (GCN layers with d >= 64): per part, per (CTA split, source phase) blobs
+    DevBuf<int64_t> bwd2_boff;
+    DevBuf<unsigned char> bwd2_blobs;
+    std::vector<int64_t> bwd2_off;  // per part: index of its first blob offset in bwd2_boff
+    std::vector<char> bwd2_ok;      // per part: every blob fits shared memory
+    int32_t bwd2_splits = 0;
+    bool use_bwd2 = false;
+    // aggregate backward of a batch layer (intra-batch targets): spmm_bwd2 where planned, else spmm_bwd
+    void spmm_bwd_batch(int32_t p, const float* gy, int64_t ldgy, int32_t dim, const float* mask, int64_t ldm,
+                        float* gx, int64_t ldgx, cudaStream_t st);
     SegTable seg_batch, seg_all;
     DevBuf<int32_t> counters, row_label, xflags, ce_done;  // xflags: value flags of X (kernels.cuh)
     DevBuf<double> partial_batch, partial_all;

@@ -266,3 +266,18 @@ def test_source_blocked_hoist_matches(oracle, monkeypatch):
         assert abs(res[1][0][ep] - lo) / abs(lo) <= TOL
     assert normwise(res[1][1], res[0][1]) <= 1e-6
     assert normwise(res[1][1], so.get_params()) <= TOL
+
+
+def test_bwd2_is_bit_identical(oracle, monkeypatch):
+    """The two-columns-per-lane aggregate backward (spmm_bwd2: packed FFMA2/FADD2, sources
+    staged in phases, per-phase padded entry lists) gives the one-column kernel's gradients
+    bit for bit. reddit_mini batches hold ~1,000 rows, so every target runs two phases."""
+    out = []
+    for v in ("0", "1"):
+        monkeypatch.setenv("GASB_BWD2", v)
+        ds, sched, tr, so = _setup(oracle, "reddit_mini", seg_edges=0)
+        assert int(sched.sizes(0)[0]) > 608
+        losses = [tr.gas_epoch(ep) for ep in range(2)]
+        out.append((losses, tr.get_params(), tr.history.layer_matrix(1)))
+    assert out[0][0] == out[1][0]
+    assert np.array_equal(out[0][1], out[1][1]) and np.array_equal(out[0][2], out[1][2])
