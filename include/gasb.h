@@ -287,6 +287,16 @@ typedef struct {
                               (host mt19937_64, copied per batch) -> bit-exact, host-bound;
                               GASB_DROPOUT_PHILOX: Philox4x32-10 on the device keyed by the same
                               derive_seed value -> same keep rate, different masks, no host work */
+    int32_t cross_batch;   /* the paper's concurrent execution across batches (GCN, fused,
+                              segmented, no dropout; gas_epoch only). 0: off. 1: batch b+1's
+                              halo aggregation (every history layer: the in-edges from rows
+                              outside V_b+1, which only earlier batches' pushes write) runs on a
+                              background stream while batch b runs its backward and Adam; the
+                              batch's own forward aggregates only its intra-batch edges and adds
+                              the halo fp64 partial. 2: as 1, and batch b+1's layer-1
+                              aggregation also runs per batch on the background stream (instead
+                              of the up-front hoisted launch), overlapped with batch b. Same
+                              results up to fp64 summation order (the segmented mode's class). */
 } gasb_trainer_options;
 #define GASB_DROPOUT_EXACT 0
 #define GASB_DROPOUT_PHILOX 1

@@ -58,7 +58,7 @@ class ModelSpecC(C.Structure):
 
 class TrainerOptionsC(C.Structure):
     _fields_ = [("seg_edges", i32), ("fused", i32), ("prefetch", i32), ("use_graphs", i32),
-                ("hoist_layer1", i32), ("device", i32), ("dropout_rng", i32)]
+                ("hoist_layer1", i32), ("device", i32), ("dropout_rng", i32), ("cross_batch", i32)]
 
 
 class EpochReportC(C.Structure):  # gasb_epoch_report

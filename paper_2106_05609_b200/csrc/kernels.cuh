@@ -111,6 +111,9 @@ void launch_spmm_fwd(const SpmmSegs& s, const int32_t* cols, const double* coeff
                      int32_t dim, float* y, int64_t ldy, int64_t row_base, double* partial, int64_t partial_ld,
                      int32_t* counters, int32_t counters_ld, cudaStream_t st, const int32_t* special = nullptr,
                      const CUtensorMap* tmap = nullptr);
+// Caps the grid of this thread's flat SpMM launches at `ctas` CTAs (0: the full persistent
+// grid). Work items are grid-strided, so a capped launch does the same work on fewer SMs.
+void set_spmm_grid_cap(int32_t ctas);
 bool make_row_tmap(const float* base, int64_t rows, int32_t dim, int64_t ld, int32_t box_cols, CUtensorMap* out);
 int32_t spmm_box_cols(int32_t dim);
 int32_t spmm_cpl_for(int32_t dim);

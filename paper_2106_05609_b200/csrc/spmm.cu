@@ -882,6 +882,11 @@ __global__ void __launch_bounds__(kPipeWarps * 32, kPipeCtas) spmm_fwd_flat_kern
 #undef GASB_FLAT
 }
 
+// Grid cap of the flat SpMM launches enqueued by this thread (set_spmm_grid_cap): the
+// background stream's launches leave SMs to the batch chain running beside them.
+static thread_local int32_t t_spmm_grid_cap = 0;
+void set_spmm_grid_cap(int32_t ctas) { t_spmm_grid_cap = ctas; }
+
 template <int CPL, bool DUAL>
 static void launch_flat(const SpmmSegs& s, const int32_t* cols, const double* coeffs, int32_t dim, float* y,
                         int64_t ldy, int64_t row_base, double* partial, int64_t partial_ld, int32_t* counters,
@@ -904,7 +909,8 @@ static void launch_flat(const SpmmSegs& s, const int32_t* cols, const double* co
         GASB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     }
     const int64_t items = static_cast<int64_t>(nchunks) * s.nranges;
-    const int64_t blocks = std::min<int64_t>(ceil_div(items, kPipeWarps), static_cast<int64_t>(kPipeCtas) * sms);
+    int64_t blocks = std::min<int64_t>(ceil_div(items, kPipeWarps), static_cast<int64_t>(kPipeCtas) * sms);
+    if (t_spmm_grid_cap > 0) blocks = std::min<int64_t>(blocks, t_spmm_grid_cap);
     launch_pdl(spmm_fwd_flat_kernel<CPL, DUAL>, dim3(static_cast<unsigned>(blocks)), dim3(kPipeWarps * 32), kSmem, st,
                s.seg_beg, s.seg_row, s.seg_slot, s.row_seg0, s.row_nseg, s.range_seg, s.nranges, cols, coeffs, dim,
                nchunks, y, ldy, row_base, partial, partial_ld, counters, counters_ld, special,

@@ -350,8 +350,30 @@ void gasb_trainer_s::build(const float* h_features, const int32_t* h_labels, con
         GASB_CUDA(cudaMemGetInfo(&fr, &tot));
         mem_free_at_build = fr;
     }
-    GASB_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
-    GASB_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+    // cross-batch mode (gasb.h cross_batch; GASB_XBATCH overrides): GCN over the fused,
+    // segmented path without dropout
+    {
+        const char* xe = getenv("GASB_XBATCH");
+        xmode = xe ? atoi(xe) : opt.cross_batch;
+        const bool ok = !residual && opt.fused && !drop && L >= 2 && opt.seg_edges > 0;
+        xmode = ok ? std::max(0, std::min(2, xmode)) : 0;
+        if (xmode == 1 && !opt.hoist_layer1) xmode = 2;  // layer 1 per batch then
+        const char* be = getenv("GASB_BG_CTAS");
+        bg_ctas = be ? std::max(0, atoi(be)) : 148;
+    }
+    if (xmode) {
+        // the batch chain (stream, side) outranks the background aggregations at CTA dispatch
+        int least = 0, greatest = 0;
+        GASB_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+        GASB_CUDA(cudaStreamCreateWithPriority(&stream, cudaStreamNonBlocking, greatest));
+        GASB_CUDA(cudaStreamCreateWithPriority(&side, cudaStreamNonBlocking, greatest));
+        GASB_CUDA(cudaStreamCreateWithPriority(&bg, cudaStreamNonBlocking, least));
+        for (cudaEvent_t* e : {&ev_xstart, &ev_xfwd, &ev_xbg})
+            GASB_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+    } else {
+        GASB_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+        GASB_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+    }
     GASB_CUDA(cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking));
     GASB_CUDA(cudaEventCreateWithFlags(&ev_staged, cudaEventDisableTiming));
     GASB_CUDA(cudaEventCreateWithFlags(&ev_stage_free, cudaEventDisableTiming));
@@ -411,6 +433,10 @@ void gasb_trainer_s::build(const float* h_features, const int32_t* h_labels, con
         build_segments(h_rp, one, opt.seg_edges > 0, false, seg_all);
     }
     trace("segments");
+    if (xmode) {
+        build_xbatch(h_rp, h_cg, h_cf);
+        trace("cross-batch tables");
+    }
     max_chunks = static_cast<int32_t>(ceil_div(std::max(F, H), 64));
     counters.alloc(R * max_chunks);
     counters.zero();
@@ -496,7 +522,7 @@ void gasb_trainer_s::build(const float* h_features, const int32_t* h_labels, con
     if (!residual) {
         for (int32_t l = 1; l <= L; ++l) agg[l].alloc(static_cast<int64_t>(nb_max) * ld_of(dims[l - 1]));
         for (int32_t l = 1; l < L; ++l) act[l].alloc(static_cast<int64_t>(nb_max) * ldH);
-        if (opt.hoist_layer1) agg_all.alloc(R * ldF);
+        if (opt.hoist_layer1 || xmode) agg_all.alloc(R * ldF);
     } else {
         build_residual(h_arp, h_asrc, h_acf, h_brow);
     }
@@ -987,14 +1013,21 @@ void gasb_trainer_s::enqueue_batch(int32_t p, bool train, bool push, bool use_ho
     const int32_t* bn = batch_nodes.p + r0;
     const bool dr = drop && train;  // dropout only while training (ForwardOptions.training)
     require(!dr || !fused, "trainer: dropout batches run the materialized path");
-    if (!fused && halo_pf.p) enqueue_prefetch(p);
+    if (!fused && halo_pf.p && xphase != 2) enqueue_prefetch(p);
+    // cross-batch phases (run_epoch_x): the forward, or the loss + backward, of the batch;
+    // the forward's history layers aggregate only the intra-batch block (enqueue_bg ran the halo)
+    const bool xsplit = xphase != 0;
+    require(!xsplit || (fused && use_hoisted && !dr), "trainer: cross-batch phases need the fused hoisted path");
     // ---------------- forward (Model::forward, trainer.cpp:174-251) ----------------
-    for (int32_t l = 1; l <= L; ++l) {
+    for (int32_t l = 1; l <= L && xphase != 2; ++l) {
         const int32_t din = dims[l - 1], dout = dims[l];
         const int64_t lda = ld_of(din);
         float* a = agg[l].p;
         if (l == 1 && use_hoisted) {
             a = agg_all.p + r0 * ldF;
+        } else if (xsplit) {
+            launch_spmm_fwd(xsegs(p, false), xcols.p, xcoef.p, history_table(hist, l - 1), history_ld(hist), din, a,
+                            lda, r0, xpartial(l), pldx, xcounters(l), cxld, stream, source_flags(l), source_tmap(l));
         } else if (fused) {
             const float* src = l == 1 ? X.p : history_table(hist, l - 1);
             const int64_t lds = l == 1 ? ldF : history_ld(hist);
@@ -1047,6 +1080,7 @@ void gasb_trainer_s::enqueue_batch(int32_t p, bool train, bool push, bool use_ho
             launch_gemm(0, m, dout, din, a, lda, Wl, pp(layer_param[l]), logits.p, ldC, 0.f, false, nullptr, stream);
         }
     }
+    if (xphase == 1) return;
     // ---------------- loss + backward (run_batch, trainer.cpp:295-339) ----------------
     const bool stepped = ntrain[p] > 0 && train;
     if (ntrain[p] > 0)
@@ -1168,6 +1202,12 @@ void gasb_trainer_s::run_epoch(int64_t epoch, bool shuffle, int32_t begin, int32
     int64_t steps = 0;
     for (int32_t p : order) steps += ntrain[p] > 0 ? 1 : 0;
     ensure_bc(t_host + steps + 2);
+    if (xmode) {
+        run_epoch_x(order);
+        t_host += steps;
+        last_order = order;
+        return;
+    }
     const bool hoisted = opt.hoist_layer1 && opt.fused && !residual && !drop;
     const int64_t l0 = t_launches;
     if (hoisted) enqueue_hoisted();
@@ -1182,6 +1222,173 @@ void gasb_trainer_s::run_epoch(int64_t epoch, bool shuffle, int32_t begin, int32
     }
     t_host += steps;
     last_order = order;
+}
+
+// ---------------- cross-batch concurrent execution (opt.cross_batch) ----------------
+// The reference overlaps batch b+1's history pulls with batch b's compute (Prefetcher,
+// history.cpp:184-252; trainer.cpp:416-418). The fused path has no pulls: batch b+1's halo
+// rows are read in place by its aggregations. What can move is the aggregation over the halo
+// in-edges itself: they read H_{l-1} rows of nodes outside V_{b+1}, which only earlier
+// batches' pushes write, and batch b's last push is in its forward. So right after batch b's
+// forward, the background stream aggregates every history layer's halo block of batch b+1
+// into fp64 partials, overlapped with batch b's backward and Adam; batch b+1's forward then
+// aggregates its intra-batch block and the last-arriving segment of each row combines the
+// row's partials in segment order (halo block first) and stores the fp32 row.
+//
+// Edge layout: per part, the edges are re-laid as [halo-source block | intra-source block],
+// each row-major and in CSR order inside a row; every row gets >= 1 segment in each block
+// (possibly empty), all with partial slots, so the store is always made by the intra launch.
+void gasb_trainer_s::build_xbatch(const std::vector<int64_t>& rp, const HVec<int32_t>& cg, const HVec<double>& cf) {
+    const int64_t R = row_off[num_parts], E = edge_off[num_parts];
+    HVec<int32_t> xc(static_cast<size_t>(E));
+    HVec<double> xf(static_cast<size_t>(E));
+    std::vector<int64_t> rph(static_cast<size_t>(R)), rpi(static_cast<size_t>(R)), hend(num_parts);
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int32_t p = 0; p < num_parts; ++p) {
+        const HostPlan& P = sched->plans[p];
+        const int64_t e0 = edge_off[p];
+        int64_t nhal = 0;
+        for (int32_t c : P.gcn_cols) nhal += P.is_halo[c] ? 1 : 0;
+        int64_t kh = e0, ki = e0 + nhal;
+        for (int64_t r = row_off[p]; r < row_off[p + 1]; ++r) {
+            rph[r] = kh;
+            rpi[r] = ki;
+            for (int64_t e = rp[r]; e < rp[r + 1]; ++e) {
+                if (P.is_halo[P.gcn_cols[e - e0]]) {
+                    xc[kh] = cg[e];
+                    xf[kh++] = cf[e];
+                } else {
+                    xc[ki] = cg[e];
+                    xf[ki++] = cf[e];
+                }
+            }
+        }
+        hend[p] = e0 + nhal;
+    }
+    xcols.upload(xc);
+    xcoef.upload(xf);
+    // segments: per part the halo group (2p) then the intra group (2p + 1); slots restart per part
+    const int32_t nr = spmm_ranges_per_launch();
+    seg_x.nranges = nr;
+    seg_x.split = true;
+    std::vector<int64_t> sb, tmp(static_cast<size_t>(R) + 1);
+    std::vector<int32_t> sr, ss, r0h(R), rnh(R), r0i(R), rni(R), rs(static_cast<size_t>(2 * num_parts) * (nr + 1));
+    std::vector<int32_t> seg0(R), nseg(R), slots;
+    xslots = 0;
+    for (int32_t p = 0; p < num_parts; ++p) {
+        const int64_t lo = row_off[p], hi = row_off[p + 1];
+        int64_t dummy = 0;
+        const int64_t g0 = static_cast<int64_t>(sr.size());
+        for (int64_t r = lo; r < hi; ++r) tmp[r] = rph[r];
+        tmp[hi] = hend[p];
+        if (!sb.empty()) sb.pop_back();
+        segment_launch(tmp.data(), lo, hi, true, nr, sb, sr, ss, r0h.data(), rnh.data(), dummy,
+                       rs.data() + static_cast<int64_t>(2 * p) * (nr + 1));
+        for (int64_t r = lo; r < hi; ++r) tmp[r] = rpi[r];
+        tmp[hi] = edge_off[p + 1];
+        sb.pop_back();
+        segment_launch(tmp.data(), lo, hi, true, nr, sb, sr, ss, r0i.data(), rni.data(), dummy,
+                       rs.data() + static_cast<int64_t>(2 * p + 1) * (nr + 1));
+        const int64_t g2 = static_cast<int64_t>(sr.size());
+        for (int64_t s2 = g0; s2 < g2; ++s2) ss[s2] = static_cast<int32_t>(s2 - g0);
+        xslots = std::max(xslots, g2 - g0);
+        for (int64_t r = lo; r < hi; ++r) {
+            seg0[r] = static_cast<int32_t>(slots.size());
+            nseg[r] = rnh[r] + rni[r];
+            for (int32_t i = 0; i < rnh[r]; ++i) slots.push_back(ss[r0h[r] + i]);
+            for (int32_t i = 0; i < rni[r]; ++i) slots.push_back(ss[r0i[r] + i]);
+        }
+    }
+    seg_x.ranges.upload(rs);
+    seg_x.seg_beg.upload(sb);
+    seg_x.seg_row.upload(sr);
+    seg_x.seg_slot.upload(ss);
+    seg_x.row_seg0.upload(seg0);
+    seg_x.row_nseg.upload(nseg);
+    seg_x.row_slots.upload(slots);
+    seg_x.max_group_slots = seg_x.total_slots = xslots;
+    pldx = round_up(std::max(H, 1), 256);
+    cxld = static_cast<int32_t>(ceil_div(std::max(H, 1), 64));
+    partial_x.alloc(static_cast<int64_t>(L - 1) * std::max<int64_t>(xslots, 1) * pldx);
+    counters_x.alloc(static_cast<int64_t>(L - 1) * R * cxld);
+    counters_x.zero();
+}
+
+// Background work of batch q on `bg`: (xmode 2) its layer-1 rows of agg_all, then — after the
+// previous batch's forward (ev_xfwd) when wait_fwd — the halo block of every history layer.
+void gasb_trainer_s::enqueue_bg(int32_t q, bool wait_fwd) {
+    set_spmm_grid_cap(bg_ctas);
+    if (xmode == 2)
+        launch_spmm_fwd(seg_batch.segs(q), cols_g.p, coef64.p, X.p, ldF, F, agg_all.p, ldF, 0, partial_batch.p, pld,
+                        counters.p, max_chunks, bg, source_flags(1), source_tmap(1));
+    if (wait_fwd) GASB_CUDA(cudaStreamWaitEvent(bg, ev_xfwd, 0));
+    for (int32_t l = 2; l <= L; ++l)  // (rows are stored by the intra launch: y is never written here)
+        launch_spmm_fwd(xsegs(q, true), xcols.p, xcoef.p, history_table(hist, l - 1), history_ld(hist), dims[l - 1],
+                        agg[l].p, ld_of(dims[l - 1]), row_off[q], xpartial(l), pldx, xcounters(l), cxld, bg,
+                        source_flags(l), source_tmap(l));
+    set_spmm_grid_cap(0);
+}
+
+// One phase (1 forward, 2 loss + backward + Adam) of batch p on `stream`, through its captured
+// graph when use_graphs. Returns the kernels its graph launches.
+int64_t gasb_trainer_s::launch_x_graph(int32_t p, int32_t phase) {
+    if (!opt.use_graphs) {  // (direct launches: counted by t_launches)
+        xphase = phase;
+        enqueue_batch(p, true, true, true, true, false);
+        xphase = 0;
+        return 0;
+    }
+    std::vector<cudaGraphExec_t>& gs = phase == 1 ? graphs_xf : graphs_xb;
+    std::vector<int64_t>& gl = phase == 1 ? graph_launches_xf : graph_launches_xb;
+    if (gs.empty()) {
+        gs.assign(num_parts, nullptr);
+        gl.assign(num_parts, 0);
+    }
+    if (!gs[p]) {
+        cudaGraph_t graph;
+        const int64_t c0 = t_launches;
+        xphase = phase;
+        GASB_CUDA(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
+        enqueue_batch(p, true, true, true, true, false);
+        GASB_CUDA(cudaStreamEndCapture(stream, &graph));
+        xphase = 0;
+        gl[p] = t_launches - c0;
+        t_launches = c0;
+        GASB_CUDA(cudaGraphInstantiate(&gs[p], graph, 0));
+        GASB_CUDA(cudaGraphDestroy(graph));
+    }
+    GASB_CUDA(cudaGraphLaunch(gs[p], stream));
+    return gl[p];
+}
+
+// The epoch's batches with batch i+1's background work overlapped with batch i:
+//   bg:     [L1(o0)] halo(o0) | [L1(o1)] .. wait fwd(o0) .. halo(o1) | [L1(o2)] .. wait fwd(o1) ..
+//   stream: wait bg | fwd(o0) bwd(o0) | wait bg | fwd(o1) bwd(o1) | ...
+void gasb_trainer_s::run_epoch_x(const std::vector<int32_t>& order) {
+    const int64_t l0 = t_launches;
+    int64_t launches = 0;
+    if (xmode == 1) enqueue_hoisted();
+    GASB_CUDA(cudaEventRecord(ev_xstart, stream));  // X (set_features), the hoisted layer 1, the last epoch
+    GASB_CUDA(cudaStreamWaitEvent(bg, ev_xstart, 0));
+    const size_t nbat = order.size();
+    if (nbat > 0) {
+        enqueue_bg(order[0], false);
+        GASB_CUDA(cudaEventRecord(ev_xbg, bg));
+        GASB_CUDA(cudaStreamWaitEvent(stream, ev_xbg, 0));
+    }
+    for (size_t i = 0; i < nbat; ++i) {
+        const int32_t p = order[i];
+        launches += launch_x_graph(p, 1);
+        const bool next = i + 1 < nbat;
+        if (next) {
+            GASB_CUDA(cudaEventRecord(ev_xfwd, stream));
+            enqueue_bg(order[i + 1], true);
+            GASB_CUDA(cudaEventRecord(ev_xbg, bg));
+        }
+        launches += launch_x_graph(p, 2);
+        if (next) GASB_CUDA(cudaStreamWaitEvent(stream, ev_xbg, 0));
+    }
+    epoch_launches = t_launches - l0 + launches;
 }
 
 // gas_forward_snapshot (trainer.cpp:466-483): every batch in PART order, forward only against

@@ -293,6 +293,32 @@ struct gasb_trainer_s {
                         const HVec<float>& h_acf, const std::vector<int32_t>& h_brow);
     void enqueue_batch_res(int32_t p, bool train, bool push, bool fused, bool dp = false);
 
+    // ---- cross-batch concurrent execution (opt.cross_batch; the paper's concurrent pulls,
+    // SURVEY north_star 5): batch b+1's halo aggregations run on the low-priority stream `bg`
+    // while batch b runs its backward; batch b+1's forward then aggregates only its intra-batch
+    // edges and adds the halo fp64 partials (one segment table over both launches) ----
+    int32_t xmode = 0;          // 0 off, 1 halo on bg (layer 1 hoisted), 2 + per-batch layer 1 on bg
+    int32_t bg_ctas = 0;        // grid cap of the bg launches (0: full grid)
+    int32_t xphase = 0;         // enqueue_batch: 0 whole batch, 1 forward only, 2 loss + backward only
+    cudaStream_t bg = nullptr;
+    cudaEvent_t ev_xstart = nullptr, ev_xfwd = nullptr, ev_xbg = nullptr;
+    DevBuf<int32_t> xcols;      // per part, edges re-laid [halo-source block | intra-source block],
+    DevBuf<double> xcoef;       //   each row-major in CSR order (same offsets as cols_g)
+    SegTable seg_x;             // groups 2p (halo block) and 2p + 1 (intra block); row_slots
+    DevBuf<double> partial_x;   // per history layer: xslots x pldx fp64 partials
+    DevBuf<int32_t> counters_x; // per history layer: R x cxld arrival counters (self-resetting)
+    int64_t pldx = 0, xslots = 0;
+    int32_t cxld = 0;
+    std::vector<cudaGraphExec_t> graphs_xf, graphs_xb;
+    std::vector<int64_t> graph_launches_xf, graph_launches_xb;
+    void build_xbatch(const std::vector<int64_t>& rp, const HVec<int32_t>& cg, const HVec<double>& cf);
+    void enqueue_bg(int32_t q, bool wait_fwd);
+    int64_t launch_x_graph(int32_t p, int32_t phase);
+    void run_epoch_x(const std::vector<int32_t>& order);
+    SpmmSegs xsegs(int32_t p, bool halo) const { return seg_x.segs(2 * static_cast<int64_t>(p) + (halo ? 0 : 1)); }
+    double* xpartial(int32_t l) { return partial_x.p + static_cast<int64_t>(l - 2) * xslots * pldx; }
+    int32_t* xcounters(int32_t l) { return counters_x.p + static_cast<int64_t>(l - 2) * row_off[num_parts] * cxld; }
+
     // graphs
     std::vector<cudaGraphExec_t> graphs;
     std::vector<int64_t> graph_launches;
@@ -306,6 +332,14 @@ struct gasb_trainer_s {
             if (g) cudaGraphExecDestroy(g);
         for (auto g : graphs_dp)
             if (g) cudaGraphExecDestroy(g);
+        for (auto g : graphs_xf)
+            if (g) cudaGraphExecDestroy(g);
+        for (auto g : graphs_xb)
+            if (g) cudaGraphExecDestroy(g);
+        if (bg) cudaStreamSynchronize(bg);
+        for (auto e : {ev_xstart, ev_xfwd, ev_xbg})
+            if (e) cudaEventDestroy(e);
+        if (bg) cudaStreamDestroy(bg);
         if (hist) history_destroy(hist);
         for (auto e : ev_fork) cudaEventDestroy(e);
         for (auto e : ev_wdone) cudaEventDestroy(e);
@@ -373,6 +407,10 @@ struct gasb_trainer_s {
         for (auto& g : graphs)
             if (g) cudaGraphExecDestroy(g), g = nullptr;
         for (auto& g : graphs_dp)
+            if (g) cudaGraphExecDestroy(g), g = nullptr;
+        for (auto& g : graphs_xf)
+            if (g) cudaGraphExecDestroy(g), g = nullptr;
+        for (auto& g : graphs_xb)
             if (g) cudaGraphExecDestroy(g), g = nullptr;
     }
 

@@ -50,10 +50,12 @@ class TrainerOptions:
     hoist_layer1: bool = True
     device: int = 0
     dropout_rng: str = "exact"  # "exact" (the reference's mt19937_64 masks) or "philox" (gasb.h)
+    cross_batch: int = 0      # 1: batch b+1's halo aggregation overlapped with batch b (gasb.h); 2: + layer 1
 
     def to_c(self) -> TrainerOptionsC:
         return TrainerOptionsC(self.seg_edges, int(self.fused), int(self.prefetch), int(self.use_graphs),
-                               int(self.hoist_layer1), self.device, {"exact": 0, "philox": 1}[self.dropout_rng])
+                               int(self.hoist_layer1), self.device, {"exact": 0, "philox": 1}[self.dropout_rng],
+                               int(self.cross_batch))
 
 
 class GasTrainer:
