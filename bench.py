@@ -363,6 +363,25 @@ def run_ours(args):
             roof["traffic"] = json.loads(prof.read_text()).get("dram_bytes_per_launch")
         except Exception:
             pass
+    # third ceiling, the one the gathers are actually bound by: the launch's gathered bytes at
+    # the measured TMA tile::gather4 rates (tools/l2bw/tma_gather_bw on a B200: 1 KB rows from
+    # an L2-resident table vs a DRAM-resident one), split into L2 hits and DRAM misses by the
+    # kernel's ncu DRAM traffic
+    tg = ROOT / "profiles" / "r2_tma_gather_ceiling.jsonl"
+    if tg.exists() and roof["traffic"]:
+        try:
+            rows = [json.loads(x) for x in tg.read_text().splitlines() if x.startswith("{")]
+            l2r = max(r["gbs"] for r in rows if r["table_mb"] <= 64 and r["row_bytes"] == 1024)
+            drr = max(r["gbs"] for r in rows if r["table_mb"] >= 1024 and r["row_bytes"] == 1024)
+            gathered = tot_eff / len(parts)
+            miss = min(float(roof["traffic"]), gathered)
+            t_min = (gathered - miss) / (l2r * 1e9) + miss / (drr * 1e9)
+            roof["gather_model"] = {"l2_hit_GBps": l2r, "dram_miss_GBps": drr, "gathered_bytes": gathered,
+                                    "dram_bytes": miss, "t_min_us": 1e6 * t_min,
+                                    "frac": t_min / (tot_t / len(parts) / 1000.0),
+                                    "source": "profiles/r2_tma_gather_ceiling.jsonl"}
+        except Exception:
+            pass
     extra = {}
     if ws > 1:  # exchange bytes of the last timed epoch (dp.cu bookkeeping), max over ranks
         tf = runner.traffic()
