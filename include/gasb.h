@@ -206,6 +206,28 @@ gasb_status gasb_spmm_fwd(const int32_t* d_rowptr, int32_t num_dst, const int32_
 gasb_status gasb_spmm_bwd(const int32_t* d_t_rowptr, int32_t num_targets, const int32_t* d_t_src,
                           const float* d_t_coeffs, const float* d_gy, int64_t ldgy, int32_t num_src, int32_t dim,
                           const float* d_mask, int64_t ldm, float* d_gx, int64_t ldgx, gasb_stream stream);
+/* max and mean aggregation (north_star 3: sum/mean/max SpMM) over the same CSR stencils
+ * (device int32 rowptr starting at 0, int32 cols into x's num_src rows). The reference has
+ * only weighted sums (aggregate, tensor.cpp:514-549), so these are pinned to their
+ * definitions (oracle/aggregators.py), not to a reference function:
+ *  max_fwd : y[r,j] = the first edge's x[c,j], replaced in CSR order by any strictly greater
+ *            value; d_argmax[r,j] (optional) = that edge's index; empty rows give 0 and -1;
+ *  max_bwd : gx[s,j] = fp32 sum over rows r ascending of gy[r,j] for the edges (r -> s) that
+ *            are argmax[r,j] (deterministic; overwrites gx's num_src rows);
+ *  mean_fwd: y[r,j] = float(fp64 CSR-order sum of x[c,j] / deg r), 0 for an empty row;
+ *  mean backward = gasb_spmm_bwd with the coefficients gasb_mean_coefficients writes
+ *            (float(1.0 / deg r) per edge, host arrays).
+ * Range errors raise the reference's aggregate message (tensor.cpp:515). */
+gasb_status gasb_spmm_max_fwd(const int32_t* d_rowptr, int32_t num_dst, const int32_t* d_cols, const float* d_x,
+                              int32_t num_src, int64_t ldx, int32_t dim, float* d_y, int64_t ldy, int32_t* d_argmax,
+                              int64_t ld_arg, gasb_stream stream);
+gasb_status gasb_spmm_max_bwd(const int32_t* d_rowptr, int32_t num_dst, const int32_t* d_cols,
+                              const int32_t* d_argmax, int64_t ld_arg, const float* d_gy, int64_t ldgy,
+                              int32_t num_src, int32_t dim, float* d_gx, int64_t ldgx, gasb_stream stream);
+gasb_status gasb_spmm_mean_fwd(const int32_t* d_rowptr, int32_t num_dst, const int32_t* d_cols, const float* d_x,
+                               int32_t num_src, int64_t ldx, int32_t dim, float* d_y, int64_t ldy,
+                               gasb_stream stream);
+gasb_status gasb_mean_coefficients(const int32_t* h_rowptr, int32_t num_dst, float* h_coeffs);
 /* matmul (tensor.cpp:148-204) on fp32 row-major operands, fp32 accumulation:
  * op = 0: C = A[m,k] B[k,n]; 1: C = A[m,k] B[n,k]^T; 2: C = A[k,m]^T B[k,n].
  * beta == 0 overwrites C, beta == 1 accumulates. */

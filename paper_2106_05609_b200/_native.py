@@ -117,6 +117,10 @@ _SIGS = {
     "gasb_spmm_fwd": (i32, [vp, i32, vp, vp, vp, i32, i64, i32, vp, i64, i32, vp]),
     "gasb_spmm_bwd": (i32, [vp, i32, vp, vp, vp, i64, i32, i32, vp, i64, vp, i64, vp]),
     "gasb_gemm": (i32, [i32, i32, i32, i32, vp, i64, vp, i64, vp, i64, f32, vp]),
+    "gasb_spmm_max_fwd": (i32, [vp, i32, vp, vp, i32, i64, i32, vp, i64, vp, i64, vp]),
+    "gasb_spmm_max_bwd": (i32, [vp, i32, vp, vp, i64, vp, i64, i32, i32, vp, i64, vp]),
+    "gasb_spmm_mean_fwd": (i32, [vp, i32, vp, vp, i32, i64, i32, vp, i64, vp]),
+    "gasb_mean_coefficients": (i32, [vp, i32, vp]),
     "gasb_batch_ops_create": (i32, [vp, i32, i32, P(vp)]),
     "gasb_batch_ops_sizes": (i32, [vp, P(i32), P(i32)]),
     "gasb_batch_ops_destroy": (i32, [vp]),
