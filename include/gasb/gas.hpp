@@ -353,6 +353,32 @@ inline void aggregate_backward(const std::int32_t* d_t_rowptr, std::int32_t num_
     check(gasb_spmm_bwd(d_t_rowptr, num_targets, d_t_src, d_t_coeffs, d_gy, ldgy, num_src, dim, d_mask, ldm, d_gx,
                         ldgx, stream));
 }
+// max / mean neighbourhood aggregation (north_star's sum/mean/max SpMM; no reference
+// counterpart, semantics fixed in gasb.h): forward with argmax, backward by argmax.
+inline void aggregate_max_forward(const std::int32_t* d_rowptr, std::int32_t num_dst, const NodeId* d_cols,
+                                  const float* d_x, std::int32_t num_src, std::int64_t ldx, std::int32_t dim,
+                                  float* d_y, std::int64_t ldy, std::int32_t* d_argmax, std::int64_t ld_arg,
+                                  gasb_stream stream) {
+    check(gasb_spmm_max_fwd(d_rowptr, num_dst, d_cols, d_x, num_src, ldx, dim, d_y, ldy, d_argmax, ld_arg, stream));
+}
+inline void aggregate_max_backward(const std::int32_t* d_rowptr, std::int32_t num_dst, const NodeId* d_cols,
+                                   const std::int32_t* d_argmax, std::int64_t ld_arg, const float* d_gy,
+                                   std::int64_t ldgy, std::int32_t num_src, std::int32_t dim, float* d_gx,
+                                   std::int64_t ldgx, gasb_stream stream) {
+    check(gasb_spmm_max_bwd(d_rowptr, num_dst, d_cols, d_argmax, ld_arg, d_gy, ldgy, num_src, dim, d_gx, ldgx,
+                            stream));
+}
+inline void aggregate_mean_forward(const std::int32_t* d_rowptr, std::int32_t num_dst, const NodeId* d_cols,
+                                   const float* d_x, std::int32_t num_src, std::int64_t ldx, std::int32_t dim,
+                                   float* d_y, std::int64_t ldy, gasb_stream stream) {
+    check(gasb_spmm_mean_fwd(d_rowptr, num_dst, d_cols, d_x, num_src, ldx, dim, d_y, ldy, stream));
+}
+// float(1/deg) per edge: aggregate_backward with these coefficients is the mean's backward
+inline std::vector<float> mean_coefficients(const std::vector<std::int32_t>& rowptr) {
+    std::vector<float> c(rowptr.empty() ? 0 : static_cast<std::size_t>(rowptr.back()));
+    check(gasb_mean_coefficients(rowptr.data(), static_cast<std::int32_t>(rowptr.size()) - 1, c.data()));
+    return c;
+}
 enum class MatmulOp : std::int32_t { NN = 0, NT = 1, TN = 2 };
 inline void matmul(MatmulOp op, std::int32_t m, std::int32_t n, std::int32_t k, const float* d_a, std::int64_t lda,
                    const float* d_b, std::int64_t ldb, float* d_c, std::int64_t ldc, bool accumulate,
