@@ -114,6 +114,10 @@ void launch_spmm_fwd(const SpmmSegs& s, const int32_t* cols, const double* coeff
 // Caps the grid of this thread's flat SpMM launches at `ctas` CTAs (0: the full persistent
 // grid). Work items are grid-strided, so a capped launch does the same work on fewer SMs.
 void set_spmm_grid_cap(int32_t ctas);
+// Row-sum hand-off for this thread's next flat SpMM launches (reset with nullptrs): out: each
+// finished row's fp64 sum is written to out[row - row_base] (ld doubles per row) instead of
+// the fp32 row; in: the fp32 row stored is float(sum + in[row - row_base]).
+void set_spmm_row_sums(double* out, const double* in, int64_t ld);
 bool make_row_tmap(const float* base, int64_t rows, int32_t dim, int64_t ld, int32_t box_cols, CUtensorMap* out);
 int32_t spmm_box_cols(int32_t dim);
 int32_t spmm_cpl_for(int32_t dim);

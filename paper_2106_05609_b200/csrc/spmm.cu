@@ -472,6 +472,15 @@ __device__ __forceinline__ int32_t col_of(int32_t col, int k) {
     return CPL == 8 ? col + (k & 3) + ((k >> 2) << 7) : col + k;
 }
 
+// Optional row-sum hand-off between two launches over the same rows (cross-batch mode):
+// out != nullptr: a finished row's fp64 sum goes to out[row - row_base] (ld doubles per row)
+// instead of y; in != nullptr: the stored fp32 row is float(sum + in[row - row_base]).
+struct RowSums {
+    double* out = nullptr;
+    const double* in = nullptr;
+    int64_t ld = 0;
+};
+
 // Ends segment `k` of the warp's window: store the row (single-segment row) or publish an
 // fp64 partial, the last-arriving warp of the row summing the partials in segment order.
 template <int CPL>
@@ -481,7 +490,7 @@ __device__ __forceinline__ void seg_finish(double (&acc)[CPL], int32_t row, int3
                                            int32_t* __restrict__ counters, int32_t cld,
                                            const int32_t* __restrict__ seg_slot,
                                            const int32_t* __restrict__ row_seg0,
-                                           const int32_t* __restrict__ row_nseg) {
+                                           const int32_t* __restrict__ row_nseg, const RowSums& rs = RowSums{}) {
     bool store = true;
     if (slot >= 0) {
         double* pp = partial + static_cast<int64_t>(slot) * pld;
@@ -507,10 +516,20 @@ __device__ __forceinline__ void seg_finish(double (&acc)[CPL], int32_t row, int3
         }
     }
     if (store) {
-        float* yr = y + (static_cast<int64_t>(row) - row_base) * ldy;
+        if (rs.out) {  // the row's fp64 sum for a later launch (no fp32 row)
+            double* o = rs.out + (static_cast<int64_t>(row) - row_base) * rs.ld;
 #pragma unroll
-        for (int k = 0; k < CPL; ++k)
-            if (col_of<CPL>(col, k) < dim) yr[col_of<CPL>(col, k)] = static_cast<float>(acc[k]);
+            for (int k = 0; k < CPL; ++k)
+                if (col_of<CPL>(col, k) < dim) o[col_of<CPL>(col, k)] = acc[k];
+        } else {
+            float* yr = y + (static_cast<int64_t>(row) - row_base) * ldy;
+            const double* si = rs.in ? rs.in + (static_cast<int64_t>(row) - row_base) * rs.ld : nullptr;
+#pragma unroll
+            for (int k = 0; k < CPL; ++k)
+                if (col_of<CPL>(col, k) < dim)
+                    yr[col_of<CPL>(col, k)] =
+                        static_cast<float>(si ? __dadd_rn(acc[k], __ldcg(si + col_of<CPL>(col, k))) : acc[k]);
+        }
     }
 #pragma unroll
     for (int k = 0; k < CPL; ++k) acc[k] = 0.0;
@@ -698,7 +717,7 @@ __device__ __forceinline__ void flat_items(
     int32_t nchunks, float* __restrict__ y, int64_t ldy, int64_t row_base, double* __restrict__ partial, int64_t pld,
     int32_t* __restrict__ counters, int32_t cld, const int32_t* __restrict__ slot_list, const CUtensorMap* tmap,
     unsigned char* wbase, uint64_t* bars,
-    int32_t* ring_c, double* ring_f) {
+    int32_t* ring_c, double* ring_f, const RowSums& rsum) {
     using Cfg = PipeCfg<CPL>;
     constexpr int KE = Cfg::kEdges;
     static_assert(KE == 8 || KE == 16 || KE == 32, "a flat stage is a quarter, half or all of a 32-edge window");
@@ -789,7 +808,7 @@ __device__ __forceinline__ void flat_items(
                 }
             }
             seg_finish<CPL>(acc, row, slot, lane, col, chunk, dim, y, ldy, row_base, partial, pld, counters, cld,
-                            slot_list, row_seg0, row_nseg);
+                            slot_list, row_seg0, row_nseg, rsum);
             ++cur;
             if (cur < s_hi) {
                 if (cur - wseg >= 32) load_window(cur);
@@ -854,7 +873,7 @@ __global__ void __launch_bounds__(kPipeWarps * 32, kPipeCtas) spmm_fwd_flat_kern
     int32_t nranges, const int32_t* __restrict__ cols, const double* __restrict__ coeffs, int32_t dim,
     int32_t nchunks, float* __restrict__ y, int64_t ldy, int64_t row_base, double* __restrict__ partial, int64_t pld,
     int32_t* __restrict__ counters, int32_t cld, const int32_t* __restrict__ table_flags,
-    const int32_t* __restrict__ slot_list, const __grid_constant__ CUtensorMap tmap) {
+    const int32_t* __restrict__ slot_list, const __grid_constant__ CUtensorMap tmap, const RowSums rsum) {
     using Cfg = PipeCfg<CPL>;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     pdl_trigger();
@@ -875,7 +894,7 @@ __global__ void __launch_bounds__(kPipeWarps * 32, kPipeCtas) spmm_fwd_flat_kern
     const int mode = widen_mode(table_flags);
 #define GASB_FLAT(M)                                                                                              \
     flat_items<CPL, M, DUAL>(seg_beg, seg_row, seg_slot, row_seg0, row_nseg, range_seg, nranges, cols, coeffs, dim, nchunks, \
-                  y, ldy, row_base, partial, pld, counters, cld, slot_list, &tmap, wbase, bars, ring_c, ring_f)
+                  y, ldy, row_base, partial, pld, counters, cld, slot_list, &tmap, wbase, bars, ring_c, ring_f, rsum)
     if (mode == kWidenNonNeg) GASB_FLAT(kWidenNonNeg);
     else if (mode == kWidenSigned) GASB_FLAT(kWidenSigned);
     else GASB_FLAT(kWidenF2F);
@@ -886,6 +905,9 @@ __global__ void __launch_bounds__(kPipeWarps * 32, kPipeCtas) spmm_fwd_flat_kern
 // background stream's launches leave SMs to the batch chain running beside them.
 static thread_local int32_t t_spmm_grid_cap = 0;
 void set_spmm_grid_cap(int32_t ctas) { t_spmm_grid_cap = ctas; }
+// Row-sum hand-off of this thread's next flat SpMM launches (set_spmm_row_sums).
+static thread_local RowSums t_row_sums{};
+void set_spmm_row_sums(double* out, const double* in, int64_t ld) { t_row_sums = RowSums{out, in, ld}; }
 
 template <int CPL, bool DUAL>
 static void launch_flat(const SpmmSegs& s, const int32_t* cols, const double* coeffs, int32_t dim, float* y,
@@ -914,7 +936,7 @@ static void launch_flat(const SpmmSegs& s, const int32_t* cols, const double* co
     launch_pdl(spmm_fwd_flat_kernel<CPL, DUAL>, dim3(static_cast<unsigned>(blocks)), dim3(kPipeWarps * 32), kSmem, st,
                s.seg_beg, s.seg_row, s.seg_slot, s.row_seg0, s.row_nseg, s.range_seg, s.nranges, cols, coeffs, dim,
                nchunks, y, ldy, row_base, partial, partial_ld, counters, counters_ld, special,
-               s.row_slots ? s.row_slots : s.seg_slot, *tmap);
+               s.row_slots ? s.row_slots : s.seg_slot, *tmap, t_row_sums);
 }
 
 static int g_pipe_smem_set[2][2] = {};

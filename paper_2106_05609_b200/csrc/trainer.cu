@@ -1026,8 +1026,10 @@ void gasb_trainer_s::enqueue_batch(int32_t p, bool train, bool push, bool use_ho
         if (l == 1 && use_hoisted) {
             a = agg_all.p + r0 * ldF;
         } else if (xsplit) {
+            set_spmm_row_sums(nullptr, xsums(l), pldx);  // y = float(intra sum + halo sum)
             launch_spmm_fwd(xsegs(p, false), xcols.p, xcoef.p, history_table(hist, l - 1), history_ld(hist), din, a,
                             lda, r0, xpartial(l), pldx, xcounters(l), cxld, stream, source_flags(l), source_tmap(l));
+            set_spmm_row_sums(nullptr, nullptr, 0);
         } else if (fused) {
             const float* src = l == 1 ? X.p : history_table(hist, l - 1);
             const int64_t lds = l == 1 ? ldF : history_ld(hist);
@@ -1267,51 +1269,55 @@ void gasb_trainer_s::build_xbatch(const std::vector<int64_t>& rp, const HVec<int
     }
     xcols.upload(xc);
     xcoef.upload(xf);
-    // segments: per part the halo group (2p) then the intra group (2p + 1); slots restart per part
-    const int32_t nr = spmm_ranges_per_launch();
-    seg_x.nranges = nr;
-    seg_x.split = true;
-    std::vector<int64_t> sb, tmp(static_cast<size_t>(R) + 1);
-    std::vector<int32_t> sr, ss, r0h(R), rnh(R), r0i(R), rni(R), rs(static_cast<size_t>(2 * num_parts) * (nr + 1));
-    std::vector<int32_t> seg0(R), nseg(R), slots;
-    xslots = 0;
-    for (int32_t p = 0; p < num_parts; ++p) {
-        const int64_t lo = row_off[p], hi = row_off[p + 1];
-        int64_t dummy = 0;
-        const int64_t g0 = static_cast<int64_t>(sr.size());
-        for (int64_t r = lo; r < hi; ++r) tmp[r] = rph[r];
-        tmp[hi] = hend[p];
-        if (!sb.empty()) sb.pop_back();
-        segment_launch(tmp.data(), lo, hi, true, nr, sb, sr, ss, r0h.data(), rnh.data(), dummy,
-                       rs.data() + static_cast<int64_t>(2 * p) * (nr + 1));
-        for (int64_t r = lo; r < hi; ++r) tmp[r] = rpi[r];
-        tmp[hi] = edge_off[p + 1];
-        sb.pop_back();
-        segment_launch(tmp.data(), lo, hi, true, nr, sb, sr, ss, r0i.data(), rni.data(), dummy,
-                       rs.data() + static_cast<int64_t>(2 * p + 1) * (nr + 1));
-        const int64_t g2 = static_cast<int64_t>(sr.size());
-        for (int64_t s2 = g0; s2 < g2; ++s2) ss[s2] = static_cast<int32_t>(s2 - g0);
-        xslots = std::max(xslots, g2 - g0);
-        for (int64_t r = lo; r < hi; ++r) {
-            seg0[r] = static_cast<int32_t>(slots.size());
-            nseg[r] = rnh[r] + rni[r];
-            for (int32_t i = 0; i < rnh[r]; ++i) slots.push_back(ss[r0h[r] + i]);
-            for (int32_t i = 0; i < rni[r]; ++i) slots.push_back(ss[r0i[r] + i]);
-        }
-    }
-    seg_x.ranges.upload(rs);
-    seg_x.seg_beg.upload(sb);
-    seg_x.seg_row.upload(sr);
-    seg_x.seg_slot.upload(ss);
-    seg_x.row_seg0.upload(seg0);
-    seg_x.row_nseg.upload(nseg);
-    seg_x.row_slots.upload(slots);
-    seg_x.max_group_slots = seg_x.total_slots = xslots;
+    std::vector<int64_t> iend(num_parts);
+    for (int32_t p = 0; p < num_parts; ++p) iend[p] = edge_off[p + 1];
+    build_block_segments(rph, hend, seg_xh);
+    build_block_segments(rpi, iend, seg_xi);
+    xslots = std::max(seg_xh.max_group_slots, seg_xi.max_group_slots);
     pldx = round_up(std::max(H, 1), 256);
     cxld = static_cast<int32_t>(ceil_div(std::max(H, 1), 64));
     partial_x.alloc(static_cast<int64_t>(L - 1) * std::max<int64_t>(xslots, 1) * pldx);
     counters_x.alloc(static_cast<int64_t>(L - 1) * R * cxld);
     counters_x.zero();
+    xsum.alloc(static_cast<int64_t>(L - 1) * nb_max * pldx);
+}
+
+// Segment table of one block per part (rows' edges at row_start[r] .., the part's block ending
+// at part_end[p]): the split segmentation of segment_launch, one launch (group) per part. A
+// zero-length gap segment after each part keeps seg_beg[group end] at the block's end (the
+// next part's block starts elsewhere).
+void gasb_trainer_s::build_block_segments(const std::vector<int64_t>& row_start, const std::vector<int64_t>& part_end,
+                                          SegTable& t) {
+    const int64_t R = row_off[num_parts];
+    const int32_t nr = spmm_ranges_per_launch();
+    t.nranges = nr;
+    t.split = true;
+    std::vector<int64_t> sb, tmp(static_cast<size_t>(R) + 1);
+    std::vector<int32_t> sr, ss, r0(R), rn(R), rs(static_cast<size_t>(num_parts) * (nr + 1));
+    t.group_seg0.assign(num_parts, 0);
+    t.group_nseg.assign(num_parts, 0);
+    t.max_group_slots = 0;
+    for (int32_t p = 0; p < num_parts; ++p) {
+        const int64_t lo = row_off[p], hi = row_off[p + 1];
+        for (int64_t r = lo; r < hi; ++r) tmp[r] = row_start[r];
+        tmp[hi] = part_end[p];
+        t.group_seg0[p] = static_cast<int64_t>(sr.size());
+        int64_t slot = 0;
+        segment_launch(tmp.data(), lo, hi, true, nr, sb, sr, ss, r0.data(), rn.data(), slot,
+                       rs.data() + static_cast<int64_t>(p) * (nr + 1));
+        t.group_nseg[p] = static_cast<int64_t>(sr.size()) - t.group_seg0[p];
+        t.max_group_slots = std::max(t.max_group_slots, slot);
+        sr.push_back(static_cast<int32_t>(lo));  // the gap segment (sb's sentinel stays as its start)
+        ss.push_back(-1);
+    }
+    sb.push_back(sb.empty() ? 0 : sb.back());
+    t.total_slots = t.max_group_slots;
+    t.ranges.upload(rs);
+    t.seg_beg.upload(sb);
+    t.seg_row.upload(sr);
+    t.seg_slot.upload(ss);
+    t.row_seg0.upload(r0);
+    t.row_nseg.upload(rn);
 }
 
 // Background work of batch q on `bg`: (xmode 2) its layer-1 rows of agg_all, then — after the
@@ -1322,10 +1328,13 @@ void gasb_trainer_s::enqueue_bg(int32_t q, bool wait_fwd) {
         launch_spmm_fwd(seg_batch.segs(q), cols_g.p, coef64.p, X.p, ldF, F, agg_all.p, ldF, 0, partial_batch.p, pld,
                         counters.p, max_chunks, bg, source_flags(1), source_tmap(1));
     if (wait_fwd) GASB_CUDA(cudaStreamWaitEvent(bg, ev_xfwd, 0));
-    for (int32_t l = 2; l <= L; ++l)  // (rows are stored by the intra launch: y is never written here)
+    for (int32_t l = 2; l <= L; ++l) {  // fp64 row sums of the halo block (the intra launch stores the rows)
+        set_spmm_row_sums(xsums(l), nullptr, pldx);
         launch_spmm_fwd(xsegs(q, true), xcols.p, xcoef.p, history_table(hist, l - 1), history_ld(hist), dims[l - 1],
                         agg[l].p, ld_of(dims[l - 1]), row_off[q], xpartial(l), pldx, xcounters(l), cxld, bg,
                         source_flags(l), source_tmap(l));
+    }
+    set_spmm_row_sums(nullptr, nullptr, 0);
     set_spmm_grid_cap(0);
 }
 

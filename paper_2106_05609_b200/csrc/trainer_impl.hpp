@@ -304,9 +304,10 @@ struct gasb_trainer_s {
     cudaEvent_t ev_xstart = nullptr, ev_xfwd = nullptr, ev_xbg = nullptr;
     DevBuf<int32_t> xcols;      // per part, edges re-laid [halo-source block | intra-source block],
     DevBuf<double> xcoef;       //   each row-major in CSR order (same offsets as cols_g)
-    SegTable seg_x;             // groups 2p (halo block) and 2p + 1 (intra block); row_slots
+    SegTable seg_xh, seg_xi;    // per part: the halo block's / the intra block's segments
     DevBuf<double> partial_x;   // per history layer: xslots x pldx fp64 partials
     DevBuf<int32_t> counters_x; // per history layer: R x cxld arrival counters (self-resetting)
+    DevBuf<double> xsum;        // per history layer: the halo block's fp64 row sums (nb_max x pldx)
     int64_t pldx = 0, xslots = 0;
     int32_t cxld = 0;
     std::vector<cudaGraphExec_t> graphs_xf, graphs_xb;
@@ -315,7 +316,10 @@ struct gasb_trainer_s {
     void enqueue_bg(int32_t q, bool wait_fwd);
     int64_t launch_x_graph(int32_t p, int32_t phase);
     void run_epoch_x(const std::vector<int32_t>& order);
-    SpmmSegs xsegs(int32_t p, bool halo) const { return seg_x.segs(2 * static_cast<int64_t>(p) + (halo ? 0 : 1)); }
+    SpmmSegs xsegs(int32_t p, bool halo) const { return (halo ? seg_xh : seg_xi).segs(p); }
+    double* xsums(int32_t l) { return xsum.p + static_cast<int64_t>(l - 2) * nb_max * pldx; }
+    void build_block_segments(const std::vector<int64_t>& row_start, const std::vector<int64_t>& part_end,
+                              SegTable& t);
     double* xpartial(int32_t l) { return partial_x.p + static_cast<int64_t>(l - 2) * xslots * pldx; }
     int32_t* xcounters(int32_t l) { return counters_x.p + static_cast<int64_t>(l - 2) * row_off[num_parts] * cxld; }
 
