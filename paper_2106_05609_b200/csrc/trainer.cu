@@ -1001,6 +1001,17 @@ void gasb_trainer_s::enqueue_batch_res(int32_t p, bool train, bool push, bool fu
     GASB_CUDA(cudaGetLastError());
 }
 
+namespace {
+// Restores the thread's flat-SpMM launch state (grid cap, row-sum hand-off) on every exit path,
+// so an exception between setting and clearing it cannot leak into later launches.
+struct SpmmLaunchState {
+    ~SpmmLaunchState() {
+        set_spmm_grid_cap(0);
+        set_spmm_row_sums(nullptr, nullptr, 0);
+    }
+};
+}  // namespace
+
 void gasb_trainer_s::enqueue_batch(int32_t p, bool train, bool push, bool use_hoisted, bool fused, bool dp) {
     WsGuard ws(gemm_ws, &colsum_ws);
     if (residual) {
@@ -1026,10 +1037,10 @@ void gasb_trainer_s::enqueue_batch(int32_t p, bool train, bool push, bool use_ho
         if (l == 1 && use_hoisted) {
             a = agg_all.p + r0 * ldF;
         } else if (xsplit) {
+            SpmmLaunchState restore;
             set_spmm_row_sums(nullptr, xsums(l), pldx);  // y = float(intra sum + halo sum)
             launch_spmm_fwd(xsegs(p, false), xcols.p, xcoef.p, history_table(hist, l - 1), history_ld(hist), din, a,
                             lda, r0, xpartial(l), pldx, xcounters(l), cxld, stream, source_flags(l), source_tmap(l));
-            set_spmm_row_sums(nullptr, nullptr, 0);
         } else if (fused) {
             const float* src = l == 1 ? X.p : history_table(hist, l - 1);
             const int64_t lds = l == 1 ? ldF : history_ld(hist);
@@ -1323,6 +1334,7 @@ void gasb_trainer_s::build_block_segments(const std::vector<int64_t>& row_start,
 // Background work of batch q on `bg`: (xmode 2) its layer-1 rows of agg_all, then — after the
 // previous batch's forward (ev_xfwd) when wait_fwd — the halo block of every history layer.
 void gasb_trainer_s::enqueue_bg(int32_t q, bool wait_fwd) {
+    SpmmLaunchState restore;
     set_spmm_grid_cap(bg_ctas);
     if (xmode == 2)
         launch_spmm_fwd(seg_batch.segs(q), cols_g.p, coef64.p, X.p, ldF, F, agg_all.p, ldF, 0, partial_batch.p, pld,
@@ -1334,8 +1346,6 @@ void gasb_trainer_s::enqueue_bg(int32_t q, bool wait_fwd) {
                         agg[l].p, ld_of(dims[l - 1]), row_off[q], xpartial(l), pldx, xcounters(l), cxld, bg,
                         source_flags(l), source_tmap(l));
     }
-    set_spmm_row_sums(nullptr, nullptr, 0);
-    set_spmm_grid_cap(0);
 }
 
 // One phase (1 forward, 2 loss + backward + Adam) of batch p on `stream`, through its captured
